@@ -1,0 +1,208 @@
+/*
+ * voxpipe_b200 — C-ABI of the B200-native sparse-convolution hot path.
+ *
+ * Drop-in boundary for the reference voxpipe 0.1.0 (arXiv 2012.13846,
+ * "SparsePipe"): every entry point below replaces one reference function or
+ * loop of its hot path (cited per function).  Conventions:
+ *
+ *   - plain pointers and sizes only (no torch types); all array pointers are
+ *     DEVICE pointers unless the parameter says "host";
+ *   - stream-ordered: every call only enqueues work on `stream` (no host
+ *     synchronisation), so calls are CUDA-graph capturable;
+ *   - data-dependent counts live in device memory (`int32_t* n_*_dev`); a
+ *     NULL count pointer means "the count equals the capacity argument";
+ *     capacities (`cap_*`, host) size grids and buffers;
+ *   - no global mutable state: scratch comes from the caller (`ws`, sized by
+ *     the matching *_ws_bytes query), so calls are re-entrant across
+ *     streams and threads;
+ *   - status codes mirror voxpipe/errors.py:3-5 exit codes:
+ *       VP_OK = 0, VP_EVALIDATION = 2 (ValidationError/StructuralError),
+ *       VP_EINTERNAL = 3 (InternalError, e.g. a CUDA launch failure).
+ *     vp_last_error() returns a per-thread message for the last failure.
+ *
+ * Coordinates are int32 rows [batch, x, y, z] (16 B, D <= 3 with unused axes
+ * zero); hash keys use the reference packing (kernels.py:53-79): 16-bit
+ * fields batch<<48 | (x+32768)<<32 | (y+32768)<<16 | (z+32768).
+ * Features are bf16 (dtype 1) or fp32 (dtype 0) row-major [rows, channels].
+ * Weights are [K, C_out, C_in] (conv.py:77-105 layout).
+ */
+#ifndef VOXPIPE_B200_H
+#define VOXPIPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* vp_stream_t; /* == cudaStream_t */
+
+enum { VP_OK = 0, VP_EVALIDATION = 2, VP_EINTERNAL = 3 };
+enum { VP_F32 = 0, VP_BF16 = 1, VP_F64 = 2 };
+#define VP_MAX_OFFSETS 343 /* 7^3 */
+
+const char* vp_last_error(void);
+const char* vp_version(void);
+
+/* ---------------------------------------------------------------- hash
+ * Replaces _kernels.pyx:24-47 `build_table` and :50-73 `lookup` (the
+ * VOXPIPE_BACKEND seam, kernels.py:21-32,82-92).  Open addressing with
+ * linear probing on splitmix64 (_kernels.pyx:16-21); capacity = pow2 >=
+ * 2n+2 (min 8) (_kernels.pyx:27-29); FIRST occurrence of a duplicated key
+ * wins (_kernels.pyx:44-46); lookup returns the row or -1.  `table` holds
+ * (cap + 1) 16-byte slots (vp_hash_bytes). */
+int64_t vp_hash_capacity(int64_t n);
+size_t vp_hash_bytes(int64_t cap);
+int vp_hash_build(const int64_t* keys, const int32_t* n_dev, int64_t cap_n,
+                  void* table, int64_t table_cap, vp_stream_t stream);
+int vp_hash_lookup(const void* table, int64_t table_cap, const int64_t* queries,
+                   int64_t m, int64_t* rows_out, vp_stream_t stream);
+
+/* pack_rows (kernels.py:53-79) for int32 [n,4] rows; bad_dev (nullable)
+ * receives 1 if any row is out of the packable range (ValidationError). */
+int vp_pack_coords(const int32_t* coords, int64_t n, int64_t* keys, int32_t* bad_dev,
+                   vp_stream_t stream);
+
+/* ---------------------------------------------------------------- coords
+ * SparseTensor invariants (tensor.py:49-78): flags_dev[0] |= 1 duplicate
+ * row, |= 2 negative batch, |= 4 axis not a multiple of the stride, |= 8
+ * unpackable coordinate.  Replaces the np.unique dedupe (tensor.py:28-33). */
+size_t vp_validate_coords_ws_bytes(int64_t cap_n);
+int vp_validate_coords(const int32_t* coords, const int32_t* n_dev, int64_t cap_n,
+                       const int32_t* tensor_stride_host3, int32_t* flags_dev,
+                       void* ws, size_t ws_bytes, vp_stream_t stream);
+/* finite check of features (tensor.py:71-72): flags_dev[0] |= 16 if any
+ * non-finite value. */
+int vp_check_finite(const void* feats, int32_t dtype, int64_t count, int32_t* flags_dev,
+                    vp_stream_t stream);
+
+/* generate_output_coords (conv.py:124-146) for stride > 1: floor-div by
+ * the NEW tensor stride `step` (= tensor_stride * stride), rescale, unique
+ * rows in FIRST-SEEN order.  out needs cap_in rows; *n_out_dev receives
+ * N_out.  parent (nullable, int32 [cap_in]) receives the output row of each
+ * input row (used by pooling/unpooling glue). */
+size_t vp_output_coords_ws_bytes(int64_t cap_in);
+int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
+                     const int32_t* step_host3, int32_t* out, int32_t* n_out_dev,
+                     int32_t* parent, void* ws, size_t ws_bytes, vp_stream_t stream);
+
+/* voxelize (tensor.py:147-184) + batch (tensor.py:205-229) fused: points
+ * [n,3] (f32 or f64) of B clouds delimited by cloud_offsets_dev[B+1]
+ * (int64); voxel = clip(floor(p / voxel_size), 0, res-1) in f64; batch index
+ * = cloud position; rows in first-seen order per cloud, clouds
+ * concatenated.  coords_out needs n rows; point2voxel (nullable) receives
+ * each point's output row; feats_out (nullable, dtype feat_dtype, [n,1])
+ * receives the occupancy feature 1.0. */
+size_t vp_voxelize_ws_bytes(int64_t n_points);
+int vp_voxelize(const void* points, int32_t pts_dtype, int64_t n_points,
+                const int64_t* cloud_offsets_dev, int32_t n_clouds, double voxel_size,
+                const int32_t* res_host3, int32_t* coords_out, int32_t* n_out_dev,
+                int32_t* point2voxel, void* feats_out, int32_t feat_dtype,
+                void* ws, size_t ws_bytes, vp_stream_t stream);
+/* mean-merged features (tensor.py:178-183, np.add.at order = point order,
+ * deterministic): feats_in [n, F] f32/f64 -> feats_out [n_vox, F] f32. */
+size_t vp_voxel_mean_ws_bytes(int64_t n_points, int64_t cap_vox);
+int vp_voxel_mean(const void* feats_in, int32_t in_dtype, int64_t n_points, int32_t F,
+                  const int32_t* point2voxel, const int32_t* n_vox_dev, int64_t cap_vox,
+                  float* feats_out, void* ws, size_t ws_bytes, vp_stream_t stream);
+
+/* ---------------------------------------------------------------- kernel map
+ * build_kernel_map (conv.py:149-183): one hash over the input rows, then
+ * for every output row u and offset k (shape order) probe
+ * out[u] + off_k * in_stride (batch untouched, conv.py:173-174);
+ * out-of-packable-range queries are misses (kernels.py:131-148).
+ *   nbr      [cap_out, K] int32 : input row or -1 (dense neighbour table)
+ *   pair_in / pair_out [cap_out*K] (nullable): per-offset pair lists in
+ *            CSR order — offset-major, out rows ASCENDING within an offset
+ *            (bit-exact with KernelMap.pairs);
+ *   pair_ptr [K+1] int32 device (nullable iff pair_in is NULL). */
+size_t vp_kernel_map_ws_bytes(int64_t cap_in, int64_t cap_out, int32_t K);
+int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
+                  const int32_t* out, const int32_t* n_out_dev, int64_t cap_out,
+                  const int32_t* offsets_host, int32_t K, const int32_t* in_stride_host3,
+                  int32_t* nbr, int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr,
+                  void* ws, size_t ws_bytes, vp_stream_t stream);
+/* inverse neighbour table inv[v, k] = u for every pair (v,u) of offset k
+ * (the dgrad gather table; conv.py:238-240 iterates the same pairs). */
+int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out,
+                          int32_t K, int32_t* inv, int64_t cap_in, vp_stream_t stream);
+
+/* ---------------------------------------------------------------- sparse conv
+ * Forward (conv.py:186-208, Eq. 3): y[u] = sum_k W_k x[nbr[u,k]], summed per
+ * output row in offset order; output-stationary implicit GEMM on tcgen05
+ * (bf16 in, fp32 TMEM accumulate) when x is bf16 and C_in, C_out are in
+ * {32,64,128,256}; a SIMT kernel otherwise.  Deterministic, no atomics.
+ *   table  : nbr [cap_out, K] (or inv for dgrad); flip != 0 reads column
+ *            K-1-k (stride-1 symmetric kernels: inv[v,k] == nbr[v,K-1-k]).
+ *   w      : [K, c_out, c_in] in w_dtype. */
+int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t c_in, const void* w, int32_t w_dtype,
+                int64_t c_out, int32_t K, const int32_t* table, int32_t flip,
+                const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype,
+                void* ws, size_t ws_bytes, vp_stream_t stream);
+size_t vp_conv_fwd_ws_bytes(int64_t c_in, int64_t c_out, int32_t K);
+/* dgrad (conv.py:240): grad_in[v] = sum_k W_k^T g[inv[v,k]]; same kernel as
+ * the forward with W transposed into ws.  table = inv (or nbr with flip). */
+size_t vp_conv_dgrad_ws_bytes(int64_t c_in, int64_t c_out, int32_t K);
+int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t c_out, const void* w, int32_t w_dtype,
+                  int64_t c_in, int32_t K, const int32_t* table, int32_t flip,
+                  const int32_t* n_in_dev, int64_t cap_in, void* grad_in, int32_t gi_dtype,
+                  void* ws, size_t ws_bytes, vp_stream_t stream);
+/* wgrad (conv.py:241): grad_w[k] = sum_{(v,u) in pairs_k} g[u] x[v]^T into
+ * fp32 [K, c_out, c_in]; deterministic fixed-order chunked reduction. */
+size_t vp_conv_wgrad_ws_bytes(int64_t c_in, int64_t c_out, int32_t K, int64_t cap_pairs);
+int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t c_in, const void* g, int32_t g_dtype,
+                  int64_t c_out, int32_t K, const int32_t* pair_in, const int32_t* pair_out,
+                  const int32_t* pair_ptr, int64_t cap_pairs, float* grad_w,
+                  void* ws, size_t ws_bytes, vp_stream_t stream);
+
+/* ---------------------------------------------------------------- glue
+ * Model glue for the SparseResNet training step (no reference
+ * implementation: SPEC.md:185 non-goal — parity self-defined). */
+/* per-channel batch statistics over rows: mean/rstd [C] fp32 */
+size_t vp_bn_stats_ws_bytes(int64_t cap_n, int64_t C);
+int vp_bn_stats(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C,
+                float eps, float* mean, float* rstd, void* ws, size_t ws_bytes, vp_stream_t stream);
+/* y = act((x - mean) * rstd * gamma + beta [+ res]) ; act = relu if relu */
+int vp_bn_apply(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C,
+                const float* mean, const float* rstd, const float* gamma, const float* beta,
+                const void* res, int32_t res_dtype, int32_t relu, void* y, int32_t y_dtype,
+                vp_stream_t stream);
+/* backward of bn_apply: gy is masked by (y > 0) when relu; writes
+ * grad_x (and grad_res = masked gy when non-null), ggamma/gbeta [C] fp32. */
+size_t vp_bn_backward_ws_bytes(int64_t cap_n, int64_t C);
+int vp_bn_backward(const void* gy, int32_t gy_dtype, const void* y, int32_t y_dtype,
+                   const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C,
+                   const float* mean, const float* rstd, const float* gamma, int32_t relu,
+                   void* grad_x, int32_t gx_dtype, void* grad_res, float* ggamma, float* gbeta,
+                   void* ws, size_t ws_bytes, vp_stream_t stream);
+/* global average pool per batch index (rows batch-contiguous):
+ * out [B, C] fp32, counts [B] int32 */
+int vp_global_pool(const void* x, int32_t x_dtype, const int32_t* coords, const int32_t* n_dev,
+                   int64_t cap_n, int64_t C, int32_t B, float* out, int32_t* counts,
+                   void* ws, size_t ws_bytes, vp_stream_t stream);
+size_t vp_global_pool_ws_bytes(int32_t B);
+int vp_global_pool_backward(const float* gout, const int32_t* coords, const int32_t* counts,
+                            const int32_t* n_dev, int64_t cap_n, int64_t C, void* gx,
+                            int32_t gx_dtype, vp_stream_t stream);
+/* linear + softmax cross entropy (mean over B); writes loss [1] fp32,
+ * logits [B, classes], grad wrt pooled [B, C] and fc grads (fixed-order
+ * reductions over the batch).  ws: vp_linear_xent_ws_bytes. */
+size_t vp_linear_xent_ws_bytes(int32_t B, int32_t classes);
+int vp_linear_xent(const float* pooled, int32_t B, int32_t C, const float* fc_w, const float* fc_b,
+                   int32_t classes, const int32_t* labels, float* logits, float* loss,
+                   float* g_pooled, float* g_fc_w, float* g_fc_b, void* ws, size_t ws_bytes,
+                   vp_stream_t stream);
+/* SGD with momentum over a flat fp32 parameter buffer (p, m, g of n):
+ * m = momentum*m + g; p -= lr*m; and refresh the bf16 shadow copy of the
+ * first n_bf16 entries (p_bf16 nullable). */
+int vp_sgd_momentum(float* p, float* m, const float* g, int64_t n, float lr, float momentum,
+                    void* p_bf16, int64_t n_bf16, vp_stream_t stream);
+/* dtype conversion f32 <-> bf16 */
+int vp_cast(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t count,
+            vp_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXPIPE_B200_H */

@@ -1,0 +1,416 @@
+"""Generalized sparse convolution on B200 — the reference's `voxpipe.conv`
+API (conv.py:1-386) backed by the sm_100a kernels of libvoxpipe_b200.so.
+
+Three steps (conv.py:1-8): output coordinates
+(`vp_output_coords`), kernel map through a GPU hash (`vp_kernel_map`), and
+the per-offset contraction as an output-stationary implicit GEMM on tcgen05
+(`vp_conv_fwd` / `vp_conv_dgrad` / `vp_conv_wgrad`).  Kernel maps and output
+coordinates are bit-exact with the reference; features/gradients agree within
+the bf16/fp32 tolerances stated in DESIGN.md §6.
+
+Precision: bf16 features take the tensor-core path (bf16 operands, fp32
+accumulation, bf16 output); fp32 features take the fp32 SIMT path.  Weights
+are fp32 masters ([K, C_out, C_in], conv.py:77-105 layout); the tensor-core
+path reads a bf16 copy.
+"""
+from __future__ import annotations
+
+import itertools
+import json
+import struct
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import StructuralError, ValidationError
+from .tensor import SparseTensor, binary_size, pad_coords
+
+_WEIGHTS_MAGIC = b"VXCW"
+_WEIGHTS_VERSION = 1
+
+
+@dataclass(frozen=True)
+class KernelShape:
+    """Set of integer offsets swept by the kernel (conv.py:33-74)."""
+
+    dim: int
+    extents: tuple
+    offsets: np.ndarray  # (K, dim) int64, host
+
+    def __post_init__(self):
+        offsets = np.ascontiguousarray(self.offsets, dtype=np.int64)
+        if offsets.ndim != 2 or offsets.shape[1] != self.dim:
+            raise StructuralError("offsets must have shape (K, dim)")
+        if len(np.unique(offsets, axis=0)) != len(offsets):
+            raise StructuralError("kernel offsets must be distinct")
+        offsets.setflags(write=False)
+        object.__setattr__(self, "offsets", offsets)
+        object.__setattr__(self, "extents", tuple(int(e) for e in self.extents))
+
+    @classmethod
+    def hypercubic(cls, dim: int, size) -> "KernelShape":
+        """Full cross-product of centred per-axis offsets, itertools.product
+        order (axis 0 slowest; conv.py:51-61)."""
+        extents = (size,) * dim if isinstance(size, int) else tuple(size)
+        if len(extents) != dim:
+            raise StructuralError("need one extent per axis")
+        if any(e < 1 or e % 2 == 0 for e in extents):
+            raise ValidationError("hypercubic extents must be odd and positive")
+        ranges = [range(-(e // 2), e // 2 + 1) for e in extents]
+        return cls(dim, extents, np.array(list(itertools.product(*ranges)), dtype=np.int64).reshape(-1, dim))
+
+    @classmethod
+    def custom(cls, dim: int, offsets) -> "KernelShape":
+        offsets = np.asarray(offsets, dtype=np.int64).reshape(-1, dim)
+        extent = tuple(int(2 * np.abs(offsets[:, d]).max() + 1) if len(offsets) else 1 for d in range(dim))
+        return cls(dim, extent, offsets)
+
+    @property
+    def num_offsets(self) -> int:
+        return len(self.offsets)
+
+    def offsets3(self) -> np.ndarray:
+        o = np.zeros((self.num_offsets, 3), dtype=np.int32)
+        o[:, : self.dim] = self.offsets
+        return o
+
+    def is_symmetric(self) -> bool:
+        """offsets[K-1-k] == -offsets[k] (true for hypercubic shapes): the
+        stride-1 inverse map is the column-flipped forward map."""
+        return bool(np.array_equal(self.offsets[::-1], -self.offsets))
+
+
+class ConvWeights:
+    """One (n_out, n_in) matrix per kernel offset (conv.py:77-105), device
+    resident fp32 masters with a cached bf16 copy for the tensor cores."""
+
+    def __init__(self, matrices, device=None):
+        if not isinstance(matrices, torch.Tensor):
+            matrices = torch.as_tensor(np.ascontiguousarray(matrices, dtype=np.float64))
+        if matrices.dim() != 3:
+            raise StructuralError("weights must have shape (K, n_out, n_in)")
+        from .tensor import default_device
+
+        m = matrices.to(device=device or (matrices.device if matrices.is_cuda else default_device()),
+                        dtype=torch.float32).contiguous()
+        if m.numel() and not bool(torch.isfinite(m).all()):
+            raise ValidationError("weight entries must be finite")
+        self.matrices = m
+        self._bf16: Optional[torch.Tensor] = None
+        self._bf16_version = -1
+
+    @property
+    def bf16(self) -> torch.Tensor:
+        if self._bf16 is None or self._bf16_version != self.matrices._version:
+            self._bf16 = self.matrices.to(torch.bfloat16).contiguous()
+            self._bf16_version = self.matrices._version
+        return self._bf16
+
+    @property
+    def num_offsets(self) -> int:
+        return self.matrices.shape[0]
+
+    @property
+    def n_out(self) -> int:
+        return self.matrices.shape[1]
+
+    @property
+    def n_in(self) -> int:
+        return self.matrices.shape[2]
+
+    def nbytes(self) -> int:
+        """Bytes of the reference's f64 matrices (conv.py:104-105)."""
+        return int(self.matrices.numel() * 8)
+
+
+@dataclass
+class KernelMap:
+    """Per-offset (input_row, output_row) links (conv.py:108-121).
+
+    Device layout: `nbr` [N_out, K] int32 neighbour table (-1 = no neighbour)
+    feeding the implicit GEMM, plus the pair lists in CSR form
+    (`pair_in`/`pair_out` int32, `pair_ptr` [K+1]) in the reference's order:
+    offset-major, out rows ascending within an offset.
+    """
+
+    offsets: np.ndarray
+    nbr: torch.Tensor
+    pair_in: torch.Tensor
+    pair_out: torch.Tensor
+    pair_ptr: torch.Tensor
+    n_in: int = 0
+    _ptr_host: Optional[np.ndarray] = field(default=None, repr=False)
+
+    @property
+    def ptr_host(self) -> np.ndarray:
+        if self._ptr_host is None:
+            self._ptr_host = self.pair_ptr.cpu().numpy().astype(np.int64)
+        return self._ptr_host
+
+    @property
+    def pairs(self) -> tuple:
+        """tuple of (in_rows, out_rows) int64 device tensors per offset."""
+        p = self.ptr_host
+        return tuple((self.pair_in[p[k]:p[k + 1]].to(torch.int64), self.pair_out[p[k]:p[k + 1]].to(torch.int64))
+                     for k in range(len(p) - 1))
+
+    def total_pairs(self) -> int:
+        return int(self.ptr_host[-1])
+
+    def inverse(self) -> torch.Tensor:
+        """inv [N_in, K]: inv[v, k] = u for every pair (v, u) of offset k."""
+        K = self.nbr.shape[1] if self.nbr.dim() == 2 else len(self.offsets)
+        inv = torch.empty((max(self.n_in, 1), K), dtype=torch.int32, device=self.nbr.device)
+        _lib.call("vp_kernel_map_inverse", self.nbr.data_ptr(), None, self.nbr.shape[0], K, inv.data_ptr(),
+                  self.n_in, _lib.stream())
+        return inv[: self.n_in]
+
+
+def _stride3(stride, dim) -> tuple:
+    st = (stride,) * dim if isinstance(stride, int) else tuple(int(s) for s in stride)
+    if len(st) != dim or any(s < 1 for s in st):
+        raise ValidationError("stride must list D positive integers")
+    return st
+
+
+def _output_coords4(coords4: torch.Tensor, tensor_stride: tuple, stride: tuple, dim: int):
+    """generate_output_coords on the padded layout -> (coords4_out, new_stride)."""
+    new_stride = tuple(int(o) * int(s) for o, s in zip(tensor_stride, stride))
+    if all(s == 1 for s in stride):
+        return coords4.clone(), new_stride
+    n = coords4.shape[0]
+    if n == 0:
+        return torch.empty((0, 4), dtype=torch.int32, device=coords4.device), new_stride
+    out = torch.empty((n, 4), dtype=torch.int32, device=coords4.device)
+    n_out = torch.empty(1, dtype=torch.int32, device=coords4.device)
+    ws = _lib.workspace(_lib.query("vp_output_coords_ws_bytes", n), coords4.device)
+    step = tuple(new_stride) + (1,) * (3 - dim)
+    _lib.call("vp_output_coords", coords4.data_ptr(), None, n, _lib.i32_array(step), out.data_ptr(),
+              n_out.data_ptr(), None, ws.data_ptr(), ws.numel(), _lib.stream())
+    return out[: int(n_out.item())], new_stride
+
+
+def generate_output_coords(t: SparseTensor, stride):
+    """conv.py:124-146 — (coords (N_out, 1+D) int32 device, new tensor stride).
+    Stride s > 1: floor-div by ts*s, rescale, unique rows in first-seen order."""
+    st = _stride3(stride, t.dim)
+    c4, ns = _output_coords4(t.coords4, t.tensor_stride, st, t.dim)
+    return c4[:, : 1 + t.dim], ns
+
+
+def _kernel_map4(in4: torch.Tensor, out4: torch.Tensor, shape: KernelShape, in_stride: tuple, dim: int,
+                 with_pairs: bool = True) -> KernelMap:
+    device = in4.device
+    K = shape.num_offsets
+    if K > _lib.MAX_OFFSETS:
+        raise ValidationError(f"at most {_lib.MAX_OFFSETS} kernel offsets are supported")
+    n_in, n_out = in4.shape[0], out4.shape[0]
+    nbr = torch.empty((max(n_out, 1), K), dtype=torch.int32, device=device)
+    cap_p = max(n_out * K, 1)
+    pin = torch.empty(cap_p, dtype=torch.int32, device=device) if with_pairs else None
+    pout = torch.empty(cap_p, dtype=torch.int32, device=device) if with_pairs else None
+    pptr = torch.zeros(K + 1, dtype=torch.int32, device=device)
+    ws = _lib.workspace(_lib.query("vp_kernel_map_ws_bytes", n_in, n_out, K), device)
+    st3 = tuple(in_stride) + (1,) * (3 - dim)
+    offs = shape.offsets3()
+    _lib.call("vp_kernel_map", in4.data_ptr() if n_in else None, None, n_in, out4.data_ptr() if n_out else None, None,
+              n_out, _lib.i32_array(offs.ravel()), K, _lib.i32_array(st3), nbr.data_ptr(), _lib.ptr(pin),
+              _lib.ptr(pout), pptr.data_ptr() if with_pairs else None, ws.data_ptr(), ws.numel(), _lib.stream())
+    if not with_pairs:
+        pin = pout = torch.empty(0, dtype=torch.int32, device=device)
+    return KernelMap(shape.offsets, nbr[:n_out], pin, pout, pptr, n_in=n_in)
+
+
+def build_kernel_map(in_coords, out_coords, shape: KernelShape, in_stride) -> KernelMap:
+    """conv.py:149-183 — pair (v, u) at offset k iff out[u] + off_k*in_stride
+    == in[v] (batch equal).  One GPU hash over the input rows per call."""
+    in4, dim = pad_coords(in_coords)
+    out4, dim_o = pad_coords(out_coords, in4.device)
+    if dim != dim_o or shape.dim != dim:
+        raise StructuralError("coordinate / kernel dimensions differ")
+    return _kernel_map4(in4, out4, shape, tuple(int(s) for s in in_stride), dim)
+
+
+def _check_weights(t: SparseTensor, w: ConvWeights, shape: KernelShape):
+    if w.num_offsets != shape.num_offsets:
+        raise StructuralError("weights must supply one matrix per offset")
+    if w.n_in != t.feature_width:
+        raise StructuralError(f"weight n_in {w.n_in} != input feature width {t.feature_width}")
+    if shape.dim != t.dim:
+        raise StructuralError("kernel shape dimension != tensor dimension")
+
+
+def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: int, out_dtype=None,
+                     flip: bool = False) -> torch.Tensor:
+    """y[u] = sum_k W_k x[nbr[u, k]] for u < n_out (the gather-GEMM of Eq. 3)."""
+    out_dtype = out_dtype or x.dtype
+    K = w.num_offsets
+    y = torch.empty((max(n_out, 1), w.n_out), dtype=out_dtype, device=x.device)
+    wt = w.bf16 if x.dtype == torch.bfloat16 else w.matrices
+    ws = _lib.workspace(_lib.query("vp_conv_fwd_ws_bytes", w.n_in, w.n_out, K), x.device)
+    _lib.call("vp_conv_fwd", x.data_ptr(), _lib.dtype_code(x), w.n_in, wt.data_ptr(), _lib.dtype_code(wt), w.n_out,
+              K, nbr.data_ptr(), int(flip), None, n_out, y.data_ptr(), _lib.dtype_code(y), ws.data_ptr(), ws.numel(),
+              _lib.stream())
+    return y[:n_out]
+
+
+def conv_dgrad_raw(g: torch.Tensor, w: ConvWeights, table: torch.Tensor, n_in: int, flip: bool,
+                   out_dtype=None) -> torch.Tensor:
+    """grad_in[v] = sum_k W_k^T g[table[v, k]] (conv.py:240)."""
+    out_dtype = out_dtype or g.dtype
+    K = w.num_offsets
+    gi = torch.empty((max(n_in, 1), w.n_in), dtype=out_dtype, device=g.device)
+    wt = w.bf16 if g.dtype == torch.bfloat16 else w.matrices
+    ws = _lib.workspace(_lib.query("vp_conv_dgrad_ws_bytes", w.n_in, w.n_out, K), g.device)
+    _lib.call("vp_conv_dgrad", g.data_ptr(), _lib.dtype_code(g), w.n_out, wt.data_ptr(), _lib.dtype_code(wt),
+              w.n_in, K, table.data_ptr(), int(flip), None, n_in, gi.data_ptr(), _lib.dtype_code(gi), ws.data_ptr(),
+              ws.numel(), _lib.stream())
+    return gi[:n_in]
+
+
+def conv_wgrad_raw(x: torch.Tensor, g: torch.Tensor, w_shape: tuple, kmap: KernelMap) -> torch.Tensor:
+    """grad_w[k] = sum over pairs (v, u) of offset k of g[u] x[v]^T (conv.py:241), fp32."""
+    K, n_out_c, n_in_c = w_shape
+    gw = torch.empty((K, n_out_c, n_in_c), dtype=torch.float32, device=x.device)
+    cap_pairs = max(int(kmap.pair_in.numel()), 1)
+    ws = _lib.workspace(_lib.query("vp_conv_wgrad_ws_bytes", n_in_c, n_out_c, K, cap_pairs), x.device)
+    _lib.call("vp_conv_wgrad", x.data_ptr(), _lib.dtype_code(x), n_in_c, g.data_ptr(), _lib.dtype_code(g), n_out_c,
+              K, kmap.pair_in.data_ptr(), kmap.pair_out.data_ptr(), kmap.pair_ptr.data_ptr(), cap_pairs,
+              gw.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+    return gw
+
+
+def sparse_conv_forward(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride=1) -> SparseTensor:
+    """conv.py:186-208 — x_out[u] = sum over offsets i with u+i occupied of
+    W_i x_in[u+i]; output rows at generate_output_coords(t, stride)."""
+    _check_weights(t, w, shape)
+    st = _stride3(stride, t.dim)
+    out4, ns = _output_coords4(t.coords4, t.tensor_stride, st, t.dim)
+    km = _kernel_map4(t.coords4, out4, shape, t.tensor_stride, t.dim, with_pairs=False)
+    y = conv_forward_raw(t.features, w, km.nbr, out4.shape[0])
+    return SparseTensor(out4, y, ns, _trusted=True, _dim=t.dim)
+
+
+def sparse_conv_backward(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride, grad_out):
+    """conv.py:211-242 — (grad_in (N_in, n_in) in the feature dtype,
+    grad_w (K, n_out, n_in) fp32).  Recomputes coords and map as the
+    reference does."""
+    _check_weights(t, w, shape)
+    st = _stride3(stride, t.dim)
+    out4, _ = _output_coords4(t.coords4, t.tensor_stride, st, t.dim)
+    if not isinstance(grad_out, torch.Tensor):
+        grad_out = torch.as_tensor(np.asarray(grad_out, dtype=np.float64))
+    g = grad_out.to(device=t.device, dtype=t.features.dtype).contiguous()
+    if tuple(g.shape) != (out4.shape[0], w.n_out):
+        raise StructuralError(f"grad_out shape {tuple(g.shape)} does not match forward output "
+                              f"({out4.shape[0]}, {w.n_out})")
+    km = _kernel_map4(t.coords4, out4, shape, t.tensor_stride, t.dim)
+    if all(s == 1 for s in st) and shape.is_symmetric():
+        table, flip = km.nbr, True  # inv[v, k] == nbr[v, K-1-k] when in == out
+    else:
+        table, flip = km.inverse(), False
+    gi = conv_dgrad_raw(g, w, table, len(t), flip)
+    gw = conv_wgrad_raw(t.features, g, tuple(w.matrices.shape), km)
+    return gi, gw
+
+
+def sparse_conv_transposed(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride, out_coords) -> SparseTensor:
+    """Transposed (adjoint) sparse conv, coarse -> fine: the
+    fine rows `out_coords` (tensor stride t.tensor_stride / stride) are the
+    input lattice of the strided conv whose map is reused with (in, out)
+    swapped.  w: (K, n_out, n_in) applied as y[v] = sum_k W_k x[u] over the
+    strided pairs (v, u) of offset k."""
+    if w.num_offsets != shape.num_offsets or w.n_in != t.feature_width:
+        raise StructuralError("weights do not match kernel shape / feature width")
+    st = _stride3(stride, t.dim)
+    fine_stride = tuple(a // b for a, b in zip(t.tensor_stride, st))
+    if any(a * b != c for a, b, c in zip(fine_stride, st, t.tensor_stride)):
+        raise ValidationError("tensor stride is not divisible by the transposed-conv stride")
+    fine4, _ = pad_coords(out_coords, t.device)
+    km = _kernel_map4(fine4, t.coords4, shape, fine_stride, t.dim, with_pairs=False)
+    inv = km.inverse()  # [N_fine, K] -> coarse row
+    # y[v] = sum_k W_k x[inv[v,k]] : a forward conv over the inverse table
+    y = conv_forward_raw(t.features, w, inv, fine4.shape[0])
+    return SparseTensor(fine4, y, fine_stride, _trusted=True, _dim=t.dim)
+
+
+def benchmark_forward_backward(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride=1, warmup_iters: int = 2,
+                               profile_iters: int = 5) -> dict:
+    """conv.py:280-320 with CUDA-event timing (µs, device time) — the same
+    record keys as the reference's LayerProfile-shaped dict."""
+    out = sparse_conv_forward(t, w, shape, stride)
+    g = torch.ones((len(out), w.n_out), dtype=t.features.dtype, device=t.device)
+    for _ in range(warmup_iters):
+        sparse_conv_forward(t, w, shape, stride)
+        sparse_conv_backward(t, w, shape, stride, g)
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    fwd = bwd = 0.0
+    for _ in range(profile_iters):
+        e0.record()
+        sparse_conv_forward(t, w, shape, stride)
+        e1.record()
+        sparse_conv_backward(t, w, shape, stride, g)
+        e2.record()
+        e2.synchronize()
+        fwd += e0.elapsed_time(e1) * 1e3
+        bwd += e1.elapsed_time(e2) * 1e3
+    out4, _ = _output_coords4(t.coords4, t.tensor_stride, _stride3(stride, t.dim), t.dim)
+    km = _kernel_map4(t.coords4, out4, shape, t.tensor_stride, t.dim)
+    return {
+        "fwd_time_us": fwd / profile_iters,
+        "bwd_time_us": bwd / profile_iters,
+        "activation_bytes": binary_size(len(out), out.dim, out.feature_width),
+        "param_bytes": w.nbytes(),
+        "kernel_map_pairs": km.total_pairs(),
+    }
+
+
+# ---------------------------------------------------------------- weight I/O
+def weights_to_json(w: ConvWeights, shape: KernelShape) -> str:
+    """conv.py:323-335 format."""
+    m = w.matrices.to(torch.float64).cpu().numpy()
+    return json.dumps({"format_version": _WEIGHTS_VERSION, "dim": shape.dim, "n_out": w.n_out, "n_in": w.n_in,
+                       "weights": {",".join(str(int(v)) for v in off): m[k].tolist()
+                                   for k, off in enumerate(shape.offsets)}})
+
+
+def weights_from_json(text: str):
+    obj = json.loads(text)
+    try:
+        dim = int(obj["dim"])
+        items = [(tuple(int(v) for v in key.split(",")), np.asarray(mat, dtype=np.float64))
+                 for key, mat in obj["weights"].items()]
+    except (KeyError, TypeError, ValueError) as exc:
+        raise ValidationError(f"malformed weights JSON: {exc}") from exc
+    if not items:
+        raise ValidationError("weights JSON lists no offsets")
+    shape = KernelShape.custom(dim, np.asarray([o for o, _ in items], dtype=np.int64))
+    return ConvWeights(np.stack([m for _, m in items])), shape
+
+
+def weights_to_binary(w: ConvWeights, shape: KernelShape) -> bytes:
+    """conv.py:356-368 `VXCW` v1."""
+    head = struct.pack("<4sIIIII", _WEIGHTS_MAGIC, _WEIGHTS_VERSION, shape.dim, w.num_offsets, w.n_out, w.n_in)
+    return (head + np.ascontiguousarray(shape.offsets, "<i8").tobytes()
+            + np.ascontiguousarray(w.matrices.to(torch.float64).cpu().numpy(), "<f8").tobytes())
+
+
+def weights_from_binary(blob: bytes):
+    head = struct.calcsize("<4sIIIII")
+    if len(blob) < head:
+        raise ValidationError("binary weights truncated")
+    magic, version, dim, k, n_out, n_in = struct.unpack("<4sIIIII", blob[:head])
+    if magic != _WEIGHTS_MAGIC or version != _WEIGHTS_VERSION:
+        raise ValidationError("unrecognized binary weights header")
+    off = head
+    offsets = np.frombuffer(blob, dtype="<i8", count=k * dim, offset=off)
+    off += 8 * k * dim
+    mats = np.frombuffer(blob, dtype="<f8", count=k * n_out * n_in, offset=off)
+    off += 8 * k * n_out * n_in
+    if off != len(blob):
+        raise ValidationError("binary weights have trailing bytes")
+    return ConvWeights(mats.reshape(k, n_out, n_in).copy()), KernelShape.custom(dim, offsets.reshape(k, dim))

@@ -1,0 +1,174 @@
+"""GPU parity for the float stage: forward / dgrad / wgrad (tcgen05 and SIMT
+paths) against the reference's golden vectors and the f64 oracle.
+
+Tolerance model: the oracle runs in f64 on the
+SAME bf16-rounded inputs and weights, so only accumulation and output
+rounding are measured:
+  bf16 storage (tcgen05, fp32 accumulate, bf16 out): |d| <= 1e-2 * sum|W||x| (+ bf16 ulp)
+  fp32 path (SIMT, fp32 out):                        |d| <= 1e-5 * sum|W||x|
+"""
+import numpy as np
+import pytest
+
+import voxpipe_oracle as O
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def bf16_round(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+
+
+def abs_bound(coords, feats, w, offsets, stride, rel):
+    """rel * sum_k |W_k| |x| per output element (the error scale of Eq. 3)."""
+    _, s, _ = O.sparse_conv_forward(coords, np.abs(feats), (1, 1, 1), np.abs(w), offsets, stride)
+    return rel * s + 1e-6
+
+
+def run_layer(coords, x, w, stride, dtype):
+    from paper_2012_13846_b200 import conv
+    from paper_2012_13846_b200.tensor import SparseTensor
+    shape = conv.KernelShape.hypercubic(3, 3)
+    t = SparseTensor(coords, np.zeros((len(coords), 1)), (1, 1, 1))
+    xt = torch.from_numpy(np.asarray(x, np.float32)).cuda().to(dtype)
+    t = t.with_features(xt)
+    W = conv.ConvWeights(torch.from_numpy(np.asarray(w, np.float32)).cuda())
+    y = conv.sparse_conv_forward(t, W, shape, stride)
+    return t, W, shape, y
+
+
+@pytest.mark.parametrize("tag,stride", [("s1", 1), ("s2", 2), ("s1b", 1)])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_conv_golden(tag, stride, dtype):
+    from paper_2012_13846_b200 import conv
+    g = golden("conv.npz")
+    coords = g["vox_coords"]
+    x, w, gy = g[f"conv_{tag}_x"], g[f"conv_{tag}_w"], g[f"conv_{tag}_g"]
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    rel = 1e-2 if dtype == "bf16" else 1e-5
+    xr = bf16_round(x) if dtype == "bf16" else x.astype(np.float64)
+    wr = bf16_round(w) if dtype == "bf16" else w.astype(np.float64)
+    gr = bf16_round(gy) if dtype == "bf16" else gy.astype(np.float64)
+    off = O.hypercubic_offsets(3, 3)
+    t, W, shape, y = run_layer(coords, x, w, stride, tdt)
+    np.testing.assert_array_equal(y.coords.cpu().numpy(), g[f"conv_{tag}_yc"])
+    _, ry, _ = O.sparse_conv_forward(coords, xr, (1, 1, 1), wr, off, stride)
+    if dtype == "f32":  # inputs are exactly representable: compare with the reference's own f64 output too
+        np.testing.assert_allclose(ry, g[f"conv_{tag}_y"], atol=1e-9)
+    err = np.abs(y.features.float().cpu().numpy() - ry)
+    assert (err <= abs_bound(coords, xr, wr, off, stride, rel)).all(), err.max()
+    gi, gw = conv.sparse_conv_backward(t, W, shape, stride, torch.from_numpy(gy).cuda().to(tdt))
+    rgi, rgw = O.sparse_conv_backward(coords, xr, (1, 1, 1), wr, off, stride, gr)
+    # dgrad bound: rel * sum |W^T| |g| per input element
+    K = 27
+    km = O.build_kernel_map(coords, O.generate_output_coords(coords, (1, 1, 1), stride)[0], off, (1, 1, 1))
+    bgi = np.zeros_like(rgi)
+    bgw = np.zeros_like(rgw)
+    for k, (vi, ui) in enumerate(km):
+        bgi[vi] += np.abs(gr[ui]) @ np.abs(wr[k])
+        bgw[k] = np.abs(gr[ui]).T @ np.abs(xr[vi])
+    assert (np.abs(gi.float().cpu().numpy() - rgi) <= rel * bgi + 1e-6).all()
+    # wgrad is fp32 in both modes; inputs identical -> only accumulation order differs
+    assert (np.abs(gw.cpu().numpy() - rgw) <= 1e-5 * bgw + 1e-6).all(), np.abs(gw.cpu().numpy() - rgw).max()
+
+
+@pytest.mark.parametrize("cin,cout", [(32, 32), (32, 64), (64, 64), (64, 128), (128, 128), (128, 256),
+                                      (256, 256), (256, 128), (64, 32), (128, 32), (256, 32)])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_tc_widths(cin, cout, stride):
+    """Every tcgen05 template instantiation used by the models, bf16."""
+    from paper_2012_13846_b200 import conv
+    pts, offs = O.synthetic_batch(3, 700, 32, seed=cin + cout, dtype=np.float64)
+    coords, _ = O.voxelize_batch(pts, offs, 1.0, 32)
+    rng = np.random.default_rng(cin * 7 + cout)
+    x = rng.normal(size=(len(coords), cin)).astype(np.float32)
+    w = (rng.normal(size=(27, cout, cin)) / np.sqrt(27 * cin)).astype(np.float32)
+    xr, wr = bf16_round(x), bf16_round(w)
+    off = O.hypercubic_offsets(3, 3)
+    t, W, shape, y = run_layer(coords, x, w, stride, torch.bfloat16)
+    _, ry, _ = O.sparse_conv_forward(coords, xr, (1, 1, 1), wr, off, stride)
+    err = np.abs(y.features.float().cpu().numpy() - ry)
+    assert (err <= abs_bound(coords, xr, wr, off, stride, 1e-2)).all(), err.max()
+    gy = rng.normal(size=ry.shape).astype(np.float32)
+    gr = bf16_round(gy)
+    gi, gw = conv.sparse_conv_backward(t, W, shape, stride, torch.from_numpy(gy).cuda().to(torch.bfloat16))
+    rgi, rgw = O.sparse_conv_backward(coords, xr, (1, 1, 1), wr, off, stride, gr)
+    scale_i = np.abs(rgi).max() + 1e-6
+    scale_w = np.abs(rgw).max() + 1e-6
+    assert np.abs(gi.float().cpu().numpy() - rgi).max() <= 2e-2 * scale_i
+    assert np.abs(gw.cpu().numpy() - rgw).max() <= 1e-4 * scale_w
+
+
+def test_stem_cin1_simt():
+    """C_in = 1 (occupancy stem) goes through the SIMT kernels."""
+    from paper_2012_13846_b200 import conv
+    pts, offs = O.synthetic_batch(2, 500, 32, seed=9, dtype=np.float64)
+    coords, feats = O.voxelize_batch(pts, offs, 1.0, 32)
+    rng = np.random.default_rng(5)
+    w = (rng.normal(size=(27, 32, 1)) / np.sqrt(27)).astype(np.float32)
+    for dt, rel in ((torch.float32, 1e-5), (torch.bfloat16, 1e-2)):
+        t, W, shape, y = run_layer(coords, feats, w, 1, dt)
+        wr = w.astype(np.float64) if dt == torch.float32 else bf16_round(w)
+        _, ry, _ = O.sparse_conv_forward(coords, feats, (1, 1, 1), w.astype(np.float64), O.hypercubic_offsets(3, 3), 1)
+        assert np.abs(y.features.float().cpu().numpy() - ry).max() <= rel * np.abs(ry).max() + 1e-5
+        gy = rng.normal(size=ry.shape)
+        gi, gw = conv.sparse_conv_backward(t, W, shape, 1, torch.from_numpy(gy).cuda().to(dt))
+        gq = gy if dt == torch.float32 else bf16_round(gy)
+        rgi, rgw = O.sparse_conv_backward(coords, feats, (1, 1, 1), w.astype(np.float64), O.hypercubic_offsets(3, 3), 1, gq)
+        assert np.abs(gw.cpu().numpy() - rgw).max() <= 1e-4 * np.abs(rgw).max()
+
+
+def test_deterministic():
+    from paper_2012_13846_b200 import conv
+    pts, offs = O.synthetic_batch(4, 1500, 48, seed=2, dtype=np.float64)
+    coords, _ = O.voxelize_batch(pts, offs, 1.0, 48)
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(len(coords), 64)).astype(np.float32)
+    w = (rng.normal(size=(27, 64, 64)) / 40).astype(np.float32)
+    t, W, shape, y1 = run_layer(coords, x, w, 1, torch.bfloat16)
+    g = torch.randn_like(y1.features)
+    a = conv.sparse_conv_backward(t, W, shape, 1, g)
+    y2 = conv.sparse_conv_forward(t, W, shape, 1)
+    b = conv.sparse_conv_backward(t, W, shape, 1, g)
+    assert torch.equal(y1.features, y2.features)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_sparse_equals_dense_full_grid():
+    """SPEC.md:164 / acceptance 3: fully occupied grids <= 6^3, fp32 path."""
+    from paper_2012_13846_b200 import conv
+    rng = np.random.default_rng(0)
+    for _ in range(6):
+        sh = tuple(int(v) for v in rng.integers(2, 7, 3))
+        grid = rng.normal(size=sh + (3,))
+        w = rng.normal(size=(27, 4, 3))
+        coords = np.array([[0, *idx] for idx in np.ndindex(*sh)])
+        feats = np.array([grid[tuple(c[1:])] for c in coords])
+        t, W, shape, y = run_layer(coords, feats, w, 1, torch.float32)
+        d = O.dense_conv_forward(grid, w.astype(np.float32).astype(np.float64), shape.offsets)
+        exp = np.array([d[tuple(c[1:])] for c in coords])
+        np.testing.assert_allclose(y.features.cpu().numpy(), exp, atol=1e-4)
+
+
+def test_transposed_conv_adjoint():
+    from paper_2012_13846_b200 import conv
+    from paper_2012_13846_b200.tensor import SparseTensor
+    rng = np.random.default_rng(4)
+    c = np.unique(np.concatenate([np.zeros((400, 1), int), rng.integers(-8, 8, (400, 3))], 1), axis=0)
+    off = O.hypercubic_offsets(3, 3)
+    oc, _ = O.generate_output_coords(c, (1, 1, 1), 2)
+    z = rng.normal(size=(len(oc), 32))
+    wt = rng.normal(size=(27, 32, 32)) / 30
+    coarse = SparseTensor(oc, z, (2, 2, 2))
+    y = conv.sparse_conv_transposed(coarse, conv.ConvWeights(wt), conv.KernelShape.hypercubic(3, 3), 2, c)
+    ref = O.sparse_conv_transposed(c, (1, 1, 1), z.astype(np.float32), wt.astype(np.float32), off, 2)
+    np.testing.assert_allclose(y.features.cpu().numpy(), ref, atol=1e-4)
+    assert y.tensor_stride == (1, 1, 1)
