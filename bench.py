@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark: SparseResNet training throughput (point clouds / s) on B200.
+
+Workload (BASELINE.json configs[2], "C3"): 64 synthetic ModelNet40-shaped
+clouds x 2048 points at 64^3 voxels per GPU, bf16 features, 13-conv
+SparseResNet, SGD momentum 0.9.  A step = one full training step from raw
+points: GPU voxelization, strided output coordinates, 9 kernel maps, forward,
+backward, optimizer (nothing cached across steps).
+
+  value : whole-job clouds/s with the points already in HBM (device timed,
+          CUDA events per step, L2 flushed between steps with a 256 MiB write)
+  e2e   : clouds/s through the public trainer API from pinned HOST memory:
+          H2D of the step's points + labels, the step, D2H of the loss, all
+          inside the timed region
+  roofline : dominant kernel (largest-FLOP tensor-core conv forward of the
+          step), re-launched standalone on the step's own data, CUDA events
+  cpu_baseline : the reference's own CPU path (oracle/_ref voxpipe, convs via
+          voxpipe.conv + numpy glue) on a bounded sample of the same workload
+
+Multi-GPU (torchrun, one process per GPU, NCCL): data parallel, each rank a
+full 64-cloud batch (weak scaling), one NCCL all_reduce of the flat gradient
+buffer per step; time = max over ranks.
+
+`--impl reference` times the reference CPU path alone (rank 0; other ranks exit).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+METRIC = "point clouds/sec train (SparseResNet, 64x2048 pts @ 64^3, bf16)"
+CONFIG = {"workload": "C3: sparse-ResNet classifier, 64 clouds x 2048 pts/cloud at 64^3 voxels per GPU, "
+                      "13 convs (blocks=1), bf16 features, SGD momentum",
+          "global_batch_per_gpu": 64, "points_per_cloud": 2048, "resolution": 64, "planes": [32, 64, 128, 256],
+          "blocks": 1, "classes": 40, "l2": "flushed between timed steps (256 MiB memset, outside the events)"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--points", type=int, default=2048)
+    ap.add_argument("--res", type=int, default=64)
+    ap.add_argument("--blocks", type=int, default=1)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="clouds per CPU-baseline step")
+    ap.add_argument("--profile-only", action="store_true", help="warm-up + a few steps, no JSON (for ncu)")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(args, steps=2, warmup=1, seed=0):
+    import ref_runner
+
+    nthreads = os.cpu_count() or 1
+    r = ref_runner.time_steps(args.cpu_sample, args.points, args.res, steps, warmup, seed=seed)
+    return {"value": round(r["clouds_per_s"], 3), "unit": "clouds/s", "cores": nthreads, "kind":
+            "reference" if r["kind"] == "reference" else "port",
+            "sample": f"{steps} timed steps (+{warmup} warm-up) of {args.cpu_sample} clouds x {args.points} pts @ "
+                      f"{args.res}^3 through voxpipe.tensor.voxelize/batch + voxpipe.conv fwd/bwd (compiled hash) + "
+                      f"numpy BN/pool/linear/SGD glue; OpenBLAS threads={nthreads}"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import ref_runner
+
+    t0 = time.time()
+    r = ref_runner.time_steps(args.cpu_sample, args.points, args.res, max(1, args.steps), max(0, args.warmup))
+    value = r["clouds_per_s"]
+    cores = os.cpu_count() or 1
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "clouds/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["s_per_step"] * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(CONFIG, sample_clouds_per_step=args.cpu_sample),
+            "cpu_baseline": {"value": round(value, 3), "unit": "clouds/s", "cores": cores,
+                             "kind": "reference" if r["kind"] == "reference" else "port",
+                             "sample": f"each step {args.cpu_sample} clouds of the C3 workload (bounded sample)"},
+            "e2e": {"value": round(value, 3), "unit": "clouds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": round(time.time() - t0, 1)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import voxpipe_oracle as O
+    from paper_2012_13846_b200 import _lib, model
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    allreduce = None
+    if world > 1:
+        def allreduce(flat):  # one NCCL all_reduce of the flat fp32 gradient buffer per step
+            dist.all_reduce(flat)
+            flat.div_(world)
+
+    tr = model.SparseResNetTrainer(batch=args.batch, points=args.points, resolution=args.res, blocks=args.blocks,
+                                   device=dev, grad_allreduce=allreduce)
+    # synthetic data pool: 4 distinct batches per rank, resident in HBM and pinned host memory
+    pool_n = 4
+    host_pts, host_lab, dev_pts, dev_lab = [], [], [], []
+    for i in range(pool_n):
+        pts, _ = O.synthetic_batch(args.batch, args.points, args.res, seed=1000 * rank + i, dtype=np.float32)
+        lab = ((np.arange(args.batch) + 7 * i) % 40).astype(np.int32)
+        hp = torch.from_numpy(pts).pin_memory()
+        hl = torch.from_numpy(lab).pin_memory()
+        host_pts.append(hp)
+        host_lab.append(hl)
+        dev_pts.append(hp.to(dev))
+        dev_lab.append(hl.to(dev))
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    tr.set_batch(dev_pts[0], dev_lab[0])
+    use_graph = not args.no_graph and world == 1
+    k0 = _lib.load().vp_kernel_launches()
+    if use_graph:
+        tr.capture(warmup=1)
+        launches_per_step = tr.launch_count
+        kern_per_step = None
+    else:
+        tr.step_body()
+        launches_per_step = tr.launch_count
+    k1 = _lib.load().vp_kernel_launches()
+    # kernels enqueued by one step_body() (capture() runs one eager + one captured step)
+    kern_per_step = (k1 - k0) // (2 if use_graph else 1)
+
+    def one_step(i):
+        tr.set_batch(dev_pts[i % pool_n], dev_lab[i % pool_n])  # D2D into the static input buffers
+        tr.step()
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    if args.profile_only:
+        for i in range(3):
+            one_step(i)
+        torch.cuda.synchronize()
+        print(f"profile-only done: levels={tr.level_sizes()} pairs={tr.pair_counts()} kernels/step={kern_per_step}")
+        return
+
+    # ---------------- device-resident timed region
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the events
+            evs[i][0].record(stream)
+            one_step(i)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.batch * args.steps / (ms / 1e3)
+    loss = float(tr.loss.item())
+
+    # ---------------- e2e through the public API from pinned host memory
+    h2d = int(host_pts[0].numel() * host_pts[0].element_size() + host_lab[0].numel() * 4)
+    d2h = 4
+    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        tr.points.copy_(host_pts[i % pool_n], non_blocking=True)
+        tr.labels.copy_(host_lab[i % pool_n], non_blocking=True)
+        tr.step()
+        loss_host.copy_(tr.loss, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * args.batch * args.steps / (e2e_ms / 1e3)
+
+    # ---------------- roofline of the dominant kernel (standalone, same data)
+    roof = roofline(tr, dev)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(args)
+            except Exception as exc:  # pragma: no cover
+                cpu = {"value": None, "unit": "clouds/s", "cores": os.cpu_count(), "kind": "port",
+                       "sample": f"failed: {exc}"}
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "clouds/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": dict(CONFIG, parallelism=f"dp{world}", cuda_graph=use_graph,
+                               level_rows=tr.level_sizes(), map_pairs=tr.pair_counts()),
+                "e2e": {"value": round(e2e_value, 2), "unit": "clouds/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(kern_per_step * args.steps),
+                "gpu_launches_per_step": int(kern_per_step),
+                "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(), "final_loss": round(loss, 5)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(tr, dev, iters=50):
+    """Dominant tensor-core kernel of the step: the conv forward with the most
+    useful FLOPs (2 * pairs * C_in * C_out), relaunched standalone on the
+    step's own activations/maps.  Also reports the kernel-map builder's
+    algorithmic GB/s (16 N_in + 16 N_out + 8 P) for the largest map."""
+    import torch
+
+    from paper_2012_13846_b200 import _lib
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+        src = "measured"
+    except OSError:
+        src = "fallback"
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    tc_peak = peaks.get("bf16_tflops", 1590.0)
+    best = None
+    for L in tr.layers:
+        if L["cin"] < 32:
+            continue
+        P = int(L["map"].ptr[-1].item())
+        fl = 2.0 * P * L["cin"] * L["cout"]
+        if best is None or fl > best[0]:
+            best = (fl, L, P)
+    fl, L, P = best
+    st = torch.cuda.current_stream()
+    dst = L["dst"]
+    n_out = int(dst.n.item())
+    n_in = int(L["src"].n.item())
+
+    def launch():
+        _lib.call("vp_conv_fwd", L["x"].data_ptr(), _lib.VP_BF16, L["cin"], L["wb"].data_ptr(), _lib.VP_BF16,
+                  L["cout"], tr.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(),
+                  _lib.VP_BF16, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st.cuda_stream)
+
+    for _ in range(5):
+        launch()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(st)
+    for _ in range(iters):
+        launch()
+    b.record(st)
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / iters / 1e3
+    byts = 2 * n_in * L["cin"] + 2 * n_out * L["cout"] + 2 * 27 * L["cin"] * L["cout"] + 4 * n_out * 27
+    ai = fl / byts
+    tflops = fl / t / 1e12
+    gbs = byts / t / 1e9
+    bound = "tensor" if ai * hbm / 1e3 > tc_peak else "hbm"
+    if bound == "tensor":
+        ach, peak, unit = tflops, tc_peak, "TFLOP/s"
+    else:
+        ach, peak, unit = gbs, hbm, "GB/s"
+    return {"kernel": f"conv_fwd_tc<{L['cin']},{L['cout']}> layer {L['name']} (N_out={n_out}, pairs={P})",
+            "bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit, "frac": round(ach / peak, 4),
+            "traffic": None, "peak_source": src, "us_per_launch": round(t * 1e6, 2),
+            "algorithmic_flops": fl, "algorithmic_bytes": byts, "tflops": round(tflops, 2), "gbs": round(gbs, 1)}
+
+
+if __name__ == "__main__":
+    main()

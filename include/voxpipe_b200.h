@@ -44,6 +44,9 @@ enum { VP_F32 = 0, VP_BF16 = 1, VP_F64 = 2 };
 
 const char* vp_last_error(void);
 const char* vp_version(void);
+/* diagnostic: number of kernels this thread has enqueued through the library
+ * (bench.py's gpu_launches claim; a CUDA graph capture counts each node once) */
+long long vp_kernel_launches(void);
 
 /* ---------------------------------------------------------------- hash
  * Replaces _kernels.pyx:24-47 `build_table` and :50-73 `lookup` (the
@@ -168,10 +171,11 @@ int vp_bn_apply(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t ca
                 const float* mean, const float* rstd, const float* gamma, const float* beta,
                 const void* res, int32_t res_dtype, int32_t relu, void* y, int32_t y_dtype,
                 vp_stream_t stream);
-/* backward of bn_apply: gy is masked by (y > 0) when relu; writes
- * grad_x (and grad_res = masked gy when non-null), ggamma/gbeta [C] fp32. */
+/* backward of bn_apply: the incoming gradient is gy (+ gy2 when non-null,
+ * same dtype: the residual-branch sum), masked by (y > 0) when relu; writes
+ * grad_x (and grad_res = masked gradient when non-null), ggamma/gbeta [C]. */
 size_t vp_bn_backward_ws_bytes(int64_t cap_n, int64_t C);
-int vp_bn_backward(const void* gy, int32_t gy_dtype, const void* y, int32_t y_dtype,
+int vp_bn_backward(const void* gy, const void* gy2, int32_t gy_dtype, const void* y, int32_t y_dtype,
                    const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C,
                    const float* mean, const float* rstd, const float* gamma, int32_t relu,
                    void* grad_x, int32_t gx_dtype, void* grad_res, float* ggamma, float* gbeta,

@@ -412,13 +412,21 @@ def init_params(cin=1, planes=(32, 64, 128, 256), blocks=1, classes=40, seed=2, 
 
 
 def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256), blocks=1,
-                      lr=1e-2, momentum=0.9, mom=None, wdtype=None):
+                      lr=1e-2, momentum=0.9, mom=None, wdtype=None, conv_impl=None, act_round=None):
     """One SGD step of the SparseResNet in float64 with the reference's conv
     functions (conv.py:186-242) and the glue above.  `wdtype`, when given
     (e.g. a bf16-rounding function), is applied to conv weights and conv
     inputs before each conv so the comparison measures only accumulation.
+    `conv_impl` = (forward, backward) with the signatures of
+    sparse_conv_forward / sparse_conv_backward above (default: this module's
+    restatement; oracle/ref_runner.py passes the reference's own functions).
+    `act_round`, when given, rounds every tensor the GPU engine STORES in
+    bf16 (conv outputs, BN/residual/ReLU outputs, activation gradients) so a
+    bf16 engine can be compared at accumulation-order tolerance.
     Returns (loss, grads, new_params, new_mom)."""
     rnd = wdtype if wdtype is not None else (lambda a: a)
+    ra = act_round if act_round is not None else (lambda a: a)
+    cfwd, cbwd = conv_impl if conv_impl is not None else (sparse_conv_forward, sparse_conv_backward)
     offsets = hypercubic_offsets(3, 3)
     convs, _ = resnet_layout(feats.shape[1], planes, blocks, params["fc.w"].shape[0])
     tape = []
@@ -427,9 +435,9 @@ def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256
     def conv(name, x, c, ts, stride):
         xw = rnd(x)
         w = rnd(params[name + ".w"])
-        oc, y, ost = sparse_conv_forward(c, xw, ts, w, offsets, stride)
+        oc, y, ost = cfwd(c, xw, ts, w, offsets, stride)
         tape.append(("conv", name, c, xw, ts, w, stride))
-        return y, oc, ost
+        return ra(y), oc, ost
 
     def bnrelu(name, y, relu=True):
         z, cache = bn_forward(y, params[name + ".gamma"], params[name + ".beta"])
@@ -437,7 +445,7 @@ def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256
         if relu:
             tape.append(("relu", z > 0))
             z = np.maximum(z, 0)
-        return z
+        return ra(z) if relu else z
 
     y, c, ts = conv("stem", x, c, ts, 1)
     x = bnrelu("stem", y)
@@ -452,14 +460,14 @@ def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256
             y, _, _ = conv(f"s{s}.b{b}.c2", h, c, ts, 1)
             z = bnrelu(f"s{s}.b{b}.c2", y, relu=False) + idn
             tape.append(("res_end", z > 0))
-            x = np.maximum(z, 0)
+            x = ra(np.maximum(z, 0))
     pooled, cnt = global_avg_pool(x, c, B)
     logits = pooled @ params["fc.w"].T + params["fc.b"]
     loss, gl = cross_entropy(logits, labels)
     grads = {"fc.w": gl.T @ pooled, "fc.b": gl.sum(axis=0)}
     gp = gl @ params["fc.w"]
     seg = segment_ids(c)
-    g = gp[seg] / np.maximum(cnt, 1)[seg][:, None]
+    g = ra(gp[seg] / np.maximum(cnt, 1)[seg][:, None])
     # reverse pass
     res_stack = []
     pending = {}
@@ -467,7 +475,7 @@ def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256
         kind = item[0]
         if kind == "res_end":
             g = g * item[1]
-            res_stack.append(g.copy())  # gradient flowing to identity branch
+            res_stack.append(ra(g))  # gradient flowing to identity branch
         elif kind == "res_begin":
             g = g + res_stack.pop()
         elif kind == "relu":
@@ -475,13 +483,14 @@ def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256
         elif kind == "bn":
             _, name, cache = item
             g, gg, gb = bn_backward(g, cache, params[name + ".gamma"])
+            g = ra(g)
             grads[name + ".gamma"] = gg
             grads[name + ".beta"] = gb
         elif kind == "conv":
             _, name, cc, xw, tss, w, stride = item
-            gi, gw = sparse_conv_backward(cc, xw, tss, w, offsets, stride, g)
+            gi, gw = cbwd(cc, xw, tss, w, offsets, stride, g)
             grads[name + ".w"] = gw
-            g = gi
+            g = ra(gi)
     del pending
     new_mom = {}
     new_p = {}

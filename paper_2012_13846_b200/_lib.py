@@ -30,6 +30,7 @@ F64 = C.c_double
 SIGNATURES = {
     "vp_last_error": (C.c_char_p, []),
     "vp_version": (C.c_char_p, []),
+    "vp_kernel_launches": (C.c_longlong, []),
     "vp_hash_capacity": (I64, [I64]),
     "vp_hash_bytes": (SZ, [I64]),
     "vp_hash_build": (C.c_int, [P, P, I64, P, I64, P]),
@@ -57,7 +58,7 @@ SIGNATURES = {
     "vp_bn_stats": (C.c_int, [P, I32, P, I64, I64, F32, P, P, P, SZ, P]),
     "vp_bn_apply": (C.c_int, [P, I32, P, I64, I64, P, P, P, P, P, I32, I32, P, I32, P]),
     "vp_bn_backward_ws_bytes": (SZ, [I64, I64]),
-    "vp_bn_backward": (C.c_int, [P, I32, P, I32, P, I32, P, I64, I64, P, P, P, I32, P, I32, P, P, P, P, SZ, P]),
+    "vp_bn_backward": (C.c_int, [P, P, I32, P, I32, P, I32, P, I64, I64, P, P, P, I32, P, I32, P, P, P, P, SZ, P]),
     "vp_global_pool_ws_bytes": (SZ, [I32]),
     "vp_global_pool": (C.c_int, [P, I32, P, P, I64, I64, I32, P, P, P, SZ, P]),
     "vp_global_pool_backward": (C.c_int, [P, P, P, P, I64, I64, P, I32, P]),

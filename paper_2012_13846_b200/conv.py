@@ -127,7 +127,7 @@ class ConvWeights:
         return int(self.matrices.numel() * 8)
 
 
-@dataclass
+@dataclass(eq=False)
 class KernelMap:
     """Per-offset (input_row, output_row) links (conv.py:108-121).
 

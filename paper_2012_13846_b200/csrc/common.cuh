@@ -11,11 +11,18 @@ namespace vp {
 
 // ------------------------------------------------------------------ errors
 void set_error(const std::string& msg);
-int check_launch(const char* what);
+int check_launch(const char* what, int kernels);
 
+// after a kernel launch: counts it (vp_kernel_launches) and checks errors
 #define VP_CHECK_LAUNCH(what)                    \
   do {                                           \
-    int _st = ::vp::check_launch(what);          \
+    int _st = ::vp::check_launch(what, 1);       \
+    if (_st != VP_OK) return _st;                \
+  } while (0)
+// after a memset/memcpy: checks errors only
+#define VP_CHECK_ASYNC(what)                     \
+  do {                                           \
+    int _st = ::vp::check_launch(what, 0);       \
     if (_st != VP_OK) return _st;                \
   } while (0)
 

@@ -15,9 +15,9 @@ constexpr int kGlueThreads = 256;
 // row lane r = tid / C_eff (C_eff = min(C, 256); channels beyond loop).
 __global__ void __launch_bounds__(kGlueThreads)
 bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int64_t cap, int C,
-                  const void* __restrict__ gy, int gy_dtype, const void* __restrict__ y, int y_dtype,
-                  int relu, const float* __restrict__ mean, const float* __restrict__ rstd,
-                  float* __restrict__ part /*[blocks][2][C]*/) {
+                  const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype,
+                  const void* __restrict__ y, int y_dtype, int relu, const float* __restrict__ mean,
+                  const float* __restrict__ rstd, float* __restrict__ part /*[blocks][2][C]*/) {
   __shared__ float s_a[kGlueThreads], s_b[kGlueThreads];
   const int n = load_count(n_dev, cap);
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
@@ -39,6 +39,7 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
         const float mu = mean[c], rs = rstd[c];
         for (int64_t r = r0 + tr; r < r1; r += lanes) {
           float g = ldf(gy, gy_dtype, r * C + c);
+          if (gy2) g += ldf(gy2, gy_dtype, r * C + c);
           if (relu && ldf(y, y_dtype, r * C + c) <= 0.f) g = 0.f;
           float xh = (ldf(x, dtype, r * C + c) - mu) * rs;
           a += g;
@@ -103,7 +104,7 @@ __global__ void bn_apply_kernel(const void* __restrict__ x, int dtype, const int
   }
 }
 
-__global__ void bn_backward_apply_kernel(const void* __restrict__ gy, int gy_dtype, const void* __restrict__ y,
+__global__ void bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype, const void* __restrict__ y,
                                          int y_dtype, const void* __restrict__ x, int x_dtype, const int32_t* n_dev,
                                          int64_t cap, int C, const float* __restrict__ mean,
                                          const float* __restrict__ rstd, const float* __restrict__ gamma,
@@ -116,6 +117,7 @@ __global__ void bn_backward_apply_kernel(const void* __restrict__ gy, int gy_dty
        e += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(e % C);
     float g = ldf(gy, gy_dtype, e);
+    if (gy2) g += ldf(gy2, gy_dtype, e);
     if (relu && ldf(y, y_dtype, e) <= 0.f) g = 0.f;
     const float xh = (ldf(x, x_dtype, e) - mean[c]) * rstd[c];
     const float v = gamma[c] * rstd[c] * (g - inv_n * gbeta[c] - xh * inv_n * ggamma[c]);
@@ -268,8 +270,8 @@ int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(ws_bytes >= vp_bn_stats_ws_bytes(cap, C), VP_EVALIDATION, "bn_stats: workspace too small");
   const int nb = (int)std::max<int64_t>(1, ceil_div(cap, kRowsPerBlock));
-  bn_partial_kernel<<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, 0, nullptr, 0, 0, nullptr,
-                                                  nullptr, (float*)ws);
+  bn_partial_kernel<<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
+                                                  nullptr, nullptr, (float*)ws);
   VP_CHECK_LAUNCH("bn_partial");
   bn_finalize_kernel<<<(int)ceil_div(C, 128), 128, 0, st>>>((const float*)ws, nb, n_dev, cap, (int)C, eps, mean,
                                                             rstd, 0);
@@ -289,21 +291,21 @@ int vp_bn_apply(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
 
 size_t vp_bn_backward_ws_bytes(int64_t cap_n, int64_t C) { return vp_bn_stats_ws_bytes(cap_n, C); }
 
-int vp_bn_backward(const void* gy, int32_t gyd, const void* y, int32_t yd, const void* x, int32_t xd,
+int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, int32_t yd, const void* x, int32_t xd,
                    const int32_t* n_dev, int64_t cap, int64_t C, const float* mean, const float* rstd,
                    const float* gamma, int32_t relu, void* gx, int32_t gxd, void* gres, float* ggamma, float* gbeta,
                    void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(ws_bytes >= vp_bn_backward_ws_bytes(cap, C), VP_EVALIDATION, "bn_backward: workspace too small");
   const int nb = (int)std::max<int64_t>(1, ceil_div(cap, kRowsPerBlock));
-  bn_partial_kernel<<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gyd, y, yd, relu, mean, rstd,
+  bn_partial_kernel<<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
                                                   (float*)ws);
   VP_CHECK_LAUNCH("bn_bwd_partial");
   bn_finalize_kernel<<<(int)ceil_div(C, 128), 128, 0, st>>>((const float*)ws, nb, n_dev, cap, (int)C, 0.f, ggamma,
                                                             gbeta, 1);
   VP_CHECK_LAUNCH("bn_bwd_finalize");
   if (cap > 0) {
-    bn_backward_apply_kernel<<<grid_for(cap * C), 256, 0, st>>>(gy, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean, rstd,
+    bn_backward_apply_kernel<<<grid_for(cap * C), 256, 0, st>>>(gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean, rstd,
                                                                 gamma, relu, ggamma, gbeta, gx, gxd, gres);
     VP_CHECK_LAUNCH("bn_bwd_apply");
   }

@@ -12,10 +12,12 @@
 namespace vp {
 
 static thread_local std::string g_last_error;
+static thread_local long long g_kernel_launches = 0;  // diagnostic: kernels enqueued by this thread
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
-int check_launch(const char* what) {
+int check_launch(const char* what, int kernels) {
+  g_kernel_launches += kernels;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -422,6 +424,7 @@ extern "C" {
 
 const char* vp_last_error(void) { return g_last_error.c_str(); }
 const char* vp_version(void) { return "voxpipe_b200 0.1.0 sm_100a"; }
+long long vp_kernel_launches(void) { return g_kernel_launches; }
 
 int64_t vp_hash_capacity(int64_t n) { return (int64_t)hash_cap_for(n); }
 size_t vp_hash_bytes(int64_t cap) { return (size_t)(cap + 1) * sizeof(Slot); }
@@ -528,7 +531,7 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "output_coords: workspace too small");
   if (cap_in <= 0) {
     cudaMemsetAsync(n_out_dev, 0, sizeof(int32_t), st);
-    VP_CHECK_LAUNCH("output_coords(empty)");
+    VP_CHECK_ASYNC("output_coords(empty)");
     return VP_OK;
   }
   int r = hash_clear(t, cap, st);
@@ -588,7 +591,7 @@ int vp_voxelize(const void* points, int32_t pts_dtype, int64_t n, const int64_t*
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "voxelize: workspace too small");
   if (n <= 0) {
     cudaMemsetAsync(n_out_dev, 0, sizeof(int32_t), st);
-    VP_CHECK_LAUNCH("voxelize(empty)");
+    VP_CHECK_ASYNC("voxelize(empty)");
     return VP_OK;
   }
   int r = hash_clear(t, cap, st);

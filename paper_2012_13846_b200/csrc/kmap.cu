@@ -188,7 +188,7 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
   }
   if (cap_out <= 0) {
     if (pair_ptr) cudaMemsetAsync(pair_ptr, 0, sizeof(int32_t) * (K + 1), st);
-    VP_CHECK_LAUNCH("kernel_map(empty)");
+    VP_CHECK_ASYNC("kernel_map(empty)");
     return VP_OK;
   }
   size_t smem = kMapTile * 16 + K * 4;
@@ -211,11 +211,12 @@ int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t 
                           int32_t* inv, int64_t cap_in, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (cap_in > 0) cudaMemsetAsync(inv, 0xff, sizeof(int32_t) * cap_in * K, st);
+  VP_CHECK_ASYNC("kernel_map_inverse(memset)");
   if (cap_out > 0) {
     int blocks = (int)std::min<int64_t>(ceil_div(cap_out * K, 256), kNumSMs * 16);
     map_inverse_kernel<<<blocks, 256, 0, st>>>(nbr, n_out_dev, cap_out, K, inv);
+    VP_CHECK_LAUNCH("kernel_map_inverse");
   }
-  VP_CHECK_LAUNCH("kernel_map_inverse");
   return VP_OK;
 }
 

@@ -1,0 +1,401 @@
+"""SparseResNet classifier training on one B200 (SURVEY §8(d) model; BASELINE
+config 3: 64 clouds x 2048 points at 64^3, bf16 features).
+
+The whole training step — GPU voxelization of the raw points, strided output
+coordinates, the nine kernel maps, 13 sparse convs forward, BN/ReLU/residual,
+global pool, linear + cross entropy, the backward pass (dgrad + deterministic
+wgrad), and SGD with momentum — is a fixed sequence of C-ABI calls on one
+stream over statically allocated, capacity-sized buffers whose live row
+counts stay in device memory.  Nothing reads a size back to the host, so the
+step is captured once into a CUDA graph and replayed (launch-bound inner
+loop -> one graph launch).
+
+Layer list (blocks=1 -> 13 convs): stem conv3 s1 (C_in -> 32); per stage
+s in 0..3 with planes (32, 64, 128, 256): conv3 s2 (prev -> p) then `blocks`
+BasicBlocks (conv3 s1 p->p, BN, ReLU, conv3 s1 p->p, BN, + identity, ReLU).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .conv import KernelShape
+
+BF16 = torch.bfloat16
+
+
+@dataclass(eq=False)
+class Level:
+    """Coordinates of one tensor-stride level (rows batch-contiguous)."""
+
+    coords: torch.Tensor  # (cap, 4) int32
+    n: torch.Tensor  # (1,) int32, live rows
+    cap: int
+    stride: int
+
+
+@dataclass(eq=False)
+class Map:
+    """Kernel map between two levels (conv.py:149-183 layout, device)."""
+
+    nbr: torch.Tensor  # (cap_out, K)
+    pin: torch.Tensor
+    pout: torch.Tensor
+    ptr: torch.Tensor  # (K+1,)
+    inv: Optional[torch.Tensor]  # (cap_in, K) for strided maps (dgrad table)
+    src: Level
+    dst: Level
+    ws: torch.Tensor
+
+
+class ParamBuffer:
+    """Flat fp32 parameter / gradient / momentum buffers; conv weights first so
+    the bf16 shadow (tensor-core operand) is one contiguous prefix."""
+
+    def __init__(self, device):
+        self.device = device
+        self.specs: list[tuple[str, tuple]] = []
+        self.offsets: dict[str, tuple[int, tuple]] = {}
+        self.size = 0
+        self.n_bf16 = 0
+
+    def add(self, name, shape, bf16=False):
+        n = int(np.prod(shape))
+        if bf16:
+            assert self.n_bf16 == self.size, "bf16 params must come first"
+            self.n_bf16 += n
+        self.offsets[name] = (self.size, tuple(shape))
+        self.size += n
+
+    def finalize(self):
+        self.p = torch.zeros(self.size, dtype=torch.float32, device=self.device)
+        self.g = torch.zeros_like(self.p)
+        self.m = torch.zeros_like(self.p)
+        self.pb = torch.zeros(max(self.n_bf16, 1), dtype=BF16, device=self.device)
+
+    def view(self, buf, name):
+        off, shape = self.offsets[name]
+        return buf[off: off + int(np.prod(shape))].view(shape)
+
+    def bf16_view(self, name):
+        off, shape = self.offsets[name]
+        return self.pb[off: off + int(np.prod(shape))].view(shape)
+
+
+class SparseResNetTrainer:
+    """Graph-capturable SparseResNet training engine on one GPU."""
+
+    def __init__(self, batch=64, points=2048, resolution=64, planes=(32, 64, 128, 256), blocks=1, classes=40,
+                 in_channels=1, lr=1e-2, momentum=0.9, seed=2, voxel_size=1.0, device=None,
+                 points_dtype=torch.float32, grad_allreduce=None):
+        self.B, self.P, self.res = batch, points, resolution
+        self.planes, self.blocks, self.classes, self.cin = tuple(planes), blocks, classes, in_channels
+        self.lr, self.momentum, self.voxel_size = lr, momentum, voxel_size
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.grad_allreduce = grad_allreduce  # callable(flat_grad) for data parallel, or None
+        self.shape = KernelShape.hypercubic(3, 3)
+        self.K = self.shape.num_offsets
+        self.offs3 = _lib.i32_array(self.shape.offsets3().ravel())
+        self.eps = 1e-5
+        dev = self.device
+        cap = batch * points
+        self.cap = cap
+        # ---- inputs (static; copied into before each replay)
+        self.points = torch.zeros((cap, 3), dtype=points_dtype, device=dev)
+        self.offsets = torch.arange(batch + 1, dtype=torch.int64, device=dev) * points
+        self.labels = torch.zeros(batch, dtype=torch.int32, device=dev)
+        # ---- levels
+        nlev = len(planes) + 1
+        self.levels = [Level(torch.zeros((cap, 4), dtype=torch.int32, device=dev),
+                             torch.zeros(1, dtype=torch.int32, device=dev), cap, 2 ** i) for i in range(nlev)]
+        self.feat0 = torch.zeros((cap, in_channels), dtype=BF16, device=dev)
+        self.vox_ws = _lib.workspace(_lib.query("vp_voxelize_ws_bytes", cap), dev)
+        self.oc_ws = _lib.workspace(_lib.query("vp_output_coords_ws_bytes", cap), dev)
+        # ---- maps: stride-1 per level, strided between consecutive levels
+        self.map_s1 = [self._alloc_map(self.levels[i], self.levels[i], strided=False) for i in range(nlev)]
+        self.map_dn = [self._alloc_map(self.levels[i], self.levels[i + 1], strided=True) for i in range(nlev - 1)]
+        # ---- parameters
+        self.layers = self._layer_list()
+        pb = ParamBuffer(dev)
+        for L in self.layers:
+            pb.add(L["name"] + ".w", (self.K, L["cout"], L["cin"]), bf16=True)
+        for L in self.layers:
+            pb.add(L["name"] + ".gamma", (L["cout"],))
+            pb.add(L["name"] + ".beta", (L["cout"],))
+        pb.add("fc.w", (classes, planes[-1]))
+        pb.add("fc.b", (classes,))
+        pb.finalize()
+        self.params = pb
+        self._init_params(seed)
+        # ---- activations (capacity sized)
+        for L in self.layers:
+            n = L["dst"].cap
+            L["y"] = torch.zeros((n, L["cout"]), dtype=BF16, device=dev)  # conv output (pre-BN)
+            L["a"] = torch.zeros((n, L["cout"]), dtype=BF16, device=dev)  # BN(+res)(+ReLU) output
+            L["mean"] = torch.zeros(L["cout"], dtype=torch.float32, device=dev)
+            L["rstd"] = torch.zeros(L["cout"], dtype=torch.float32, device=dev)
+            L["gy"] = torch.zeros((n, L["cout"]), dtype=BF16, device=dev)  # grad wrt conv output
+            L["w"] = pb.view(pb.p, L["name"] + ".w")
+            L["wb"] = pb.bf16_view(L["name"] + ".w")
+            L["gw"] = pb.view(pb.g, L["name"] + ".w")
+            for k in ("gamma", "beta"):
+                L[k] = pb.view(pb.p, f"{L['name']}.{k}")
+                L["g" + k] = pb.view(pb.g, f"{L['name']}.{k}")
+            L["fwd_ws"] = _lib.workspace(_lib.query("vp_conv_fwd_ws_bytes", L["cin"], L["cout"], self.K), dev)
+            L["dg_ws"] = _lib.workspace(_lib.query("vp_conv_dgrad_ws_bytes", L["cin"], L["cout"], self.K), dev)
+            L["wg_ws"] = _lib.workspace(_lib.query("vp_conv_wgrad_ws_bytes", L["cin"], L["cout"], self.K,
+                                                   L["map"].pin.numel()), dev)
+            L["bn_ws"] = _lib.workspace(_lib.query("vp_bn_stats_ws_bytes", n, L["cout"]), dev)
+        # gradient buffers per level for the activation flowing back
+        self.gact = [torch.zeros((lv.cap, self._width_at(i)), dtype=BF16, device=dev) for i, lv in enumerate(self.levels)]
+        self.gid = [torch.zeros((lv.cap, self._width_at(i)), dtype=BF16, device=dev) for i, lv in enumerate(self.levels)]
+        C = planes[-1]
+        self.pooled = torch.zeros((batch, C), dtype=torch.float32, device=dev)
+        self.pool_counts = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.pool_ws = _lib.workspace(_lib.query("vp_global_pool_ws_bytes", batch), dev)
+        self.logits = torch.zeros((batch, classes), dtype=torch.float32, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.g_pooled = torch.zeros((batch, C), dtype=torch.float32, device=dev)
+        self.xent_ws = _lib.workspace(_lib.query("vp_linear_xent_ws_bytes", batch, classes), dev)
+        self.graph: Optional[torch.cuda.CUDAGraph] = None
+        self.launch_count = 0
+
+    # ------------------------------------------------------------------ setup
+    def _width_at(self, level):
+        return self.planes[0] if level == 0 else self.planes[level - 1]
+
+    def _alloc_map(self, src: Level, dst: Level, strided: bool) -> Map:
+        dev, K = self.device, self.K
+        cap_p = dst.cap * K
+        return Map(
+            nbr=torch.zeros((dst.cap, K), dtype=torch.int32, device=dev),
+            pin=torch.zeros(cap_p, dtype=torch.int32, device=dev),
+            pout=torch.zeros(cap_p, dtype=torch.int32, device=dev),
+            ptr=torch.zeros(K + 1, dtype=torch.int32, device=dev),
+            inv=torch.zeros((src.cap, K), dtype=torch.int32, device=dev) if strided else None,
+            src=src, dst=dst,
+            ws=_lib.workspace(_lib.query("vp_kernel_map_ws_bytes", src.cap, dst.cap, K), dev))
+
+    def _layer_list(self):
+        L = [dict(name="stem", cin=self.cin, cout=self.planes[0], src=self.levels[0], dst=self.levels[0],
+                  map=self.map_s1[0], kind="stem")]
+        prev = self.planes[0]
+        for s, p in enumerate(self.planes):
+            L.append(dict(name=f"s{s}.down", cin=prev, cout=p, src=self.levels[s], dst=self.levels[s + 1],
+                          map=self.map_dn[s], kind="down"))
+            for b in range(self.blocks):
+                L.append(dict(name=f"s{s}.b{b}.c1", cin=p, cout=p, src=self.levels[s + 1], dst=self.levels[s + 1],
+                              map=self.map_s1[s + 1], kind="c1"))
+                L.append(dict(name=f"s{s}.b{b}.c2", cin=p, cout=p, src=self.levels[s + 1], dst=self.levels[s + 1],
+                              map=self.map_s1[s + 1], kind="c2"))
+            prev = p
+        for i, l in enumerate(L):
+            l["index"] = i
+            l["level"] = self.levels.index(l["dst"])
+        return L
+
+    def _init_params(self, seed):
+        """Weights ~ N(0,1)/sqrt(K*C_in) via default_rng(seed), layout (K, C_out,
+        C_in) (oracle.init_params / SURVEY §8(d)); BN gamma 1, beta 0; fc
+        N(0,1)/sqrt(C)."""
+        rng = np.random.default_rng(seed)
+        pb = self.params
+        for L in self.layers:
+            w = rng.normal(size=(self.K, L["cout"], L["cin"])) / math.sqrt(self.K * L["cin"])
+            pb.view(pb.p, L["name"] + ".w").copy_(torch.from_numpy(w))
+            pb.view(pb.p, L["name"] + ".gamma").fill_(1.0)
+        fcw = rng.normal(size=(self.classes, self.planes[-1])) / math.sqrt(self.planes[-1])
+        pb.view(pb.p, "fc.w").copy_(torch.from_numpy(fcw))
+        pb.pb[: pb.n_bf16].copy_(pb.p[: pb.n_bf16].to(BF16))
+
+    def load_params(self, params: dict):
+        pb = self.params
+        for k, v in params.items():
+            pb.view(pb.p, k).copy_(torch.as_tensor(np.asarray(v), dtype=torch.float32))
+        pb.pb[: pb.n_bf16].copy_(pb.p[: pb.n_bf16].to(BF16))
+
+    def state_numpy(self) -> dict:
+        pb = self.params
+        return {k: pb.view(pb.p, k).cpu().numpy().astype(np.float64) for k in pb.offsets}
+
+    def grads_numpy(self) -> dict:
+        pb = self.params
+        return {k: pb.view(pb.g, k).cpu().numpy().astype(np.float64) for k in pb.offsets}
+
+    # ------------------------------------------------------------------ step pieces
+    def _c(self, name, *args):
+        self.launch_count += 1
+        _lib.call(name, *args)
+
+    def _integer_stage(self, st):
+        lv = self.levels
+        res3 = _lib.i32_array((self.res,) * 3)
+        self._c("vp_voxelize", self.points.data_ptr(), _lib.dtype_code(self.points), self.cap, self.offsets.data_ptr(),
+                self.B, float(self.voxel_size), res3, lv[0].coords.data_ptr(), lv[0].n.data_ptr(), None,
+                self.feat0.data_ptr(), _lib.VP_BF16, self.vox_ws.data_ptr(), self.vox_ws.numel(), st)
+        for i in range(1, len(lv)):
+            step = _lib.i32_array((lv[i].stride,) * 3)
+            self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
+                    lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(), st)
+        for m in self.map_s1 + self.map_dn:
+            ist = _lib.i32_array((m.src.stride,) * 3)
+            self._c("vp_kernel_map", m.src.coords.data_ptr(), m.src.n.data_ptr(), m.src.cap, m.dst.coords.data_ptr(),
+                    m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(), m.pin.data_ptr(),
+                    m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st)
+            if m.inv is not None:
+                self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
+                        m.inv.data_ptr(), m.src.cap, st)
+
+    def _conv_bn(self, L, x, res, relu, st):
+        dst = L["dst"]
+        self._c("vp_conv_fwd", x.data_ptr(), _lib.VP_BF16, L["cin"], L["wb"].data_ptr(), _lib.VP_BF16, L["cout"],
+                self.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(), _lib.VP_BF16,
+                L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
+        self._c("vp_bn_stats", L["y"].data_ptr(), _lib.VP_BF16, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
+                L["mean"].data_ptr(), L["rstd"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
+        self._c("vp_bn_apply", L["y"].data_ptr(), _lib.VP_BF16, dst.n.data_ptr(), dst.cap, L["cout"],
+                L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(), L["beta"].data_ptr(),
+                _lib.ptr(res), _lib.VP_BF16, int(relu), L["a"].data_ptr(), _lib.VP_BF16, st)
+        L["x"] = x
+        return L["a"]
+
+    def _forward(self, st):
+        Ls = self.layers
+        x = self._conv_bn(Ls[0], self.feat0, None, True, st)
+        i = 1
+        for s in range(len(self.planes)):
+            x = self._conv_bn(Ls[i], x, None, True, st)
+            i += 1
+            for _ in range(self.blocks):
+                idn = x
+                h = self._conv_bn(Ls[i], x, None, True, st)
+                x = self._conv_bn(Ls[i + 1], h, idn, True, st)
+                i += 2
+        last = self.levels[-1]
+        C = self.planes[-1]
+        self._c("vp_global_pool", x.data_ptr(), _lib.VP_BF16, last.coords.data_ptr(), last.n.data_ptr(), last.cap, C,
+                self.B, self.pooled.data_ptr(), self.pool_counts.data_ptr(), self.pool_ws.data_ptr(),
+                self.pool_ws.numel(), st)
+        pb = self.params
+        self._c("vp_linear_xent", self.pooled.data_ptr(), self.B, C, pb.view(pb.p, "fc.w").data_ptr(),
+                pb.view(pb.p, "fc.b").data_ptr(), self.classes, self.labels.data_ptr(), self.logits.data_ptr(),
+                self.loss.data_ptr(), self.g_pooled.data_ptr(), pb.view(pb.g, "fc.w").data_ptr(),
+                pb.view(pb.g, "fc.b").data_ptr(), self.xent_ws.data_ptr(), self.xent_ws.numel(), st)
+        return x
+
+    def _bn_conv_backward(self, L, g_out, g_out2, g_res, st, need_dgrad=True):
+        """BN(+ReLU) backward then conv dgrad/wgrad.  g_out (+g_out2) is the
+        gradient wrt L['a']; returns the gradient wrt the conv input."""
+        dst, src, m = L["dst"], L["src"], L["map"]
+        self._c("vp_bn_backward", g_out.data_ptr(), _lib.ptr(g_out2), _lib.VP_BF16, L["a"].data_ptr(), _lib.VP_BF16,
+                L["y"].data_ptr(), _lib.VP_BF16, dst.n.data_ptr(), dst.cap, L["cout"], L["mean"].data_ptr(),
+                L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(), _lib.VP_BF16, _lib.ptr(g_res),
+                L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
+        x = L["x"]
+        self._c("vp_conv_wgrad", x.data_ptr(), _lib.VP_BF16, L["cin"], L["gy"].data_ptr(), _lib.VP_BF16, L["cout"],
+                self.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(),
+                L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st)
+        if not need_dgrad:
+            return None
+        gin = self.gact[self.levels.index(src)]
+        if m.inv is None:
+            table, flip = m.nbr, 1  # stride 1, symmetric 3^3: inv[v,k] == nbr[v,K-1-k]
+        else:
+            table, flip = m.inv, 0
+        self._c("vp_conv_dgrad", L["gy"].data_ptr(), _lib.VP_BF16, L["cout"], L["wb"].data_ptr(), _lib.VP_BF16,
+                L["cin"], self.K, table.data_ptr(), flip, src.n.data_ptr(), src.cap, gin.data_ptr(), _lib.VP_BF16,
+                L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
+        return gin
+
+    def _backward(self, st):
+        last = self.levels[-1]
+        C = self.planes[-1]
+        g = self.gact[-1]
+        self._c("vp_global_pool_backward", self.g_pooled.data_ptr(), last.coords.data_ptr(),
+                self.pool_counts.data_ptr(), last.n.data_ptr(), last.cap, C, g.data_ptr(), _lib.VP_BF16, st)
+        g2 = None  # pending identity-branch gradient for the current activation
+        Ls = self.layers
+        i = len(Ls) - 1
+        for s in reversed(range(len(self.planes))):
+            lvl = s + 1
+            for _ in range(self.blocks):
+                c1, c2 = Ls[i - 1], Ls[i]
+                gid = self.gid[lvl]
+                # out = relu(bn2(conv2(h)) + idn): mask by out, identity grad -> gid
+                gh = self._bn_conv_backward(c2, g, g2, gid, st)
+                # gh lives in gact[lvl]; c1 backward writes its dgrad into gact[lvl] too,
+                # so move it aside (gy of c2 already consumed it in dgrad->gh)
+                gx = self._bn_conv_backward(c1, gh, None, None, st)
+                g, g2 = gx, gid
+                i -= 2
+            down = Ls[i]
+            g = self._bn_conv_backward(down, g, g2, None, st)
+            g2 = None
+            i -= 1
+        self._bn_conv_backward(Ls[0], g, g2, None, st, need_dgrad=False)
+
+    def _optimizer(self, st):
+        pb = self.params
+        if self.grad_allreduce is not None:
+            self.grad_allreduce(pb.g)
+        self._c("vp_sgd_momentum", pb.p.data_ptr(), pb.m.data_ptr(), pb.g.data_ptr(), pb.size, float(self.lr),
+                float(self.momentum), pb.pb.data_ptr(), pb.n_bf16, st)
+
+    def step_body(self):
+        """One full training step on the current stream (graph-capturable)."""
+        st = _lib.stream()
+        self.launch_count = 0
+        self._integer_stage(st)
+        self._forward(st)
+        self._backward(st)
+        self._optimizer(st)
+
+    # ------------------------------------------------------------------ public
+    def set_batch(self, points: torch.Tensor, labels: torch.Tensor, non_blocking=True):
+        self.points.copy_(points, non_blocking=non_blocking)
+        self.labels.copy_(labels, non_blocking=non_blocking)
+
+    def capture(self, warmup: int = 1):
+        """Record the step into a CUDA graph (after eager warm-up steps that
+        populate the kernels' one-time attribute caches)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.step_body()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step_body()
+        self.graph = g
+        return g
+
+    def step(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.step_body()
+
+    def train_step_from_host(self, points_np, offsets_np, labels_np) -> float:
+        """End-to-end convenience call: host points -> device, one step, loss."""
+        pts = torch.as_tensor(np.ascontiguousarray(points_np)).to(self.points.dtype)
+        if pts.shape[0] != self.cap:
+            raise ValueError("point count must equal batch * points")
+        offs = np.asarray(offsets_np)
+        if not np.array_equal(offs, np.arange(self.B + 1) * self.P):
+            raise ValueError("fixed-size clouds expected (offsets = arange(B+1) * points)")
+        self.set_batch(pts.to(self.device), torch.as_tensor(np.asarray(labels_np), dtype=torch.int32).to(self.device))
+        self.step()
+        return float(self.loss.item())
+
+    def level_sizes(self) -> list[int]:
+        return [int(l.n.item()) for l in self.levels]
+
+    def pair_counts(self) -> list[int]:
+        return [int(m.ptr[-1].item()) for m in self.map_s1 + self.map_dn]

@@ -1,0 +1,71 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads without a GPU,
+exports every symbol include/voxpipe_b200.h declares, and the ctypes table
+matches the header (no compute calls here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "voxpipe_b200.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(vp_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2012_13846_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2012_13846_b200 import build_lib
+        build_lib.build(verbose=False)
+    return _lib.load()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = header_functions()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_ctypes_table_matches_header():
+    from paper_2012_13846_b200 import _lib
+    assert sorted(_lib.SIGNATURES) == header_functions()
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    for name, (_, args) in _lib.SIGNATURES.items():
+        m = re.search(r"\b" + name + r"\s*\(([^)]*)\)", src)
+        params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
+        assert len(params) == len(args), (name, len(params), len(args))
+
+
+def test_pure_queries_without_gpu(lib):
+    from paper_2012_13846_b200 import _lib
+    assert _lib.query("vp_hash_capacity", 0) == 8
+    assert _lib.query("vp_hash_capacity", 3) == 8
+    assert _lib.query("vp_hash_capacity", 4) == 16  # pow2 >= 2n+2 (_kernels.pyx:27-29)
+    assert _lib.query("vp_hash_capacity", 115918) == 262144
+    assert _lib.query("vp_hash_bytes", 8) == 9 * 16
+    assert lib.vp_version().startswith(b"voxpipe_b200")
+    assert _lib.query("vp_kernel_map_ws_bytes", 1000, 1000, 27) > 0
+    assert _lib.query("vp_conv_wgrad_ws_bytes", 64, 64, 27, 100000) >= 27 * 64 * 64 * 4
+
+
+def test_library_is_sm100a_and_uses_tcgen05(lib):
+    from paper_2012_13846_b200 import _lib
+    out = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in out and "LDTM" in out  # tcgen05.mma / tcgen05.ld in SASS
+
+
+def test_product_has_no_oracle_import():
+    pkg = os.path.join(ROOT, "paper_2012_13846_b200")
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            src = open(os.path.join(pkg, f)).read()
+            assert "voxpipe_oracle" not in src and "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\S+)", src, re.M), f
