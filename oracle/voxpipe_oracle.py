@@ -412,7 +412,8 @@ def init_params(cin=1, planes=(32, 64, 128, 256), blocks=1, classes=40, seed=2, 
 
 
 def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256), blocks=1,
-                      lr=1e-2, momentum=0.9, mom=None, wdtype=None, conv_impl=None, act_round=None):
+                      lr=1e-2, momentum=0.9, mom=None, wdtype=None, conv_impl=None, act_round=None,
+                      trace=None):
     """One SGD step of the SparseResNet in float64 with the reference's conv
     functions (conv.py:186-242) and the glue above.  `wdtype`, when given
     (e.g. a bf16-rounding function), is applied to conv weights and conv
@@ -437,11 +438,15 @@ def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256
         w = rnd(params[name + ".w"])
         oc, y, ost = cfwd(c, xw, ts, w, offsets, stride)
         tape.append(("conv", name, c, xw, ts, w, stride))
+        if trace is not None:
+            trace[name + ".y"] = ra(y)
         return ra(y), oc, ost
 
     def bnrelu(name, y, relu=True):
         z, cache = bn_forward(y, params[name + ".gamma"], params[name + ".beta"])
         tape.append(("bn", name, cache))
+        if trace is not None:
+            trace[name + ".mean"], trace[name + ".rstd"] = cache[2], cache[1]
         if relu:
             tape.append(("relu", z > 0))
             z = np.maximum(z, 0)
@@ -484,6 +489,8 @@ def resnet_train_step(params, coords, feats, labels, B, planes=(32, 64, 128, 256
             _, name, cache = item
             g, gg, gb = bn_backward(g, cache, params[name + ".gamma"])
             g = ra(g)
+            if trace is not None:
+                trace[name + ".gy"] = g
             grads[name + ".gamma"] = gg
             grads[name + ".beta"] = gb
         elif kind == "conv":

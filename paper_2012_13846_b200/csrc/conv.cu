@@ -21,387 +21,12 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "conv_fwd_tc.cuh"
+#include "conv_wgrad_tc.cuh"
 #include "tc.cuh"
 
 namespace vp {
 
-using bf16 = __nv_bfloat16;
-constexpr int kTileM = 128;
-constexpr int kConvThreads = 128;
-constexpr int kMaskWords = (VP_MAX_OFFSETS + 31) / 32;
-
-template <int CIN, int COUT>
-struct FwdCfg {
-  static constexpr int KC = CIN >= 64 ? 64 : CIN;  // K elements per stage
-  static constexpr int NC = CIN / KC;              // stages per offset
-  static constexpr int PITCH = KC * 2;             // bytes per smem row
-  static constexpr uint32_t SWZ = PITCH == 128 ? tc::kSwizzle128 : tc::kSwizzle64;
-  static constexpr int A_BYTES = kTileM * PITCH;
-  static constexpr int B_BYTES = COUT * PITCH;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (4 * STAGE_BYTES <= 200 * 1024) ? 4 : 3;
-  static constexpr int TMEM_COLS = COUT < 32 ? 32 : COUT;
-  static constexpr uint32_t IDESC = tc::idesc_bf16(kTileM, COUT, 0, 0);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 2048 /*bookkeeping*/;
-};
-
-// byte offset of 16B chunk j of row r in a K-major swizzled tile
-template <int PITCH>
-__device__ __forceinline__ uint32_t kmajor_off(int r, int j) {
-  if (PITCH == 128) return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
-  return (uint32_t)(r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
-}
-
-template <int CIN, int COUT>
-__global__ void __launch_bounds__(kConvThreads, 1)
-conv_fwd_tc_kernel(const bf16* __restrict__ x, const bf16* __restrict__ w, int K,
-                   const int32_t* __restrict__ table, int flip, const int32_t* n_out_dev,
-                   int64_t cap_out, void* __restrict__ y, int y_dtype) {
-  using C = FwdCfg<CIN, COUT>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* book = smem + C::STAGES * C::STAGE_BYTES;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(book);                 // STAGES
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(book + 64);
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(book + 128);         // kMaskWords
-  int16_t* s_active = reinterpret_cast<int16_t*>(book + 192);         // <= 343 entries
-  int* s_nact = reinterpret_cast<int*>(book + 192 + 2 * VP_MAX_OFFSETS + 2);
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int n_out = load_count(n_out_dev, cap_out);
-  const int ntiles = (n_out + kTileM - 1) / kTileM;
-  if ((int)blockIdx.x >= ntiles) return;
-
-  if (tid == 0) {
-    for (int s = 0; s < C::STAGES; ++s) tc::mbar_init(&mbar[s], 1);
-    tc::fence_mbar_init();
-  }
-  if (warp == 0) tc::tmem_alloc(s_tmem, C::TMEM_COLS);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *s_tmem;
-  const uint32_t smem_base = tc::smem_u32(smem);
-
-  uint32_t g = 0;  // global pipeline iteration (stage = g % STAGES)
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t u = (int64_t)tile * kTileM + tid;
-    const bool valid = u < n_out;
-    const int32_t* trow = table + u * K;
-    // ---- active offsets of this tile (bit k set iff some row has neighbour k)
-    if (tid < kMaskWords) s_mask[tid] = 0;
-    __syncthreads();
-    if (valid) {
-      for (int kb = 0; kb < K; kb += 32) {
-        uint32_t bits = 0;
-        const int kend = min(32, K - kb);
-        for (int j = 0; j < kend; ++j) {
-          int k = kb + j;
-          int col = flip ? K - 1 - k : k;
-          if (__ldg(trow + col) >= 0) bits |= 1u << j;
-        }
-        if (bits) atomicOr(&s_mask[kb >> 5], bits);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int na = 0;
-      for (int k = 0; k < K; ++k)
-        if (s_mask[k >> 5] & (1u << (k & 31))) s_active[na++] = (int16_t)k;
-      *s_nact = na;
-    }
-    __syncthreads();
-    const int n_iter = *s_nact * C::NC;
-
-    auto load_stage = [&](int it, uint32_t gi) {
-      const int stage = gi % C::STAGES;
-      const int k = s_active[it / C::NC];
-      const int c = it % C::NC;
-      const uint32_t a_s = smem_base + stage * C::STAGE_BYTES;
-      const uint32_t b_s = a_s + C::A_BYTES;
-      // A: row tid <- x[table[u, col]] slice c (zero-fill on miss)
-      const int col = flip ? K - 1 - k : k;
-      const int v = valid ? __ldg(trow + col) : -1;
-      const bf16* src = x + (int64_t)(v >= 0 ? v : 0) * CIN + c * C::KC;
-      const int nbytes = v >= 0 ? 16 : 0;
-#pragma unroll
-      for (int j = 0; j < C::KC / 8; ++j) tc::cp_async16(a_s + kmajor_off<C::PITCH>(tid, j), src + j * 8, nbytes);
-      // B: W_k[n, slice c] for n in [0, COUT)
-      const bf16* wk = w + ((int64_t)k * COUT) * CIN + c * C::KC;
-      constexpr int CHUNKS = COUT * (C::KC / 8);
-#pragma unroll
-      for (int e = tid; e < CHUNKS; e += kConvThreads) {
-        const int n = e / (C::KC / 8), j = e % (C::KC / 8);
-        tc::cp_async16(b_s + kmajor_off<C::PITCH>(n, j), wk + (int64_t)n * CIN + j * 8, 16);
-      }
-    };
-
-    // ---- prologue
-    for (int p = 0; p < C::STAGES - 1; ++p) {
-      if (p < n_iter) {
-        const uint32_t gi = g + p;
-        if (gi >= (uint32_t)C::STAGES) tc::mbar_wait(&mbar[gi % C::STAGES], ((gi / C::STAGES) - 1) & 1);
-        load_stage(p, gi);
-      }
-      tc::cp_async_commit();
-    }
-    // ---- main loop
-    for (int it = 0; it < n_iter; ++it) {
-      const int nxt = it + C::STAGES - 1;
-      if (nxt < n_iter) {
-        const uint32_t gi = g + nxt;
-        if (gi >= (uint32_t)C::STAGES) tc::mbar_wait(&mbar[gi % C::STAGES], ((gi / C::STAGES) - 1) & 1);
-        load_stage(nxt, gi);
-      }
-      tc::cp_async_commit();
-      tc::cp_async_wait<C::STAGES - 1>();
-      tc::fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        tc::tc_fence_after();
-        const uint32_t gi = g + it;
-        const int stage = gi % C::STAGES;
-        const uint32_t a_s = smem_base + stage * C::STAGE_BYTES;
-        const uint32_t b_s = a_s + C::A_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < C::KC / 16; ++kk) {
-          const uint64_t ad = tc::smem_desc(a_s + kk * 32, 16, 8 * C::PITCH, C::SWZ);
-          const uint64_t bd = tc::smem_desc(b_s + kk * 32, 16, 8 * C::PITCH, C::SWZ);
-          tc::mma_bf16(tmem, ad, bd, C::IDESC, (it > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(&mbar[stage]);
-      }
-    }
-    // ---- epilogue: wait for the last MMA of this tile
-    if (n_iter > 0) {
-      const uint32_t gl = g + n_iter - 1;
-      tc::mbar_wait(&mbar[gl % C::STAGES], (gl / C::STAGES) & 1);
-      tc::tc_fence_after();
-    }
-    g += n_iter;
-#pragma unroll 1
-    for (int c0 = 0; c0 < COUT; c0 += 32) {
-      float v[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-      if (n_iter == 0) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
-      const int64_t row = (int64_t)tile * kTileM + warp * 32 + lane;
-      if (row < n_out) {
-        if (y_dtype == VP_BF16) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(y) + row * COUT + c0);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 pk;
-            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * q + 0], v[8 * q + 1]);
-            __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * q + 2], v[8 * q + 3]);
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * q + 4], v[8 * q + 5]);
-            __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * q + 6], v[8 * q + 7]);
-            pk.x = *reinterpret_cast<uint32_t*>(&h0);
-            pk.y = *reinterpret_cast<uint32_t*>(&h1);
-            pk.z = *reinterpret_cast<uint32_t*>(&h2);
-            pk.w = *reinterpret_cast<uint32_t*>(&h3);
-            dst[q] = pk;
-          }
-        } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + row * COUT + c0);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
-      }
-    }
-    // TMEM reads done before the next tile's first MMA overwrites the accumulator
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-  }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, C::TMEM_COLS);
-}
-
-// ------------------------------------------------------------------ wgrad (tcgen05)
-template <int CIN, int COUT>
-struct WgCfg {
-  static constexpr int PK = 64;                        // pairs per stage (MMA K)
-  static constexpr int MPAD = COUT < 64 ? 64 : COUT;   // A MN extent in smem
-  static constexpr int NPAD = CIN < 64 ? 64 : CIN;     // B MN extent in smem
-  static constexpr int M = COUT >= 128 ? 128 : 64;     // MMA M
-  static constexpr int MT = COUT > 128 ? 2 : 1;        // accumulators (M blocks)
-  static constexpr int N = CIN;                        // MMA N
-  static constexpr int A_BYTES = MPAD * PK * 2;
-  static constexpr int B_BYTES = NPAD * PK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (4 * STAGE_BYTES <= 200 * 1024) ? 4 : (3 * STAGE_BYTES <= 200 * 1024 ? 3 : 2);
-  static constexpr int COLS = MT * N;
-  static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
-  static constexpr uint32_t IDESC = tc::idesc_bf16(M, N, 1, 1);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 1024;
-  static constexpr int LBO = 8 * 1024;  // stride between 64-wide MN blocks (PK=64 -> 8 k-groups)
-  static constexpr int SBO = 1024;      // stride between 8-row k groups
-};
-
-// byte offset of element chunk (mn/8) for pair-row kk in an MN-major SW128 tile
-__device__ __forceinline__ uint32_t mnmajor_off(int mn_chunk, int kk) {
-  const int blk = mn_chunk >> 3, j = mn_chunk & 7;
-  return (uint32_t)(blk * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + ((j ^ (kk & 7)) << 4));
-}
-
-template <int CIN, int COUT>
-__global__ void __launch_bounds__(kConvThreads, 1)
-conv_wgrad_tc_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gy, int K,
-                     const int32_t* __restrict__ pin, const int32_t* __restrict__ pout,
-                     const int32_t* __restrict__ pptr, int chunk, float* __restrict__ part) {
-  using C = WgCfg<CIN, COUT>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* book = smem + C::STAGES * C::STAGE_BYTES;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(book);
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(book + 64);
-  int* s_pref = reinterpret_cast<int*>(book + 128);  // K+1 item prefix (K <= 125 here)
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  if (tid == 0) {
-    int acc = 0;
-    for (int k = 0; k < K; ++k) {
-      s_pref[k] = acc;
-      int p = pptr[k + 1] - pptr[k];
-      acc += (p + chunk - 1) / chunk;
-    }
-    s_pref[K] = acc;
-    for (int s = 0; s < C::STAGES; ++s) tc::mbar_init(&mbar[s], 1);
-    tc::fence_mbar_init();
-  }
-  __syncthreads();
-  const int n_items = s_pref[K];
-  if ((int)blockIdx.x >= n_items) return;
-  if (warp == 0) tc::tmem_alloc(s_tmem, C::TMEM_COLS);
-  const uint32_t smem_base = tc::smem_u32(smem);
-  // zero padding regions once (never written by loads)
-  if (COUT < 64 || CIN < 64) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      uint4* p = reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES);
-      for (int i = tid; i < C::STAGE_BYTES / 16; i += kConvThreads) p[i] = make_uint4(0, 0, 0, 0);
-    }
-    tc::fence_proxy_async_smem();
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *s_tmem;
-
-  uint32_t g = 0;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    int k = 0;
-    while (s_pref[k + 1] <= item) ++k;
-    const int p0 = pptr[k] + (item - s_pref[k]) * chunk;
-    const int p1 = min(pptr[k + 1], p0 + chunk);
-    const int n_iter = (p1 - p0 + C::PK - 1) / C::PK;
-
-    auto load_stage = [&](int it, uint32_t gi) {
-      const int stage = gi % C::STAGES;
-      const uint32_t a_s = smem_base + stage * C::STAGE_BYTES;
-      const uint32_t b_s = a_s + C::A_BYTES;
-      const int q0 = p0 + it * C::PK;
-      constexpr int CA = COUT / 8, CB = CIN / 8;
-#pragma unroll
-      for (int e = tid; e < C::PK * CA; e += kConvThreads) {
-        const int kk = e / CA, j = e % CA;
-        const int q = q0 + kk;
-        const bool ok = q < p1;
-        const int uo = ok ? __ldg(pout + q) : 0;
-        tc::cp_async16(a_s + mnmajor_off(j, kk), gy + (int64_t)uo * COUT + j * 8, ok ? 16 : 0);
-      }
-#pragma unroll
-      for (int e = tid; e < C::PK * CB; e += kConvThreads) {
-        const int kk = e / CB, j = e % CB;
-        const int q = q0 + kk;
-        const bool ok = q < p1;
-        const int vi = ok ? __ldg(pin + q) : 0;
-        tc::cp_async16(b_s + mnmajor_off(j, kk), x + (int64_t)vi * CIN + j * 8, ok ? 16 : 0);
-      }
-    };
-
-    for (int p = 0; p < C::STAGES - 1; ++p) {
-      if (p < n_iter) {
-        const uint32_t gi = g + p;
-        if (gi >= (uint32_t)C::STAGES) tc::mbar_wait(&mbar[gi % C::STAGES], ((gi / C::STAGES) - 1) & 1);
-        load_stage(p, gi);
-      }
-      tc::cp_async_commit();
-    }
-    for (int it = 0; it < n_iter; ++it) {
-      const int nxt = it + C::STAGES - 1;
-      if (nxt < n_iter) {
-        const uint32_t gi = g + nxt;
-        if (gi >= (uint32_t)C::STAGES) tc::mbar_wait(&mbar[gi % C::STAGES], ((gi / C::STAGES) - 1) & 1);
-        load_stage(nxt, gi);
-      }
-      tc::cp_async_commit();
-      tc::cp_async_wait<C::STAGES - 1>();
-      tc::fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        tc::tc_fence_after();
-        const uint32_t gi = g + it;
-        const int stage = gi % C::STAGES;
-        const uint32_t a_s = smem_base + stage * C::STAGE_BYTES;
-        const uint32_t b_s = a_s + C::A_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < C::PK / 16; ++kk) {
-          const uint64_t bd = tc::smem_desc(b_s + kk * 2048, C::LBO, C::SBO, tc::kSwizzle128);
-#pragma unroll
-          for (int mt = 0; mt < C::MT; ++mt) {
-            const uint64_t ad = tc::smem_desc(a_s + mt * 2 * C::LBO + kk * 2048, C::LBO, C::SBO, tc::kSwizzle128);
-            tc::mma_bf16(tmem + mt * C::N, ad, bd, C::IDESC, (it > 0 || kk > 0) ? 1u : 0u);
-          }
-        }
-        tc::mma_commit(&mbar[stage]);
-      }
-    }
-    if (n_iter > 0) {
-      const uint32_t gl = g + n_iter - 1;
-      tc::mbar_wait(&mbar[gl % C::STAGES], (gl / C::STAGES) & 1);
-      tc::tc_fence_after();
-    }
-    g += n_iter;
-    float* dst = part + (int64_t)item * COUT * CIN;
-#pragma unroll 1
-    for (int mt = 0; mt < C::MT; ++mt) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < CIN; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + mt * C::N + c0, v);
-        int m;
-        bool ok;
-        if (C::M == 128) {
-          m = mt * 128 + warp * 32 + lane;
-          ok = true;
-        } else {  // M=64: row r lives in TMEM lane (r%16) + 32*(r/16)
-          m = warp * 16 + lane;
-          ok = lane < 16;
-        }
-        ok = ok && m < COUT;
-        if (ok) {
-          float4* d = reinterpret_cast<float4*>(dst + (int64_t)m * CIN + c0);
-          if (n_iter == 0) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) d[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          }
-        }
-      }
-    }
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-  }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, C::TMEM_COLS);
-}
 
 // sum the chunk partials of each offset in chunk order (deterministic)
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, const int32_t* __restrict__ pptr,
@@ -516,96 +141,148 @@ __global__ void cast_kernel(const void* __restrict__ src, int sd, void* __restri
     stf(dst, dd, i, ldf(src, sd, i));
 }
 
-// ------------------------------------------------------------------ dispatch
-static bool tc_width(int64_t c) { return c == 32 || c == 64 || c == 128 || c == 256; }
-
-template <int CIN, int COUT>
-static int launch_fwd_tc(const bf16* x, const bf16* w, int K, const int32_t* table, int flip,
-                         const int32_t* n_out_dev, int64_t cap_out, void* y, int y_dtype, cudaStream_t st) {
-  using C = FwdCfg<CIN, COUT>;
-  auto kern = conv_fwd_tc_kernel<CIN, COUT>;
-  static int occ = -1;  // immutable per-instantiation occupancy cache
-  if (occ < 0) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kConvThreads, C::SMEM);
-    occ = std::max(1, std::min(o, 512 / C::TMEM_COLS));
+// Small C_in (the occupancy stem, C_in = 1): thread per output row, weights
+// broadcast from shared memory as [K][C_in][C_out], 32 outputs per pass.
+__global__ void __launch_bounds__(128)
+conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* __restrict__ w, int w_dtype,
+                      int cout, int K, const int32_t* __restrict__ table, int flip, const int32_t* n_out_dev,
+                      int64_t cap_out, void* __restrict__ y, int y_dtype) {
+  extern __shared__ float s_w[];  // [K][cin][cout]
+  for (int e = threadIdx.x; e < K * cin * cout; e += blockDim.x) {
+    const int k = e / (cin * cout), r = e - k * cin * cout, ci = r / cout, co = r - ci * cout;
+    s_w[e] = ldf(w, w_dtype, ((int64_t)k * cout + co) * cin + ci);
   }
-  const int64_t tiles = ceil_div(cap_out, kTileM);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)kNumSMs * occ));
-  kern<<<grid, kConvThreads, C::SMEM, st>>>(x, w, K, table, flip, n_out_dev, cap_out, y, y_dtype);
-  VP_CHECK_LAUNCH("conv_fwd_tc");
+  __syncthreads();
+  const int n_out = load_count(n_out_dev, cap_out);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_out; u += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* trow = table + u * K;
+    for (int c0 = 0; c0 < cout; c0 += 32) {
+      float acc[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+      for (int k = 0; k < K; ++k) {
+        const int v = __ldg(trow + (flip ? K - 1 - k : k));
+        if (v < 0) continue;
+        for (int ci = 0; ci < cin; ++ci) {
+          const float xv = ldf(x, x_dtype, (int64_t)v * cin + ci);
+          const float* wr = s_w + (k * cin + ci) * cout + c0;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] += (c0 + c < cout) ? wr[c] * xv : 0.f;
+        }
+      }
+      for (int c = 0; c < 32 && c0 + c < cout; ++c) stf(y, y_dtype, u * cout + c0 + c, acc[c]);
+    }
+  }
+}
+
+static bool small_fwd_ok(int64_t cin, int64_t cout, int K) { return cin <= 4 && (int64_t)K * cin * cout <= 12288; }
+
+static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int wd, int cout, int K,
+                            const int32_t* table, int flip, const int32_t* n_out_dev, int64_t cap_out, void* y, int yd,
+                            cudaStream_t st) {
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), kNumSMs * 8));
+  conv_fwd_small_kernel<<<blocks, 128, (size_t)K * cin * cout * 4, st>>>(x, xd, cin, w, wd, cout, K, table, flip,
+                                                                         n_out_dev, cap_out, y, yd);
+  VP_CHECK_LAUNCH("conv_fwd_small");
   return VP_OK;
 }
 
-template <int CIN>
-static int fwd_tc_cout(int64_t cout, const bf16* x, const bf16* w, int K, const int32_t* table, int flip,
-                       const int32_t* n, int64_t cap, void* y, int yd, cudaStream_t st) {
-  switch (cout) {
-    case 32: return launch_fwd_tc<CIN, 32>(x, w, K, table, flip, n, cap, y, yd, st);
-    case 64: return launch_fwd_tc<CIN, 64>(x, w, K, table, flip, n, cap, y, yd, st);
-    case 128: return launch_fwd_tc<CIN, 128>(x, w, K, table, flip, n, cap, y, yd, st);
-    case 256: return launch_fwd_tc<CIN, 256>(x, w, K, table, flip, n, cap, y, yd, st);
+// ------------------------------------------------------------------ dispatch
+static bool tc_width(int64_t c) { return c == 32 || c == 64 || c == 128 || c == 256; }
+
+constexpr int kMaxSplit = 8;
+
+template <int KD, int ND, bool BMN>
+static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
+  using C = FwdTC<KD, ND, BMN>;
+  auto kern = conv_tc_kernel<KD, ND, BMN>;
+  static bool attr = false;  // immutable per-instantiation attribute cache
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  const int64_t tiles = ceil_div(p0.cap_out, 128);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * kMaxSplit, kNumSMs));
+  FwdParams p = p0;
+  p.part = (float*)part;
+  p.max_split = part ? kMaxSplit : 1;
+  kern<<<grid, kTcThreads, C::SMEM, st>>>(p);
+  VP_CHECK_LAUNCH("conv_tc");
+  if (part) {
+    const int64_t work = p.cap_out * ND / 4;
+    split_reduce_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), kNumSMs * 8)), 256, 0, st>>>(
+        (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.y, p.y_dtype);
+    VP_CHECK_LAUNCH("split_reduce");
+  }
+  return VP_OK;
+}
+
+template <int KD, bool BMN>
+static int conv_tc_nd(int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
+  switch (nd) {
+    case 32: return launch_conv_tc<KD, 32, BMN>(p, part, st);
+    case 64: return launch_conv_tc<KD, 64, BMN>(p, part, st);
+    case 128: return launch_conv_tc<KD, 128, BMN>(p, part, st);
+    case 256: return launch_conv_tc<KD, 256, BMN>(p, part, st);
   }
   return VP_EINTERNAL;
 }
 
-static int fwd_tc(int64_t cin, int64_t cout, const bf16* x, const bf16* w, int K, const int32_t* table,
-                  int flip, const int32_t* n, int64_t cap, void* y, int yd, cudaStream_t st) {
-  switch (cin) {
-    case 32: return fwd_tc_cout<32>(cout, x, w, K, table, flip, n, cap, y, yd, st);
-    case 64: return fwd_tc_cout<64>(cout, x, w, K, table, flip, n, cap, y, yd, st);
-    case 128: return fwd_tc_cout<128>(cout, x, w, K, table, flip, n, cap, y, yd, st);
-    case 256: return fwd_tc_cout<256>(cout, x, w, K, table, flip, n, cap, y, yd, st);
+template <bool BMN>
+static int conv_tc(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
+  switch (kd) {
+    case 32: return conv_tc_nd<32, BMN>(nd, p, part, st);
+    case 64: return conv_tc_nd<64, BMN>(nd, p, part, st);
+    case 128: return conv_tc_nd<128, BMN>(nd, p, part, st);
+    case 256: return conv_tc_nd<256, BMN>(nd, p, part, st);
   }
   return VP_EINTERNAL;
 }
+
+static size_t split_ws_bytes(int64_t nd) { return align_up((size_t)kNumSMs * 128 * nd * 4, 256); }
 
 template <int CIN, int COUT>
-static int launch_wg_tc(const bf16* x, const bf16* gy, int K, const int32_t* pin, const int32_t* pout,
-                        const int32_t* pptr, int chunk, int max_items, float* part, cudaStream_t st) {
-  using C = WgCfg<CIN, COUT>;
+static int launch_wg_tc(const WgParams& p, int max_items, cudaStream_t st) {
+  using C = WgTC<CIN, COUT>;
   auto kern = conv_wgrad_tc_kernel<CIN, COUT>;
-  static int occ = -1;
-  if (occ < 0) {
+  static bool attr = false;
+  if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kConvThreads, C::SMEM);
-    occ = std::max(1, std::min(o, 512 / C::TMEM_COLS));
+    attr = true;
   }
-  const int grid = std::max(1, std::min(max_items, kNumSMs * occ));
-  kern<<<grid, kConvThreads, C::SMEM, st>>>(x, gy, K, pin, pout, pptr, chunk, part);
+  const int grid = std::max(1, std::min(max_items, kNumSMs));
+  kern<<<grid, kTcThreads, C::SMEM, st>>>(p);
   VP_CHECK_LAUNCH("conv_wgrad_tc");
   return VP_OK;
 }
 
 template <int CIN>
-static int wg_tc_cout(int64_t cout, const bf16* x, const bf16* gy, int K, const int32_t* pin,
-                      const int32_t* pout, const int32_t* pptr, int chunk, int mi, float* part, cudaStream_t st) {
+static int wg_tc_cout(int64_t cout, const WgParams& p, int mi, cudaStream_t st) {
   switch (cout) {
-    case 32: return launch_wg_tc<CIN, 32>(x, gy, K, pin, pout, pptr, chunk, mi, part, st);
-    case 64: return launch_wg_tc<CIN, 64>(x, gy, K, pin, pout, pptr, chunk, mi, part, st);
-    case 128: return launch_wg_tc<CIN, 128>(x, gy, K, pin, pout, pptr, chunk, mi, part, st);
-    case 256: return launch_wg_tc<CIN, 256>(x, gy, K, pin, pout, pptr, chunk, mi, part, st);
+    case 32: return launch_wg_tc<CIN, 32>(p, mi, st);
+    case 64: return launch_wg_tc<CIN, 64>(p, mi, st);
+    case 128: return launch_wg_tc<CIN, 128>(p, mi, st);
+    case 256: return launch_wg_tc<CIN, 256>(p, mi, st);
   }
   return VP_EINTERNAL;
 }
 
-static int wg_tc(int64_t cin, int64_t cout, const bf16* x, const bf16* gy, int K, const int32_t* pin,
-                 const int32_t* pout, const int32_t* pptr, int chunk, int mi, float* part, cudaStream_t st) {
+static int wg_tc(int64_t cin, int64_t cout, const WgParams& p, int mi, cudaStream_t st) {
   switch (cin) {
-    case 32: return wg_tc_cout<32>(cout, x, gy, K, pin, pout, pptr, chunk, mi, part, st);
-    case 64: return wg_tc_cout<64>(cout, x, gy, K, pin, pout, pptr, chunk, mi, part, st);
-    case 128: return wg_tc_cout<128>(cout, x, gy, K, pin, pout, pptr, chunk, mi, part, st);
-    case 256: return wg_tc_cout<256>(cout, x, gy, K, pin, pout, pptr, chunk, mi, part, st);
+    case 32: return wg_tc_cout<32>(cout, p, mi, st);
+    case 64: return wg_tc_cout<64>(cout, p, mi, st);
+    case 128: return wg_tc_cout<128>(cout, p, mi, st);
+    case 256: return wg_tc_cout<256>(cout, p, mi, st);
   }
   return VP_EINTERNAL;
 }
 
-static int wgrad_chunk(int64_t cin, int64_t cout) {
-  (void)cin;
-  (void)cout;
-  return 1024;  // pairs per partial (fixed: results independent of timing)
+// pairs per work item: ~2 items per SM at the pair capacity, multiple of 64,
+// depends only on static capacities -> results independent of timing
+static int wgrad_chunk(int64_t cap_pairs) {
+  int64_t c = ceil_div(std::max<int64_t>(cap_pairs, 1), 2 * kNumSMs);
+  c = ceil_div(c, 64) * 64;
+  return (int)std::min<int64_t>(std::max<int64_t>(c, 256), kWgMaxChunk);
 }
 
 }  // namespace vp
@@ -615,7 +292,7 @@ using namespace vp;
 extern "C" {
 
 size_t vp_conv_fwd_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
-  return align_up((size_t)K * cin * cout * 2, 256);
+  return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cout);
 }
 
 int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t cin, const void* w, int32_t w_dtype, int64_t cout,
@@ -627,17 +304,20 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t cin, const void* w, int3
   VP_REQUIRE(y_dtype == VP_F32 || y_dtype == VP_BF16, VP_EVALIDATION, "output dtype must be f32 or bf16");
   if (cap_out <= 0) return VP_OK;
   if (x_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
+    VP_REQUIRE(ws && ws_bytes >= vp_conv_fwd_ws_bytes(cin, cout, K), VP_EVALIDATION, "conv_fwd: workspace too small");
     const bf16* wb = (const bf16*)w;
+    char* part = (char*)ws + align_up((size_t)K * cin * cout * 2, 256);
     if (w_dtype != VP_BF16) {
-      VP_REQUIRE(ws && ws_bytes >= vp_conv_fwd_ws_bytes(cin, cout, K), VP_EVALIDATION,
-                 "conv_fwd: workspace too small for weight conversion");
       int64_t cnt = (int64_t)K * cin * cout;
       cast_kernel<<<(int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st>>>(w, w_dtype, ws, VP_BF16, cnt);
       VP_CHECK_LAUNCH("conv_fwd: cast w");
       wb = (const bf16*)ws;
     }
-    return fwd_tc(cin, cout, (const bf16*)x, wb, K, table, flip, n_out_dev, cap_out, y, y_dtype, st);
+    FwdParams p{(const bf16*)x, wb, K, table, flip, n_out_dev, cap_out, y, y_dtype, nullptr, 1};
+    return conv_tc<false>(cin, cout, p, part, st);
   }
+  if (small_fwd_ok(cin, cout, K)) return launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip,
+                                                          n_out_dev, cap_out, y, y_dtype, st);
   const int64_t total = cap_out * cout;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
   conv_fwd_simt_kernel<<<blocks, 256, 0, st>>>(x, x_dtype, (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout,
@@ -647,7 +327,7 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t cin, const void* w, int3
 }
 
 size_t vp_conv_dgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
-  return align_up((size_t)K * cin * cout * 2, 256);
+  return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cin);
 }
 
 int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t cout, const void* w, int32_t w_dtype, int64_t cin,
@@ -659,12 +339,17 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t cout, const void* w, i
   if (g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
     VP_REQUIRE(ws && ws_bytes >= vp_conv_dgrad_ws_bytes(cin, cout, K), VP_EVALIDATION,
                "conv_dgrad: workspace too small");
-    int64_t cnt = (int64_t)K * cin * cout;
-    transpose_w_kernel<<<(int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st>>>(w, w_dtype, K, (int)cout,
-                                                                                       (int)cin, (bf16*)ws);
-    VP_CHECK_LAUNCH("conv_dgrad: transpose w");
-    // grad_in = sum_k (W_k^T) g[table] : a forward conv with C_in'=cout, C_out'=cin
-    return fwd_tc(cout, cin, (const bf16*)g, (const bf16*)ws, K, table, flip, n_in_dev, cap_in, gi, gi_dtype, st);
+    const bf16* wb = (const bf16*)w;
+    char* part = (char*)ws + align_up((size_t)K * cin * cout * 2, 256);
+    if (w_dtype != VP_BF16) {
+      int64_t cnt = (int64_t)K * cin * cout;
+      cast_kernel<<<(int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st>>>(w, w_dtype, ws, VP_BF16, cnt);
+      VP_CHECK_LAUNCH("conv_dgrad: cast w");
+      wb = (const bf16*)ws;
+    }
+    // grad_in = sum_k W_k^T g[table]: GEMM K-dim = C_out, N = C_in, W read as MN-major B
+    FwdParams p{(const bf16*)g, wb, K, table, flip, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1};
+    return conv_tc<true>(cout, cin, p, part, st);
   }
   const int64_t total = cap_in * cin;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
@@ -676,9 +361,9 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t cout, const void* w, i
 }
 
 size_t vp_conv_wgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K, int64_t cap_pairs) {
-  const int chunk = wgrad_chunk(cin, cout);
+  const int chunk = wgrad_chunk(cap_pairs);
   const int64_t items = cap_pairs / chunk + K + 1;
-  return align_up((size_t)items * cin * cout * 4, 256);
+  return align_up((size_t)items * cin * cout * 4, 256) + align_up((size_t)(K + 1) * 4, 256);
 }
 
 int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
@@ -688,18 +373,21 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(ws && ws_bytes >= vp_conv_wgrad_ws_bytes(cin, cout, K, cap_pairs), VP_EVALIDATION,
              "conv_wgrad: workspace too small");
-  const int chunk = wgrad_chunk(cin, cout);
+  const int chunk = wgrad_chunk(cap_pairs);
   const int max_items = (int)(cap_pairs / chunk + K + 1);
   float* part = (float*)ws;
-  if (x_dtype == VP_BF16 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout) && K <= 125) {
-    int r = wg_tc(cin, cout, (const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, max_items, part, st);
-    if (r) return r;
-  } else {
-    const int grid = std::max(1, std::min(max_items, kNumSMs * 8));
-    wgrad_simt_kernel<<<grid, kWgSimtThreads, 0, st>>>(x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
-                                                       pptr, chunk, part);
-    VP_CHECK_LAUNCH("conv_wgrad_simt");
+  int32_t* ticket = (int32_t*)((char*)ws + align_up((size_t)max_items * cin * cout * 4, 256));
+  if (x_dtype == VP_BF16 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
+    cudaMemsetAsync(gw, 0, sizeof(float) * K * cin * cout, st);
+    cudaMemsetAsync(ticket, 0, sizeof(int32_t) * K, st);
+    VP_CHECK_ASYNC("conv_wgrad: memset");
+    WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, gw, part, ticket};
+    return wg_tc(cin, cout, p, max_items, st);
   }
+  const int grid = std::max(1, std::min(max_items, kNumSMs * 8));
+  wgrad_simt_kernel<<<grid, kWgSimtThreads, 0, st>>>(x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
+                                                     pptr, chunk, part);
+  VP_CHECK_LAUNCH("conv_wgrad_simt");
   const int64_t total = (int64_t)K * cin * cout;
   wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st>>>(
       part, pptr, K, chunk, cin * cout, gw);

@@ -8,122 +8,255 @@
 
 namespace vp {
 
-constexpr int kRowsPerBlock = 512;
 constexpr int kGlueThreads = 256;
 
-// Per-block per-channel partial sums. Thread layout: channel c = tid % C_eff,
-// row lane r = tid / C_eff (C_eff = min(C, 256); channels beyond loop).
+// 8-wide (16 B for bf16) vector access; VEC == 1 is the scalar fallback for
+// channel counts that are not a multiple of 8.
+template <int VEC>
+__device__ __forceinline__ void ldv(const void* p, int dtype, int64_t i, float* v) {
+  if (VEC == 8 && dtype == VP_BF16) {
+    uint4 raw = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p) + i);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float2 f = __bfloat1622float2(h[q]);
+      v[2 * q] = f.x;
+      v[2 * q + 1] = f.y;
+    }
+  } else if (VEC == 8 && dtype == VP_F32) {
+    const float4* f = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p) + i);
+    float4 a = f[0], b = f[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) v[q] = ldf(p, dtype, i + q);
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void stv(void* p, int dtype, int64_t i, const float* v) {
+  if (VEC == 8 && dtype == VP_BF16) {
+    uint4 raw;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) h[q] = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p) + i) = raw;
+  } else if (VEC == 8 && dtype == VP_F32) {
+    float4* f = reinterpret_cast<float4*>(reinterpret_cast<float*>(p) + i);
+    f[0] = make_float4(v[0], v[1], v[2], v[3]);
+    f[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) stf(p, dtype, i + q, v[q]);
+  }
+}
+
+// Per-block per-channel partial sums over `rpb` rows.  Thread layout: tpr =
+// C/VEC threads cover one row (VEC channels each), lanes = 256/tpr rows in
+// flight.  stats mode (gy == null): (sum x, sum x^2); backward mode:
+// (sum g, sum g*xhat) with g = (gy [+ gy2]) masked by (y > 0) when relu.
+template <int VEC>
 __global__ void __launch_bounds__(kGlueThreads)
 bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int64_t cap, int C,
                   const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype,
                   const void* __restrict__ y, int y_dtype, int relu, const float* __restrict__ mean,
                   const float* __restrict__ rstd, float* __restrict__ part /*[blocks][2][C]*/) {
-  __shared__ float s_a[kGlueThreads], s_b[kGlueThreads];
+  __shared__ float s_a[kGlueThreads * VEC], s_b[kGlueThreads * VEC];
   const int n = load_count(n_dev, cap);
-  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
-  const int64_t r1 = (r0 + kRowsPerBlock < (int64_t)n) ? r0 + kRowsPerBlock : (int64_t)n;
-  const int ceff = C < kGlueThreads ? C : kGlueThreads;
-  const int lanes = kGlueThreads / ceff;
-  const int tc = threadIdx.x % ceff, tr = threadIdx.x / ceff;
-  for (int c0 = 0; c0 < C; c0 += ceff) {
-    const int c = c0 + tc;
-    float a = 0.f, b = 0.f;
-    if (tr < lanes && c < C) {
-      if (gy == nullptr) {  // stats: sum x, sum x^2
-        for (int64_t r = r0 + tr; r < r1; r += lanes) {
-          float v = ldf(x, dtype, r * C + c);
-          a += v;
-          b += v * v;
+  const int tpr = C / VEC;
+  const int lanes = kGlueThreads / tpr;
+  const int cv = threadIdx.x % tpr, lr = threadIdx.x / tpr;
+  const int c0 = cv * VEC;
+  float a[VEC], b[VEC], mu[VEC], rs[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) a[q] = b[q] = 0.f;
+  if (lr < lanes) {
+    if (gy == nullptr) {
+      // block b owns row groups b, b+G, b+2G, ... (G = gridDim.x, fixed per
+      // capacity) -> balanced for any live n, fixed summation order
+#pragma unroll 4
+      for (int64_t r = (int64_t)blockIdx.x * lanes + lr; r < n; r += (int64_t)gridDim.x * lanes) {
+        float v[VEC];
+        ldv<VEC>(x, dtype, r * C + c0, v);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          a[q] += v[q];
+          b[q] += v[q] * v[q];
         }
-      } else {  // backward: sum gy', sum gy' * xhat
-        const float mu = mean[c], rs = rstd[c];
-        for (int64_t r = r0 + tr; r < r1; r += lanes) {
-          float g = ldf(gy, gy_dtype, r * C + c);
-          if (gy2) g += ldf(gy2, gy_dtype, r * C + c);
-          if (relu && ldf(y, y_dtype, r * C + c) <= 0.f) g = 0.f;
-          float xh = (ldf(x, dtype, r * C + c) - mu) * rs;
-          a += g;
-          b += g * xh;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        mu[q] = mean[c0 + q];
+        rs[q] = rstd[c0 + q];
+      }
+#pragma unroll 2
+      for (int64_t r = (int64_t)blockIdx.x * lanes + lr; r < n; r += (int64_t)gridDim.x * lanes) {
+        float g[VEC], g2[VEC], yy[VEC], xv[VEC];
+        ldv<VEC>(gy, gy_dtype, r * C + c0, g);
+        if (gy2) {
+          ldv<VEC>(gy2, gy_dtype, r * C + c0, g2);
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) g[q] += g2[q];
+        }
+        if (relu) ldv<VEC>(y, y_dtype, r * C + c0, yy);
+        ldv<VEC>(x, dtype, r * C + c0, xv);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          float gq = (relu && yy[q] <= 0.f) ? 0.f : g[q];
+          a[q] += gq;
+          b[q] += gq * (xv[q] - mu[q]) * rs[q];
         }
       }
     }
-    s_a[threadIdx.x] = a;
-    s_b[threadIdx.x] = b;
-    __syncthreads();
-    if (tr == 0 && c < C) {
-      float sa = 0.f, sb = 0.f;
-      for (int l = 0; l < lanes; ++l) {
-        sa += s_a[l * ceff + tc];
-        sb += s_b[l * ceff + tc];
-      }
-      part[((int64_t)blockIdx.x * 2) * C + c] = sa;
-      part[((int64_t)blockIdx.x * 2 + 1) * C + c] = sb;
+  }
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) {
+    s_a[threadIdx.x * VEC + q] = a[q];
+    s_b[threadIdx.x * VEC + q] = b[q];
+  }
+  __syncthreads();
+  // fixed-order reduction over the row lanes: thread (cv, q) sums lanes 0..lanes-1
+  for (int e = threadIdx.x; e < C; e += kGlueThreads) {
+    const int ecv = e / VEC, q = e % VEC;
+    float sa = 0.f, sb = 0.f;
+    for (int l = 0; l < lanes; ++l) {
+      sa += s_a[(l * tpr + ecv) * VEC + q];
+      sb += s_b[(l * tpr + ecv) * VEC + q];
     }
-    __syncthreads();
+    part[((int64_t)blockIdx.x * 2) * C + e] = sa;
+    part[((int64_t)blockIdx.x * 2 + 1) * C + e] = sb;
   }
 }
 
-// Ordered sum over the blocks' partials (f64); block per channel chunk.
-__global__ void bn_finalize_kernel(const float* __restrict__ part, int nblocks_cap, const int32_t* n_dev,
-                                   int64_t cap, int C, float eps, float* out_a, float* out_b, int mode) {
+// One warp per channel: lane-strided f64 sum over the blocks' partials, then
+// a fixed xor-shuffle tree -> deterministic.
+__global__ void bn_finalize_kernel(const float* __restrict__ part, const int32_t* n_dev, int64_t cap, int C,
+                                   int nb, float eps, float* out_a, float* out_b, int mode) {
   const int n = load_count(n_dev, cap);
-  const int nb = (int)((n + kRowsPerBlock - 1) / kRowsPerBlock);
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    double sa = 0.0, sb = 0.0;
-    for (int b = 0; b < nb; ++b) {
-      sa += part[((int64_t)b * 2) * C + c];
-      sb += part[((int64_t)b * 2 + 1) * C + c];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= C) return;
+  const int c = warp;
+  // 4 independent accumulator chains (loads in flight), combined in a fixed order
+  double sa4[4] = {0.0, 0.0, 0.0, 0.0}, sb4[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int b0 = lane; b0 < nb; b0 += 128) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int b = b0 + 32 * q;
+      if (b < nb) {
+        sa4[q] += part[((int64_t)b * 2) * C + c];
+        sb4[q] += part[((int64_t)b * 2 + 1) * C + c];
+      }
     }
-    if (mode == 0) {  // mean, rstd (biased variance, as in training-mode BN)
+  }
+  double sa = (sa4[0] + sa4[1]) + (sa4[2] + sa4[3]);
+  double sb = (sb4[0] + sb4[1]) + (sb4[2] + sb4[3]);
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  if (lane == 0) {
+    if (mode == 0) {  // mean, rstd (biased variance, training-mode BN)
       double mu = n > 0 ? sa / n : 0.0;
       double var = n > 0 ? sb / n - mu * mu : 0.0;
       if (var < 0) var = 0;
       out_a[c] = (float)mu;
       out_b[c] = (float)(1.0 / sqrt(var + (double)eps));
-    } else {  // gbeta, ggamma
-      out_a[c] = (float)sb;  // ggamma = sum gy' xhat
-      out_b[c] = (float)sa;  // gbeta  = sum gy'
+    } else {  // ggamma = sum g*xhat, gbeta = sum g
+      out_a[c] = (float)sb;
+      out_b[c] = (float)sa;
     }
   }
 }
 
-__global__ void bn_apply_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int64_t cap, int C,
-                                const float* __restrict__ mean, const float* __restrict__ rstd,
-                                const float* __restrict__ gamma, const float* __restrict__ beta,
-                                const void* __restrict__ res, int res_dtype, int relu, void* __restrict__ y,
-                                int y_dtype) {
+template <int VEC>
+__global__ void __launch_bounds__(kGlueThreads)
+bn_apply_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int64_t cap, int C,
+                const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
+                const float* __restrict__ beta, const void* __restrict__ res, int res_dtype, int relu,
+                void* __restrict__ y, int y_dtype) {
   const int n = load_count(n_dev, cap);
-  const int64_t total = (int64_t)n * C;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % C);
-    float v = (ldf(x, dtype, e) - mean[c]) * rstd[c] * gamma[c] + beta[c];
-    if (res) v += ldf(res, res_dtype, e);
-    if (relu) v = fmaxf(v, 0.f);
-    stf(y, y_dtype, e, v);
+  const int tpr = C / VEC, lanes = kGlueThreads / tpr;
+  const int cv = threadIdx.x % tpr, lr = threadIdx.x / tpr;
+  if (lr >= lanes) return;
+  const int c0 = cv * VEC;
+  float sc[VEC], sh[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) {
+    sc[q] = rstd[c0 + q] * gamma[c0 + q];
+    sh[q] = beta[c0 + q] - mean[c0 + q] * sc[q];
+  }
+  for (int64_t r = (int64_t)blockIdx.x * lanes + lr; r < n; r += (int64_t)gridDim.x * lanes) {
+    float v[VEC], rv[VEC];
+    ldv<VEC>(x, dtype, r * C + c0, v);
+    if (res) ldv<VEC>(res, res_dtype, r * C + c0, rv);
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      float o = v[q] * sc[q] + sh[q];
+      if (res) o += rv[q];
+      v[q] = relu ? fmaxf(o, 0.f) : o;
+    }
+    stv<VEC>(y, y_dtype, r * C + c0, v);
   }
 }
 
-__global__ void bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype, const void* __restrict__ y,
-                                         int y_dtype, const void* __restrict__ x, int x_dtype, const int32_t* n_dev,
-                                         int64_t cap, int C, const float* __restrict__ mean,
-                                         const float* __restrict__ rstd, const float* __restrict__ gamma,
-                                         int relu, const float* __restrict__ ggamma, const float* __restrict__ gbeta,
-                                         void* __restrict__ gx, int gx_dtype, void* __restrict__ gres) {
+template <int VEC>
+__global__ void __launch_bounds__(kGlueThreads)
+bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype,
+                         const void* __restrict__ y, int y_dtype, const void* __restrict__ x, int x_dtype,
+                         const int32_t* n_dev, int64_t cap, int C, const float* __restrict__ mean,
+                         const float* __restrict__ rstd, const float* __restrict__ gamma, int relu,
+                         const float* __restrict__ ggamma, const float* __restrict__ gbeta, void* __restrict__ gx,
+                         int gx_dtype, void* __restrict__ gres) {
   const int n = load_count(n_dev, cap);
-  const int64_t total = (int64_t)n * C;
+  const int tpr = C / VEC, lanes = kGlueThreads / tpr;
+  const int cv = threadIdx.x % tpr, lr = threadIdx.x / tpr;
+  if (lr >= lanes) return;
+  const int c0 = cv * VEC;
   const float inv_n = n > 0 ? 1.f / (float)n : 0.f;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % C);
-    float g = ldf(gy, gy_dtype, e);
-    if (gy2) g += ldf(gy2, gy_dtype, e);
-    if (relu && ldf(y, y_dtype, e) <= 0.f) g = 0.f;
-    const float xh = (ldf(x, x_dtype, e) - mean[c]) * rstd[c];
-    const float v = gamma[c] * rstd[c] * (g - inv_n * gbeta[c] - xh * inv_n * ggamma[c]);
-    stf(gx, gx_dtype, e, v);
-    if (gres) stf(gres, gx_dtype, e, g);
+  float k1[VEC], k2[VEC], k3[VEC], mu[VEC], rs[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) {
+    const int c = c0 + q;
+    mu[q] = mean[c];
+    rs[q] = rstd[c];
+    k1[q] = gamma[c] * rs[q];         // gx = k1*(g - gbeta/n - xhat*ggamma/n)
+    k2[q] = inv_n * gbeta[c];
+    k3[q] = inv_n * ggamma[c];
   }
+  for (int64_t r = (int64_t)blockIdx.x * lanes + lr; r < n; r += (int64_t)gridDim.x * lanes) {
+    float g[VEC], g2[VEC], yy[VEC], xv[VEC];
+    ldv<VEC>(gy, gy_dtype, r * C + c0, g);
+    if (gy2) {
+      ldv<VEC>(gy2, gy_dtype, r * C + c0, g2);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) g[q] += g2[q];
+    }
+    if (relu) ldv<VEC>(y, y_dtype, r * C + c0, yy);
+    ldv<VEC>(x, x_dtype, r * C + c0, xv);
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      if (relu && yy[q] <= 0.f) g[q] = 0.f;
+      const float xh = (xv[q] - mu[q]) * rs[q];
+      xv[q] = k1[q] * (g[q] - k2[q] - xh * k3[q]);
+    }
+    stv<VEC>(gx, gx_dtype, r * C + c0, xv);
+    if (gres) stv<VEC>(gres, gx_dtype, r * C + c0, g);
+  }
+}
+
+// number of partial blocks: <= 4 per SM, no more than there are row groups
+static int bn_partial_blocks(int64_t cap, int64_t C) {
+  const int vec = (C % 8 == 0) ? 8 : 1;
+  const int lanes = std::max<int>(1, kGlueThreads / (int)(C / vec));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(cap, 1), lanes), kNumSMs * 2));
+}
+
+static bool bn_shape_ok(int64_t C) { return (C % 8 == 0 && C / 8 <= kGlueThreads) || C <= kGlueThreads; }
+
+static int bn_grid_rows(int64_t cap, int64_t C) {
+  const int vec = (C % 8 == 0) ? 8 : 1;
+  const int lanes = std::max<int>(1, kGlueThreads / (int)(C / vec));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(cap, 1), lanes), kNumSMs * 8));
 }
 
 // ------------------------------------------------------------------ pooling
@@ -262,19 +395,24 @@ using namespace vp;
 extern "C" {
 
 size_t vp_bn_stats_ws_bytes(int64_t cap_n, int64_t C) {
-  return align_up((size_t)std::max<int64_t>(1, ceil_div(cap_n, kRowsPerBlock)) * 2 * C * 4, 256);
+  return align_up((size_t)bn_partial_blocks(cap_n, C) * 2 * C * 4, 256);
 }
 
 int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, int64_t C, float eps, float* mean,
                 float* rstd, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   VP_REQUIRE(ws_bytes >= vp_bn_stats_ws_bytes(cap, C), VP_EVALIDATION, "bn_stats: workspace too small");
-  const int nb = (int)std::max<int64_t>(1, ceil_div(cap, kRowsPerBlock));
-  bn_partial_kernel<<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
-                                                  nullptr, nullptr, (float*)ws);
+  const int nb = bn_partial_blocks(cap, C);
+  if (C % 8 == 0)
+    bn_partial_kernel<8><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
+                                                       nullptr, nullptr, (float*)ws);
+  else
+    bn_partial_kernel<1><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
+                                                       nullptr, nullptr, (float*)ws);
   VP_CHECK_LAUNCH("bn_partial");
-  bn_finalize_kernel<<<(int)ceil_div(C, 128), 128, 0, st>>>((const float*)ws, nb, n_dev, cap, (int)C, eps, mean,
-                                                            rstd, 0);
+  bn_finalize_kernel<<<(int)ceil_div(C * 32, 256), 256, 0, st>>>((const float*)ws, n_dev, cap, (int)C, nb, eps, mean,
+                                                                 rstd, 0);
   VP_CHECK_LAUNCH("bn_finalize");
   return VP_OK;
 }
@@ -282,9 +420,16 @@ int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
 int vp_bn_apply(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, int64_t C, const float* mean,
                 const float* rstd, const float* gamma, const float* beta, const void* res, int32_t rd, int32_t relu,
                 void* y, int32_t yd, vp_stream_t stream) {
+  VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   if (cap <= 0) return VP_OK;
-  bn_apply_kernel<<<grid_for(cap * C), 256, 0, (cudaStream_t)stream>>>(x, xd, n_dev, cap, (int)C, mean, rstd, gamma,
-                                                                      beta, res, rd, relu, y, yd);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = bn_grid_rows(cap, C);
+  if (C % 8 == 0)
+    bn_apply_kernel<8><<<grid, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
+                                                       relu, y, yd);
+  else
+    bn_apply_kernel<1><<<grid, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
+                                                       relu, y, yd);
   VP_CHECK_LAUNCH("bn_apply");
   return VP_OK;
 }
@@ -296,17 +441,27 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
                    const float* gamma, int32_t relu, void* gx, int32_t gxd, void* gres, float* ggamma, float* gbeta,
                    void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   VP_REQUIRE(ws_bytes >= vp_bn_backward_ws_bytes(cap, C), VP_EVALIDATION, "bn_backward: workspace too small");
-  const int nb = (int)std::max<int64_t>(1, ceil_div(cap, kRowsPerBlock));
-  bn_partial_kernel<<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
-                                                  (float*)ws);
+  const int nb = bn_partial_blocks(cap, C);
+  if (C % 8 == 0)
+    bn_partial_kernel<8><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
+                                                       (float*)ws);
+  else
+    bn_partial_kernel<1><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
+                                                       (float*)ws);
   VP_CHECK_LAUNCH("bn_bwd_partial");
-  bn_finalize_kernel<<<(int)ceil_div(C, 128), 128, 0, st>>>((const float*)ws, nb, n_dev, cap, (int)C, 0.f, ggamma,
-                                                            gbeta, 1);
+  bn_finalize_kernel<<<(int)ceil_div(C * 32, 256), 256, 0, st>>>((const float*)ws, n_dev, cap, (int)C, nb, 0.f, ggamma,
+                                                                 gbeta, 1);
   VP_CHECK_LAUNCH("bn_bwd_finalize");
   if (cap > 0) {
-    bn_backward_apply_kernel<<<grid_for(cap * C), 256, 0, st>>>(gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean, rstd,
-                                                                gamma, relu, ggamma, gbeta, gx, gxd, gres);
+    const int grid = bn_grid_rows(cap, C);
+    if (C % 8 == 0)
+      bn_backward_apply_kernel<8><<<grid, kGlueThreads, 0, st>>>(gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
+                                                                  rstd, gamma, relu, ggamma, gbeta, gx, gxd, gres);
+    else
+      bn_backward_apply_kernel<1><<<grid, kGlueThreads, 0, st>>>(gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
+                                                                  rstd, gamma, relu, ggamma, gbeta, gx, gxd, gres);
     VP_CHECK_LAUNCH("bn_bwd_apply");
   }
   return VP_OK;

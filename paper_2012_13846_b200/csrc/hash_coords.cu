@@ -33,6 +33,14 @@ uint64_t hash_cap_for(int64_t n) {
   return cap;
 }
 
+uint64_t hash_cap_internal(int64_t n) {
+  // internal tables (maps, coordinates): load factor <= 1/4 so most probes
+  // resolve in the first 4-slot group (the slot layout is not semantic)
+  uint64_t cap = 8;
+  while (cap < (uint64_t)(4 * n + 4)) cap <<= 1;
+  return cap;
+}
+
 __global__ void hash_clear_kernel(Slot* t, uint64_t cap) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -161,37 +169,44 @@ __global__ void oc_insert_kernel(const int4* __restrict__ in, const int32_t* n_d
 }
 
 constexpr int kCompactBlock = 256;
-constexpr int kCompactItems = 8;  // rows per thread
+constexpr int kCompactItems = 16;  // rows per thread (tile 4096 -> short look-back chains)
 constexpr int kCompactTile = kCompactBlock * kCompactItems;
 
+// first_of[i] = first (minimum) input row whose (downsampled) key equals row
+// i's; one row per thread so every lookup is an independent memory request.
+__global__ void first_of_kernel(const int4* __restrict__ rows, const int32_t* n_dev, int64_t cap_n, int sx, int sy,
+                                int sz, const Slot* __restrict__ t, uint64_t cap, int32_t* __restrict__ first_of) {
+  const int n = load_count(n_dev, cap_n);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 r = rows[i];
+    first_of[i] = hash_find(t, cap, pack_key(r.x, floordiv_mul(r.y, sx), floordiv_mul(r.z, sy), floordiv_mul(r.w, sz)));
+  }
+}
+
+// Ordered compaction of the first-occurrence rows (first_of[i] == i) with a
+// single-pass decoupled look-back scan: out keeps ascending i == first-seen
+// order (conv.py:145-146, tensor.py:138-144).  rank_of_first (nullable)
+// receives each kept row's output position.
 __global__ void __launch_bounds__(kCompactBlock)
-oc_compact_kernel(const int4* __restrict__ in, const int32_t* n_dev, int64_t cap_n, int sx, int sy,
-                  int sz, const Slot* __restrict__ t, uint64_t cap, ScanState ss,
-                  int4* __restrict__ out, int32_t* n_out, int32_t* parent_first) {
+compact_first_kernel(const int4* __restrict__ rows, const int32_t* n_dev, int64_t cap_n, int sx, int sy, int sz,
+                     const int32_t* __restrict__ first_of, ScanState ss, int4* __restrict__ out, int32_t* n_out,
+                     int32_t* rank_of_first) {
   __shared__ int s_tile;
   __shared__ int s_warp[kCompactBlock / 32 + 1];
   __shared__ long long s_prefix;
-  int n = load_count(n_dev, cap_n);
+  const int n = load_count(n_dev, cap_n);
   if (threadIdx.x == 0) s_tile = scan_next_tile(ss);
   __syncthreads();
   const int tile = s_tile;
   const int64_t base = (int64_t)tile * kCompactTile;
   if (base >= n && tile > 0) return;  // past the end: nobody waits on us
+  const int64_t i0 = base + (int64_t)threadIdx.x * kCompactItems;
   int flags = 0;
-  int4 rows[kCompactItems];
 #pragma unroll
   for (int j = 0; j < kCompactItems; ++j) {
-    int64_t i = base + (int64_t)threadIdx.x * kCompactItems + j;
-    if (i < n) {
-      int4 r = in[i];
-      r.y = floordiv_mul(r.y, sx);
-      r.z = floordiv_mul(r.z, sy);
-      r.w = floordiv_mul(r.w, sz);
-      rows[j] = r;
-      int first = hash_find(t, cap, pack_key(r.x, r.y, r.z, r.w));
-      if (parent_first) parent_first[i] = first;
-      if (first == (int)i) flags |= 1 << j;
-    }
+    const int64_t i = i0 + j;
+    if (i < n && __ldg(first_of + i) == (int)i) flags |= 1 << j;
   }
   int cnt = __popc(flags), total;
   int excl = block_exclusive_scan<kCompactBlock>(cnt, s_warp, &total);
@@ -202,58 +217,28 @@ oc_compact_kernel(const int4* __restrict__ in, const int32_t* n_dev, int64_t cap
   __syncthreads();
   long long pos = s_prefix + excl;
 #pragma unroll
-  for (int j = 0; j < kCompactItems; ++j)
-    if (flags & (1 << j)) out[pos++] = rows[j];
-  int64_t last = (int64_t)n - 1;
-  if (n == 0 && tile == 0 && threadIdx.x == 0) *n_out = 0;
-  if (last >= base && last < base + kCompactTile && threadIdx.x == 0) {
-    // the tile holding the last row publishes the total
-    *n_out = (int)(s_prefix + total);
+  for (int j = 0; j < kCompactItems; ++j) {
+    if (flags & (1 << j)) {
+      int4 r = rows[i0 + j];
+      r.y = floordiv_mul(r.y, sx);
+      r.z = floordiv_mul(r.z, sy);
+      r.w = floordiv_mul(r.w, sz);
+      if (rank_of_first) rank_of_first[i0 + j] = (int)pos;
+      out[pos++] = r;
+    }
   }
+  if (n == 0 && tile == 0 && threadIdx.x == 0) *n_out = 0;
+  const int64_t last = (int64_t)n - 1;
+  if (last >= base && last < base + kCompactTile && threadIdx.x == 0) *n_out = (int)(s_prefix + total);
 }
 
-// rank of each kept row: parent[i] = out row of input row i (needs out rows
-// for first rows: first rows are ordered, so out row = #first rows before).
+// parent[i] = output row of input row i = rank of its first row
 __global__ void oc_parent_kernel(const int32_t* n_dev, int64_t cap_n, const int32_t* first_of,
                                  const int32_t* rank_of_first, int32_t* parent) {
   int n = load_count(n_dev, cap_n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     parent[i] = rank_of_first[first_of[i]];
-}
-
-// writes rank (output row) at the first-row positions using the same scan
-__global__ void __launch_bounds__(kCompactBlock)
-rank_first_kernel(const int32_t* n_dev, int64_t cap_n, const int32_t* first_of, ScanState ss,
-                  int32_t* rank_of_first) {
-  __shared__ int s_tile;
-  __shared__ int s_warp[kCompactBlock / 32 + 1];
-  __shared__ long long s_prefix;
-  int n = load_count(n_dev, cap_n);
-  if (threadIdx.x == 0) s_tile = scan_next_tile(ss);
-  __syncthreads();
-  const int tile = s_tile;
-  const int64_t base = (int64_t)tile * kCompactTile;
-  if (base >= n && tile > 0) return;
-  int flags = 0;
-#pragma unroll
-  for (int j = 0; j < kCompactItems; ++j) {
-    int64_t i = base + (int64_t)threadIdx.x * kCompactItems + j;
-    if (i < n && first_of[i] == (int)i) flags |= 1 << j;
-  }
-  int cnt = __popc(flags), total;
-  int excl = block_exclusive_scan<kCompactBlock>(cnt, s_warp, &total);
-  if (threadIdx.x < 32) {
-    long long p = scan_lookback_warp(ss, tile, total);
-    if (threadIdx.x == 0) s_prefix = p;
-  }
-  __syncthreads();
-  long long pos = s_prefix + excl;
-#pragma unroll
-  for (int j = 0; j < kCompactItems; ++j) {
-    int64_t i = base + (int64_t)threadIdx.x * kCompactItems + j;
-    if (flags & (1 << j)) rank_of_first[i] = (int)(pos++);
-  }
 }
 
 // ------------------------------------------------------------------ voxelize
@@ -296,51 +281,6 @@ __global__ void vox_insert_kernel(const void* pts, int dtype, int64_t n, const i
     vox_tmp[i] = v;
     hash_insert(t, cap, pack_key(v.x, v.y, v.z, v.w), (int)i);
   }
-}
-
-__global__ void __launch_bounds__(kCompactBlock)
-vox_compact_kernel(const int4* __restrict__ vox, int64_t n, const Slot* __restrict__ t, uint64_t cap,
-                   ScanState ss, int4* __restrict__ out, int32_t* n_out, int32_t* first_of,
-                   int32_t* rank_of_first) {
-  __shared__ int s_tile;
-  __shared__ int s_warp[kCompactBlock / 32 + 1];
-  __shared__ long long s_prefix;
-  if (threadIdx.x == 0) s_tile = scan_next_tile(ss);
-  __syncthreads();
-  const int tile = s_tile;
-  const int64_t base = (int64_t)tile * kCompactTile;
-  if (base >= n && tile > 0) return;
-  int flags = 0;
-  int4 rows[kCompactItems];
-#pragma unroll
-  for (int j = 0; j < kCompactItems; ++j) {
-    int64_t i = base + (int64_t)threadIdx.x * kCompactItems + j;
-    if (i < n) {
-      int4 r = vox[i];
-      rows[j] = r;
-      int first = hash_find(t, cap, pack_key(r.x, r.y, r.z, r.w));
-      first_of[i] = first;
-      if (first == (int)i) flags |= 1 << j;
-    }
-  }
-  int cnt = __popc(flags), total;
-  int excl = block_exclusive_scan<kCompactBlock>(cnt, s_warp, &total);
-  if (threadIdx.x < 32) {
-    long long p = scan_lookback_warp(ss, tile, total);
-    if (threadIdx.x == 0) s_prefix = p;
-  }
-  __syncthreads();
-  long long pos = s_prefix + excl;
-#pragma unroll
-  for (int j = 0; j < kCompactItems; ++j) {
-    int64_t i = base + (int64_t)threadIdx.x * kCompactItems + j;
-    if (flags & (1 << j)) {
-      rank_of_first[i] = (int)pos;
-      out[pos++] = rows[j];
-    }
-  }
-  if (n == 0 && threadIdx.x == 0) *n_out = 0;
-  if (n - 1 >= base && n - 1 < base + kCompactTile && threadIdx.x == 0) *n_out = (int)(s_prefix + total);
 }
 
 __global__ void fill_kernel(void* p, int dtype, const int32_t* n_dev, int64_t cap, float v) {
@@ -426,7 +366,7 @@ const char* vp_last_error(void) { return g_last_error.c_str(); }
 const char* vp_version(void) { return "voxpipe_b200 0.1.0 sm_100a"; }
 long long vp_kernel_launches(void) { return g_kernel_launches; }
 
-int64_t vp_hash_capacity(int64_t n) { return (int64_t)hash_cap_for(n); }
+int64_t vp_hash_capacity(int64_t n) { return (int64_t)hash_cap_internal(n); }
 size_t vp_hash_bytes(int64_t cap) { return (size_t)(cap + 1) * sizeof(Slot); }
 
 int vp_hash_build(const int64_t* keys, const int32_t* n_dev, int64_t cap_n, void* table,
@@ -465,7 +405,7 @@ int vp_pack_coords(const int32_t* coords, int64_t n, int64_t* keys, int32_t* bad
 
 size_t vp_validate_coords_ws_bytes(int64_t cap_n) {
   Carver c(nullptr, 0);
-  c.take<Slot>(hash_cap_for(cap_n) + 1);
+  c.take<Slot>(hash_cap_internal(cap_n) + 1);
   return c.off;
 }
 
@@ -474,7 +414,7 @@ int vp_validate_coords(const int32_t* coords, const int32_t* n_dev, int64_t cap_
                        vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   Carver c(ws, ws_bytes);
-  uint64_t cap = hash_cap_for(cap_n);
+  uint64_t cap = hash_cap_internal(cap_n);
   Slot* t = c.take<Slot>(cap + 1);
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "validate_coords: workspace too small");
   VP_REQUIRE(ts[0] > 0 && ts[1] > 0 && ts[2] > 0, VP_EVALIDATION, "tensor_stride entries must be positive");
@@ -501,7 +441,7 @@ int vp_check_finite(const void* feats, int32_t dtype, int64_t count, int32_t* fl
 
 size_t vp_output_coords_ws_bytes(int64_t cap_in) {
   Carver c(nullptr, 0);
-  c.take<Slot>(hash_cap_for(cap_in) + 1);
+  c.take<Slot>(hash_cap_internal(cap_in) + 1);
   int64_t tiles = ceil_div(std::max<int64_t>(cap_in, 1), kCompactTile);
   c.take<unsigned int>(4);
   c.take<unsigned long long>(tiles);
@@ -519,7 +459,7 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
   VP_REQUIRE(step[0] > 0 && step[1] > 0 && step[2] > 0, VP_EVALIDATION,
              "stride must list D positive integers");
   Carver c(ws, ws_bytes);
-  uint64_t cap = hash_cap_for(cap_in);
+  uint64_t cap = hash_cap_internal(cap_in);
   Slot* t = c.take<Slot>(cap + 1);
   int64_t tiles = ceil_div(std::max<int64_t>(cap_in, 1), kCompactTile);
   ScanState s1{c.take<unsigned int>(4), nullptr};
@@ -541,15 +481,15 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
   oc_insert_kernel<<<blocks, 256, 0, st>>>((const int4*)in, n_in_dev, cap_in, step[0], step[1], step[2],
                                            t, cap);
   VP_CHECK_LAUNCH("oc_insert");
-  oc_compact_kernel<<<(int)tiles, kCompactBlock, 0, st>>>((const int4*)in, n_in_dev, cap_in, step[0],
-                                                          step[1], step[2], t, cap, s1, (int4*)out,
-                                                          n_out_dev, parent ? first_of : nullptr);
+  (void)s2;
+  first_of_kernel<<<(int)ceil_div(cap_in, 256), 256, 0, st>>>((const int4*)in, n_in_dev, cap_in, step[0], step[1],
+                                                               step[2], t, cap, first_of);
+  VP_CHECK_LAUNCH("oc_first_of");
+  compact_first_kernel<<<(int)tiles, kCompactBlock, 0, st>>>((const int4*)in, n_in_dev, cap_in, step[0], step[1],
+                                                             step[2], first_of, s1, (int4*)out, n_out_dev,
+                                                             parent ? rank_of_first : nullptr);
   VP_CHECK_LAUNCH("oc_compact");
   if (parent) {
-    cudaMemsetAsync(s2.counter, 0, 256 + tiles * 8, st);
-    rank_first_kernel<<<(int)tiles, kCompactBlock, 0, st>>>(n_in_dev, cap_in, first_of, s2,
-                                                            rank_of_first);
-    VP_CHECK_LAUNCH("rank_first");
     oc_parent_kernel<<<blocks, 256, 0, st>>>(n_in_dev, cap_in, first_of, rank_of_first, parent);
     VP_CHECK_LAUNCH("oc_parent");
   }
@@ -558,7 +498,7 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
 
 size_t vp_voxelize_ws_bytes(int64_t n) {
   Carver c(nullptr, 0);
-  c.take<Slot>(hash_cap_for(n) + 1);
+  c.take<Slot>(hash_cap_internal(n) + 1);
   int64_t tiles = ceil_div(std::max<int64_t>(n, 1), kCompactTile);
   c.take<unsigned int>(4);
   c.take<unsigned long long>(tiles);
@@ -580,7 +520,7 @@ int vp_voxelize(const void* points, int32_t pts_dtype, int64_t n, const int64_t*
              "resolution / batch exceed the packable coordinate range");
   VP_REQUIRE(pts_dtype == VP_F32 || pts_dtype == VP_F64, VP_EVALIDATION, "points must be f32 or f64");
   Carver c(ws, ws_bytes);
-  uint64_t cap = hash_cap_for(n);
+  uint64_t cap = hash_cap_internal(n);
   Slot* t = c.take<Slot>(cap + 1);
   int64_t tiles = ceil_div(std::max<int64_t>(n, 1), kCompactTile);
   ScanState s1{c.take<unsigned int>(4), nullptr};
@@ -601,8 +541,11 @@ int vp_voxelize(const void* points, int32_t pts_dtype, int64_t n, const int64_t*
   vox_insert_kernel<<<blocks, 256, 0, st>>>(points, pts_dtype, n, offs, nc, vs, res[0], res[1], res[2],
                                             t, cap, vox);
   VP_CHECK_LAUNCH("vox_insert");
-  vox_compact_kernel<<<(int)tiles, kCompactBlock, 0, st>>>(vox, n, t, cap, s1, (int4*)coords_out,
-                                                           n_out_dev, first_of, rank_of_first);
+  first_of_kernel<<<(int)ceil_div(n, 256), 256, 0, st>>>(vox, nullptr, n, 1, 1, 1, t, cap, first_of);
+  VP_CHECK_LAUNCH("vox_first_of");
+  compact_first_kernel<<<(int)tiles, kCompactBlock, 0, st>>>(vox, nullptr, n, 1, 1, 1, first_of, s1,
+                                                             (int4*)coords_out, n_out_dev,
+                                                             p2v ? rank_of_first : nullptr);
   VP_CHECK_LAUNCH("vox_compact");
   if (p2v) {
     oc_parent_kernel<<<blocks, 256, 0, st>>>(nullptr, n, first_of, rank_of_first, p2v);

@@ -12,7 +12,8 @@
 
 namespace vp {
 
-constexpr int kMapTile = 256;  // output rows per tile (== threads per CTA)
+constexpr int kMapTile = 128;  // output rows per tile (== threads per CTA)
+constexpr int kMapSmemK = 32;  // neighbour tile staged in smem when K <= 32
 
 struct Offsets {
   int32_t d[VP_MAX_OFFSETS * 3];
@@ -28,39 +29,65 @@ __global__ void map_insert_kernel(const int4* __restrict__ in, const int32_t* n_
   }
 }
 
-// grid: one CTA per tile of kMapTile output rows.  counts[k * ntiles + tile].
-__global__ void __launch_bounds__(kMapTile)
+// kMapTPR threads per output row split the K probes (k = j, j + 8, ...), so a
+// thread's chain of dependent hash walks is short and 1024 independent walks
+// are in flight per CTA; hits are counted per (warp, k) with ballots masked
+// to the lanes owning k.  For K <= 32 the [128, K] neighbour tile is staged
+// in shared memory and written back fully coalesced.  counts[k*ntiles+tile].
+constexpr int kMapTPR = 8;
+constexpr int kProbeThreads = kMapTile * kMapTPR;  // 1024
+constexpr int kProbeWarps = kProbeThreads / 32;
+
+__global__ void __launch_bounds__(kProbeThreads)
 map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t cap_out,
                  const Slot* __restrict__ t, uint64_t cap, const __grid_constant__ Offsets offs,
                  int K, int sx, int sy, int sz, int32_t* __restrict__ nbr, int32_t* counts,
                  int ntiles) {
-  extern __shared__ int smem[];
-  int4* s_rows = reinterpret_cast<int4*>(smem);         // kMapTile rows
-  int* s_cnt = smem + kMapTile * 4;                     // K counters
+  __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
+  __shared__ unsigned short s_cnt[kProbeWarps][VP_MAX_OFFSETS];
   const int n_out = load_count(n_out_dev, cap_out);
   const int tile = blockIdx.x;
   const int64_t u0 = (int64_t)tile * kMapTile;
   if (u0 >= n_out) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row = tid / kMapTPR, j = tid % kMapTPR;
   const int rows = (n_out - u0) < kMapTile ? (int)(n_out - u0) : kMapTile;
-  if (threadIdx.x < rows) s_rows[threadIdx.x] = out[u0 + threadIdx.x];
-  for (int k = threadIdx.x; k < K; k += kMapTile) s_cnt[k] = 0;
-  __syncthreads();
-  const int total = rows * K;
-  int32_t* dst = nbr + u0 * K;
-  for (int e = threadIdx.x; e < total; e += kMapTile) {
-    int u = e / K, k = e - u * K;
-    int4 r = s_rows[u];
-    long long qx = (long long)r.y + (long long)offs.d[3 * k] * sx;
-    long long qy = (long long)r.z + (long long)offs.d[3 * k + 1] * sy;
-    long long qz = (long long)r.w + (long long)offs.d[3 * k + 2] * sz;
+  const bool valid = row < rows;
+  const bool staged = K <= kMapSmemK;
+  const int4 r = valid ? out[u0 + row] : make_int4(-1, 0, 0, 0);
+  const unsigned jmask = 0x01010101u << j;  // lanes of this warp with the same j
+  for (int kb = 0; kb < K; kb += kMapTPR) {
+    const int k = kb + j;
     int v = -1;
-    // out-of-range queries are plain misses (kernels.py:135-148)
-    if (packable64(r.x, qx, qy, qz)) v = hash_find(t, cap, pack_key(r.x, (int)qx, (int)qy, (int)qz));
-    dst[e] = v;
-    if (v >= 0) atomicAdd(&s_cnt[k], 1);
+    if (valid && k < K) {
+      const long long qx = (long long)r.y + (long long)offs.d[3 * k] * sx;
+      const long long qy = (long long)r.z + (long long)offs.d[3 * k + 1] * sy;
+      const long long qz = (long long)r.w + (long long)offs.d[3 * k + 2] * sz;
+      // out-of-range queries are plain misses (kernels.py:135-148)
+      if (packable64(r.x, qx, qy, qz)) v = hash_find(t, cap, pack_key(r.x, (int)qx, (int)qy, (int)qz));
+    }
+    if (k < K) {
+      if (staged) s_nbr[row * (kMapSmemK + 1) + k] = v;
+      else if (valid) nbr[(u0 + row) * K + k] = v;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, v >= 0);
+    if (lane < kMapTPR && kb + lane < K) s_cnt[warp][kb + lane] = (unsigned short)__popc(m & (0x01010101u << lane));
   }
+  (void)jmask;
   __syncthreads();
-  for (int k = threadIdx.x; k < K; k += kMapTile) counts[(int64_t)k * ntiles + tile] = s_cnt[k];
+  if (staged) {
+    int32_t* dst = nbr + u0 * K;
+    for (int e = tid; e < rows * K; e += kProbeThreads) {
+      const int rr = e / K, k = e - rr * K;
+      dst[e] = s_nbr[rr * (kMapSmemK + 1) + k];
+    }
+  }
+  for (int k = tid; k < K; k += kProbeThreads) {
+    int c = 0;
+#pragma unroll 8
+    for (int w = 0; w < kProbeWarps; ++w) c += s_cnt[w][k];
+    counts[(int64_t)k * ntiles + tile] = c;
+  }
 }
 
 // one CTA per offset: exclusive scan over the tiles' counts, total[k].
@@ -86,48 +113,71 @@ map_scan_kernel(int32_t* counts, const int32_t* n_out_dev, int64_t cap_out, int 
   if (threadIdx.x == 0) totals[blockIdx.x] = s_carry;
 }
 
-// per tile: for each offset, ordered compaction of hit rows.
+// per tile: for each offset, ordered compaction of the hit rows (ascending
+// out row == conv.py:181 flatnonzero order) with warp ballots; the per-warp
+// hit counts of all offsets are gathered first so the loop has no barriers.
 __global__ void __launch_bounds__(kMapTile)
 map_emit_kernel(const int32_t* __restrict__ nbr, const int32_t* n_out_dev, int64_t cap_out, int K,
                 const int32_t* __restrict__ counts, const int32_t* __restrict__ totals, int ntiles_cap,
                 int32_t* __restrict__ pair_in, int32_t* __restrict__ pair_out, int32_t* pair_ptr) {
-  extern __shared__ int smem[];
-  int* s_base = smem;                 // K+1 offset bases
-  int* s_warp = smem + VP_MAX_OFFSETS + 1;  // kMapTile/32
+  __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
+  __shared__ int s_w[kMapTile / 32][VP_MAX_OFFSETS];
+  __shared__ int s_base[VP_MAX_OFFSETS + 1];
+  __shared__ int s_tot[VP_MAX_OFFSETS];
   const int n_out = load_count(n_out_dev, cap_out);
   const int tile = blockIdx.x;
   const int64_t u0 = (int64_t)tile * kMapTile;
-  if (threadIdx.x == 0) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // all global loads of the offset bases issued in parallel, then a serial
+  // prefix over K values in shared memory
+  for (int k = tid; k < K; k += kMapTile) s_tot[k] = __ldg(totals + k);
+  __syncthreads();
+  if (tid == 0) {
     int acc = 0;
     for (int k = 0; k < K; ++k) {
       s_base[k] = acc;
-      acc += totals[k];
+      acc += s_tot[k];
     }
     s_base[K] = acc;
     if (tile == 0)
       for (int k = 0; k <= K; ++k) pair_ptr[k] = s_base[k];
   }
-  __syncthreads();
   if (u0 >= n_out) return;
-  const int64_t u = u0 + threadIdx.x;
-  const bool valid = u < n_out;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* row = nbr + u * K;
-  for (int k = 0; k < K; ++k) {
-    int v = valid ? row[k] : -1;
-    unsigned m = __ballot_sync(0xffffffffu, v >= 0);
-    if (lane == 0) s_warp[warp] = __popc(m);
-    __syncthreads();
-    int before = 0;
-#pragma unroll
-    for (int w = 0; w < kMapTile / 32; ++w) before += (w < warp) ? s_warp[w] : 0;
-    if (v >= 0) {
-      int pos = s_base[k] + counts[(int64_t)k * ntiles_cap + tile] + before +
-                __popc(m & ((1u << lane) - 1u));
-      pair_in[pos] = v;
-      pair_out[pos] = (int32_t)u;
+  for (int k = tid; k < K; k += kMapTile) s_w[0][k] = __ldg(counts + (int64_t)k * ntiles_cap + tile);
+  __syncthreads();  // thread 0 is done reading s_tot (totals)
+  for (int k = tid; k < K; k += kMapTile) s_tot[k] = s_w[0][k];
+  const int rows = (n_out - u0) < kMapTile ? (int)(n_out - u0) : kMapTile;
+  const bool staged = K <= kMapSmemK;
+  if (staged) {
+    const int32_t* src = nbr + u0 * K;
+    for (int e = tid; e < rows * K; e += kMapTile) {
+      const int rr = e / K, k = e - rr * K;
+      s_nbr[rr * (kMapSmemK + 1) + k] = src[e];
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  const bool valid = tid < rows;
+  auto nb = [&](int k) -> int {
+    if (!valid) return -1;
+    return staged ? s_nbr[tid * (kMapSmemK + 1) + k] : nbr[(u0 + tid) * K + k];
+  };
+  for (int k = 0; k < K; ++k) {
+    const unsigned m = __ballot_sync(0xffffffffu, nb(k) >= 0);
+    if (lane == 0) s_w[warp][k] = __popc(m);
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k = 0; k < K; ++k) {
+    const int v = nb(k);
+    const unsigned m = __ballot_sync(0xffffffffu, v >= 0);
+    if (v >= 0) {
+      int before = 0;
+#pragma unroll
+      for (int w = 0; w < kMapTile / 32; ++w) before += (w < warp) ? s_w[w][k] : 0;
+      const int pos = s_base[k] + s_tot[k] + before + __popc(m & lt);
+      pair_in[pos] = v;
+      pair_out[pos] = (int32_t)(u0 + tid);
+    }
   }
 }
 
@@ -154,7 +204,7 @@ extern "C" {
 
 size_t vp_kernel_map_ws_bytes(int64_t cap_in, int64_t cap_out, int32_t K) {
   Carver c(nullptr, 0);
-  c.take<Slot>(hash_cap_for(cap_in) + 1);
+  c.take<Slot>(hash_cap_internal(cap_in) + 1);
   int64_t ntiles = ceil_div(std::max<int64_t>(cap_out, 1), kMapTile);
   c.take<int32_t>(ntiles * K);
   c.take<int32_t>(K + 1);
@@ -170,7 +220,7 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
   VP_REQUIRE((pair_in == nullptr) == (pair_out == nullptr) && (pair_in == nullptr || pair_ptr),
              VP_EVALIDATION, "pair_in/pair_out/pair_ptr must be given together");
   Carver c(ws, ws_bytes);
-  uint64_t cap = hash_cap_for(cap_in);
+  uint64_t cap = hash_cap_internal(cap_in);
   Slot* t = c.take<Slot>(cap + 1);
   int ntiles = (int)ceil_div(std::max<int64_t>(cap_out, 1), kMapTile);
   int32_t* counts = c.take<int32_t>((int64_t)ntiles * K);
@@ -191,16 +241,14 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
     VP_CHECK_ASYNC("kernel_map(empty)");
     return VP_OK;
   }
-  size_t smem = kMapTile * 16 + K * 4;
-  map_probe_kernel<<<ntiles, kMapTile, smem, st>>>((const int4*)out, n_out_dev, cap_out, t, cap, offs, K,
+  map_probe_kernel<<<ntiles, kProbeThreads, 0, st>>>((const int4*)out, n_out_dev, cap_out, t, cap, offs, K,
                                                    in_stride[0], in_stride[1], in_stride[2], nbr, counts,
                                                    ntiles);
   VP_CHECK_LAUNCH("map_probe");
   if (pair_in) {
     map_scan_kernel<<<K, 1024, 0, st>>>(counts, n_out_dev, cap_out, ntiles, totals);
     VP_CHECK_LAUNCH("map_scan");
-    size_t smem2 = (VP_MAX_OFFSETS + 1 + kMapTile / 32) * 4;
-    map_emit_kernel<<<ntiles, kMapTile, smem2, st>>>(nbr, n_out_dev, cap_out, K, counts, totals, ntiles,
+    map_emit_kernel<<<ntiles, kMapTile, 0, st>>>(nbr, n_out_dev, cap_out, K, counts, totals, ntiles,
                                                      pair_in, pair_out, pair_ptr);
     VP_CHECK_LAUNCH("map_emit");
   }

@@ -92,7 +92,10 @@ class SparseResNetTrainer:
 
     def __init__(self, batch=64, points=2048, resolution=64, planes=(32, 64, 128, 256), blocks=1, classes=40,
                  in_channels=1, lr=1e-2, momentum=0.9, seed=2, voxel_size=1.0, device=None,
-                 points_dtype=torch.float32, grad_allreduce=None):
+                 points_dtype=torch.float32, grad_allreduce=None, feature_dtype=BF16):
+        """feature_dtype: bf16 (tensor-core path, the product) or fp32 (SIMT
+        kernels; used to validate the engine's dataflow against the f64
+        oracle at fp32 tolerance)."""
         self.B, self.P, self.res = batch, points, resolution
         self.planes, self.blocks, self.classes, self.cin = tuple(planes), blocks, classes, in_channels
         self.lr, self.momentum, self.voxel_size = lr, momentum, voxel_size
@@ -102,6 +105,8 @@ class SparseResNetTrainer:
         self.K = self.shape.num_offsets
         self.offs3 = _lib.i32_array(self.shape.offsets3().ravel())
         self.eps = 1e-5
+        self.fdt = feature_dtype
+        self.fcode = _lib.VP_BF16 if feature_dtype == BF16 else _lib.VP_F32
         dev = self.device
         cap = batch * points
         self.cap = cap
@@ -111,9 +116,15 @@ class SparseResNetTrainer:
         self.labels = torch.zeros(batch, dtype=torch.int32, device=dev)
         # ---- levels
         nlev = len(planes) + 1
-        self.levels = [Level(torch.zeros((cap, 4), dtype=torch.int32, device=dev),
-                             torch.zeros(1, dtype=torch.int32, device=dev), cap, 2 ** i) for i in range(nlev)]
-        self.feat0 = torch.zeros((cap, in_channels), dtype=BF16, device=dev)
+        # capacities: level i holds at most min(N_{i-1}, B * ceil(res / 2^i)^3)
+        # rows (voxelize clips to [0, res-1]; stride-2^i cells per axis)
+        caps = [cap]
+        for i in range(1, nlev):
+            cells = -(-resolution // (2 ** i))
+            caps.append(min(caps[-1], batch * cells ** 3))
+        self.levels = [Level(torch.zeros((caps[i], 4), dtype=torch.int32, device=dev),
+                             torch.zeros(1, dtype=torch.int32, device=dev), caps[i], 2 ** i) for i in range(nlev)]
+        self.feat0 = torch.zeros((cap, in_channels), dtype=feature_dtype, device=dev)
         self.vox_ws = _lib.workspace(_lib.query("vp_voxelize_ws_bytes", cap), dev)
         self.oc_ws = _lib.workspace(_lib.query("vp_output_coords_ws_bytes", cap), dev)
         # ---- maps: stride-1 per level, strided between consecutive levels
@@ -135,13 +146,15 @@ class SparseResNetTrainer:
         # ---- activations (capacity sized)
         for L in self.layers:
             n = L["dst"].cap
-            L["y"] = torch.zeros((n, L["cout"]), dtype=BF16, device=dev)  # conv output (pre-BN)
-            L["a"] = torch.zeros((n, L["cout"]), dtype=BF16, device=dev)  # BN(+res)(+ReLU) output
+            L["y"] = torch.zeros((n, L["cout"]), dtype=feature_dtype, device=dev)  # conv output (pre-BN)
+            L["a"] = torch.zeros((n, L["cout"]), dtype=feature_dtype, device=dev)  # BN(+res)(+ReLU) output
             L["mean"] = torch.zeros(L["cout"], dtype=torch.float32, device=dev)
             L["rstd"] = torch.zeros(L["cout"], dtype=torch.float32, device=dev)
-            L["gy"] = torch.zeros((n, L["cout"]), dtype=BF16, device=dev)  # grad wrt conv output
+            L["gy"] = torch.zeros((n, L["cout"]), dtype=feature_dtype, device=dev)  # grad wrt conv output
             L["w"] = pb.view(pb.p, L["name"] + ".w")
-            L["wb"] = pb.bf16_view(L["name"] + ".w")
+            # the conv operand: bf16 shadow on the tensor-core path, fp32 master otherwise
+            L["wb"] = pb.bf16_view(L["name"] + ".w") if feature_dtype == BF16 else L["w"]
+            L["wcode"] = _lib.VP_BF16 if feature_dtype == BF16 else _lib.VP_F32
             L["gw"] = pb.view(pb.g, L["name"] + ".w")
             for k in ("gamma", "beta"):
                 L[k] = pb.view(pb.p, f"{L['name']}.{k}")
@@ -152,8 +165,10 @@ class SparseResNetTrainer:
                                                    L["map"].pin.numel()), dev)
             L["bn_ws"] = _lib.workspace(_lib.query("vp_bn_stats_ws_bytes", n, L["cout"]), dev)
         # gradient buffers per level for the activation flowing back
-        self.gact = [torch.zeros((lv.cap, self._width_at(i)), dtype=BF16, device=dev) for i, lv in enumerate(self.levels)]
-        self.gid = [torch.zeros((lv.cap, self._width_at(i)), dtype=BF16, device=dev) for i, lv in enumerate(self.levels)]
+        self.gact = [torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
+                     for i, lv in enumerate(self.levels)]
+        self.gid = [torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
+                    for i, lv in enumerate(self.levels)]
         C = planes[-1]
         self.pooled = torch.zeros((batch, C), dtype=torch.float32, device=dev)
         self.pool_counts = torch.zeros(batch, dtype=torch.int32, device=dev)
@@ -237,7 +252,7 @@ class SparseResNetTrainer:
         res3 = _lib.i32_array((self.res,) * 3)
         self._c("vp_voxelize", self.points.data_ptr(), _lib.dtype_code(self.points), self.cap, self.offsets.data_ptr(),
                 self.B, float(self.voxel_size), res3, lv[0].coords.data_ptr(), lv[0].n.data_ptr(), None,
-                self.feat0.data_ptr(), _lib.VP_BF16, self.vox_ws.data_ptr(), self.vox_ws.numel(), st)
+                self.feat0.data_ptr(), self.fcode, self.vox_ws.data_ptr(), self.vox_ws.numel(), st)
         for i in range(1, len(lv)):
             step = _lib.i32_array((lv[i].stride,) * 3)
             self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
@@ -253,14 +268,15 @@ class SparseResNetTrainer:
 
     def _conv_bn(self, L, x, res, relu, st):
         dst = L["dst"]
-        self._c("vp_conv_fwd", x.data_ptr(), _lib.VP_BF16, L["cin"], L["wb"].data_ptr(), _lib.VP_BF16, L["cout"],
-                self.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(), _lib.VP_BF16,
+        fc = self.fcode
+        self._c("vp_conv_fwd", x.data_ptr(), fc, L["cin"], L["wb"].data_ptr(), L["wcode"], L["cout"],
+                self.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(), fc,
                 L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
-        self._c("vp_bn_stats", L["y"].data_ptr(), _lib.VP_BF16, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
+        self._c("vp_bn_stats", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
                 L["mean"].data_ptr(), L["rstd"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
-        self._c("vp_bn_apply", L["y"].data_ptr(), _lib.VP_BF16, dst.n.data_ptr(), dst.cap, L["cout"],
+        self._c("vp_bn_apply", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"],
                 L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(), L["beta"].data_ptr(),
-                _lib.ptr(res), _lib.VP_BF16, int(relu), L["a"].data_ptr(), _lib.VP_BF16, st)
+                _lib.ptr(res), fc, int(relu), L["a"].data_ptr(), fc, st)
         L["x"] = x
         return L["a"]
 
@@ -278,7 +294,7 @@ class SparseResNetTrainer:
                 i += 2
         last = self.levels[-1]
         C = self.planes[-1]
-        self._c("vp_global_pool", x.data_ptr(), _lib.VP_BF16, last.coords.data_ptr(), last.n.data_ptr(), last.cap, C,
+        self._c("vp_global_pool", x.data_ptr(), self.fcode, last.coords.data_ptr(), last.n.data_ptr(), last.cap, C,
                 self.B, self.pooled.data_ptr(), self.pool_counts.data_ptr(), self.pool_ws.data_ptr(),
                 self.pool_ws.numel(), st)
         pb = self.params
@@ -292,12 +308,13 @@ class SparseResNetTrainer:
         """BN(+ReLU) backward then conv dgrad/wgrad.  g_out (+g_out2) is the
         gradient wrt L['a']; returns the gradient wrt the conv input."""
         dst, src, m = L["dst"], L["src"], L["map"]
-        self._c("vp_bn_backward", g_out.data_ptr(), _lib.ptr(g_out2), _lib.VP_BF16, L["a"].data_ptr(), _lib.VP_BF16,
-                L["y"].data_ptr(), _lib.VP_BF16, dst.n.data_ptr(), dst.cap, L["cout"], L["mean"].data_ptr(),
-                L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(), _lib.VP_BF16, _lib.ptr(g_res),
+        fc = self.fcode
+        self._c("vp_bn_backward", g_out.data_ptr(), _lib.ptr(g_out2), fc, L["a"].data_ptr(), fc,
+                L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], L["mean"].data_ptr(),
+                L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(), fc, _lib.ptr(g_res),
                 L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
         x = L["x"]
-        self._c("vp_conv_wgrad", x.data_ptr(), _lib.VP_BF16, L["cin"], L["gy"].data_ptr(), _lib.VP_BF16, L["cout"],
+        self._c("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
                 self.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(),
                 L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st)
         if not need_dgrad:
@@ -307,8 +324,8 @@ class SparseResNetTrainer:
             table, flip = m.nbr, 1  # stride 1, symmetric 3^3: inv[v,k] == nbr[v,K-1-k]
         else:
             table, flip = m.inv, 0
-        self._c("vp_conv_dgrad", L["gy"].data_ptr(), _lib.VP_BF16, L["cout"], L["wb"].data_ptr(), _lib.VP_BF16,
-                L["cin"], self.K, table.data_ptr(), flip, src.n.data_ptr(), src.cap, gin.data_ptr(), _lib.VP_BF16,
+        self._c("vp_conv_dgrad", L["gy"].data_ptr(), fc, L["cout"], L["wb"].data_ptr(), L["wcode"],
+                L["cin"], self.K, table.data_ptr(), flip, src.n.data_ptr(), src.cap, gin.data_ptr(), fc,
                 L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
         return gin
 
@@ -317,7 +334,7 @@ class SparseResNetTrainer:
         C = self.planes[-1]
         g = self.gact[-1]
         self._c("vp_global_pool_backward", self.g_pooled.data_ptr(), last.coords.data_ptr(),
-                self.pool_counts.data_ptr(), last.n.data_ptr(), last.cap, C, g.data_ptr(), _lib.VP_BF16, st)
+                self.pool_counts.data_ptr(), last.n.data_ptr(), last.cap, C, g.data_ptr(), self.fcode, st)
         g2 = None  # pending identity-branch gradient for the current activation
         Ls = self.layers
         i = len(Ls) - 1
