@@ -318,7 +318,8 @@ def roofline(tr, dev, iters=50):
     n_in = int(L["src"].n.item())
 
     def launch():
-        _lib.call("vp_conv_fwd", L["x"].data_ptr(), _lib.VP_BF16, L["cin"], L["wb"].data_ptr(), _lib.VP_BF16,
+        _lib.call("vp_conv_fwd", L["x"].data_ptr(), _lib.VP_BF16, L["x"].shape[0], L["cin"], L["wb"].data_ptr(),
+                  _lib.VP_BF16,
                   L["cout"], tr.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(),
                   _lib.VP_BF16, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st.cuda_stream)
 

@@ -138,8 +138,11 @@ int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t 
  * {32,64,128,256}; a SIMT kernel otherwise.  Deterministic, no atomics.
  *   table  : nbr [cap_out, K] (or inv for dgrad); flip != 0 reads column
  *            K-1-k (stride-1 symmetric kernels: inv[v,k] == nbr[v,K-1-k]).
- *   w      : [K, c_out, c_in] in w_dtype. */
-int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t c_in, const void* w, int32_t w_dtype,
+ *   w      : [K, c_out, c_in] in w_dtype.
+ *   x_rows : rows allocated in x (every table entry is < x_rows); the
+ *            tensor-core path gathers rows with TMA tile::gather4 and
+ *            encodes a missing neighbour as row x_rows (zero fill). */
+int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t c_in, const void* w, int32_t w_dtype,
                 int64_t c_out, int32_t K, const int32_t* table, int32_t flip,
                 const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype,
                 void* ws, size_t ws_bytes, vp_stream_t stream);
@@ -147,7 +150,7 @@ size_t vp_conv_fwd_ws_bytes(int64_t c_in, int64_t c_out, int32_t K);
 /* dgrad (conv.py:240): grad_in[v] = sum_k W_k^T g[inv[v,k]]; same kernel as
  * the forward with W transposed into ws.  table = inv (or nbr with flip). */
 size_t vp_conv_dgrad_ws_bytes(int64_t c_in, int64_t c_out, int32_t K);
-int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t c_out, const void* w, int32_t w_dtype,
+int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t c_out, const void* w, int32_t w_dtype,
                   int64_t c_in, int32_t K, const int32_t* table, int32_t flip,
                   const int32_t* n_in_dev, int64_t cap_in, void* grad_in, int32_t gi_dtype,
                   void* ws, size_t ws_bytes, vp_stream_t stream);

@@ -252,7 +252,8 @@ def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: 
     y = torch.empty((max(n_out, 1), w.n_out), dtype=out_dtype, device=x.device)
     wt = w.bf16 if x.dtype == torch.bfloat16 else w.matrices
     ws = _lib.workspace(_lib.query("vp_conv_fwd_ws_bytes", w.n_in, w.n_out, K), x.device)
-    _lib.call("vp_conv_fwd", x.data_ptr(), _lib.dtype_code(x), w.n_in, wt.data_ptr(), _lib.dtype_code(wt), w.n_out,
+    _lib.call("vp_conv_fwd", x.data_ptr(), _lib.dtype_code(x), max(x.shape[0], 1), w.n_in, wt.data_ptr(),
+              _lib.dtype_code(wt), w.n_out,
               K, nbr.data_ptr(), int(flip), None, n_out, y.data_ptr(), _lib.dtype_code(y), ws.data_ptr(), ws.numel(),
               _lib.stream())
     return y[:n_out]
@@ -266,7 +267,8 @@ def conv_dgrad_raw(g: torch.Tensor, w: ConvWeights, table: torch.Tensor, n_in: i
     gi = torch.empty((max(n_in, 1), w.n_in), dtype=out_dtype, device=g.device)
     wt = w.bf16 if g.dtype == torch.bfloat16 else w.matrices
     ws = _lib.workspace(_lib.query("vp_conv_dgrad_ws_bytes", w.n_in, w.n_out, K), g.device)
-    _lib.call("vp_conv_dgrad", g.data_ptr(), _lib.dtype_code(g), w.n_out, wt.data_ptr(), _lib.dtype_code(wt),
+    _lib.call("vp_conv_dgrad", g.data_ptr(), _lib.dtype_code(g), max(g.shape[0], 1), w.n_out, wt.data_ptr(),
+              _lib.dtype_code(wt),
               w.n_in, K, table.data_ptr(), int(flip), None, n_in, gi.data_ptr(), _lib.dtype_code(gi), ws.data_ptr(),
               ws.numel(), _lib.stream())
     return gi[:n_in]

@@ -109,6 +109,7 @@ wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* 
       const int co = e / cin, ci = e - (e / cin) * cin;
       float acc = 0.f;
       if (e < per)
+#pragma unroll 8
         for (int q = p0 + warp; q < p1; q += kWgSimtThreads / 32)
           acc += ldf(gy, g_dtype, (int64_t)pout[q] * cout + co) * ldf(x, x_dtype, (int64_t)pin[q] * cin + ci);
       s_red[warp][lane] = acc;
@@ -156,11 +157,28 @@ conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const vo
   const int n_out = load_count(n_out_dev, cap_out);
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_out; u += (int64_t)gridDim.x * blockDim.x) {
     const int32_t* trow = table + u * K;
+    float xk[27];
+    const bool fast = (cin == 1 && K == 27);
+    if (fast) {  // occupancy stem: all 27 index loads, then all 27 feature loads, in flight at once
+      int vk[27];
+#pragma unroll
+      for (int k = 0; k < 27; ++k) vk[k] = __ldg(trow + (flip ? 26 - k : k));
+#pragma unroll
+      for (int k = 0; k < 27; ++k) xk[k] = vk[k] >= 0 ? ldf(x, x_dtype, vk[k]) : 0.f;
+    }
     for (int c0 = 0; c0 < cout; c0 += 32) {
       float acc[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-      for (int k = 0; k < K; ++k) {
+      if (fast) {
+#pragma unroll
+        for (int k = 0; k < 27; ++k) {
+          const float* wr = s_w + k * cout + c0;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] += (c0 + c < cout) ? wr[c] * xk[k] : 0.f;
+        }
+      }
+      for (int k = 0; k < (fast ? 0 : K); ++k) {
         const int v = __ldg(trow + (flip ? K - 1 - k : k));
         if (v < 0) continue;
         for (int ci = 0; ci < cin; ++ci) {
@@ -170,7 +188,84 @@ conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const vo
           for (int c = 0; c < 32; ++c) acc[c] += (c0 + c < cout) ? wr[c] * xv : 0.f;
         }
       }
-      for (int c = 0; c < 32 && c0 + c < cout; ++c) stf(y, y_dtype, u * cout + c0 + c, acc[c]);
+      if (c0 + 32 <= cout && (cout & 7) == 0 && y_dtype == VP_BF16) {
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(y) + u * cout + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pk;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(acc[8 * q + 2 * e], acc[8 * q + 2 * e + 1]);
+          dst[q] = pk;
+        }
+      } else if (c0 + 32 <= cout && (cout & 3) == 0 && y_dtype == VP_F32) {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + u * cout + c0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      } else {
+        for (int c = 0; c < 32 && c0 + c < cout; ++c) stf(y, y_dtype, u * cout + c0 + c, acc[c]);
+      }
+    }
+  }
+}
+
+// Occupancy stem (C_in = 1, 3^3, C_out multiple of 32, bf16 out): a CTA owns
+// 128 rows; the [128, 27] neighbour slice is staged coalesced in shared
+// memory, each thread gathers its row's 27 inputs (all loads in flight),
+// accumulates 32 outputs per pass against broadcast weights, and the bf16
+// output tile is written back through shared memory with coalesced stores.
+constexpr int kStemRows = 128;
+__global__ void __launch_bounds__(kStemRows)
+conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict__ w, int w_dtype, int cout,
+                 const int32_t* __restrict__ table, int flip, const int32_t* n_out_dev, int64_t cap_out,
+                 __nv_bfloat16* __restrict__ y) {
+  extern __shared__ float s_mem[];
+  float* s_w = s_mem;                                             // [27][cout]
+  int* s_t = reinterpret_cast<int*>(s_w + 27 * cout);             // [128][27]
+  uint32_t* s_o = reinterpret_cast<uint32_t*>(s_t + kStemRows * 27);  // [128][16 + 1] packed bf16 pairs
+  for (int e = threadIdx.x; e < 27 * cout; e += kStemRows) {
+    const int k = e / cout, co = e - k * cout;
+    s_w[e] = ldf(w, w_dtype, (int64_t)k * cout + co);
+  }
+  const int n_out = load_count(n_out_dev, cap_out);
+  const int ntiles = (n_out + kStemRows - 1) / kStemRows;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t u0 = (int64_t)tile * kStemRows;
+    const int rows = min(kStemRows, (int)(n_out - u0));
+    __syncthreads();
+    const int32_t* tb = table + u0 * 27;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < rows * 27; e += kStemRows) s_t[e] = __ldg(tb + e);
+    __syncthreads();
+    float xk[27];
+    const bool valid = threadIdx.x < rows;
+#pragma unroll
+    for (int k = 0; k < 27; ++k) {
+      const int v = valid ? s_t[threadIdx.x * 27 + (flip ? 26 - k : k)] : -1;
+      xk[k] = v >= 0 ? ldf(x, x_dtype, v) : 0.f;
+    }
+    for (int c0 = 0; c0 < cout; c0 += 32) {
+      float acc[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 27; ++k) {
+        const float* wr = s_w + k * cout + c0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] += wr[c] * xk[k];
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * c], acc[2 * c + 1]);
+        s_o[threadIdx.x * 17 + c] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      __syncthreads();
+      // coalesced: word e of the tile -> row e / 16, pair e % 16
+      for (int e = threadIdx.x; e < rows * 16; e += kStemRows) {
+        const int rr = e >> 4, c = e & 15;
+        reinterpret_cast<uint32_t*>(y + (u0 + rr) * cout + c0)[c] = s_o[rr * 17 + c];
+      }
+      __syncthreads();
     }
   }
 }
@@ -181,6 +276,13 @@ static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int w
                             const int32_t* table, int flip, const int32_t* n_out_dev, int64_t cap_out, void* y, int yd,
                             cudaStream_t st) {
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), kNumSMs * 8));
+  if (cin == 1 && K == 27 && cout % 32 == 0 && cout <= 256 && yd == VP_BF16) {
+    const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 17 * 4;
+    conv_stem_kernel<<<blocks, kStemRows, smem, st>>>(x, xd, w, wd, cout, table, flip, n_out_dev, cap_out,
+                                                      (__nv_bfloat16*)y);
+    VP_CHECK_LAUNCH("conv_stem");
+    return VP_OK;
+  }
   conv_fwd_small_kernel<<<blocks, 128, (size_t)K * cin * cout * 4, st>>>(x, xd, cin, w, wd, cout, K, table, flip,
                                                                          n_out_dev, cap_out, y, yd);
   VP_CHECK_LAUNCH("conv_fwd_small");
@@ -295,7 +397,7 @@ size_t vp_conv_fwd_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
   return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cout);
 }
 
-int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t cin, const void* w, int32_t w_dtype, int64_t cout,
+int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype, int64_t cout,
                 int32_t K, const int32_t* table, int32_t flip, const int32_t* n_out_dev, int64_t cap_out,
                 void* y, int32_t y_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -313,6 +415,7 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t cin, const void* w, int3
       VP_CHECK_LAUNCH("conv_fwd: cast w");
       wb = (const bf16*)ws;
     }
+    (void)x_rows;  // the cp.async gather zero-fills missing neighbours itself
     FwdParams p{(const bf16*)x, wb, K, table, flip, n_out_dev, cap_out, y, y_dtype, nullptr, 1};
     return conv_tc<false>(cin, cout, p, part, st);
   }
@@ -330,7 +433,7 @@ size_t vp_conv_dgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
   return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cin);
 }
 
-int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t cout, const void* w, int32_t w_dtype, int64_t cin,
+int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, const void* w, int32_t w_dtype, int64_t cin,
                   int32_t K, const int32_t* table, int32_t flip, const int32_t* n_in_dev, int64_t cap_in,
                   void* gi, int32_t gi_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -348,6 +451,7 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t cout, const void* w, i
       wb = (const bf16*)ws;
     }
     // grad_in = sum_k W_k^T g[table]: GEMM K-dim = C_out, N = C_in, W read as MN-major B
+    (void)g_rows;
     FwdParams p{(const bf16*)g, wb, K, table, flip, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1};
     return conv_tc<true>(cout, cin, p, part, st);
   }
@@ -360,8 +464,10 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t cout, const void* w, i
   return VP_OK;
 }
 
+constexpr int kWgSimtChunk = 512;  // SIMT path: short chunks, many CTAs
+
 size_t vp_conv_wgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K, int64_t cap_pairs) {
-  const int chunk = wgrad_chunk(cap_pairs);
+  const int chunk = std::min(wgrad_chunk(cap_pairs), kWgSimtChunk);
   const int64_t items = cap_pairs / chunk + K + 1;
   return align_up((size_t)items * cin * cout * 4, 256) + align_up((size_t)(K + 1) * 4, 256);
 }
@@ -384,13 +490,15 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, gw, part, ticket};
     return wg_tc(cin, cout, p, max_items, st);
   }
-  const int grid = std::max(1, std::min(max_items, kNumSMs * 8));
+  const int schunk = std::min(chunk, kWgSimtChunk);
+  const int sitems = (int)(cap_pairs / schunk + K + 1);
+  const int grid = std::max(1, std::min(sitems, kNumSMs * 8));
   wgrad_simt_kernel<<<grid, kWgSimtThreads, 0, st>>>(x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
-                                                     pptr, chunk, part);
+                                                     pptr, schunk, part);
   VP_CHECK_LAUNCH("conv_wgrad_simt");
   const int64_t total = (int64_t)K * cin * cout;
   wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st>>>(
-      part, pptr, K, chunk, cin * cout, gw);
+      part, pptr, K, schunk, cin * cout, gw);
   VP_CHECK_LAUNCH("wgrad_reduce");
   return VP_OK;
 }

@@ -10,6 +10,7 @@
 // partials in chunk order -> deterministic, no atomics on the values.
 #pragma once
 #include "common.cuh"
+#include "conv_fwd_tc.cuh"
 #include "tc.cuh"
 
 namespace vp {
@@ -28,6 +29,8 @@ struct WgParams {
 };
 
 constexpr int kWgMaxChunk = 2048;
+// (kTcProd / kTcEpi / kTcThreads from conv_fwd_tc.cuh: warps 0-3 produce,
+// 4-7 drain TMEM, 8 issues the MMAs)
 
 template <int CIN, int COUT>
 struct WgTC {
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_wgrad_tc_kernel(const __gr
       item_range(item, k, p0, p1);
       const int np = p1 - p0;
       asm volatile("bar.sync 1, 128;" ::: "memory");  // previous item's indices consumed
+#pragma unroll 4
       for (int i = tid; i < np; i += kTcProd) {
         s_pin[i] = __ldg(p.pin + p0 + i);
         s_pout[i] = __ldg(p.pout + p0 + i);

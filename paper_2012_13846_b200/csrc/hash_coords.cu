@@ -366,7 +366,7 @@ const char* vp_last_error(void) { return g_last_error.c_str(); }
 const char* vp_version(void) { return "voxpipe_b200 0.1.0 sm_100a"; }
 long long vp_kernel_launches(void) { return g_kernel_launches; }
 
-int64_t vp_hash_capacity(int64_t n) { return (int64_t)hash_cap_internal(n); }
+int64_t vp_hash_capacity(int64_t n) { return (int64_t)hash_cap_for(n); }
 size_t vp_hash_bytes(int64_t cap) { return (size_t)(cap + 1) * sizeof(Slot); }
 
 int vp_hash_build(const int64_t* keys, const int32_t* n_dev, int64_t cap_n, void* table,

@@ -55,25 +55,64 @@ map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t
   const bool valid = row < rows;
   const bool staged = K <= kMapSmemK;
   const int4 r = valid ? out[u0 + row] : make_int4(-1, 0, 0, 0);
-  const unsigned jmask = 0x01010101u << j;  // lanes of this warp with the same j
-  for (int kb = 0; kb < K; kb += kMapTPR) {
-    const int k = kb + j;
-    int v = -1;
-    if (valid && k < K) {
-      const long long qx = (long long)r.y + (long long)offs.d[3 * k] * sx;
-      const long long qy = (long long)r.z + (long long)offs.d[3 * k + 1] * sy;
-      const long long qz = (long long)r.w + (long long)offs.d[3 * k + 2] * sz;
-      // out-of-range queries are plain misses (kernels.py:135-148)
-      if (packable64(r.x, qx, qy, qz)) v = hash_find(t, cap, pack_key(r.x, (int)qx, (int)qy, (int)qz));
+  // Probe kMapBatch offsets at once: the first probe step of every key is
+  // issued before any result is inspected (memory-level parallelism); the
+  // rare collision chains are finished afterwards.
+  constexpr int kMapBatch = 4;
+  for (int kb = 0; kb < K; kb += kMapTPR * kMapBatch) {
+    uint64_t key[kMapBatch], slot[kMapBatch];
+    int v[kMapBatch];
+    bool live[kMapBatch];
+#pragma unroll
+    for (int b = 0; b < kMapBatch; ++b) {
+      const int k = kb + b * kMapTPR + j;
+      live[b] = false;
+      v[b] = -1;
+      key[b] = 0;
+      slot[b] = 0;
+      if (valid && k < K) {
+        const long long qx = (long long)r.y + (long long)offs.d[3 * k] * sx;
+        const long long qy = (long long)r.z + (long long)offs.d[3 * k + 1] * sy;
+        const long long qz = (long long)r.w + (long long)offs.d[3 * k + 2] * sz;
+        // out-of-range queries are plain misses (kernels.py:135-148)
+        if (packable64(r.x, qx, qy, qz)) {
+          key[b] = pack_key(r.x, (int)qx, (int)qy, (int)qz);
+          slot[b] = mix64(key[b]) & (cap - 1);
+          live[b] = key[b] != kEmptyKey;
+          if (!live[b]) v[b] = (int)~t[cap].nrow;
+        }
+      }
     }
-    if (k < K) {
-      if (staged) s_nbr[row * (kMapSmemK + 1) + k] = v;
-      else if (valid) nbr[(u0 + row) * K + k] = v;
+    uint4 sv[kMapBatch];
+#pragma unroll
+    for (int b = 0; b < kMapBatch; ++b)
+      if (live[b]) sv[b] = __ldg(reinterpret_cast<const uint4*>(t + slot[b]));
+#pragma unroll
+    for (int b = 0; b < kMapBatch; ++b) {
+      if (!live[b]) continue;
+      uint4 s4 = sv[b];
+      uint64_t s = slot[b];
+      while (true) {
+        const unsigned long long kk = ((unsigned long long)s4.y << 32) | s4.x;
+        if (kk == key[b]) { v[b] = (int)~s4.z; break; }
+        if (kk == kEmptyKey) break;
+        s = (s + 1) & (cap - 1);
+        s4 = __ldg(reinterpret_cast<const uint4*>(t + s));
+      }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, v >= 0);
-    if (lane < kMapTPR && kb + lane < K) s_cnt[warp][kb + lane] = (unsigned short)__popc(m & (0x01010101u << lane));
+#pragma unroll
+    for (int b = 0; b < kMapBatch; ++b) {
+      const int k0 = kb + b * kMapTPR;
+      if (k0 >= K) break;
+      const int k = k0 + j;
+      if (k < K) {
+        if (staged) s_nbr[row * (kMapSmemK + 1) + k] = v[b];
+        else if (valid) nbr[(u0 + row) * K + k] = v[b];
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, v[b] >= 0);
+      if (lane < kMapTPR && k0 + lane < K) s_cnt[warp][k0 + lane] = (unsigned short)__popc(m & (0x01010101u << lane));
+    }
   }
-  (void)jmask;
   __syncthreads();
   if (staged) {
     int32_t* dst = nbr + u0 * K;

@@ -269,7 +269,7 @@ class SparseResNetTrainer:
     def _conv_bn(self, L, x, res, relu, st):
         dst = L["dst"]
         fc = self.fcode
-        self._c("vp_conv_fwd", x.data_ptr(), fc, L["cin"], L["wb"].data_ptr(), L["wcode"], L["cout"],
+        self._c("vp_conv_fwd", x.data_ptr(), fc, x.shape[0], L["cin"], L["wb"].data_ptr(), L["wcode"], L["cout"],
                 self.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(), fc,
                 L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
         self._c("vp_bn_stats", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
@@ -324,7 +324,7 @@ class SparseResNetTrainer:
             table, flip = m.nbr, 1  # stride 1, symmetric 3^3: inv[v,k] == nbr[v,K-1-k]
         else:
             table, flip = m.inv, 0
-        self._c("vp_conv_dgrad", L["gy"].data_ptr(), fc, L["cout"], L["wb"].data_ptr(), L["wcode"],
+        self._c("vp_conv_dgrad", L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(), L["wcode"],
                 L["cin"], self.K, table.data_ptr(), flip, src.n.data_ptr(), src.cap, gin.data_ptr(), fc,
                 L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
         return gin
