@@ -285,45 +285,19 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(tr, dev, iters=50):
-    """Dominant tensor-core kernel of the step: the conv forward with the most
-    useful FLOPs (2 * pairs * C_in * C_out), relaunched standalone on the
-    step's own activations/maps.  Also reports the kernel-map builder's
-    algorithmic GB/s (16 N_in + 16 N_out + 8 P) for the largest map."""
-    import torch
-
-    from paper_2012_13846_b200 import _lib
-
-    peaks = {}
+def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-        src = "measured"
+            return json.load(f), "measured"
     except OSError:
-        src = "fallback"
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    tc_peak = peaks.get("bf16_tflops", 1590.0)
-    best = None
-    for L in tr.layers:
-        if L["cin"] < 32:
-            continue
-        P = int(L["map"].ptr[-1].item())
-        fl = 2.0 * P * L["cin"] * L["cout"]
-        if best is None or fl > best[0]:
-            best = (fl, L, P)
-    fl, L, P = best
+        return {}, "fallback"
+
+
+def _time_launch(launch, iters):
+    import torch
+
     st = torch.cuda.current_stream()
-    dst = L["dst"]
-    n_out = int(dst.n.item())
-    n_in = int(L["src"].n.item())
-
-    def launch():
-        _lib.call("vp_conv_fwd", L["x"].data_ptr(), _lib.VP_BF16, L["x"].shape[0], L["cin"], L["wb"].data_ptr(),
-                  _lib.VP_BF16,
-                  L["cout"], tr.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(),
-                  _lib.VP_BF16, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st.cuda_stream)
-
-    for _ in range(5):
+    for _ in range(3):
         launch()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -332,20 +306,81 @@ def roofline(tr, dev, iters=50):
         launch()
     b.record(st)
     torch.cuda.synchronize()
-    t = a.elapsed_time(b) / iters / 1e3
+    return a.elapsed_time(b) / iters / 1e3
+
+
+def _ncu_traffic(kernel_key):
+    """dram read+write bytes per launch of `kernel_key` from the committed ncu
+    --set full summary (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+def roofline(tr, dev, iters=30):
+    """Roofline of the dominant tensor-core kernel of the step and of the
+    kernel-map builder, each relaunched standalone on the step's own data
+    (CUDA events on the launching stream, warm L2).
+
+    Dominant kernel = the conv forward (vp_conv_fwd, tcgen05 path) with the
+    largest device time per launch.  Algorithmic work per launch (SURVEY
+    §8(d)): F = 2 * P * C_in * C_out useful FLOPs; compulsory bytes
+    B = 2 N_in C_in + 2 N_out C_out + 2*27*C_in*C_out + 4*27*N_out (neighbour
+    table).  Bound = tensor if F/B * HBM > tensor peak, else hbm.
+    Map: B_map = 16 N_in + 16 N_out + 8 P for the largest stride-1 map."""
+    import torch
+
+    from paper_2012_13846_b200 import _lib
+
+    peaks, src = _peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    tc_peak = peaks.get("bf16_tflops", 1590.0)
+    st = torch.cuda.current_stream()
+    rows = []
+    for L in tr.layers:
+        if L["cin"] < 32:
+            continue
+        dst = L["dst"]
+
+        def launch(L=L, dst=dst):
+            _lib.call("vp_conv_fwd", L["x"].data_ptr(), _lib.VP_BF16, L["x"].shape[0], L["cin"], L["wb"].data_ptr(),
+                      _lib.VP_BF16, L["cout"], tr.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap,
+                      L["y"].data_ptr(), _lib.VP_BF16, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st.cuda_stream)
+
+        rows.append((_time_launch(launch, iters), L))
+    t, L = max(rows, key=lambda r: r[0])
+    P = int(L["map"].ptr[-1].item())
+    n_out, n_in = int(L["dst"].n.item()), int(L["src"].n.item())
+    fl = 2.0 * P * L["cin"] * L["cout"]
     byts = 2 * n_in * L["cin"] + 2 * n_out * L["cout"] + 2 * 27 * L["cin"] * L["cout"] + 4 * n_out * 27
-    ai = fl / byts
-    tflops = fl / t / 1e12
-    gbs = byts / t / 1e9
-    bound = "tensor" if ai * hbm / 1e3 > tc_peak else "hbm"
-    if bound == "tensor":
-        ach, peak, unit = tflops, tc_peak, "TFLOP/s"
-    else:
-        ach, peak, unit = gbs, hbm, "GB/s"
-    return {"kernel": f"conv_fwd_tc<{L['cin']},{L['cout']}> layer {L['name']} (N_out={n_out}, pairs={P})",
-            "bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit, "frac": round(ach / peak, 4),
-            "traffic": None, "peak_source": src, "us_per_launch": round(t * 1e6, 2),
-            "algorithmic_flops": fl, "algorithmic_bytes": byts, "tflops": round(tflops, 2), "gbs": round(gbs, 1)}
+    tflops, gbs = fl / t / 1e12, byts / t / 1e9
+    bound = "tensor" if (fl / byts) * hbm / 1e3 > tc_peak else "hbm"
+    ach, peak, unit = (tflops, tc_peak, "TFLOP/s") if bound == "tensor" else (gbs, hbm, "GB/s")
+    key = f"conv_fwd_tc<{L['cin']},{L['cout']}>"
+    out = {"kernel": f"{key} layer {L['name']} (N_out={n_out}, pairs={P})", "bound": bound,
+           "achieved": round(ach, 2), "peak": peak, "unit": unit, "frac": round(ach / peak, 4),
+           "traffic": _ncu_traffic(key), "peak_source": src, "us_per_launch": round(t * 1e6, 2),
+           "algorithmic_flops": fl, "algorithmic_bytes": byts, "tflops": round(tflops, 2), "gbs": round(gbs, 1),
+           "per_layer_fwd_us": {l["name"]: round(tt * 1e6, 1) for tt, l in rows}}
+    # kernel map builder (hash + probe + ordered pair compaction), level 0 stride-1
+    m = tr.map_s1[0]
+    ist = _lib.i32_array((1, 1, 1))
+
+    def map_launch():
+        _lib.call("vp_kernel_map", m.src.coords.data_ptr(), m.src.n.data_ptr(), m.src.cap, m.dst.coords.data_ptr(),
+                  m.dst.n.data_ptr(), m.dst.cap, tr.offs3, tr.K, ist, m.nbr.data_ptr(), m.pin.data_ptr(),
+                  m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st.cuda_stream)
+
+    tm = _time_launch(map_launch, iters)
+    nm = int(m.src.n.item())
+    pm = int(m.ptr[-1].item())
+    bm = 16 * nm + 16 * nm + 8 * pm
+    out["map"] = {"kernel": f"vp_kernel_map level0 stride-1 (N={nm}, pairs={pm})", "bound": "hbm",
+                  "achieved": round(bm / tm / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                  "frac": round(bm / tm / 1e9 / hbm, 4), "us_per_call": round(tm * 1e6, 2), "algorithmic_bytes": bm}
+    return out
 
 
 if __name__ == "__main__":

@@ -179,6 +179,10 @@ class SparseResNetTrainer:
         self.xent_ws = _lib.workspace(_lib.query("vp_linear_xent_ws_bytes", batch, classes), dev)
         self.graph: Optional[torch.cuda.CUDAGraph] = None
         self.launch_count = 0
+        # side streams: the coordinate chain, kernel maps and weight gradients
+        # run off the critical path (parallel branches of the captured graph)
+        self.concurrent = True
+        self.side = [torch.cuda.Stream(device=dev) for _ in range(4)]
 
     # ------------------------------------------------------------------ setup
     def _width_at(self, level):
@@ -247,28 +251,71 @@ class SparseResNetTrainer:
         self.launch_count += 1
         _lib.call(name, *args)
 
+    def _build_map(self, m, st):
+        ist = _lib.i32_array((m.src.stride,) * 3)
+        self._c("vp_kernel_map", m.src.coords.data_ptr(), m.src.n.data_ptr(), m.src.cap, m.dst.coords.data_ptr(),
+                m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(), m.pin.data_ptr(),
+                m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st)
+        if m.inv is not None:
+            self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
+                    m.inv.data_ptr(), m.src.cap, st)
+
     def _integer_stage(self, st):
+        """Voxelize -> strided coordinate chain -> the 9 kernel maps.  With
+        `concurrent`, the coordinate chain and the maps of levels >= 1 run on
+        side streams (waiting only on the level they read), overlapping the
+        level-0 map and the first convolutions on the main stream."""
         lv = self.levels
         res3 = _lib.i32_array((self.res,) * 3)
         self._c("vp_voxelize", self.points.data_ptr(), _lib.dtype_code(self.points), self.cap, self.offsets.data_ptr(),
                 self.B, float(self.voxel_size), res3, lv[0].coords.data_ptr(), lv[0].n.data_ptr(), None,
                 self.feat0.data_ptr(), self.fcode, self.vox_ws.data_ptr(), self.vox_ws.numel(), st)
-        for i in range(1, len(lv)):
-            step = _lib.i32_array((lv[i].stride,) * 3)
-            self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
-                    lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(), st)
-        for m in self.map_s1 + self.map_dn:
-            ist = _lib.i32_array((m.src.stride,) * 3)
-            self._c("vp_kernel_map", m.src.coords.data_ptr(), m.src.n.data_ptr(), m.src.cap, m.dst.coords.data_ptr(),
-                    m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(), m.pin.data_ptr(),
-                    m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st)
-            if m.inv is not None:
-                self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
-                        m.inv.data_ptr(), m.src.cap, st)
+        self.map_events = {}
+        if not self.concurrent:
+            for i in range(1, len(lv)):
+                step = _lib.i32_array((lv[i].stride,) * 3)
+                self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
+                        lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
+                        st)
+            for m in self.map_s1 + self.map_dn:
+                self._build_map(m, st)
+            return
+        main = torch.cuda.current_stream()
+        chain = self.side[0]
+        chain.wait_stream(main)
+        lev_ev = [None] * len(lv)
+        with torch.cuda.stream(chain):
+            cs = chain.cuda_stream
+            for i in range(1, len(lv)):
+                step = _lib.i32_array((lv[i].stride,) * 3)
+                self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
+                        lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
+                        cs)
+                lev_ev[i] = torch.cuda.Event()
+                lev_ev[i].record(chain)
+        self._build_map(self.map_s1[0], st)  # needed first (stem), on the critical path
+        plan = []
+        for i in range(len(lv) - 1):
+            plan.append((self.map_dn[i], i + 1))
+            plan.append((self.map_s1[i + 1], i + 1))
+        for j, (m, need) in enumerate(plan):
+            side = self.side[1 + (j % 2)]
+            side.wait_event(lev_ev[need])
+            with torch.cuda.stream(side):
+                self._build_map(m, side.cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            self.map_events[id(m)] = ev
+
+    def _wait_map(self, m):
+        ev = getattr(self, "map_events", {}).get(id(m))
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
 
     def _conv_bn(self, L, x, res, relu, st):
         dst = L["dst"]
         fc = self.fcode
+        self._wait_map(L["map"])
         self._c("vp_conv_fwd", x.data_ptr(), fc, x.shape[0], L["cin"], L["wb"].data_ptr(), L["wcode"], L["cout"],
                 self.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(), fc,
                 L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
@@ -314,9 +361,17 @@ class SparseResNetTrainer:
                 L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(), fc, _lib.ptr(g_res),
                 L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
         x = L["x"]
-        self._c("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
-                self.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(),
-                L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st)
+        if self.concurrent:  # weight gradient off the critical path
+            ws = self.side[3 - (L["index"] % 2)]
+            ws.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(ws):
+                self._c("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
+                        self.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(),
+                        L["gw"].data_ptr(), L["wg_ws"].data_ptr(), L["wg_ws"].numel(), ws.cuda_stream)
+        else:
+            self._c("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
+                    self.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(),
+                    L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st)
         if not need_dgrad:
             return None
         gin = self.gact[self.levels.index(src)]
@@ -358,6 +413,10 @@ class SparseResNetTrainer:
 
     def _optimizer(self, st):
         pb = self.params
+        if self.concurrent:
+            main = torch.cuda.current_stream()
+            for sd in self.side:
+                main.wait_stream(sd)
         if self.grad_allreduce is not None:
             self.grad_allreduce(pb.g)
         self._c("vp_sgd_momentum", pb.p.data_ptr(), pb.m.data_ptr(), pb.g.data_ptr(), pb.size, float(self.lr),

@@ -115,3 +115,15 @@ def test_loss_decreases():
     tr, pts, offs, labels = make(B=8, P=400)
     losses = [tr.train_step_from_host(pts, offs, labels) for _ in range(8)]
     assert losses[-1] < losses[0]
+
+
+def test_concurrent_streams_equal_serial():
+    """Side-stream maps / weight gradients give bit-identical results."""
+    a, pts, offs, labels = make()
+    b, _, _, _ = make()
+    b.concurrent = False
+    for _ in range(2):
+        la = a.train_step_from_host(pts, offs, labels)
+        lb = b.train_step_from_host(pts, offs, labels)
+        assert la == lb
+    assert torch.equal(a.params.p, b.params.p)
