@@ -50,7 +50,7 @@ CONFIG = {"workload": "C3: sparse-ResNet classifier, 64 clouds x 2048 pts/cloud 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=64)
@@ -65,15 +65,43 @@ def parse():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region (NVML via
+    nvidia_ml_py, polled every ~2 ms from a thread, so even a short timed
+    region gets samples); falls back to `nvidia-smi -lms` when NVML is absent."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.nvml = index, [], None, None
+        self.stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        bits = [0x8, 0x40, 0x20, 0x4]  # HwSlowdown, HwThermalSlowdown, SwThermalSlowdown, SwPowerCap
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append([str(sm), str(self.max_sm)] + ["Active" if rs & b else "Not Active" for b in bits])
+            except Exception:
+                return
+            time.sleep(0.002)
 
     def __enter__(self):
+        if self.nvml is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -89,6 +117,9 @@ class ClockSampler:
             self.rows.append([v.strip() for v in line.split(",")])
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -101,10 +132,9 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def cpu_baseline(args, steps=2, warmup=1, seed=0):
@@ -364,20 +394,23 @@ def roofline(tr, dev, iters=30):
            "traffic": _ncu_traffic(key), "peak_source": src, "us_per_launch": round(t * 1e6, 2),
            "algorithmic_flops": fl, "algorithmic_bytes": byts, "tflops": round(tflops, 2), "gbs": round(gbs, 1),
            "per_layer_fwd_us": {l["name"]: round(tt * 1e6, 1) for tt, l in rows}}
-    # kernel map builder (hash + probe + ordered pair compaction), level 0 stride-1
+    # kernel-map builder as the step runs it, level 0 stride-1: index insert
+    # (dense grid, or hash) + probe + ordered pair compaction (+ grid clear)
     m = tr.map_s1[0]
-    ist = _lib.i32_array((1, 1, 1))
 
     def map_launch():
-        _lib.call("vp_kernel_map", m.src.coords.data_ptr(), m.src.n.data_ptr(), m.src.cap, m.dst.coords.data_ptr(),
-                  m.dst.n.data_ptr(), m.dst.cap, tr.offs3, tr.K, ist, m.nbr.data_ptr(), m.pin.data_ptr(),
-                  m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st.cuda_stream)
+        if tr.use_grid:
+            tr._grid_set(0, st.cuda_stream, clear=False)
+        tr._build_map(m, st.cuda_stream)
+        if tr.use_grid:
+            tr._grid_set(0, st.cuda_stream, clear=True)
 
     tm = _time_launch(map_launch, iters)
     nm = int(m.src.n.item())
     pm = int(m.ptr[-1].item())
     bm = 16 * nm + 16 * nm + 8 * pm
-    out["map"] = {"kernel": f"vp_kernel_map level0 stride-1 (N={nm}, pairs={pm})", "bound": "hbm",
+    name = "vp_grid_set + vp_kernel_map_grid" if tr.use_grid else "vp_kernel_map"
+    out["map"] = {"kernel": f"{name} level0 stride-1 (N={nm}, pairs={pm})", "bound": "hbm",
                   "achieved": round(bm / tm / 1e9, 1), "peak": hbm, "unit": "GB/s",
                   "frac": round(bm / tm / 1e9 / hbm, 4), "us_per_call": round(tm * 1e6, 2), "algorithmic_bytes": bm}
     return out

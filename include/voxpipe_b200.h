@@ -47,6 +47,9 @@ const char* vp_version(void);
 /* diagnostic: number of kernels this thread has enqueued through the library
  * (bench.py's gpu_launches claim; a CUDA graph capture counts each node once) */
 long long vp_kernel_launches(void);
+/* diagnostics: record a clock64 timeline of CTA 0 of the conv kernels into
+ * buf (device, >= 1280 int64; null disables) — see conv_fwd_tc.cuh */
+int vp_debug_conv_trace(long long* buf);
 
 /* ---------------------------------------------------------------- hash
  * Replaces _kernels.pyx:24-47 `build_table` and :50-73 `lookup` (the
@@ -126,6 +129,19 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
                   const int32_t* offsets_host, int32_t K, const int32_t* in_stride_host3,
                   int32_t* nbr, int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr,
                   void* ws, size_t ws_bytes, vp_stream_t stream);
+/* Dense-grid index for bounded lattices (batch < B, every axis a multiple
+ * of s in [0, R*s)): cells [B*R^3] int32, initialised to 0x7fffffff once by
+ * the caller; vp_grid_set writes each row's index (clear=0) or restores the
+ * empty value for exactly those cells (clear=1) so the grid is reusable.
+ * vp_kernel_map_grid is build_kernel_map with the grid as the index: the
+ * same nbr / pair outputs, bit-exact with the hash path on such lattices. */
+int vp_grid_set(const int32_t* coords, const int32_t* n_dev, int64_t cap, int32_t* cells, int32_t B,
+                int32_t R, int32_t s, int32_t clear, vp_stream_t stream);
+size_t vp_kernel_map_grid_ws_bytes(int64_t cap_out, int32_t K);
+int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, const int32_t* out,
+                       const int32_t* n_out_dev, int64_t cap_out, const int32_t* offsets_host, int32_t K,
+                       const int32_t* in_stride_host3, int32_t* nbr, int32_t* pair_in, int32_t* pair_out,
+                       int32_t* pair_ptr, void* ws, size_t ws_bytes, vp_stream_t stream);
 /* inverse neighbour table inv[v, k] = u for every pair (v,u) of offset k
  * (the dgrad gather table; conv.py:238-240 iterates the same pairs). */
 int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out,

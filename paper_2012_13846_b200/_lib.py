@@ -31,6 +31,7 @@ SIGNATURES = {
     "vp_last_error": (C.c_char_p, []),
     "vp_version": (C.c_char_p, []),
     "vp_kernel_launches": (C.c_longlong, []),
+    "vp_debug_conv_trace": (C.c_int, [P]),
     "vp_hash_capacity": (I64, [I64]),
     "vp_hash_bytes": (SZ, [I64]),
     "vp_hash_build": (C.c_int, [P, P, I64, P, I64, P]),
@@ -48,6 +49,9 @@ SIGNATURES = {
     "vp_kernel_map_ws_bytes": (SZ, [I64, I64, I32]),
     "vp_kernel_map": (C.c_int, [P, P, I64, P, P, I64, P, I32, P, P, P, P, P, P, SZ, P]),
     "vp_kernel_map_inverse": (C.c_int, [P, P, I64, I32, P, I64, P]),
+    "vp_grid_set": (C.c_int, [P, P, I64, P, I32, I32, I32, I32, P]),
+    "vp_kernel_map_grid_ws_bytes": (SZ, [I64, I32]),
+    "vp_kernel_map_grid": (C.c_int, [P, I32, I32, I32, P, P, I64, P, I32, P, P, P, P, P, P, SZ, P]),
     "vp_conv_fwd_ws_bytes": (SZ, [I64, I64, I32]),
     "vp_conv_fwd": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, I64, P, I32, P, SZ, P]),
     "vp_conv_dgrad_ws_bytes": (SZ, [I64, I64, I32]),

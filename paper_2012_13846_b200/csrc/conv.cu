@@ -294,21 +294,28 @@ static bool tc_width(int64_t c) { return c == 32 || c == 64 || c == 128 || c == 
 
 constexpr int kMaxSplit = 8;
 
-template <int KD, int ND, bool BMN>
+template <int KD, int ND, bool BMN, int CPS, int RB>
 static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
-  using C = FwdTC<KD, ND, BMN>;
-  auto kern = conv_tc_kernel<KD, ND, BMN>;
-  static bool attr = false;  // immutable per-instantiation attribute cache
+  using C = FwdTC<KD, ND, BMN, CPS, RB>;
+  const bool tbl = p0.K <= kTblK && ((uintptr_t)p0.table & 15) == 0;
+  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true> : conv_tc_kernel<KD, ND, BMN, CPS, RB, false>;
+  static_assert(C::SMEM_MAX <= 227 * 1024, "conv_tc: shared memory over the per-CTA limit");
+  static bool attr_t = false, attr_f = false;  // immutable per-instantiation attribute cache
+  bool& attr = tbl ? attr_t : attr_f;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    VP_REQUIRE(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_MAX) == cudaSuccess,
+               VP_EINTERNAL, "conv_tc: cannot reserve shared memory");
     attr = true;
   }
   const int64_t tiles = ceil_div(p0.cap_out, 128);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * kMaxSplit, kNumSMs));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * kMaxSplit, (int64_t)kNumSMs * CPS));
   FwdParams p = p0;
   p.part = (float*)part;
   p.max_split = part ? kMaxSplit : 1;
-  kern<<<grid, kTcThreads, C::SMEM, st>>>(p);
+  p.stage_tbl = tbl;
+  static const int dbg = getenv("VP_CONV_DBG") ? atoi(getenv("VP_CONV_DBG")) : 0;
+  p.dbg = dbg;
+  kern<<<grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st>>>(p);
   VP_CHECK_LAUNCH("conv_tc");
   if (part) {
     const int64_t work = p.cap_out * ND / 4;
@@ -319,13 +326,52 @@ static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   return VP_OK;
 }
 
+// (CTAs per SM, atoms per stage) candidates for the gather-bound implicit
+// GEMM; conv_cfg picks one per output width (VP_CONV_CFG=i overrides, for
+// tuning).  Infeasible ones (ring < 2 stages, TMEM) fall through.
+constexpr int kCfgCps[] = {1, 1, 2, 2, 3};
+constexpr int kCfgRb[] = {2, 1, 2, 1, 1};
+
+static int conv_cfg(int64_t nd) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("VP_CONV_CFG");
+    env = e ? atoi(e) : -1;
+  }
+  if (env >= 0 && env < 5) return env;
+  return 3;
+}
+
+template <int KD, int ND, bool BMN, int I>
+static int try_cfg(const FwdParams& p, void* part, cudaStream_t st) {
+  using C = FwdTC<KD, ND, BMN, kCfgCps[I], kCfgRb[I]>;
+  if constexpr (C::FITS) return launch_conv_tc<KD, ND, BMN, kCfgCps[I], kCfgRb[I]>(p, part, st);
+  return -1;
+}
+
+template <int KD, int ND, bool BMN>
+static int launch_conv_tc_cfg(const FwdParams& p, void* part, cudaStream_t st) {
+  int r = -1;
+  switch (conv_cfg(ND)) {
+    case 0: r = try_cfg<KD, ND, BMN, 0>(p, part, st); break;
+    case 1: r = try_cfg<KD, ND, BMN, 1>(p, part, st); break;
+    case 2: r = try_cfg<KD, ND, BMN, 2>(p, part, st); break;
+    case 3: r = try_cfg<KD, ND, BMN, 3>(p, part, st); break;
+    case 4: r = try_cfg<KD, ND, BMN, 4>(p, part, st); break;
+  }
+  if (r >= 0) return r;
+  r = try_cfg<KD, ND, BMN, 0>(p, part, st);  // (1, 2): fits every width but 256
+  if (r >= 0) return r;
+  return launch_conv_tc<KD, ND, BMN, 1, 1>(p, part, st);
+}
+
 template <int KD, bool BMN>
 static int conv_tc_nd(int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
   switch (nd) {
-    case 32: return launch_conv_tc<KD, 32, BMN>(p, part, st);
-    case 64: return launch_conv_tc<KD, 64, BMN>(p, part, st);
-    case 128: return launch_conv_tc<KD, 128, BMN>(p, part, st);
-    case 256: return launch_conv_tc<KD, 256, BMN>(p, part, st);
+    case 32: return launch_conv_tc_cfg<KD, 32, BMN>(p, part, st);
+    case 64: return launch_conv_tc_cfg<KD, 64, BMN>(p, part, st);
+    case 128: return launch_conv_tc_cfg<KD, 128, BMN>(p, part, st);
+    case 256: return launch_conv_tc_cfg<KD, 256, BMN>(p, part, st);
   }
   return VP_EINTERNAL;
 }
@@ -393,6 +439,12 @@ using namespace vp;
 
 extern "C" {
 
+int vp_debug_conv_trace(long long* buf) {
+  cudaMemcpyToSymbol(g_conv_trace, &buf, sizeof(buf));
+  VP_CHECK_ASYNC("debug_conv_trace");
+  return VP_OK;
+}
+
 size_t vp_conv_fwd_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
   return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cout);
 }
@@ -416,7 +468,7 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
       wb = (const bf16*)ws;
     }
     (void)x_rows;  // the cp.async gather zero-fills missing neighbours itself
-    FwdParams p{(const bf16*)x, wb, K, table, flip, n_out_dev, cap_out, y, y_dtype, nullptr, 1};
+    FwdParams p{(const bf16*)x, wb, K, table, flip, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
     return conv_tc<false>(cin, cout, p, part, st);
   }
   if (small_fwd_ok(cin, cout, K)) return launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip,
@@ -452,7 +504,7 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
     }
     // grad_in = sum_k W_k^T g[table]: GEMM K-dim = C_out, N = C_in, W read as MN-major B
     (void)g_rows;
-    FwdParams p{(const bf16*)g, wb, K, table, flip, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1};
+    FwdParams p{(const bf16*)g, wb, K, table, flip, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1, 0, 0};
     return conv_tc<true>(cout, cin, p, part, st);
   }
   const int64_t total = cap_in * cin;

@@ -8,13 +8,16 @@
 //
 // CTA = 9 warps: warps 0-3 produce (cp.async gathers of 128 neighbour rows +
 // the weight slice into a 128B-swizzled stage ring, completion signalled per
-// stage on an mbarrier after a proxy fence), warp 8 issues tcgen05.mma from
+// stage on an mbarrier; 8 lanes per row so one warp instruction moves 4 whole
+// 128 B lines), warp 8 issues tcgen05.mma from
 // one elected lane into a double-buffered TMEM accumulator, warps 4-7 drain
 // TMEM (tcgen05.ld) and store each output row exactly once.  Work items are
 // (128-row tile, split) pairs; when the tile count cannot fill the grid the
 // active offsets of a tile are split across CTAs (fp32 partials, reduced in a
 // fixed order afterwards) -> deterministic with no atomics on the output.
-// C_in = 32 packs two offsets into one 64-wide K stage.
+// C_in = 32 packs two offsets into one 64-wide K stage.  CPS CTAs share an SM
+// (smem ring and TMEM sized to fit): random-row gather throughput scales with
+// independent CTAs per SM far more than with ring depth (tools/gather_probe2).
 #pragma once
 #include "common.cuh"
 #include "tc.cuh"
@@ -35,28 +38,54 @@ struct FwdParams {
   int y_dtype;
   float* part;    // split-K partials (grid * 128 * ND floats), may be null if max_split == 1
   int max_split;  // >= 1
+  int stage_tbl;  // stage table tiles in smem (K <= kTblK, 16 B-aligned table); set by the launcher
+  int dbg;        // experiments only: bit0 no MMA, bit1 no B copies, bit2 no A copies, bit3 plain arrive for empty
 };
 
 constexpr int kTcProd = 128, kTcEpi = 128, kTcThreads = kTcProd + kTcEpi + 32;
-constexpr int kNbrSmemK = 32;  // neighbour table cached in smem when K <= 32
+constexpr int kNbrSmemK = 32;  // (wgrad) neighbour table cached in smem when K <= 32
 constexpr int kTcMaskWords = (VP_MAX_OFFSETS + 31) / 32;
+constexpr int kTblK = 32;  // K <= kTblK: each tile's [128, K] table is staged in smem by TMA
 
-template <int KD, int ND, bool BMN>
+// Debug timeline of CTA 0 (clock64), off unless vp_debug_conv_trace() set a
+// buffer: stage events [g][4] at slot g < 256 (producer slot acquired,
+// producer issued, MMA saw full, MMA committed), tile events at 1024 + 4*ii
+// (prologue start, work published, epilogue got accumulator, epilogue done).
+__device__ long long* g_conv_trace = nullptr;
+#define trace_ev(idx, on)                           \
+  do {                                              \
+    if (trc != nullptr && (on)) trc[idx] = clock64(); \
+  } while (0)
+
+constexpr int tmem_cols_pow2(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+// A stage holds RB "atoms": one unit each (a 128-row x 64-element bf16 A
+// slab, 128 B swizzled rows, plus the matching [ND x 64] weight slab).  Big
+// stages amortise the per-stage cost (barrier round trip, row lookups) that
+// bounds small-row gathers (tools/gather_probe2: ~2x per 16 KB at RB=2).
+template <int KD, int ND, bool BMN, int CPS, int RB>
 struct FwdTC {
   static constexpr bool PAIR = (KD == 32);
   static constexpr int NCH = PAIR ? 1 : KD / 64;
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int NPAD = (BMN && ND < 64) ? 64 : ND;
   static constexpr int B_BYTES = NPAD * 128;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (180 * 1024) / STAGE;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 3 ? 3 : STAGES_RAW);
-  static constexpr int ACC = (2 * ND <= 512) ? 2 : 1;
+  static constexpr int STAGE = RB * (A_BYTES + B_BYTES);
+  static constexpr int BOOK = 4096;
+  // two [128, K <= kTblK] neighbour-table tiles (double buffer)
+  static constexpr int TBL_RESERVE = 2 * 128 * kTblK * 4;
+  // 228 KB of shared memory per SM, 1 KB reserved per CTA, 1 KB alignment slack
+  static constexpr int BUDGET = (228 * 1024) / CPS - 2048 - BOOK - TBL_RESERVE;
+  static constexpr int STAGES_RAW = BUDGET / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr bool FITS = STAGES_RAW >= 2 && tmem_cols_pow2(ND) * CPS <= 512;
+  static constexpr int ACC = (tmem_cols_pow2(2 * ND) * CPS <= 512) ? 2 : 1;
   static constexpr int COLS = ACC * ND;
-  static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
+  static constexpr int TMEM_COLS = tmem_cols_pow2(COLS);
   static constexpr uint32_t IDESC = tc::idesc_bf16(128, ND, 0, BMN ? 1 : 0);
-  static constexpr int BOOK = 4096 + 128 * (kNbrSmemK + 1) * 4;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + BOOK;
+  static constexpr int SMEM_BASE = STAGES * STAGE + 1024 + BOOK;
+  static constexpr int SMEM_MAX = SMEM_BASE + 2 * 128 * kTblK * 4;
+  static int smem_bytes(int K, bool tbl) { return SMEM_BASE + (tbl ? 2 * 128 * K * 4 : 0); }
 };
 
 __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) {
@@ -65,9 +94,9 @@ __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) 
   return s > max_split ? max_split : s;
 }
 
-template <int KD, int ND, bool BMN>
-__global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_constant__ FwdParams p) {
-  using C = FwdTC<KD, ND, BMN>;
+template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL>
+__global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_constant__ FwdParams p) {
+  using C = FwdTC<KD, ND, BMN, CPS, RB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* book = smem + C::STAGES * C::STAGE;
@@ -78,17 +107,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   uint64_t* ifull = tempty + C::ACC;
   uint64_t* iempty = ifull + 2;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(iempty + 2);
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(book + 256);   // [2] table-tile arrivals
   int* s_info = reinterpret_cast<int*>(book + 512);          // [2] units per work item (for MMA)
   int* s_work = s_info + 4;                                  // u0, n_units, n_act (producers)
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(book + 640);
   int16_t* s_act = reinterpret_cast<int16_t*>(book + 1024);  // <= 343 entries
-  int32_t* s_nbr = reinterpret_cast<int32_t*>(book + 4096);  // [128][kNbrSmemK+1]
+  int32_t* s_tbl = reinterpret_cast<int32_t*>(book + C::BOOK);  // [2][128 * K] when K <= kTblK
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
+  long long* const trc = blockIdx.x == 0 ? g_conv_trace : nullptr;
   const int n_out = load_count(p.n_out_dev, p.cap_out);
   const int ntiles = (n_out + 127) / 128;
-  const int S = split_count(ntiles, gridDim.x, p.max_split);
+  // split partials are sized for kNumSMs work items
+  const int S = split_count(ntiles, min((int)gridDim.x, kNumSMs), p.max_split);
   const int total = ntiles * S;
   if ((int)blockIdx.x >= total) return;
 
@@ -104,6 +136,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&ifull[i], 1);
       tc::mbar_init(&iempty[i], 1);
+      tc::mbar_init(&tbar[i], 1);
     }
     tc::fence_mbar_init();
   }
@@ -113,120 +146,175 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
   tc::tc_fence_after();
   const uint32_t tmem = *s_tmem;
   const uint32_t sbase = tc::smem_u32(smem);
-  const bool nbr_smem = K <= kNbrSmemK;
 
   if (warp < 4) {
     // ============================ producers ============================
+    constexpr bool tbl = TBL;
+    // stage work item w's [rows, K] table block into buffer `buf` (thread 0):
+    // one bulk copy of the 16 B-aligned prefix, the <= 3 trailing entries by
+    // hand before the arrive (its release orders them)
+    auto issue_tbl = [&](int w, int buf) {
+      const int tile = w / S;
+      const int nel = min(128, n_out - tile * 128) * K;
+      const int32_t* src = p.table + (int64_t)tile * 128 * K;
+      int32_t* dst = s_tbl + buf * 128 * K;
+      const int pre = nel & ~3;
+      for (int e = pre; e < nel; ++e) dst[e] = __ldg(src + e);
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive_expect_tx(&tbar[buf], (uint32_t)pre * 4);
+      if (pre > 0) tc::bulk_g2s(tc::smem_u32(dst), src, (uint32_t)pre * 4, &tbar[buf]);
+    };
+    if (tbl && tid == 0) issue_tbl(blockIdx.x, 0);
     uint32_t g = 0;
     int ii = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++ii) {
+      trace_ev(1024 + 4 * (ii & 63), tid == 0);
       const int tile = w / S, split = w - (w / S) * S;
-      const int64_t u = (int64_t)tile * 128 + tid;
-      const bool valid = u < n_out;
-      const int32_t* trow = p.table + u * K;
+      const int rows = min(128, n_out - tile * 128);
+      const int32_t* tt = s_tbl + (ii & 1) * 128 * K;  // this tile's staged table
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tid < kTcMaskWords) s_mask[tid] = 0;
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      for (int kb = 0; kb < K; kb += 32) {
-        uint32_t bits = 0;
-        const int kend = min(32, K - kb);
-        for (int j = 0; j < kend; ++j) {
-          const int k = kb + j;
-          const int v = valid ? __ldg(trow + (p.flip ? K - 1 - k : k)) : -1;
-          if (nbr_smem) s_nbr[tid * (kNbrSmemK + 1) + k] = v;
-          if (v >= 0) bits |= 1u << j;
+      if (tbl) {
+        tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);
+        if (rows < 128) {  // ragged last tile: rows past the end read as misses
+          int32_t* tw = s_tbl + (ii & 1) * 128 * K;
+          for (int e = rows * K + tid; e < 128 * K; e += kTcProd) tw[e] = -1;
         }
+        uint32_t bits = 0;
+        if (tid < rows)
+          for (int k = 0; k < K; ++k)
+            if (tt[tid * K + k] >= 0) bits |= 1u << (p.flip ? K - 1 - k : k);
         bits = __reduce_or_sync(0xffffffffu, bits);
-        if (lane == 0 && bits) atomicOr(&s_mask[kb >> 5], bits);
+        if (lane == 0 && bits) atomicOr(&s_mask[0], bits);
+      } else {
+        const int32_t* trow = p.table + ((int64_t)tile * 128 + tid) * K;
+        for (int kb = 0; kb < K; kb += 32) {
+          uint32_t bits = 0;
+          const int kend = min(32, K - kb);
+          for (int j = 0; j < kend; ++j) {
+            const int k = kb + j;
+            const int v = tid < rows ? __ldg(trow + (p.flip ? K - 1 - k : k)) : -1;
+            if (v >= 0) bits |= 1u << j;
+          }
+          bits = __reduce_or_sync(0xffffffffu, bits);
+          if (lane == 0 && bits) atomicOr(&s_mask[kb >> 5], bits);
+        }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tid == 0) {
+      if (warp == 0) {
+        // active offsets in ascending order (ballot prefix per 32-offset word)
         int na = 0;
-        for (int k = 0; k < K; ++k)
-          if (s_mask[k >> 5] & (1u << (k & 31))) s_act[na++] = (int16_t)k;
-        const int nu = C::PAIR ? (na + 1) / 2 : na * C::NCH;
-        const int u0 = (int)((int64_t)nu * split / S), u1 = (int)((int64_t)nu * (split + 1) / S);
-        s_work[0] = u0;
-        s_work[1] = u1 - u0;
-        s_work[2] = na;
-        const int slot = ii & 1;
-        if (ii >= 2) tc::mbar_wait(&iempty[slot], ((ii >> 1) - 1) & 1);
-        s_info[slot] = max(u1 - u0, 1);
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&ifull[slot])) : "memory");
+        for (int kb = 0; kb < K; kb += 32) {
+          const uint32_t m = s_mask[kb >> 5];
+          if (m & (1u << lane)) s_act[na + __popc(m & ((1u << lane) - 1u))] = (int16_t)(kb + lane);
+          na += __popc(m);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const int nu = C::PAIR ? (na + 1) / 2 : na * C::NCH;
+          const int u0 = (int)((int64_t)nu * split / S), u1 = (int)((int64_t)nu * (split + 1) / S);
+          s_work[0] = u0;
+          s_work[1] = u1 - u0;
+          s_work[2] = na;
+          const int slot = ii & 1;
+          if (ii >= 2) tc::mbar_wait(&iempty[slot], ((ii >> 1) - 1) & 1);
+          s_info[slot] = max(u1 - u0, 1);
+          trace_ev(1024 + 4 * (ii & 63) + 1, true);
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&ifull[slot])) : "memory");
+          // every producer is past tile ii-1 (barrier above): its buffer is free
+          if (tbl && w + (int)gridDim.x < total) issue_tbl(w + gridDim.x, (ii + 1) & 1);
+        }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const int u0 = s_work[0], nun = s_work[1], na = s_work[2];
       const int neff = nun > 0 ? nun : 1;
-      for (int j = 0; j < neff; ++j, ++g) {
-        const int stage = g % C::STAGES;
-        if (g >= (uint32_t)C::STAGES) tc::mbar_wait(&empty[stage], ((g / C::STAGES) - 1) & 1);
-        const uint32_t a_s = sbase + stage * C::STAGE;
-        const uint32_t b_s = a_s + C::A_BYTES;
-        const int unit = u0 + j;
-        // ---- which offsets / K slice this unit covers
-        int ka, kb = -1, cs = 0;
+      // unit -> (offset of A's first half / whole row, second half, 64-col slice)
+      const uint32_t s_act_s = tc::smem_u32(s_act);
+      auto unit_k = [&](int unit, int& ka, int& kb, int& cs) {
+        kb = -1;
+        cs = 0;
         if (nun == 0) {
           ka = -1;  // zero unit: A = 0, B = any finite weights
         } else if (C::PAIR) {
-          ka = s_act[2 * unit];
-          kb = (2 * unit + 1 < na) ? s_act[2 * unit + 1] : -1;
+          ka = tc::lds_s16(s_act_s + 4 * unit);
+          kb = (2 * unit + 1 < na) ? tc::lds_s16(s_act_s + 4 * unit + 2) : -1;
         } else {
-          ka = s_act[unit / C::NCH];
+          ka = tc::lds_s16(s_act_s + 2 * (unit / C::NCH));
           cs = unit % C::NCH;
         }
-        // ---- A: row tid, 8 x 16 B chunks
-        auto nb_of = [&](int k) -> int {
-          if (k < 0 || !valid) return -1;
-          const int col = p.flip ? K - 1 - k : k;
-          return nbr_smem ? s_nbr[tid * (kNbrSmemK + 1) + k] : __ldg(trow + col);
-        };
-        if (C::PAIR) {
-          const int va = nb_of(ka), vb = nb_of(kb);
-          const bf16* sa = p.x + (int64_t)(va >= 0 ? va : 0) * KD;
-          const bf16* sb = p.x + (int64_t)(vb >= 0 ? vb : 0) * KD;
+      };
+      // A: 8 lanes per row (16 B chunk q each); this lane's rows are
+      // r_i = r0 + 4i, i < 8.  Row r_i's chunk lands at a_s + r_i*128 +
+      // ((q ^ (r_i & 7)) << 4) and r_i & 7 = (lane/8) + 4*(i&1).
+      const int q = lane & 7;
+      const int r0 = warp * 32 + (lane >> 3);
+      const uint32_t a_off0 = r0 * 128 + ((q ^ (lane >> 3)) << 4);
+      const uint32_t a_off1 = r0 * 128 + ((q ^ ((lane >> 3) + 4)) << 4);
+      const uint32_t tt_s = tc::smem_u32(tt) + r0 * K * 4;  // row r0's staged table entries
+      const int32_t* trow0 = p.table + ((int64_t)tile * 128 + r0) * K;
+      const char* xb = reinterpret_cast<const char*>(p.x);
+      const int nst = (neff + RB - 1) / RB;  // stages of this work item
+      for (int sj = 0; sj < nst; ++sj, ++g) {
+        const int stage = g % C::STAGES;
+        if (g >= (uint32_t)C::STAGES) tc::mbar_wait(&empty[stage], ((g / C::STAGES) - 1) & 1);
+        const uint32_t s_base = sbase + stage * C::STAGE;
+        const int na_st = min(RB, neff - sj * RB);  // atoms in use (the MMA skips the rest)
+#pragma unroll 1
+        for (int at = 0; at < na_st; ++at) {
+          const uint32_t a_s = s_base + at * C::A_BYTES;
+          const uint32_t b_s = s_base + RB * C::A_BYTES + at * C::B_BYTES;
+          const int unit = u0 + sj * RB + at;
+          int ka, kb, cs;
+          unit_k(unit, ka, kb, cs);
+          {
+            const int kq = C::PAIR ? (q < 4 ? ka : kb) : ka;
+            const int col = p.flip ? K - 1 - kq : kq;
+            const char* xq = xb + 2 * (C::PAIR ? (q & 3) * 8 : cs * 64 + q * 8);
+            int vr[8];
+            const bool noa = p.dbg & 4;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) tc::cp_async16(a_s + tid * 128 + ((q ^ (tid & 7)) << 4), sa + q * 8, va >= 0 ? 16 : 0);
-#pragma unroll
-          for (int q = 4; q < 8; ++q)
-            tc::cp_async16(a_s + tid * 128 + ((q ^ (tid & 7)) << 4), sb + (q - 4) * 8, vb >= 0 ? 16 : 0);
-        } else {
-          const int va = nb_of(ka);
-          const bf16* sa = p.x + (int64_t)(va >= 0 ? va : 0) * KD + cs * 64;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) tc::cp_async16(a_s + tid * 128 + ((q ^ (tid & 7)) << 4), sa + q * 8, va >= 0 ? 16 : 0);
-        }
-        // ---- B
-        const int kA = ka >= 0 ? ka : 0;
-        const int kB = kb >= 0 ? kb : kA;
-        if (!BMN) {  // B[n][kk] = W[k][n][slice]  (K-major rows of W)
-          constexpr int CH = ND * 8;
-#pragma unroll
-          for (int e = tid; e < CH; e += kTcProd) {
-            const int n = e >> 3, q = e & 7;
-            const bf16* src;
-            if (C::PAIR) {
-              const int k = q < 4 ? kA : kB;
-              src = p.w + ((int64_t)k * ND + n) * KD + (q & 3) * 8;
-            } else {
-              src = p.w + ((int64_t)kA * ND + n) * KD + cs * 64 + q * 8;
+            for (int i = 0; i < 8; ++i) {
+              if (kq < 0 || noa) vr[i] = -1;
+              else if (TBL) vr[i] = tc::lds_s32(tt_s + (uint32_t)(i * 16 * K + col * 4));
+              else vr[i] = (r0 + 4 * i < rows) ? __ldg(trow0 + i * 4 * K + col) : -1;
             }
-            tc::cp_async16(b_s + n * 128 + ((q ^ (n & 7)) << 4), src, 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int v = vr[i];
+              tc::cp_async16(a_s + ((i & 1) ? a_off1 : a_off0) + i * 512,
+                             xq + (int64_t)(v > 0 ? v : 0) * (KD * 2), v >= 0 ? 16 : 0);
+            }
           }
-        } else {  // B(n, kk) = W[k][kk][n]: row kk of W_k is N-contiguous (MN-major)
-          constexpr int NCHK = ND / 8;
-          constexpr int CH = 64 * NCHK;
+          // ---- B
+          const int kA = ka >= 0 ? ka : 0;
+          const int kB = kb >= 0 ? kb : kA;
+          if (p.dbg & 2) {
+          } else if (!BMN) {  // B[n][kk] = W[k][n][slice] (K-major rows of W); thread: chunk qq = tid & 7, rows n = tid/8 + 16j
+            const int qq = tid & 7, n0 = tid >> 3;
+            const int k = (C::PAIR && qq >= 4) ? kB : kA;
+            const bf16* src = p.w + ((int64_t)k * ND + n0) * KD + (C::PAIR ? (qq & 3) * 8 : cs * 64 + qq * 8);
+            const uint32_t dst = b_s + n0 * 128 + ((qq ^ (n0 & 7)) << 4);
 #pragma unroll
-          for (int e = tid; e < CH; e += kTcProd) {
-            const int kk = e / NCHK, j = e - (e / NCHK) * NCHK;
-            const bf16* src;
-            if (C::PAIR) {
-              const int k = kk < 32 ? kA : kB;
-              src = p.w + ((int64_t)k * KD + (kk & 31)) * ND + j * 8;
-            } else {
-              src = p.w + ((int64_t)kA * KD + cs * 64 + kk) * ND + j * 8;
+            for (int j = 0; j < ND / 16; ++j) tc::cp_async16(dst + j * 2048, src + (int64_t)j * 16 * KD, 16);
+          } else {  // B(n, kk) = W[k][kk][n]: row kk of W_k is N-contiguous (MN-major)
+            constexpr int NCHK = ND / 8;        // 16 B chunks per kk row
+            constexpr int KKS = kTcProd / NCHK;  // kk rows per pass
+            const int jn = tid % NCHK, kk0 = tid / NCHK;
+#pragma unroll
+            for (int j = 0; j < 64 / KKS; ++j) {
+              const int kk = kk0 + j * KKS;
+              const bf16* src;
+              if (C::PAIR) {
+                const int k = kk < 32 ? kA : kB;
+                src = p.w + ((int64_t)k * KD + (kk & 31)) * ND + jn * 8;
+              } else {
+                src = p.w + ((int64_t)kA * KD + cs * 64 + kk) * ND + jn * 8;
+              }
+              const uint32_t off =
+                  (uint32_t)((jn >> 3) * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + (((jn & 7) ^ (kk & 7)) << 4));
+              tc::cp_async16(b_s + off, src, 16);
             }
-            const uint32_t off = (uint32_t)((j >> 3) * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + (((j & 7) ^ (kk & 7)) << 4));
-            tc::cp_async16(b_s + off, src, 16);
           }
         }
         // the stage's full barrier completes when every producer's copies have landed
@@ -242,6 +330,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       const int tile = w / S, split = w - (w / S) * S;
       const int a = ii % C::ACC;
       tc::mbar_wait(&tfull[a], (ii / C::ACC) & 1);
+      trace_ev(1024 + 4 * (ii & 63) + 2, ep == 0 && lane == 0);
       tc::tc_fence_after();
       const int lrow = ep * 32 + lane;
       const int64_t row = (int64_t)tile * 128 + lrow;
@@ -278,6 +367,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[a]);
+      trace_ev(1024 + 4 * (ii & 63) + 3, ep == 0 && lane == 0);
     }
   } else if (lane == 0) {
     // ============================ MMA issuer ============================
@@ -293,20 +383,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_tc_kernel(const __grid_con
       if (use >= 1) tc::mbar_wait(&tempty[a], (use - 1) & 1);
       tc::tc_fence_after();
       const uint32_t d = tmem + a * ND;
-      for (int j = 0; j < neff; ++j, ++g) {
+      const int nst = (neff + RB - 1) / RB;
+      for (int sj = 0; sj < nst; ++sj, ++g) {
         const int stage = g % C::STAGES;
         tc::mbar_wait(&full[stage], (g / C::STAGES) & 1);
         tc::tc_fence_after();
-        const uint32_t a_s = sbase + stage * C::STAGE;
-        const uint32_t b_s = a_s + C::A_BYTES;
+        const uint32_t s_base = sbase + stage * C::STAGE;
+        const int na_st = (p.dbg & 1) ? 0 : min(RB, neff - sj * RB);
+        for (int at = 0; at < na_st; ++at) {
+          const uint32_t a_s = s_base + at * C::A_BYTES;
+          const uint32_t b_s = s_base + RB * C::A_BYTES + at * C::B_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = tc::smem_desc(a_s + kk * 32, 16, 1024, tc::kSwizzle128);
-          const uint64_t bd = BMN ? tc::smem_desc(b_s + kk * 2048, 8192, 1024, tc::kSwizzle128)
-                                  : tc::smem_desc(b_s + kk * 32, 16, 1024, tc::kSwizzle128);
-          tc::mma_bf16(d, ad, bd, C::IDESC, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = tc::smem_desc(a_s + kk * 32, 16, 1024, tc::kSwizzle128);
+            const uint64_t bd = BMN ? tc::smem_desc(b_s + kk * 2048, 8192, 1024, tc::kSwizzle128)
+                                    : tc::smem_desc(b_s + kk * 32, 16, 1024, tc::kSwizzle128);
+            tc::mma_bf16(d, ad, bd, C::IDESC, (sj > 0 || at > 0 || kk > 0) ? 1u : 0u);
+          }
         }
-        tc::mma_commit(&empty[stage]);
+        if (p.dbg & 8) tc::mbar_arrive(&empty[stage]);
+        else tc::mma_commit(&empty[stage]);
       }
       tc::mma_commit(&tfull[a]);
     }
@@ -320,7 +416,7 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_
                                     int grid, int max_split, void* __restrict__ y, int y_dtype) {
   const int n_out = load_count(n_out_dev, cap_out);
   const int ntiles = (n_out + 127) / 128;
-  const int S = split_count(ntiles, grid, max_split);
+  const int S = split_count(ntiles, grid < kNumSMs ? grid : kNumSMs, max_split);
   if (S <= 1) return;
   const int64_t total = (int64_t)n_out * ND / 4;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {

@@ -19,6 +19,38 @@ struct Offsets {
   int32_t d[VP_MAX_OFFSETS * 3];
 };
 
+// Dense-grid coordinate index for bounded lattices (the training engine's
+// levels: batch < B, axes in [0, R*s) on multiples of s): cell ->
+// row (INT_MAX = empty).  A lookup is one 4-byte load with no probing, and
+// the 27 neighbours of a row fall in 9 z-runs of 3 adjacent cells.
+struct GridSpec {
+  int32_t* cells;
+  int B, R, s;
+};
+constexpr int32_t kGridEmpty = 0x7fffffff;
+
+// lattice cell of a row (per axis, in units of s) or false when off-lattice
+__device__ __forceinline__ bool grid_coords(const GridSpec& g, int4 r, int& cx, int& cy, int& cz) {
+  if (r.x < 0 || r.x >= g.B || r.y < 0 || r.z < 0 || r.w < 0) return false;
+  cx = r.y / g.s;
+  cy = r.z / g.s;
+  cz = r.w / g.s;
+  return cx < g.R && cy < g.R && cz < g.R && cx * g.s == r.y && cy * g.s == r.z && cz * g.s == r.w;
+}
+
+__device__ __forceinline__ int grid_linear(const GridSpec& g, int b, int cx, int cy, int cz) {
+  return ((b * g.R + cx) * g.R + cy) * g.R + cz;  // < 2^31: host caps B*R^3
+}
+
+__global__ void grid_set_kernel(const int4* __restrict__ c, const int32_t* n_dev, int64_t cap, GridSpec g, int clear) {
+  const int n = load_count(n_dev, cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 r = c[i];
+    int cx, cy, cz;
+    if (grid_coords(g, r, cx, cy, cz)) g.cells[grid_linear(g, r.x, cx, cy, cz)] = clear ? kGridEmpty : (int32_t)i;
+  }
+}
+
 __global__ void map_insert_kernel(const int4* __restrict__ in, const int32_t* n_dev, int64_t cap_n,
                                   Slot* t, uint64_t cap) {
   int n = load_count(n_dev, cap_n);
@@ -74,8 +106,8 @@ map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t
         const long long qx = (long long)r.y + (long long)offs.d[3 * k] * sx;
         const long long qy = (long long)r.z + (long long)offs.d[3 * k + 1] * sy;
         const long long qz = (long long)r.w + (long long)offs.d[3 * k + 2] * sz;
-        // out-of-range queries are plain misses (kernels.py:135-148)
         if (packable64(r.x, qx, qy, qz)) {
+          // out-of-range queries are plain misses (kernels.py:135-148)
           key[b] = pack_key(r.x, (int)qx, (int)qy, (int)qz);
           slot[b] = mix64(key[b]) & (cap - 1);
           live[b] = key[b] != kEmptyKey;
@@ -125,6 +157,75 @@ map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t
     int c = 0;
 #pragma unroll 8
     for (int w = 0; w < kProbeWarps; ++w) c += s_cnt[w][k];
+    counts[(int64_t)k * ntiles + tile] = c;
+  }
+}
+
+// Dense-grid probe: one thread per output row, offsets in batches of 9
+// independent 4-byte loads (a 3x3x3 kernel = 3 batches, each 3 z-runs of 3
+// adjacent cells).  Offsets arrive pre-scaled to cells (off * in_stride / s)
+// with their linear cell delta, so a probe is 3 unsigned compares + 1 load.
+struct GridOffsets {
+  int32_t d[VP_MAX_OFFSETS * 3];
+  int32_t lin[VP_MAX_OFFSETS];
+};
+
+__global__ void __launch_bounds__(kMapTile)
+map_probe_grid_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t cap_out, GridSpec g,
+                      const __grid_constant__ GridOffsets offs, int K, int32_t* __restrict__ nbr, int32_t* counts,
+                      int ntiles) {
+  __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
+  __shared__ int s_cnt[kMapTile / 32][VP_MAX_OFFSETS];
+  const int n_out = load_count(n_out_dev, cap_out);
+  const int tile = blockIdx.x;
+  const int64_t u0 = (int64_t)tile * kMapTile;
+  if (u0 >= n_out) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows = (n_out - u0) < kMapTile ? (int)(n_out - u0) : kMapTile;
+  const bool valid = tid < rows;
+  const bool staged = K <= kMapSmemK;
+  int cx = 0, cy = 0, cz = 0, base = 0;
+  bool on = false;
+  if (valid) {
+    const int4 r = out[u0 + tid];
+    on = grid_coords(g, r, cx, cy, cz);
+    if (on) base = grid_linear(g, r.x, cx, cy, cz);
+  }
+  const unsigned R = (unsigned)g.R;
+  constexpr int KB = 9;
+  for (int kb = 0; kb < K; kb += KB) {
+    int v[KB];
+#pragma unroll
+    for (int b = 0; b < KB; ++b) {
+      const int k = kb + b;
+      v[b] = kGridEmpty;
+      if (on && k < K && (unsigned)(cx + offs.d[3 * k]) < R && (unsigned)(cy + offs.d[3 * k + 1]) < R &&
+          (unsigned)(cz + offs.d[3 * k + 2]) < R)
+        v[b] = __ldg(g.cells + base + offs.lin[k]);
+    }
+#pragma unroll
+    for (int b = 0; b < KB; ++b) {
+      const int k = kb + b;
+      if (k >= K) break;
+      const int x = v[b] == kGridEmpty ? -1 : v[b];
+      if (staged) s_nbr[tid * (kMapSmemK + 1) + k] = x;
+      else if (valid) nbr[(u0 + tid) * K + k] = x;
+      const unsigned m = __ballot_sync(0xffffffffu, x >= 0);
+      if (lane == 0) s_cnt[warp][k] = __popc(m);
+    }
+  }
+  __syncthreads();
+  if (staged) {
+    int32_t* dst = nbr + u0 * K;
+    for (int e = tid; e < rows * K; e += kMapTile) {
+      const int rr = e / K, k = e - rr * K;
+      dst[e] = s_nbr[rr * (kMapSmemK + 1) + k];
+    }
+  }
+  for (int k = tid; k < K; k += kMapTile) {
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < kMapTile / 32; ++w) c += s_cnt[w][k];
     counts[(int64_t)k * ntiles + tile] = c;
   }
 }
@@ -291,6 +392,72 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
                                                      pair_in, pair_out, pair_ptr);
     VP_CHECK_LAUNCH("map_emit");
   }
+  return VP_OK;
+}
+
+int vp_grid_set(const int32_t* coords, const int32_t* n_dev, int64_t cap, int32_t* cells, int32_t B, int32_t R,
+                int32_t s, int32_t clear, vp_stream_t stream) {
+  VP_REQUIRE(B >= 1 && R >= 1 && s >= 1, VP_EVALIDATION, "grid: extents must be positive");
+  VP_REQUIRE((int64_t)B * R * R * R < (1ll << 31), VP_EVALIDATION, "grid: B*R^3 must be < 2^31 cells");
+  if (cap <= 0) return VP_OK;
+  int blocks = (int)std::min<int64_t>(ceil_div(cap, 256), kNumSMs * 8);
+  grid_set_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const int4*)coords, n_dev, cap, GridSpec{cells, B, R, s},
+                                                          clear);
+  VP_CHECK_LAUNCH("grid_set");
+  return VP_OK;
+}
+
+size_t vp_kernel_map_grid_ws_bytes(int64_t cap_out, int32_t K) {
+  Carver c(nullptr, 0);
+  int64_t ntiles = ceil_div(std::max<int64_t>(cap_out, 1), kMapTile);
+  c.take<int32_t>(ntiles * K);
+  c.take<int32_t>(K + 1);
+  return c.off;
+}
+
+int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, const int32_t* out,
+                       const int32_t* n_out_dev, int64_t cap_out, const int32_t* offsets_host, int32_t K,
+                       const int32_t* in_stride, int32_t* nbr, int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr,
+                       void* ws, size_t ws_bytes, vp_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
+  VP_REQUIRE(pair_in && pair_out && pair_ptr, VP_EVALIDATION, "kernel_map_grid: pair outputs required");
+  VP_REQUIRE(B >= 1 && R >= 1 && s >= 1, VP_EVALIDATION, "grid: extents must be positive");
+  Carver c(ws, ws_bytes);
+  int ntiles = (int)ceil_div(std::max<int64_t>(cap_out, 1), kMapTile);
+  int32_t* counts = c.take<int32_t>((int64_t)ntiles * K);
+  int32_t* totals = c.take<int32_t>(K + 1);
+  VP_REQUIRE(c.ok(), VP_EVALIDATION, "kernel_map_grid: workspace too small");
+  VP_REQUIRE((int64_t)B * R * R * R < (1ll << 31), VP_EVALIDATION, "grid: B*R^3 must be < 2^31 cells");
+  for (int a = 0; a < 3; ++a)
+    VP_REQUIRE(in_stride[a] >= 1 && in_stride[a] % s == 0, VP_EVALIDATION,
+               "kernel_map_grid: in_stride must be a multiple of the grid spacing");
+  GridOffsets offs;
+  memset(&offs, 0, sizeof(offs));
+  for (int k = 0; k < K; ++k) {
+    int dc[3];
+    for (int a = 0; a < 3; ++a) {
+      const int64_t d = (int64_t)offsets_host[3 * k + a] * (in_stride[a] / s);
+      // beyond the lattice in either direction: every query misses
+      dc[a] = (int)std::max<int64_t>(std::min<int64_t>(d, R), -(int64_t)R);
+      offs.d[3 * k + a] = dc[a];
+    }
+    offs.lin[k] = (dc[0] * R + dc[1]) * R + dc[2];
+  }
+  if (cap_out <= 0) {
+    cudaMemsetAsync(pair_ptr, 0, sizeof(int32_t) * (K + 1), st);
+    VP_CHECK_ASYNC("kernel_map_grid(empty)");
+    return VP_OK;
+  }
+  map_probe_grid_kernel<<<ntiles, kMapTile, 0, st>>>((const int4*)out, n_out_dev, cap_out,
+                                                     GridSpec{const_cast<int32_t*>(cells), B, R, s}, offs, K, nbr,
+                                                     counts, ntiles);
+  VP_CHECK_LAUNCH("map_probe_grid");
+  map_scan_kernel<<<K, 1024, 0, st>>>(counts, n_out_dev, cap_out, ntiles, totals);
+  VP_CHECK_LAUNCH("map_scan");
+  map_emit_kernel<<<ntiles, kMapTile, 0, st>>>(nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out,
+                                               pair_ptr);
+  VP_CHECK_LAUNCH("map_emit");
   return VP_OK;
 }
 

@@ -92,10 +92,12 @@ class SparseResNetTrainer:
 
     def __init__(self, batch=64, points=2048, resolution=64, planes=(32, 64, 128, 256), blocks=1, classes=40,
                  in_channels=1, lr=1e-2, momentum=0.9, seed=2, voxel_size=1.0, device=None,
-                 points_dtype=torch.float32, grad_allreduce=None, feature_dtype=BF16):
+                 points_dtype=torch.float32, grad_allreduce=None, feature_dtype=BF16, index="auto"):
         """feature_dtype: bf16 (tensor-core path, the product) or fp32 (SIMT
         kernels; used to validate the engine's dataflow against the f64
-        oracle at fp32 tolerance)."""
+        oracle at fp32 tolerance).  index: coordinate index of the kernel
+        maps — "grid" (dense per-level lattice), "hash" (the seam's hash
+        table) or "auto" (grid while all levels' lattices fit in 4 GiB)."""
         self.B, self.P, self.res = batch, points, resolution
         self.planes, self.blocks, self.classes, self.cin = tuple(planes), blocks, classes, in_channels
         self.lr, self.momentum, self.voxel_size = lr, momentum, voxel_size
@@ -130,6 +132,16 @@ class SparseResNetTrainer:
         # ---- maps: stride-1 per level, strided between consecutive levels
         self.map_s1 = [self._alloc_map(self.levels[i], self.levels[i], strided=False) for i in range(nlev)]
         self.map_dn = [self._alloc_map(self.levels[i], self.levels[i + 1], strided=True) for i in range(nlev - 1)]
+        # dense-grid coordinate index per level (cells = B * ceil(res/2^i)^3
+        # int32, kept empty between steps: only touched cells are cleared);
+        # used instead of a hash table while the lattice stays small
+        self.grid_R = [-(-resolution // (2 ** i)) for i in range(nlev)]
+        grid_bytes = sum(4 * batch * r ** 3 for r in self.grid_R)
+        if index not in ("auto", "grid", "hash"):
+            raise ValueError(f"index must be auto|grid|hash, got {index!r}")
+        self.use_grid = index == "grid" or (index == "auto" and grid_bytes <= (4 << 30))
+        self.grids = ([torch.full((batch * r ** 3,), 0x7FFFFFFF, dtype=torch.int32, device=dev) for r in self.grid_R]
+                      if self.use_grid else None)
         # ---- parameters
         self.layers = self._layer_list()
         pb = ParamBuffer(dev)
@@ -198,7 +210,8 @@ class SparseResNetTrainer:
             ptr=torch.zeros(K + 1, dtype=torch.int32, device=dev),
             inv=torch.zeros((src.cap, K), dtype=torch.int32, device=dev) if strided else None,
             src=src, dst=dst,
-            ws=_lib.workspace(_lib.query("vp_kernel_map_ws_bytes", src.cap, dst.cap, K), dev))
+            ws=_lib.workspace(max(_lib.query("vp_kernel_map_ws_bytes", src.cap, dst.cap, K),
+                                  _lib.query("vp_kernel_map_grid_ws_bytes", dst.cap, K)), dev))
 
     def _layer_list(self):
         L = [dict(name="stem", cin=self.cin, cout=self.planes[0], src=self.levels[0], dst=self.levels[0],
@@ -251,11 +264,22 @@ class SparseResNetTrainer:
         self.launch_count += 1
         _lib.call(name, *args)
 
+    def _grid_set(self, i, st, clear):
+        lv = self.levels[i]
+        self._c("vp_grid_set", lv.coords.data_ptr(), lv.n.data_ptr(), lv.cap, self.grids[i].data_ptr(), self.B,
+                self.grid_R[i], lv.stride, int(clear), st)
+
     def _build_map(self, m, st):
         ist = _lib.i32_array((m.src.stride,) * 3)
-        self._c("vp_kernel_map", m.src.coords.data_ptr(), m.src.n.data_ptr(), m.src.cap, m.dst.coords.data_ptr(),
-                m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(), m.pin.data_ptr(),
-                m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st)
+        if self.use_grid:
+            i = self.levels.index(m.src)
+            self._c("vp_kernel_map_grid", self.grids[i].data_ptr(), self.B, self.grid_R[i], m.src.stride,
+                    m.dst.coords.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(),
+                    m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st)
+        else:
+            self._c("vp_kernel_map", m.src.coords.data_ptr(), m.src.n.data_ptr(), m.src.cap, m.dst.coords.data_ptr(),
+                    m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(), m.pin.data_ptr(),
+                    m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st)
         if m.inv is not None:
             self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
                     m.inv.data_ptr(), m.src.cap, st)
@@ -271,41 +295,68 @@ class SparseResNetTrainer:
                 self.B, float(self.voxel_size), res3, lv[0].coords.data_ptr(), lv[0].n.data_ptr(), None,
                 self.feat0.data_ptr(), self.fcode, self.vox_ws.data_ptr(), self.vox_ws.numel(), st)
         self.map_events = {}
+        nl = len(lv)
         if not self.concurrent:
-            for i in range(1, len(lv)):
+            for i in range(1, nl):
                 step = _lib.i32_array((lv[i].stride,) * 3)
                 self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
                         lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
                         st)
-            for m in self.map_s1 + self.map_dn:
-                self._build_map(m, st)
+            for i in range(nl):
+                if self.use_grid:
+                    self._grid_set(i, st, clear=False)
+                self._build_map(self.map_s1[i], st)
+                if i + 1 < nl:
+                    self._build_map(self.map_dn[i], st)
+                if self.use_grid:
+                    self._grid_set(i, st, clear=True)
             return
         main = torch.cuda.current_stream()
         chain = self.side[0]
         chain.wait_stream(main)
-        lev_ev = [None] * len(lv)
+        lev_ev = [None] * nl
         with torch.cuda.stream(chain):
             cs = chain.cuda_stream
-            for i in range(1, len(lv)):
+            for i in range(1, nl):
                 step = _lib.i32_array((lv[i].stride,) * 3)
                 self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
                         lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
                         cs)
                 lev_ev[i] = torch.cuda.Event()
                 lev_ev[i].record(chain)
-        self._build_map(self.map_s1[0], st)  # needed first (stem), on the critical path
-        plan = []
-        for i in range(len(lv) - 1):
-            plan.append((self.map_dn[i], i + 1))
-            plan.append((self.map_s1[i + 1], i + 1))
-        for j, (m, need) in enumerate(plan):
-            side = self.side[1 + (j % 2)]
-            side.wait_event(lev_ev[need])
+        # level 0: index + stride-1 map on the critical path (the stem needs it)
+        if self.use_grid:
+            self._grid_set(0, st, clear=False)
+        self._build_map(self.map_s1[0], st)
+        idx0 = torch.cuda.Event()
+        idx0.record(main)
+        # everything else on two side streams.  Each source level's index is
+        # built once and read by both maps that gather from it (map_s1[i],
+        # map_dn[i]), then cleared on the same stream.
+        for i in range(nl):
+            side = self.side[1 + (i % 2)]
+            if i == 0:
+                side.wait_event(idx0)
+            else:
+                side.wait_event(lev_ev[i])
+            if i + 1 < nl:
+                side.wait_event(lev_ev[i + 1])
             with torch.cuda.stream(side):
-                self._build_map(m, side.cuda_stream)
-                ev = torch.cuda.Event()
-                ev.record(side)
-            self.map_events[id(m)] = ev
+                ss = side.cuda_stream
+                if i > 0:
+                    if self.use_grid:
+                        self._grid_set(i, ss, clear=False)
+                    self._build_map(self.map_s1[i], ss)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    self.map_events[id(self.map_s1[i])] = ev
+                if i + 1 < nl:
+                    self._build_map(self.map_dn[i], ss)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    self.map_events[id(self.map_dn[i])] = ev
+                if self.use_grid:
+                    self._grid_set(i, ss, clear=True)
 
     def _wait_map(self, m):
         ev = getattr(self, "map_events", {}).get(id(m))
