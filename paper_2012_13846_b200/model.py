@@ -521,6 +521,71 @@ class SparseResNetTrainer:
         self.step()
         return float(self.loss.item())
 
+    def profile_layers(self, iters: int = 20, warmup: int = 3) -> list[dict]:
+        """SmartProfile on the GPU (profiling.py:416-455): per
+        conv layer, CUDA-event device time of its forward (conv + BN stats +
+        BN apply) and of its backward split into BN backward, dgrad and wgrad,
+        each timed alone on one stream (eager, non-concurrent) on the current
+        batch.  Also the activation bytes a pipeline cut after the layer sends
+        (coords int32 [N,4] + bf16 feats [N,C]) and the fp32
+        parameter bytes.  Returns one dict per layer in layer order."""
+        conc = self.concurrent
+        self.concurrent = False
+        try:
+            st = _lib.stream()
+            self._integer_stage(st)
+            self._forward(st)
+            self._backward(st)
+            torch.cuda.synchronize()
+            esz = 2 if self.fdt == BF16 else 4
+
+            def timed(fn):
+                for _ in range(warmup):
+                    fn()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(iters):
+                    fn()
+                b.record()
+                b.synchronize()
+                return a.elapsed_time(b) * 1e3 / iters
+
+            out = []
+            for L in self.layers:
+                x = L["x"]
+                res = L["a"] if L["kind"] == "c2" else None  # any same-shape buffer: cost only
+                n_out = int(L["dst"].n.item())
+                fwd = timed(lambda: self._conv_bn(L, x, res, True, st))
+                bn_b = timed(lambda: self._c(
+                    "vp_bn_backward", L["gy"].data_ptr(), None, self.fcode, L["a"].data_ptr(), self.fcode,
+                    L["y"].data_ptr(), self.fcode, L["dst"].n.data_ptr(), L["dst"].cap, L["cout"],
+                    L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(),
+                    self.fcode, None, L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["bn_ws"].data_ptr(),
+                    L["bn_ws"].numel(), st))
+                m, fc = L["map"], self.fcode
+                wg = timed(lambda: self._c(
+                    "vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"], self.K,
+                    m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(),
+                    L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st))
+                dg = 0.0
+                if L["kind"] != "stem":
+                    src = L["src"]
+                    gin = self.gact[self.levels.index(src)]
+                    table, flip = (m.nbr, 1) if m.inv is None else (m.inv, 0)
+                    dg = timed(lambda: self._c(
+                        "vp_conv_dgrad", L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(),
+                        L["wcode"], L["cin"], self.K, table.data_ptr(), flip, src.n.data_ptr(), src.cap,
+                        gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st))
+                pairs = int(m.ptr[-1].item())
+                out.append({"name": L["name"], "cin": L["cin"], "cout": L["cout"], "n_out": n_out, "pairs": pairs,
+                            "fwd_us": fwd, "bn_bwd_us": bn_b, "dgrad_us": dg, "wgrad_us": wg,
+                            "bwd_us": bn_b + dg + wg, "gflop_fwd": 2.0 * pairs * L["cin"] * L["cout"] / 1e9,
+                            "activation_bytes": n_out * (16 + esz * L["cout"]),
+                            "param_bytes": 4 * (self.K * L["cin"] * L["cout"] + 2 * L["cout"])})
+            return out  # activations/gradients are scratch now: profile on a dedicated trainer
+        finally:
+            self.concurrent = conc
+
     def level_sizes(self) -> list[int]:
         return [int(l.n.item()) for l in self.levels]
 

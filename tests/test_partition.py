@@ -1,0 +1,244 @@
+"""Partitioner — the SPEC's worked
+examples, acceptance criteria 1/2/7 and properties, checked
+against the exhaustive brute-force oracle.  CPU only."""
+import itertools
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2012_13846_b200 import partition as P
+from paper_2012_13846_b200.errors import ConfigError, ValidationError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def profiles_from(times_by_type, act, par, model="m", fwd_frac=1 / 3):
+    """times in seconds (fwd+bwd) -> ProfileSet with fwd:bwd = 1:2."""
+    prof = {}
+    for t, times in times_by_type.items():
+        prof[t] = [P.LayerProfile(i, v * 1e6 * fwd_frac, v * 1e6 * (1 - fwd_frac), float(act[i]), float(par[i]))
+                   for i, v in enumerate(times)]
+    return P.ProfileSet(model, 8, prof)
+
+
+def cluster(types, bw):
+    return P.ClusterSpec([P.Processor(f"{t}{i}", t) for i, t in enumerate(types)], bw)
+
+
+# ---------------------------------------------------------------- Eq. 4 KATs
+def test_eq4_single_processor_is_compute_sum():
+    ps = profiles_from({"g": [1.0, 2.0, 3.0]}, [0, 0, 0], [5e9, 5e9, 5e9])
+    c = cluster(["g"], 1.0)
+    assert P.stage_time_q(0, 2, ["g0"], ps, c) == pytest.approx(6.0, rel=1e-12)
+
+
+def test_eq4_acceptance_2_worked_example():
+    # m=3, slowest-processor compute 9 s, 2(m-1) sum p / BW = 12 s -> 7 s exactly
+    ps = profiles_from({"a": [4.0, 5.0], "b": [3.0, 3.0]}, [0, 0], [1.5, 1.5])
+    c = cluster(["a", "b", "b"], 1.0)
+    assert P.stage_time_q(0, 1, ["a0", "b1", "b2"], ps, c) == 7.0
+    assert P.get_comp_time(0, 1, ["a0", "b1", "b2"], ps, c) == 7.0
+
+
+def test_eq4_homogeneous_pair():
+    # t=[6,6] s, sum p = 100 MB, BW 10 MB/s, m=2 -> (12 + 2*100/10)/2 = 16 s
+    ps = profiles_from({"g": [6.0, 6.0]}, [1e6, 0], [0, 100e6])
+    c = cluster(["g", "g"], 10e6)
+    assert P.stage_time_q(0, 1, ["g0", "g1"], ps, c) == pytest.approx(16.0, rel=1e-12)
+
+
+def test_eq4_heterogeneous_slowest_governs():
+    ps = profiles_from({"fast": [1.0], "slow": [2.0]}, [0], [0])
+    c = cluster(["fast", "slow"], 1.0)
+    assert P.stage_time_q(0, 0, ["fast0", "slow1"], ps, c) == pytest.approx(1.0)  # max(1,2)/2
+
+
+def test_unknown_type_is_config_error():
+    ps = profiles_from({"g": [1.0]}, [0], [0])
+    with pytest.raises(ConfigError):
+        P.plan(ps, cluster(["h"], 1.0))
+
+
+# ---------------------------------------------------------------- sort KATs
+def test_sort_processors_slowest_first():
+    # speed factors {RTX:1.0, TitanXP:1.11, TitanV:0.95}
+    base = [1.0, 1.0, 1.0]
+    ps = profiles_from({"RTX": base, "TitanXP": [1.11 * v for v in base], "TitanV": [0.95 * v for v in base]},
+                       [0, 0, 0], [0, 0, 0])
+    c = cluster(["RTX", "TitanV", "TitanXP", "RTX"], 1.0)
+    assert P.sort_processors(c, ps) == ["TitanXP2", "RTX0", "RTX3", "TitanV1"]
+
+
+def test_sort_homogeneous_identity_and_singleton():
+    ps = profiles_from({"g": [1.0]}, [0], [0])
+    assert P.sort_processors(cluster(["g"] * 3, 1.0), ps) == ["g0", "g1", "g2"]
+    assert P.sort_processors(cluster(["g"], 1.0), ps) == ["g0"]
+
+
+# ---------------------------------------------------------------- plan KATs
+def test_plan_split_beats_dp():
+    # "1-1" with objective max(6, 0.1, 6) = 6 s, beating DP's 16 s
+    ps = profiles_from({"g": [6.0, 6.0]}, [1e6, 0], [0, 100e6])
+    c = cluster(["g", "g"], 10e6)
+    p = P.plan(ps, c)
+    assert p.split_config == "1-1"
+    assert p.objective == pytest.approx(6.0, rel=1e-12)
+    assert P.data_parallel_plan(ps, c).objective == pytest.approx(16.0, rel=1e-12)
+
+
+def test_plan_tie_prefers_fewer_stages():
+    # DP "2" and pipeline "1-1" both 4 s; tie-break picks "2"
+    ps = profiles_from({"g": [4.0, 4.0]}, [1e-30, 0], [0, 0])
+    p = P.plan(ps, cluster(["g", "g"], 1e9))
+    assert p.objective == pytest.approx(4.0)
+    assert p.split_config == "2"
+
+
+def test_single_layer_single_stage():
+    ps = profiles_from({"g": [3.0]}, [0], [1e6])
+    c = cluster(["g"] * 3, 1e6)
+    p = P.plan(ps, c)
+    assert len(p.stages) == 1
+    bf = P.brute_force_plan(ps, c)
+    assert bf.objective == pytest.approx(p.objective, rel=1e-12)
+
+
+def _random_instance(rng):
+    L = int(rng.integers(1, 7))
+    M = int(rng.integers(1, 5))
+    ntypes = int(rng.integers(1, 4))
+    types = [f"t{i}" for i in range(ntypes)]
+    base = rng.uniform(0.1, 5.0, L)
+    speed = {t: rng.uniform(0.5, 2.0) for t in types}
+    times = {t: (base * speed[t] * rng.uniform(0.8, 1.25, L)).tolist() for t in types}
+    act = rng.uniform(0, 5e6, L)
+    par = rng.choice([0.0, 1.0], L) * rng.uniform(0, 5e7, L)
+    bw = float(rng.uniform(1e6, 1e8))
+    procs = [types[int(rng.integers(0, ntypes))] for _ in range(M)]
+    return profiles_from(times, act, par), cluster(procs, bw)
+
+
+def test_acceptance_1_dp_equals_brute_force_200_instances():
+    rng = np.random.default_rng(12345)
+    for _ in range(200):
+        ps, c = _random_instance(rng)
+        p = P.plan(ps, c)
+        bf = P.brute_force_plan(ps, c, restrict_to_prefixes=True)
+        assert abs(p.objective - bf.objective) <= 1e-9 * max(1.0, bf.objective)
+        p.validate(ps.num_layers)
+        S = int(rng.integers(1, 4))
+        p2 = P.plan(ps, c, max_stages=S)
+        assert len(p2.stages) <= S
+        bf2 = P.brute_force_plan(ps, c, max_stages=S)
+        assert abs(p2.objective - bf2.objective) <= 1e-9 * max(1.0, bf2.objective)
+
+
+def test_unrestricted_brute_force_never_worse():
+    rng = np.random.default_rng(7)
+    for _ in range(30):
+        ps, c = _random_instance(rng)
+        if len(c.processors) > 4:
+            continue
+        a = P.brute_force_plan(ps, c, restrict_to_prefixes=True).objective
+        b = P.brute_force_plan(ps, c, restrict_to_prefixes=False).objective
+        assert b <= a * (1 + 1e-12)
+
+
+def test_dominance_over_data_parallel():
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        ps, c = _random_instance(rng)
+        assert P.plan(ps, c).objective <= P.data_parallel_plan(ps, c).objective * (1 + 1e-12)
+
+
+def test_monotone_in_processors():
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        ps, c = _random_instance(rng)
+        tname = next(iter(ps.profiles))
+        bigger = P.ClusterSpec(c.processors + [P.Processor("extra", tname)], c.bandwidth_bytes_per_sec)
+        assert P.plan(ps, bigger).objective <= P.plan(ps, c).objective * (1 + 1e-12)
+
+
+def test_scale_equivariance():
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        ps, c = _random_instance(rng)
+        s = 3.5
+        scaled = P.ProfileSet(ps.model_name, ps.batch_size, {
+            t: [P.LayerProfile(r.layer_id, r.fwd_time_us * s, r.bwd_time_us * s, r.activation_bytes, r.param_bytes)
+                for r in recs] for t, recs in ps.profiles.items()})
+        c2 = P.ClusterSpec(c.processors, c.bandwidth_bytes_per_sec / s)
+        assert P.plan(scaled, c2).objective == pytest.approx(s * P.plan(ps, c).objective, rel=1e-9)
+
+
+def test_plan_json_roundtrip_and_determinism():
+    rng = np.random.default_rng(6)
+    ps, c = _random_instance(rng)
+    p = P.plan(ps, c)
+    text = p.to_json()
+    assert P.plan(ps, c).to_json() == text  # byte-identical
+    q = P.PartitionPlan.from_json(text)
+    assert q.split_config == p.split_config and q.objective == p.objective
+    assert json.loads(text)["split_config"] == p.split_config
+
+
+def test_profile_and_cluster_json_roundtrip():
+    ps = profiles_from({"B200": [1.0, 2.0]}, [10, 20], [30, 40])
+    back = P.profile_from_json(P.profile_to_json(ps, "B200"))
+    assert back.profiles["B200"] == ps.profiles["B200"]
+    c = cluster(["B200"] * 2, 7.7e11)
+    c2 = P.cluster_from_json(P.cluster_to_json(c))
+    assert c2.processors == c.processors
+    with pytest.raises(ValidationError):
+        P.profile_from_json("{}")
+
+
+def test_brute_force_guard():
+    ps = profiles_from({"g": [1.0] * 11}, [0] * 11, [0] * 11)
+    with pytest.raises(ValidationError):
+        P.brute_force_plan(ps, cluster(["g"], 1.0))
+
+
+def _ref_profiling():
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+    try:
+        from voxpipe import profiling  # the reference's own synthetic-profile generator
+    except ImportError:
+        pytest.skip("oracle/_ref (reference build) not present")
+    return profiling
+
+
+def test_reference_profile_format_is_ingested():
+    prof = _ref_profiling()
+    ps_ref = prof.synth_profile("uniform", L=5, speed_factors={"B200": 1.0})
+    ps = P.profile_from_json(prof.profile_to_json(ps_ref, "B200"))
+    assert ps.num_layers == 5
+
+
+def test_acceptance_7_table_iii_shape():
+    """Table-I-shaped cluster (4 RTX 2080Ti + 3 Titan XP + 1 Titan V; time
+    factors from the single-precision TFLOPS 13.4 / 12.1 / 13.8)
+    on the reference's vgg16bn_like profile -> "7-1" with the parameter-heavy
+    tail on the Titan V (PAPER Table III), and HETE-MP >= MP >= DP."""
+    prof = _ref_profiling()
+    f = {"RTX": 13.8 / 13.4, "TitanXP": 13.8 / 12.1, "TitanV": 1.0}
+    ps = P.profile_from_json(prof.profile_to_json(prof.synth_profile("vgg16bn_like", speed_factors=f), "RTX"))
+    for t in ("TitanXP", "TitanV"):
+        ps = ps.merged_with(P.profile_from_json(
+            prof.profile_to_json(prof.synth_profile("vgg16bn_like", speed_factors=f), t)))
+    c = cluster(["RTX"] * 4 + ["TitanXP"] * 3 + ["TitanV"], 1.25e9)  # 10 Gbit/s
+    # Table III lists two-stage configurations; unconstrained, Eq. 5 prefers a
+    # deeper "5-2-1" cut of this synthetic profile, which is never worse
+    p = P.plan(ps, c, max_stages=2)
+    assert p.split_config == "7-1", p.split_config
+    assert P.plan(ps, c).objective <= p.objective
+    assert [c.type_of(i) for i in p.stages[-1].assigned_processors] == ["TitanV"]
+    assert p.stages[-1].layer_end == ps.num_layers - 1
+    dp = P.data_parallel_plan(ps, c).objective
+    mp = P.evaluate(P.plan_with_types_as(ps, c, "TitanXP"), ps, c)
+    hete = P.plan(ps, c).objective
+    assert hete <= mp * (1 + 1e-12) <= dp * (1 + 1e-12)
