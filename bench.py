@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=16, help="clouds per CPU-baseline step")
     ap.add_argument("--profile-only", action="store_true", help="warm-up + a few steps, no JSON (for ncu)")
+    ap.add_argument("--plan", default="dp",
+                    help="N>1: 'dp' (every GPU a replica, gradient all_reduce), 'auto' (SparsePipe partitioner "
+                         "on per-unit GPU profiles -> pipeline stages), or unit cuts like '3' / '1,4,6'")
+    ap.add_argument("--p2p-gbs", type=float, default=770.0, help="NVLink P2P GB/s per direction for the planner")
     return ap.parse_args()
 
 
@@ -196,6 +200,8 @@ def main():
             dist.all_reduce(flat)
             flat.div_(world)
 
+    if world > 1 and args.plan != "dp":
+        return run_pipeline(args, rank, world, local, dev)
     tr = model.SparseResNetTrainer(batch=args.batch, points=args.points, resolution=args.res, blocks=args.blocks,
                                    device=dev, grad_allreduce=allreduce)
     # synthetic data pool: 4 distinct batches per rank, resident in HBM and pinned host memory
@@ -313,6 +319,92 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_pipeline(args, rank, world, local, dev):
+    """SparsePipe on N GPUs: stages from the partitioner fed with this box's
+    measured per-unit GPU costs (or explicit cuts), micro-batches of
+    `--batch` clouds over NCCL P2P, PipeDream 1F1B with weight stashing.
+    A step = `world` micro-batches (the same clouds per GPU as DP, weak
+    scaling); the timed region is one continuous 1F1B run of K steps
+    (fill and drain included), device-timed, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import voxpipe_oracle as O
+    from paper_2012_13846_b200 import model, partition, pipeline as PL
+
+    def make(units):
+        return model.SparseResNetTrainer(batch=args.batch, points=args.points, resolution=args.res,
+                                         blocks=args.blocks, device=dev, units=units)
+
+    probe = make(None)
+    n_units = len(probe.units)
+    if args.plan == "auto":
+        prof_json = None
+        if rank == 0:
+            pts, _ = O.synthetic_batch(args.batch, args.points, args.res, seed=0, dtype=np.float32)
+            probe.set_batch(torch.from_numpy(pts).to(dev), torch.zeros(args.batch, dtype=torch.int32, device=dev))
+            ps = PL.unit_profile(probe, probe.profile_layers(), "sparse_resnet")
+            prof_json = partition.profile_to_json(ps, "B200")
+        box = [prof_json]
+        dist.broadcast_object_list(box, src=0)
+        ps = partition.profile_from_json(box[0])
+        plan, topo = PL.plan_topology(ps, world, args.p2p_gbs * 1e9)
+        split = plan.split_config
+    else:
+        cuts = [int(c) for c in args.plan.split(",")]
+        topo = PL.Topology.even(n_units, cuts)
+        split = "-".join("1" for _ in topo.stages)
+    del probe
+    topo.validate(n_units)
+    tr = PL.DistTransport(dist, topo)  # collective: every rank builds the replica groups
+    active = topo.locate(rank) is not None  # the plan may leave a GPU idle (SPEC.md:352)
+    pool = []
+    for i in range(4):
+        pts, _ = O.synthetic_batch(args.batch, args.points, args.res, seed=1000 + i, dtype=np.float32)
+        pool.append((torch.from_numpy(pts).to(dev),
+                     torch.tensor([(b + 7 * i) % 40 for b in range(args.batch)], dtype=torch.int32, device=dev)))
+    dist.barrier()  # first collective on every rank before any P2P group
+
+    def run(n_mb):
+        return PL.StageRunner(topo, rank, n_mb, make, lambda mb: pool[mb % len(pool)], tr,
+                              use_graphs=not args.no_graph)
+
+    if active:
+        warm = run(max(1, args.warmup) * world)
+        warm.run()
+        torch.cuda.synchronize()
+        timed = run(args.steps * world)
+        # reuse the warmed engines, graphs and weights
+        timed.slots, timed.graphs = warm.slots[:len(timed.slots)], warm.graphs
+        timed.master_p, timed.master_pb, timed.master_m = warm.master_p, warm.master_pb, warm.master_m
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    if active:
+        timed.run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    value = args.steps * world * args.batch / (ms / 1e3)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "clouds/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": dict(CONFIG, parallelism=f"pipeline {split}", stages=[
+                    [s.unit_start, s.unit_end, list(s.ranks)] for s in topo.stages],
+                    micro_batch_clouds=args.batch, micro_batches_per_step=world, cuda_graph=not args.no_graph,
+                    l2="not flushed: one continuous 1F1B stream (fill + drain inside the timed region)"),
+                "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def _peaks():

@@ -521,7 +521,7 @@ constexpr int kWgSimtChunk = 512;  // SIMT path: short chunks, many CTAs
 size_t vp_conv_wgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K, int64_t cap_pairs) {
   const int chunk = std::min(wgrad_chunk(cap_pairs), kWgSimtChunk);
   const int64_t items = cap_pairs / chunk + K + 1;
-  return align_up((size_t)items * cin * cout * 4, 256) + align_up((size_t)(K + 1) * 4, 256);
+  return align_up((size_t)items * cin * cout * 4, 256);
 }
 
 int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
@@ -534,13 +534,15 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
   const int chunk = wgrad_chunk(cap_pairs);
   const int max_items = (int)(cap_pairs / chunk + K + 1);
   float* part = (float*)ws;
-  int32_t* ticket = (int32_t*)((char*)ws + align_up((size_t)max_items * cin * cout * 4, 256));
+  const int64_t total = (int64_t)K * cin * cout;
   if (x_dtype == VP_BF16 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
-    cudaMemsetAsync(gw, 0, sizeof(float) * K * cin * cout, st);
-    cudaMemsetAsync(ticket, 0, sizeof(int32_t) * K, st);
-    VP_CHECK_ASYNC("conv_wgrad: memset");
-    WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, gw, part, ticket};
-    return wg_tc(cin, cout, p, max_items, st);
+    WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, part};
+    int rc = wg_tc(cin, cout, p, max_items, st);
+    if (rc != VP_OK) return rc;
+    wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st>>>(
+        part, pptr, K, chunk, cin * cout, gw);
+    VP_CHECK_LAUNCH("wgrad_reduce");
+    return VP_OK;
   }
   const int schunk = std::min(chunk, kWgSimtChunk);
   const int sitems = (int)(cap_pairs / schunk + K + 1);
@@ -548,7 +550,6 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
   wgrad_simt_kernel<<<grid, kWgSimtThreads, 0, st>>>(x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
                                                      pptr, schunk, part);
   VP_CHECK_LAUNCH("conv_wgrad_simt");
-  const int64_t total = (int64_t)K * cin * cout;
   wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st>>>(
       part, pptr, K, schunk, cin * cout, gw);
   VP_CHECK_LAUNCH("wgrad_reduce");

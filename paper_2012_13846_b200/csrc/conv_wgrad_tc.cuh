@@ -4,10 +4,9 @@
 // item's pair indices in shared memory and gather 64 pairs per stage with
 // cp.async into MN-major 128B-swizzled tiles (g rows -> A: M = C_out,
 // x rows -> B: N = C_in; the pair index is the MMA K dimension); warp 8
-// issues tcgen05.mma into TMEM; warps 4-7 drain TMEM.  An offset with a
-// single chunk writes grad_W_k directly; otherwise every chunk writes an fp32
-// partial and the LAST chunk to finish (atomic ticket per offset) sums the
-// partials in chunk order -> deterministic, no atomics on the values.
+// issues tcgen05.mma into TMEM; warps 4-7 drain TMEM.  Every chunk writes an fp32 partial and a separate fully parallel kernel
+// (wgrad_reduce_kernel) sums each offset's partials in chunk order ->
+// deterministic, no atomics.
 #pragma once
 #include "common.cuh"
 #include "conv_fwd_tc.cuh"
@@ -23,9 +22,7 @@ struct WgParams {
   const int32_t* pout;
   const int32_t* pptr;
   int chunk;        // pairs per item (multiple of 64, <= kWgMaxChunk)
-  float* gw;        // [K, C_out, C_in], pre-zeroed
   float* part;      // partials, items * C_out * C_in
-  int32_t* ticket;  // [K], zeroed
 };
 
 constexpr int kWgMaxChunk = 2048;
@@ -72,7 +69,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_wgrad_tc_kernel(const __gr
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + C::ACC;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + C::ACC);
-  int* s_flag = reinterpret_cast<int*>(book + 256);
   int* s_pref = reinterpret_cast<int*>(book + 512);  // K+1 <= 344 ints
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -164,17 +160,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_wgrad_tc_kernel(const __gr
   } else if (warp < 8) {
     // ============================ epilogue ============================
     const int ep = warp - 4;
-    const int etid = tid - kTcProd;
     constexpr int PER = COUT * CIN;
     int ii = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++ii) {
-      int k, p0, p1;
-      item_range(item, k, p0, p1);
-      const int nch = s_pref[k + 1] - s_pref[k];
       const int a = ii % C::ACC;
       tc::mbar_wait(&tfull[a], (ii / C::ACC) & 1);
       tc::tc_fence_after();
-      float* dst = nch == 1 ? p.gw + (int64_t)k * PER : p.part + (int64_t)item * PER;
+      float* dst = p.part + (int64_t)item * PER;  // chunk partial; wgrad_reduce_kernel sums in chunk order
 #pragma unroll 1
       for (int mt = 0; mt < C::MT; ++mt) {
 #pragma unroll 1
@@ -199,28 +191,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_wgrad_tc_kernel(const __gr
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[a]);
-      if (nch > 1) {
-        // last chunk of offset k to finish sums all partials in chunk order
-        __threadfence();
-        asm volatile("bar.sync 2, 128;" ::: "memory");
-        if (etid == 0) *s_flag = atomicAdd(p.ticket + k, 1) == nch - 1;
-        asm volatile("bar.sync 2, 128;" ::: "memory");
-        if (*s_flag) {
-          __threadfence();
-          const float* base = p.part + (int64_t)s_pref[k] * PER;
-          for (int e = etid * 4; e < PER; e += kTcEpi * 4) {
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int c = 0; c < nch; ++c) {
-              const float4 v = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)c * PER + e));
-              acc.x += v.x;
-              acc.y += v.y;
-              acc.z += v.z;
-              acc.w += v.w;
-            }
-            *reinterpret_cast<float4*>(p.gw + (int64_t)k * PER + e) = acc;
-          }
-        }
-      }
     }
   } else if (lane == 0) {
     // ============================ MMA issuer ============================

@@ -92,12 +92,21 @@ class SparseResNetTrainer:
 
     def __init__(self, batch=64, points=2048, resolution=64, planes=(32, 64, 128, 256), blocks=1, classes=40,
                  in_channels=1, lr=1e-2, momentum=0.9, seed=2, voxel_size=1.0, device=None,
-                 points_dtype=torch.float32, grad_allreduce=None, feature_dtype=BF16, index="auto"):
+                 points_dtype=torch.float32, grad_allreduce=None, feature_dtype=BF16, index="auto", units=None):
         """feature_dtype: bf16 (tensor-core path, the product) or fp32 (SIMT
         kernels; used to validate the engine's dataflow against the f64
         oracle at fp32 tolerance).  index: coordinate index of the kernel
         maps — "grid" (dense per-level lattice), "hash" (the seam's hash
-        table) or "auto" (grid while all levels' lattices fit in 4 GiB)."""
+        table) or "auto" (grid while all levels' lattices fit in 4 GiB).
+        units: (first, last) inclusive range of pipeline units this engine
+        runs (a SparsePipe stage, pipeline.py); None = the whole model.  A
+        unit is a pipeline cut granule with a single activation at each end:
+        the stem, a strided conv, or a BasicBlock (the last unit also owns
+        the pool + linear + loss head).  A stage that does not start at unit
+        0 reads its input level coordinates / row count / features from
+        `levels[entry].coords`, `levels[entry].n` and `x_in`; a stage that
+        does not end at the last unit reads the gradient of its output from
+        `g_out_ext` and produces the gradient of its input in `grad_input`."""
         self.B, self.P, self.res = batch, points, resolution
         self.planes, self.blocks, self.classes, self.cin = tuple(planes), blocks, classes, in_channels
         self.lr, self.momentum, self.voxel_size = lr, momentum, voxel_size
@@ -142,16 +151,28 @@ class SparseResNetTrainer:
         self.use_grid = index == "grid" or (index == "auto" and grid_bytes <= (4 << 30))
         self.grids = ([torch.full((batch * r ** 3,), 0x7FFFFFFF, dtype=torch.int32, device=dev) for r in self.grid_R]
                       if self.use_grid else None)
+        # ---- pipeline units and the layers this engine owns
+        self.layers_all = self._layer_list()
+        self.units = self._unit_list(self.layers_all)
+        nu = len(self.units)
+        self.unit_range = (0, nu - 1) if units is None else (int(units[0]), int(units[1]))
+        u0, u1 = self.unit_range
+        if not (0 <= u0 <= u1 < nu):
+            raise ValueError(f"unit range {units} outside 0..{nu - 1}")
+        self.first, self.last = u0 == 0, u1 == nu - 1
+        self.layers = [L for u in self.units[u0:u1 + 1] for L in u["layers"]]
+        self.entry_level = self.levels.index(self.layers[0]["src"])
+        self.exit_level = self.levels.index(self.layers[-1]["dst"])
         # ---- parameters
-        self.layers = self._layer_list()
         pb = ParamBuffer(dev)
         for L in self.layers:
             pb.add(L["name"] + ".w", (self.K, L["cout"], L["cin"]), bf16=True)
         for L in self.layers:
             pb.add(L["name"] + ".gamma", (L["cout"],))
             pb.add(L["name"] + ".beta", (L["cout"],))
-        pb.add("fc.w", (classes, planes[-1]))
-        pb.add("fc.b", (classes,))
+        if self.last:
+            pb.add("fc.w", (classes, planes[-1]))
+            pb.add("fc.b", (classes,))
         pb.finalize()
         self.params = pb
         self._init_params(seed)
@@ -181,6 +202,15 @@ class SparseResNetTrainer:
                      for i, lv in enumerate(self.levels)]
         self.gid = [torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
                     for i, lv in enumerate(self.levels)]
+        # stage boundary buffers (pipeline): input features of a non-first
+        # stage, gradient of the output of a non-last stage
+        ent, ext = self.entry_level, self.exit_level
+        self.x_in = (None if self.first else
+                     torch.zeros((self.levels[ent].cap, self.layers[0]["cin"]), dtype=feature_dtype, device=dev))
+        self.g_out_ext = (None if self.last else
+                          torch.zeros((self.levels[ext].cap, self.layers[-1]["cout"]), dtype=feature_dtype,
+                                      device=dev))
+        self.grad_input = None  # gradient wrt x_in after a backward (non-first stages)
         C = planes[-1]
         self.pooled = torch.zeros((batch, C), dtype=torch.float32, device=dev)
         self.pool_counts = torch.zeros(batch, dtype=torch.int32, device=dev)
@@ -195,6 +225,7 @@ class SparseResNetTrainer:
         # run off the critical path (parallel branches of the captured graph)
         self.concurrent = True
         self.side = [torch.cuda.Stream(device=dev) for _ in range(4)]
+        self._forked = set()
 
     # ------------------------------------------------------------------ setup
     def _width_at(self, level):
@@ -231,18 +262,37 @@ class SparseResNetTrainer:
             l["level"] = self.levels.index(l["dst"])
         return L
 
+    @staticmethod
+    def _unit_list(layers):
+        """Pipeline cut granules (stem | strided conv | BasicBlock) in order."""
+        units, i = [], 0
+        while i < len(layers):
+            k = layers[i]["kind"]
+            if k == "c1":
+                units.append(dict(kind="block", layers=[layers[i], layers[i + 1]]))
+                i += 2
+            else:
+                units.append(dict(kind=k, layers=[layers[i]]))
+                i += 1
+        for j, u in enumerate(units):
+            u["index"] = j
+            u["name"] = u["layers"][0]["name"].rsplit(".c1", 1)[0]
+        return units
+
     def _init_params(self, seed):
         """Weights ~ N(0,1)/sqrt(K*C_in) via default_rng(seed), layout (K, C_out,
         C_in) (oracle.init_params / SURVEY §8(d)); BN gamma 1, beta 0; fc
         N(0,1)/sqrt(C)."""
         rng = np.random.default_rng(seed)
         pb = self.params
-        for L in self.layers:
+        for L in self.layers_all:  # draw every layer so a stage's slice equals the full model's
             w = rng.normal(size=(self.K, L["cout"], L["cin"])) / math.sqrt(self.K * L["cin"])
-            pb.view(pb.p, L["name"] + ".w").copy_(torch.from_numpy(w))
-            pb.view(pb.p, L["name"] + ".gamma").fill_(1.0)
+            if L["name"] + ".w" in pb.offsets:
+                pb.view(pb.p, L["name"] + ".w").copy_(torch.from_numpy(w))
+                pb.view(pb.p, L["name"] + ".gamma").fill_(1.0)
         fcw = rng.normal(size=(self.classes, self.planes[-1])) / math.sqrt(self.planes[-1])
-        pb.view(pb.p, "fc.w").copy_(torch.from_numpy(fcw))
+        if "fc.w" in pb.offsets:
+            pb.view(pb.p, "fc.w").copy_(torch.from_numpy(fcw))
         pb.pb[: pb.n_bf16].copy_(pb.p[: pb.n_bf16].to(BF16))
 
     def load_params(self, params: dict):
@@ -285,78 +335,95 @@ class SparseResNetTrainer:
                     m.inv.data_ptr(), m.src.cap, st)
 
     def _integer_stage(self, st):
-        """Voxelize -> strided coordinate chain -> the 9 kernel maps.  With
-        `concurrent`, the coordinate chain and the maps of levels >= 1 run on
-        side streams (waiting only on the level they read), overlapping the
-        level-0 map and the first convolutions on the main stream."""
+        """Voxelize (first stage) -> strided coordinate chain -> the kernel
+        maps this engine's layers use.  With `concurrent`, the coordinate
+        chain and every map but the first layer's run on side streams
+        (waiting only on the levels they read), overlapping the first map and
+        the first convolutions on the main stream."""
         lv = self.levels
-        res3 = _lib.i32_array((self.res,) * 3)
-        self._c("vp_voxelize", self.points.data_ptr(), _lib.dtype_code(self.points), self.cap, self.offsets.data_ptr(),
-                self.B, float(self.voxel_size), res3, lv[0].coords.data_ptr(), lv[0].n.data_ptr(), None,
-                self.feat0.data_ptr(), self.fcode, self.vox_ws.data_ptr(), self.vox_ws.numel(), st)
+        ent, ext = self.entry_level, self.exit_level
+        if self.first:
+            res3 = _lib.i32_array((self.res,) * 3)
+            self._c("vp_voxelize", self.points.data_ptr(), _lib.dtype_code(self.points), self.cap,
+                    self.offsets.data_ptr(), self.B, float(self.voxel_size), res3, lv[0].coords.data_ptr(),
+                    lv[0].n.data_ptr(), None, self.feat0.data_ptr(), self.fcode, self.vox_ws.data_ptr(),
+                    self.vox_ws.numel(), st)
         self.map_events = {}
-        nl = len(lv)
-        if not self.concurrent:
-            for i in range(1, nl):
-                step = _lib.i32_array((lv[i].stride,) * 3)
-                self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
-                        lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
-                        st)
-            for i in range(nl):
-                if self.use_grid:
-                    self._grid_set(i, st, clear=False)
-                self._build_map(self.map_s1[i], st)
-                if i + 1 < nl:
-                    self._build_map(self.map_dn[i], st)
-                if self.use_grid:
-                    self._grid_set(i, st, clear=True)
-            return
+        # maps used by this engine's layers, grouped by the level they gather from
+        by_level = {}
+        for L in self.layers:
+            i = self.levels.index(L["src"])
+            if all(m is not L["map"] for m in by_level.get(i, [])):
+                by_level.setdefault(i, []).append(L["map"])
+        first_map = self.layers[0]["map"]
         main = torch.cuda.current_stream()
-        chain = self.side[0]
-        chain.wait_stream(main)
-        lev_ev = [None] * nl
-        with torch.cuda.stream(chain):
-            cs = chain.cuda_stream
-            for i in range(1, nl):
-                step = _lib.i32_array((lv[i].stride,) * 3)
-                self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
-                        lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
-                        cs)
-                lev_ev[i] = torch.cuda.Event()
-                lev_ev[i].record(chain)
-        # level 0: index + stride-1 map on the critical path (the stem needs it)
-        if self.use_grid:
-            self._grid_set(0, st, clear=False)
-        self._build_map(self.map_s1[0], st)
-        idx0 = torch.cuda.Event()
-        idx0.record(main)
-        # everything else on two side streams.  Each source level's index is
-        # built once and read by both maps that gather from it (map_s1[i],
-        # map_dn[i]), then cleared on the same stream.
-        for i in range(nl):
+        conc = self.concurrent
+
+        def out_coords(i, stream):
+            step = _lib.i32_array((lv[i].stride,) * 3)
+            self._c("vp_output_coords", lv[i - 1].coords.data_ptr(), lv[i - 1].n.data_ptr(), lv[i - 1].cap, step,
+                    lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
+                    stream)
+
+        lev_ev = {}
+        if conc:
+            chain = self.side[0]
+            self._forked.add(id(chain))
+            chain.wait_stream(main)
+            with torch.cuda.stream(chain):
+                for i in range(ent + 1, ext + 1):
+                    out_coords(i, chain.cuda_stream)
+                    lev_ev[i] = torch.cuda.Event()
+                    lev_ev[i].record(chain)
+        else:
+            for i in range(ent + 1, ext + 1):
+                out_coords(i, st)
+
+        def needs(stream, i, maps):
+            if not conc:
+                return
+            if i in lev_ev:
+                stream.wait_event(lev_ev[i])
+            if any(m.dst is not m.src for m in maps) and (i + 1) in lev_ev:
+                stream.wait_event(lev_ev[i + 1])
+
+        def build(i, maps, stream, set_grid, clear_grid, record):
+            ss = stream.cuda_stream if conc else st
+            if self.use_grid and set_grid:
+                self._grid_set(i, ss, clear=False)
+            for m in maps:
+                self._build_map(m, ss)
+                if record:
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    self.map_events[id(m)] = ev
+            if self.use_grid and clear_grid:
+                self._grid_set(i, ss, clear=True)
+
+        for i in sorted(by_level):
+            maps = by_level[i]
+            if not conc:
+                build(i, maps, main, True, True, False)
+                continue
             side = self.side[1 + (i % 2)]
-            if i == 0:
-                side.wait_event(idx0)
+            self._forked.add(id(side))
+            if first_map in maps:
+                # the first layer's map on the critical path; the level's other
+                # map (and the index clear) on a side stream after it
+                needs(main, i, [first_map])
+                rest = [m for m in maps if m is not first_map]
+                build(i, [first_map], main, True, not rest, False)
+                if rest:
+                    ev0 = torch.cuda.Event()
+                    ev0.record(main)
+                    side.wait_event(ev0)
+                    needs(side, i, rest)
+                    with torch.cuda.stream(side):
+                        build(i, rest, side, False, True, True)
             else:
-                side.wait_event(lev_ev[i])
-            if i + 1 < nl:
-                side.wait_event(lev_ev[i + 1])
-            with torch.cuda.stream(side):
-                ss = side.cuda_stream
-                if i > 0:
-                    if self.use_grid:
-                        self._grid_set(i, ss, clear=False)
-                    self._build_map(self.map_s1[i], ss)
-                    ev = torch.cuda.Event()
-                    ev.record(side)
-                    self.map_events[id(self.map_s1[i])] = ev
-                if i + 1 < nl:
-                    self._build_map(self.map_dn[i], ss)
-                    ev = torch.cuda.Event()
-                    ev.record(side)
-                    self.map_events[id(self.map_dn[i])] = ev
-                if self.use_grid:
-                    self._grid_set(i, ss, clear=True)
+                needs(side, i, maps)
+                with torch.cuda.stream(side):
+                    build(i, maps, side, True, True, True)
 
     def _wait_map(self, m):
         ev = getattr(self, "map_events", {}).get(id(m))
@@ -379,17 +446,18 @@ class SparseResNetTrainer:
         return L["a"]
 
     def _forward(self, st):
-        Ls = self.layers
-        x = self._conv_bn(Ls[0], self.feat0, None, True, st)
-        i = 1
-        for s in range(len(self.planes)):
-            x = self._conv_bn(Ls[i], x, None, True, st)
-            i += 1
-            for _ in range(self.blocks):
+        x = self.feat0 if self.first else self.x_in
+        for u in self.units[self.unit_range[0]:self.unit_range[1] + 1]:
+            Ls = u["layers"]
+            if u["kind"] == "block":
                 idn = x
-                h = self._conv_bn(Ls[i], x, None, True, st)
-                x = self._conv_bn(Ls[i + 1], h, idn, True, st)
-                i += 2
+                h = self._conv_bn(Ls[0], x, None, True, st)
+                x = self._conv_bn(Ls[1], h, idn, True, st)
+            else:
+                x = self._conv_bn(Ls[0], x, None, True, st)
+        self.out_act = x
+        if not self.last:
+            return x
         last = self.levels[-1]
         C = self.planes[-1]
         self._c("vp_global_pool", x.data_ptr(), self.fcode, last.coords.data_ptr(), last.n.data_ptr(), last.cap, C,
@@ -414,6 +482,7 @@ class SparseResNetTrainer:
         x = L["x"]
         if self.concurrent:  # weight gradient off the critical path
             ws = self.side[3 - (L["index"] % 2)]
+            self._forked.add(id(ws))
             ws.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(ws):
                 self._c("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
@@ -436,38 +505,40 @@ class SparseResNetTrainer:
         return gin
 
     def _backward(self, st):
-        last = self.levels[-1]
-        C = self.planes[-1]
-        g = self.gact[-1]
-        self._c("vp_global_pool_backward", self.g_pooled.data_ptr(), last.coords.data_ptr(),
-                self.pool_counts.data_ptr(), last.n.data_ptr(), last.cap, C, g.data_ptr(), self.fcode, st)
+        if self.last:
+            last = self.levels[-1]
+            C = self.planes[-1]
+            g = self.gact[-1]
+            self._c("vp_global_pool_backward", self.g_pooled.data_ptr(), last.coords.data_ptr(),
+                    self.pool_counts.data_ptr(), last.n.data_ptr(), last.cap, C, g.data_ptr(), self.fcode, st)
+        else:
+            g = self.g_out_ext  # gradient of this stage's output, received from the next stage
         g2 = None  # pending identity-branch gradient for the current activation
-        Ls = self.layers
-        i = len(Ls) - 1
-        for s in reversed(range(len(self.planes))):
-            lvl = s + 1
-            for _ in range(self.blocks):
-                c1, c2 = Ls[i - 1], Ls[i]
-                gid = self.gid[lvl]
-                # out = relu(bn2(conv2(h)) + idn): mask by out, identity grad -> gid
+        units = self.units[self.unit_range[0]:self.unit_range[1] + 1]
+        for u in reversed(units):
+            Ls = u["layers"]
+            if u["kind"] == "block":
+                c1, c2 = Ls
+                gid = self.gid[c2["level"]]
+                # out = relu(bn2(conv2(h)) + idn): mask by out, identity grad -> gid;
+                # gh lives in gact[lvl] and c1's dgrad overwrites it after use
                 gh = self._bn_conv_backward(c2, g, g2, gid, st)
-                # gh lives in gact[lvl]; c1 backward writes its dgrad into gact[lvl] too,
-                # so move it aside (gy of c2 already consumed it in dgrad->gh)
                 gx = self._bn_conv_backward(c1, gh, None, None, st)
                 g, g2 = gx, gid
-                i -= 2
-            down = Ls[i]
-            g = self._bn_conv_backward(down, g, g2, None, st)
-            g2 = None
-            i -= 1
-        self._bn_conv_backward(Ls[0], g, g2, None, st, need_dgrad=False)
+            elif u["kind"] == "down":
+                g = self._bn_conv_backward(Ls[0], g, g2, None, st)
+                g2 = None
+            else:  # stem: no input gradient
+                self._bn_conv_backward(Ls[0], g, g2, None, st, need_dgrad=False)
+                g = g2 = None
+        if not self.first:
+            if g2 is not None:
+                g.add_(g2)  # the stage input fed both branches of its first block
+            self.grad_input = g
 
     def _optimizer(self, st):
         pb = self.params
-        if self.concurrent:
-            main = torch.cuda.current_stream()
-            for sd in self.side:
-                main.wait_stream(sd)
+        self.join_side_streams()
         if self.grad_allreduce is not None:
             self.grad_allreduce(pb.g)
         self._c("vp_sgd_momentum", pb.p.data_ptr(), pb.m.data_ptr(), pb.g.data_ptr(), pb.size, float(self.lr),
@@ -481,6 +552,39 @@ class SparseResNetTrainer:
         self._forward(st)
         self._backward(st)
         self._optimizer(st)
+
+    def join_side_streams(self):
+        """Join the side streams forked since the last join (a captured body
+        may only wait on streams that joined its capture)."""
+        if self.concurrent:
+            main = torch.cuda.current_stream()
+            for sd in self.side:
+                if id(sd) in self._forked:
+                    main.wait_stream(sd)
+        self._forked = set()
+
+    def forward_body(self):
+        """Pipeline stage forward (integer stage + this engine's layers [+ head])."""
+        st = _lib.stream()
+        self.launch_count = 0
+        self._integer_stage(st)
+        self._forward(st)
+        self.join_side_streams()
+
+    def backward_body(self):
+        """Pipeline stage backward: gradients into params.g (and grad_input)."""
+        st = _lib.stream()
+        self.launch_count = 0
+        self._backward(st)
+        self.join_side_streams()
+
+    def sgd_into(self, p, m, pb_shadow):
+        """SGD with momentum of this engine's gradient into external master
+        buffers (PipeDream weight stashing: the gradient computed with the
+        stashed weights updates the latest weights)."""
+        pb = self.params
+        self._c("vp_sgd_momentum", p.data_ptr(), m.data_ptr(), pb.g.data_ptr(), pb.size, float(self.lr),
+                float(self.momentum), pb_shadow.data_ptr(), pb.n_bf16, _lib.stream())
 
     # ------------------------------------------------------------------ public
     def set_batch(self, points: torch.Tensor, labels: torch.Tensor, non_blocking=True):

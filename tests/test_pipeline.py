@@ -1,0 +1,191 @@
+"""SparsePipe pipeline runtime on CPU (no GPU): 1F1B schedule invariants,
+weight-version audit (acceptance 5), round-robin routing,
+and the runtime itself — stage runners exchanging boundary tensors over
+torch.distributed gloo (world size 2 and 3, 127.0.0.1), against the
+in-process LocalPipeline and against an emulation of PipeDream's
+stashed-weight semantics on one full model."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import pipeline_fake as F
+from paper_2012_13846_b200 import pipeline as PL
+
+N_UNITS = 6
+
+
+def topo(cuts, reps=None):
+    return PL.Topology.even(N_UNITS, cuts, reps)
+
+
+TOPOS = {
+    "1": topo([]),
+    "1-1": topo([2]),
+    "1-1-1-1": topo([0, 2, 3]),
+    "2-1": topo([3], [2, 1]),
+    "1-2": topo([1], [1, 2]),
+}
+
+
+# ---------------------------------------------------------------- schedule
+def test_round_robin():
+    assert PL.route_replica(5, 2) == 1 and PL.route_replica(0, 7) == 0
+    assert [PL.route_replica(i, 3) for i in range(8)] == [0, 1, 2, 0, 1, 2, 0, 1]
+    loads = [len(PL.local_microbatches(11, 3, r)) for r in range(3)]
+    assert max(loads) - min(loads) <= 1
+
+
+@pytest.mark.parametrize("name", list(TOPOS))
+@pytest.mark.parametrize("M", [1, 3, 8])
+def test_schedule_invariants(name, M):
+    t = TOPOS[name]
+    t.validate(N_UNITS)
+    S = len(t.stages)
+    total = 0
+    for s, st in enumerate(t.stages):
+        for r, rank in enumerate(st.ranks):
+            prog = PL.schedule_1f1b(t, rank, M)
+            mine = PL.local_microbatches(M, len(st.ranks), r)
+            f = [a.mb for a in prog if a.op == "F"]
+            b = [a.mb for a in prog if a.op == "B"]
+            assert f == mine and b == mine  # each once, in order
+            total += len(f) + len(b)
+            ops = [a.op for a in prog if a.op != "comm"]
+            first_b = ops.index("B") if "B" in ops else len(ops)
+            assert first_b == min(S - s, len(mine))  # warm-up depth S - s
+            inflight = 0
+            for o in ops:
+                inflight += 1 if o == "F" else -1
+                assert 0 <= inflight <= S - s
+            # every message is sent once and received once by the right peer
+            for a in prog:
+                for c in a.comms:
+                    assert t.locate(c.peer)[0] == (s + 1 if c.kind in ("send_fwd", "recv_bwd") else s - 1)
+    assert total == 2 * M * S  # every micro-batch: one F and one B per stage
+
+
+def test_trace_row_count_4_stage():
+    # a 4-stage 1F1B trace has 2*B*S rows
+    t = TOPOS["1-1-1-1"]
+    rows = sum(1 for rank in range(4) for a in PL.schedule_1f1b(t, rank, 10) if a.op in "FB")
+    assert rows == 2 * 10 * 4
+
+
+def test_version_audit_stash_and_staleness_example():
+    t = TOPOS["1-1-1-1"]
+    audit = PL.simulate_versions(t, 12, stash=True)
+    assert len(audit) == 12 * 4 and all(fv == bv for _, _, fv, bv in audit)
+    stale = {(mb, s): (fv, bv) for mb, s, fv, bv in PL.simulate_versions(t, 12, stash=False)}
+    # PAPER §III-A: minibatch 5 (index 4) at stage 1 runs forward after the
+    # update of minibatch 1 and backward after those of minibatches 2-4
+    assert stale[(4, 0)] == (1, 4)
+    assert PL.simulate_versions(t, 1, stash=False) == [(0, s, 0, 0) for s in range(4)]
+
+
+# ---------------------------------------------------------------- runtime
+def emulate(t, M):
+    """PipeDream semantics on ONE full model: mb i runs with stage s's
+    weights at version v_s(i) (from the schedule), and each stage applies
+    its gradients in micro-batch order.  Straight pipelines only."""
+    audit = {(mb, s): fv for mb, s, fv, _ in PL.simulate_versions(t, M)}
+    w0 = F.init_weights(N_UNITS)
+    hist = [[torch.tensor(w0[st.unit_start:st.unit_end + 1], dtype=torch.float64)] for st in t.stages]
+    mom = [torch.zeros_like(h[0]) for h in hist]
+    cur = [h[0].clone() for h in hist]
+    losses = {}
+    for i in range(M):
+        e = F.FakeEngine((0, N_UNITS - 1), N_UNITS, w0)
+        e.params.pb.copy_(torch.cat([hist[s][audit[(i, s)]] for s in range(len(t.stages))]))
+        pts, lab = F.batch_of(i)
+        e.set_batch(pts, lab)
+        e.forward_body()
+        e.backward_body()
+        losses[i] = float(e.loss)
+        off = 0
+        for s, st in enumerate(t.stages):
+            k = st.unit_end - st.unit_start + 1
+            g = e.params.g[off:off + k]
+            off += k
+            mom[s].mul_(0.9).add_(g)
+            cur[s] = cur[s] - 0.05 * mom[s]
+            hist[s].append(cur[s].clone())
+    return losses, [c.numpy() for c in cur]
+
+
+@pytest.mark.parametrize("name", ["1", "1-1", "1-1-1-1"])
+def test_local_pipeline_equals_pipedream_emulation(name):
+    t, M = TOPOS[name], 9
+    stats = PL.LocalPipeline(t, M, F.make_factory(N_UNITS), F.batch_of).run()
+    ref_loss, ref_w = emulate(t, M)
+    last = t.stages[-1].ranks[0]
+    got = {mb: float(v) for mb, v in stats[last].losses.items()}
+    assert sorted(got) == list(range(M))
+    np.testing.assert_allclose([got[i] for i in range(M)], [ref_loss[i] for i in range(M)], rtol=1e-12)
+    pl = PL.LocalPipeline(t, M, F.make_factory(N_UNITS), F.batch_of)
+    pl.run()
+    for s, st in enumerate(t.stages):
+        np.testing.assert_allclose(pl.runners[st.ranks[0]].master_p.numpy(), ref_w[s], rtol=1e-12)
+        assert all(fv == bv for _, _, fv, bv in pl.runners[st.ranks[0]].stats.audit)
+
+
+def test_local_pipeline_replicated_stage_runs_and_audits():
+    for name in ("2-1", "1-2"):
+        t = TOPOS[name]
+        stats = PL.LocalPipeline(t, 8, F.make_factory(N_UNITS), F.batch_of).run()
+        for r, st in stats.items():
+            assert st.backwards == st.forwards
+            assert all(fv == bv for _, _, fv, bv in st.audit)
+        # replicas of a stage apply the same averaged updates -> identical weights
+    pl = PL.LocalPipeline(TOPOS["2-1"], 8, F.make_factory(N_UNITS), F.batch_of)
+    pl.run()
+    np.testing.assert_array_equal(pl.runners[0].master_p.numpy(), pl.runners[1].master_p.numpy())
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, name, M, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t = TOPOS[name]
+        run = PL.StageRunner(t, rank, M, F.make_factory(N_UNITS), F.batch_of, PL.DistTransport(dist, t))
+        st = run.run()
+        q.put((rank, {k: float(v) for k, v in st.losses.items()}, run.master_p.numpy().tolist(), st.audit))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["1-1", "2-1", "1-1-1-1"])
+def test_gloo_multiprocess_equals_local(name):
+    t, M = TOPOS[name], 8
+    world = t.world
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, M, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, losses, w, audit = q.get(timeout=120)
+        res[r] = (losses, w, audit)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pl = PL.LocalPipeline(t, M, F.make_factory(N_UNITS), F.batch_of)
+    stats = pl.run()
+    for r in range(world):
+        np.testing.assert_allclose(res[r][1], pl.runners[r].master_p.numpy(), rtol=1e-12)
+        assert res[r][2] == stats[r].audit
+    last = t.stages[-1].ranks[0]
+    assert res[last][0] == {k: float(v) for k, v in stats[last].losses.items()}
