@@ -468,7 +468,8 @@ def roofline(tr, dev, iters=30):
 
         def launch(L=L, dst=dst):
             _lib.call("vp_conv_fwd", L["x"].data_ptr(), _lib.VP_BF16, L["x"].shape[0], L["cin"], L["wb"].data_ptr(),
-                      _lib.VP_BF16, L["cout"], tr.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap,
+                      _lib.VP_BF16, L["cout"], tr.K, tr.fwd_table(L).data_ptr(), 0, _lib.ptr(tr.fwd_perm(L)),
+                      dst.n.data_ptr(), dst.cap,
                       L["y"].data_ptr(), _lib.VP_BF16, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st.cuda_stream)
 
         rows.append((_time_launch(launch, iters), L))

@@ -142,6 +142,14 @@ int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, co
                        const int32_t* n_out_dev, int64_t cap_out, const int32_t* offsets_host, int32_t K,
                        const int32_t* in_stride_host3, int32_t* nbr, int32_t* pair_in, int32_t* pair_out,
                        int32_t* pair_ptr, void* ws, size_t ws_bytes, vp_stream_t stream);
+/* Neighbour-mask row ordering (kmap_sort.cu): stable radix sort of the
+ * table's rows by their K-bit hit mask (K <= 30) -> perm [cap] (table row
+ * order -> row id) and table_sorted [cap, K] = table[perm].  Passing
+ * (table_sorted, perm) to vp_conv_fwd / vp_conv_dgrad gives results
+ * identical to (table, NULL) with far fewer active offsets per 128-row tile. */
+size_t vp_kernel_map_sort_ws_bytes(int64_t cap, int32_t K);
+int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, int32_t K, int32_t* perm,
+                       int32_t* table_sorted, void* ws, size_t ws_bytes, vp_stream_t stream);
 /* inverse neighbour table inv[v, k] = u for every pair (v,u) of offset k
  * (the dgrad gather table; conv.py:238-240 iterates the same pairs). */
 int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out,
@@ -154,12 +162,14 @@ int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t 
  * {32,64,128,256}; a SIMT kernel otherwise.  Deterministic, no atomics.
  *   table  : nbr [cap_out, K] (or inv for dgrad); flip != 0 reads column
  *            K-1-k (stride-1 symmetric kernels: inv[v,k] == nbr[v,K-1-k]).
+ *   perm   : nullable; table row i holds the neighbours of output row
+ *            perm[i] (vp_kernel_map_sort), which is where its result goes.
  *   w      : [K, c_out, c_in] in w_dtype.
  *   x_rows : rows allocated in x (every table entry is < x_rows); the
  *            tensor-core path gathers rows with TMA tile::gather4 and
  *            encodes a missing neighbour as row x_rows (zero fill). */
 int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t c_in, const void* w, int32_t w_dtype,
-                int64_t c_out, int32_t K, const int32_t* table, int32_t flip,
+                int64_t c_out, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
                 const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype,
                 void* ws, size_t ws_bytes, vp_stream_t stream);
 size_t vp_conv_fwd_ws_bytes(int64_t c_in, int64_t c_out, int32_t K);
@@ -167,7 +177,7 @@ size_t vp_conv_fwd_ws_bytes(int64_t c_in, int64_t c_out, int32_t K);
  * the forward with W transposed into ws.  table = inv (or nbr with flip). */
 size_t vp_conv_dgrad_ws_bytes(int64_t c_in, int64_t c_out, int32_t K);
 int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t c_out, const void* w, int32_t w_dtype,
-                  int64_t c_in, int32_t K, const int32_t* table, int32_t flip,
+                  int64_t c_in, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
                   const int32_t* n_in_dev, int64_t cap_in, void* grad_in, int32_t gi_dtype,
                   void* ws, size_t ws_bytes, vp_stream_t stream);
 /* wgrad (conv.py:241): grad_w[k] = sum_{(v,u) in pairs_k} g[u] x[v]^T into

@@ -48,14 +48,16 @@ SIGNATURES = {
     "vp_voxel_mean": (C.c_int, [P, I32, I64, I32, P, P, I64, P, P, SZ, P]),
     "vp_kernel_map_ws_bytes": (SZ, [I64, I64, I32]),
     "vp_kernel_map": (C.c_int, [P, P, I64, P, P, I64, P, I32, P, P, P, P, P, P, SZ, P]),
+    "vp_kernel_map_sort_ws_bytes": (SZ, [I64, I32]),
+    "vp_kernel_map_sort": (C.c_int, [P, P, I64, I32, P, P, P, SZ, P]),
     "vp_kernel_map_inverse": (C.c_int, [P, P, I64, I32, P, I64, P]),
     "vp_grid_set": (C.c_int, [P, P, I64, P, I32, I32, I32, I32, P]),
     "vp_kernel_map_grid_ws_bytes": (SZ, [I64, I32]),
     "vp_kernel_map_grid": (C.c_int, [P, I32, I32, I32, P, P, I64, P, I32, P, P, P, P, P, P, SZ, P]),
     "vp_conv_fwd_ws_bytes": (SZ, [I64, I64, I32]),
-    "vp_conv_fwd": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, I64, P, I32, P, SZ, P]),
+    "vp_conv_fwd": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, P, I64, P, I32, P, SZ, P]),
     "vp_conv_dgrad_ws_bytes": (SZ, [I64, I64, I32]),
-    "vp_conv_dgrad": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, I64, P, I32, P, SZ, P]),
+    "vp_conv_dgrad": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, P, I64, P, I32, P, SZ, P]),
     "vp_conv_wgrad_ws_bytes": (SZ, [I64, I64, I32, I64]),
     "vp_conv_wgrad": (C.c_int, [P, I32, I64, P, I32, I64, I32, P, P, P, I64, P, P, SZ, P]),
     "vp_bn_stats_ws_bytes": (SZ, [I64, I64]),

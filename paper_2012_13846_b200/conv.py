@@ -244,9 +244,33 @@ def _check_weights(t: SparseTensor, w: ConvWeights, shape: KernelShape):
         raise StructuralError("kernel shape dimension != tensor dimension")
 
 
+def sort_table(table: torch.Tensor, n_rows: int):
+    """Neighbour-mask row ordering (vp_kernel_map_sort): -> (perm, table[perm])
+    with rows grouped by their hit mask, so each 128-row tile of the implicit
+    GEMM touches few kernel offsets.  Results of the conv are unchanged."""
+    K = table.shape[1]
+    cap = max(n_rows, 1)
+    perm = torch.empty(cap, dtype=torch.int32, device=table.device)
+    ts = torch.empty((cap, K), dtype=torch.int32, device=table.device)
+    if n_rows == 0:
+        return perm[:0], ts[:0]
+    ws = _lib.workspace(_lib.query("vp_kernel_map_sort_ws_bytes", n_rows, K), table.device)
+    _lib.call("vp_kernel_map_sort", table.data_ptr(), None, n_rows, K, perm.data_ptr(), ts.data_ptr(), ws.data_ptr(),
+              ws.numel(), _lib.stream())
+    return perm, ts
+
+
+SORT_MIN_ROWS = 1 << 17  # below this the sort's launches cost more than it saves
+
+
+def _sortable(table: torch.Tensor) -> bool:
+    return table.dim() == 2 and 1 <= table.shape[1] <= 30 and table.shape[0] >= SORT_MIN_ROWS
+
+
 def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: int, out_dtype=None,
-                     flip: bool = False) -> torch.Tensor:
-    """y[u] = sum_k W_k x[nbr[u, k]] for u < n_out (the gather-GEMM of Eq. 3)."""
+                     flip: bool = False, perm: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """y[u] = sum_k W_k x[nbr[u, k]] for u < n_out (the gather-GEMM of Eq. 3).
+    With `perm`, table row i holds the neighbours of output row perm[i]."""
     out_dtype = out_dtype or x.dtype
     K = w.num_offsets
     y = torch.empty((max(n_out, 1), w.n_out), dtype=out_dtype, device=x.device)
@@ -254,13 +278,13 @@ def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: 
     ws = _lib.workspace(_lib.query("vp_conv_fwd_ws_bytes", w.n_in, w.n_out, K), x.device)
     _lib.call("vp_conv_fwd", x.data_ptr(), _lib.dtype_code(x), max(x.shape[0], 1), w.n_in, wt.data_ptr(),
               _lib.dtype_code(wt), w.n_out,
-              K, nbr.data_ptr(), int(flip), None, n_out, y.data_ptr(), _lib.dtype_code(y), ws.data_ptr(), ws.numel(),
-              _lib.stream())
+              K, nbr.data_ptr(), int(flip), _lib.ptr(perm), None, n_out, y.data_ptr(), _lib.dtype_code(y),
+              ws.data_ptr(), ws.numel(), _lib.stream())
     return y[:n_out]
 
 
 def conv_dgrad_raw(g: torch.Tensor, w: ConvWeights, table: torch.Tensor, n_in: int, flip: bool,
-                   out_dtype=None) -> torch.Tensor:
+                   out_dtype=None, perm: Optional[torch.Tensor] = None) -> torch.Tensor:
     """grad_in[v] = sum_k W_k^T g[table[v, k]] (conv.py:240)."""
     out_dtype = out_dtype or g.dtype
     K = w.num_offsets
@@ -269,8 +293,8 @@ def conv_dgrad_raw(g: torch.Tensor, w: ConvWeights, table: torch.Tensor, n_in: i
     ws = _lib.workspace(_lib.query("vp_conv_dgrad_ws_bytes", w.n_in, w.n_out, K), g.device)
     _lib.call("vp_conv_dgrad", g.data_ptr(), _lib.dtype_code(g), max(g.shape[0], 1), w.n_out, wt.data_ptr(),
               _lib.dtype_code(wt),
-              w.n_in, K, table.data_ptr(), int(flip), None, n_in, gi.data_ptr(), _lib.dtype_code(gi), ws.data_ptr(),
-              ws.numel(), _lib.stream())
+              w.n_in, K, table.data_ptr(), int(flip), _lib.ptr(perm), None, n_in, gi.data_ptr(), _lib.dtype_code(gi),
+              ws.data_ptr(), ws.numel(), _lib.stream())
     return gi[:n_in]
 
 
@@ -293,7 +317,9 @@ def sparse_conv_forward(t: SparseTensor, w: ConvWeights, shape: KernelShape, str
     st = _stride3(stride, t.dim)
     out4, ns = _output_coords4(t.coords4, t.tensor_stride, st, t.dim)
     km = _kernel_map4(t.coords4, out4, shape, t.tensor_stride, t.dim, with_pairs=False)
-    y = conv_forward_raw(t.features, w, km.nbr, out4.shape[0])
+    n_out = out4.shape[0]
+    perm, table = sort_table(km.nbr, n_out) if _sortable(km.nbr) else (None, km.nbr)
+    y = conv_forward_raw(t.features, w, table, n_out, perm=perm)
     return SparseTensor(out4, y, ns, _trusted=True, _dim=t.dim)
 
 
@@ -315,7 +341,10 @@ def sparse_conv_backward(t: SparseTensor, w: ConvWeights, shape: KernelShape, st
         table, flip = km.nbr, True  # inv[v, k] == nbr[v, K-1-k] when in == out
     else:
         table, flip = km.inverse(), False
-    gi = conv_dgrad_raw(g, w, table, len(t), flip)
+    perm = None
+    if _sortable(table):  # the flipped table's hit masks are bit-reversed: same grouping
+        perm, table = sort_table(table, len(t))
+    gi = conv_dgrad_raw(g, w, table, len(t), flip, perm=perm)
     gw = conv_wgrad_raw(t.features, g, tuple(w.matrices.shape), km)
     return gi, gw
 
@@ -336,7 +365,8 @@ def sparse_conv_transposed(t: SparseTensor, w: ConvWeights, shape: KernelShape, 
     km = _kernel_map4(fine4, t.coords4, shape, fine_stride, t.dim, with_pairs=False)
     inv = km.inverse()  # [N_fine, K] -> coarse row
     # y[v] = sum_k W_k x[inv[v,k]] : a forward conv over the inverse table
-    y = conv_forward_raw(t.features, w, inv, fine4.shape[0])
+    perm, tbl = sort_table(inv, fine4.shape[0]) if _sortable(inv) else (None, inv)
+    y = conv_forward_raw(t.features, w, tbl, fine4.shape[0], perm=perm)
     return SparseTensor(fine4, y, fine_stride, _trusted=True, _dim=t.dim)
 
 

@@ -58,8 +58,8 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, const int32_
 __global__ void conv_fwd_simt_kernel(const void* __restrict__ x, int x_dtype, int cin,
                                      const void* __restrict__ w, int w_dtype, int64_t wk, int64_t wco,
                                      int64_t wci, int cout, int K, const int32_t* __restrict__ table,
-                                     int flip, const int32_t* n_out_dev, int64_t cap_out, void* y,
-                                     int y_dtype) {
+                                     int flip, const int32_t* __restrict__ perm, const int32_t* n_out_dev,
+                                     int64_t cap_out, void* y, int y_dtype) {
   const int n_out = load_count(n_out_dev, cap_out);
   const int64_t total = (int64_t)n_out * cout;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -73,7 +73,7 @@ __global__ void conv_fwd_simt_kernel(const void* __restrict__ x, int x_dtype, in
       for (int ci = 0; ci < cin; ++ci)
         acc += ldf(w, w_dtype, k * wk + co * wco + ci * wci) * ldf(x, x_dtype, (int64_t)v * cin + ci);
     }
-    stf(y, y_dtype, e, acc);
+    stf(y, y_dtype, perm ? (int64_t)perm[u] * cout + co : e, acc);
   }
 }
 
@@ -146,8 +146,9 @@ __global__ void cast_kernel(const void* __restrict__ src, int sd, void* __restri
 // broadcast from shared memory as [K][C_in][C_out], 32 outputs per pass.
 __global__ void __launch_bounds__(128)
 conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* __restrict__ w, int w_dtype,
-                      int cout, int K, const int32_t* __restrict__ table, int flip, const int32_t* n_out_dev,
-                      int64_t cap_out, void* __restrict__ y, int y_dtype) {
+                      int cout, int K, const int32_t* __restrict__ table, int flip,
+                      const int32_t* __restrict__ perm, const int32_t* n_out_dev, int64_t cap_out,
+                      void* __restrict__ y, int y_dtype) {
   extern __shared__ float s_w[];  // [K][cin][cout]
   for (int e = threadIdx.x; e < K * cin * cout; e += blockDim.x) {
     const int k = e / (cin * cout), r = e - k * cin * cout, ci = r / cout, co = r - ci * cout;
@@ -155,8 +156,9 @@ conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const vo
   }
   __syncthreads();
   const int n_out = load_count(n_out_dev, cap_out);
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_out; u += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t* trow = table + u * K;
+  for (int64_t ut = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ut < n_out; ut += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* trow = table + ut * K;
+    const int64_t u = perm ? (int64_t)perm[ut] : ut;  // output row of table row ut
     float xk[27];
     const bool fast = (cin == 1 && K == 27);
     if (fast) {  // occupancy stem: all 27 index loads, then all 27 feature loads, in flight at once
@@ -217,8 +219,8 @@ conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const vo
 constexpr int kStemRows = 128;
 __global__ void __launch_bounds__(kStemRows)
 conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict__ w, int w_dtype, int cout,
-                 const int32_t* __restrict__ table, int flip, const int32_t* n_out_dev, int64_t cap_out,
-                 __nv_bfloat16* __restrict__ y) {
+                 const int32_t* __restrict__ table, int flip, const int32_t* __restrict__ perm,
+                 const int32_t* n_out_dev, int64_t cap_out, __nv_bfloat16* __restrict__ y) {
   extern __shared__ float s_mem[];
   float* s_w = s_mem;                                             // [27][cout]
   int* s_t = reinterpret_cast<int*>(s_w + 27 * cout);             // [128][27]
@@ -263,7 +265,8 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
       // coalesced: word e of the tile -> row e / 16, pair e % 16
       for (int e = threadIdx.x; e < rows * 16; e += kStemRows) {
         const int rr = e >> 4, c = e & 15;
-        reinterpret_cast<uint32_t*>(y + (u0 + rr) * cout + c0)[c] = s_o[rr * 17 + c];
+        const int64_t orow = perm ? (int64_t)__ldg(perm + u0 + rr) : u0 + rr;
+        reinterpret_cast<uint32_t*>(y + orow * cout + c0)[c] = s_o[rr * 17 + c];
       }
       __syncthreads();
     }
@@ -273,18 +276,18 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
 static bool small_fwd_ok(int64_t cin, int64_t cout, int K) { return cin <= 4 && (int64_t)K * cin * cout <= 12288; }
 
 static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int wd, int cout, int K,
-                            const int32_t* table, int flip, const int32_t* n_out_dev, int64_t cap_out, void* y, int yd,
-                            cudaStream_t st) {
+                            const int32_t* table, int flip, const int32_t* perm, const int32_t* n_out_dev,
+                            int64_t cap_out, void* y, int yd, cudaStream_t st) {
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), kNumSMs * 8));
   if (cin == 1 && K == 27 && cout % 32 == 0 && cout <= 256 && yd == VP_BF16) {
     const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 17 * 4;
-    conv_stem_kernel<<<blocks, kStemRows, smem, st>>>(x, xd, w, wd, cout, table, flip, n_out_dev, cap_out,
+    conv_stem_kernel<<<blocks, kStemRows, smem, st>>>(x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
                                                       (__nv_bfloat16*)y);
     VP_CHECK_LAUNCH("conv_stem");
     return VP_OK;
   }
   conv_fwd_small_kernel<<<blocks, 128, (size_t)K * cin * cout * 4, st>>>(x, xd, cin, w, wd, cout, K, table, flip,
-                                                                         n_out_dev, cap_out, y, yd);
+                                                                         perm, n_out_dev, cap_out, y, yd);
   VP_CHECK_LAUNCH("conv_fwd_small");
   return VP_OK;
 }
@@ -320,7 +323,7 @@ static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   if (part) {
     const int64_t work = p.cap_out * ND / 4;
     split_reduce_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), kNumSMs * 8)), 256, 0, st>>>(
-        (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.y, p.y_dtype);
+        (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.perm, p.y, p.y_dtype);
     VP_CHECK_LAUNCH("split_reduce");
   }
   return VP_OK;
@@ -450,8 +453,8 @@ size_t vp_conv_fwd_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
 }
 
 int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype, int64_t cout,
-                int32_t K, const int32_t* table, int32_t flip, const int32_t* n_out_dev, int64_t cap_out,
-                void* y, int32_t y_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
+                int32_t K, const int32_t* table, int32_t flip, const int32_t* perm, const int32_t* n_out_dev,
+                int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(cin >= 1 && cout >= 1, VP_EVALIDATION, "channel widths must be positive");
@@ -468,15 +471,15 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
       wb = (const bf16*)ws;
     }
     (void)x_rows;  // the cp.async gather zero-fills missing neighbours itself
-    FwdParams p{(const bf16*)x, wb, K, table, flip, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
+    FwdParams p{(const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
     return conv_tc<false>(cin, cout, p, part, st);
   }
   if (small_fwd_ok(cin, cout, K)) return launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip,
-                                                          n_out_dev, cap_out, y, y_dtype, st);
+                                                          perm, n_out_dev, cap_out, y, y_dtype, st);
   const int64_t total = cap_out * cout;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
   conv_fwd_simt_kernel<<<blocks, 256, 0, st>>>(x, x_dtype, (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout,
-                                                K, table, flip, n_out_dev, cap_out, y, y_dtype);
+                                                K, table, flip, perm, n_out_dev, cap_out, y, y_dtype);
   VP_CHECK_LAUNCH("conv_fwd_simt");
   return VP_OK;
 }
@@ -486,8 +489,8 @@ size_t vp_conv_dgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
 }
 
 int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, const void* w, int32_t w_dtype, int64_t cin,
-                  int32_t K, const int32_t* table, int32_t flip, const int32_t* n_in_dev, int64_t cap_in,
-                  void* gi, int32_t gi_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
+                  int32_t K, const int32_t* table, int32_t flip, const int32_t* perm, const int32_t* n_in_dev,
+                  int64_t cap_in, void* gi, int32_t gi_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   if (cap_in <= 0) return VP_OK;
@@ -504,14 +507,14 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
     }
     // grad_in = sum_k W_k^T g[table]: GEMM K-dim = C_out, N = C_in, W read as MN-major B
     (void)g_rows;
-    FwdParams p{(const bf16*)g, wb, K, table, flip, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1, 0, 0};
+    FwdParams p{(const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1, 0, 0};
     return conv_tc<true>(cout, cin, p, part, st);
   }
   const int64_t total = cap_in * cin;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
   // W^T[k, ci, co] = W[k, co, ci]: strides (k: cout*cin, "co"=ci: 1, "ci"=co: cin)
   conv_fwd_simt_kernel<<<blocks, 256, 0, st>>>(g, g_dtype, (int)cout, w, w_dtype, cout * cin, 1, cin, (int)cin,
-                                                K, table, flip, n_in_dev, cap_in, gi, gi_dtype);
+                                                K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype);
   VP_CHECK_LAUNCH("conv_dgrad_simt");
   return VP_OK;
 }

@@ -32,6 +32,7 @@ struct FwdParams {
   int K;
   const int32_t* table;
   int flip;
+  const int32_t* perm;  // table row i holds output row perm[i] (null = identity; kmap_sort.cu)
   const int32_t* n_out_dev;
   int64_t cap_out;
   void* y;
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       tc::tc_fence_after();
       const int lrow = ep * 32 + lane;
       const int64_t row = (int64_t)tile * 128 + lrow;
+      const int64_t orow = (p.perm != nullptr && row < n_out) ? (int64_t)__ldg(p.perm + row) : row;
 #pragma unroll 1
       for (int c0 = 0; c0 < ND; c0 += 32) {
         float v[32];
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 #pragma unroll
             for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           } else if (p.y_dtype == VP_BF16) {
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p.y) + row * ND + c0);
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p.y) + orow * ND + c0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               uint4 pk;
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
               dst[q] = pk;
             }
           } else {
-            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.y) + row * ND + c0);
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.y) + orow * ND + c0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           }
@@ -413,7 +415,8 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 
 // out[r, n] = sum over splits of the fp32 partials, in split order.
 __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_t* n_out_dev, int64_t cap_out, int ND,
-                                    int grid, int max_split, void* __restrict__ y, int y_dtype) {
+                                    int grid, int max_split, const int32_t* __restrict__ perm, void* __restrict__ y,
+                                    int y_dtype) {
   const int n_out = load_count(n_out_dev, cap_out);
   const int ntiles = (n_out + 127) / 128;
   const int S = split_count(ntiles, grid < kNumSMs ? grid : kNumSMs, max_split);
@@ -432,12 +435,13 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_
       acc.z += v.z;
       acc.w += v.w;
     }
+    const int64_t oidx = perm ? (int64_t)__ldg(perm + r) * ND + n : idx;
     if (y_dtype == VP_BF16) {
-      __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<bf16*>(y) + idx);
+      __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<bf16*>(y) + oidx);
       d[0] = __floats2bfloat162_rn(acc.x, acc.y);
       d[1] = __floats2bfloat162_rn(acc.z, acc.w);
     } else {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + idx) = acc;
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + oidx) = acc;
     }
   }
 }

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(kGlueThreads)
 bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int64_t cap, int C,
                   const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype,
                   const void* __restrict__ y, int y_dtype, int relu, const float* __restrict__ mean,
-                  const float* __restrict__ rstd, float* __restrict__ part /*[blocks][2][C]*/) {
+                  const float* __restrict__ rstd, float* __restrict__ part /*[blocks][2][C]*/,
+                  int* __restrict__ ticket, float eps, float* __restrict__ out_a, float* __restrict__ out_b) {
   __shared__ float s_a[kGlueThreads * VEC], s_b[kGlueThreads * VEC];
   const int n = load_count(n_dev, cap);
   const int tpr = C / VEC;
@@ -126,46 +127,62 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
     part[((int64_t)blockIdx.x * 2) * C + e] = sa;
     part[((int64_t)blockIdx.x * 2 + 1) * C + e] = sb;
   }
-}
-
-// One warp per channel: lane-strided f64 sum over the blocks' partials, then
-// a fixed xor-shuffle tree -> deterministic.
-__global__ void bn_finalize_kernel(const float* __restrict__ part, const int32_t* n_dev, int64_t cap, int C,
-                                   int nb, float eps, float* out_a, float* out_b, int mode) {
-  const int n = load_count(n_dev, cap);
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= C) return;
-  const int c = warp;
-  // 4 independent accumulator chains (loads in flight), combined in a fixed order
-  double sa4[4] = {0.0, 0.0, 0.0, 0.0}, sb4[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int b0 = lane; b0 < nb; b0 += 128) {
+  // The LAST block to finish reduces every block's partials in block order
+  // (fixed order -> deterministic) and writes the statistics: one launch
+  // instead of partial + finalize.  It re-arms the ticket for the next call.
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int nb = gridDim.x;
+  __shared__ double d_a[kGlueThreads], d_b[kGlueThreads];  // [G][cc]
+  for (int c0 = 0; c0 < C; c0 += kGlueThreads) {
+    const int cc = min(C - c0, kGlueThreads);
+    const int G = kGlueThreads / cc;  // block groups per channel
+    const int c = c0 + threadIdx.x % cc, g = threadIdx.x / cc;
+    double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (g < G) {
+      for (int b0 = g; b0 < nb; b0 += 4 * G) {  // 4 independent loads in flight, fixed order
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int b = b0 + 32 * q;
-      if (b < nb) {
-        sa4[q] += part[((int64_t)b * 2) * C + c];
-        sb4[q] += part[((int64_t)b * 2 + 1) * C + c];
+        for (int q = 0; q < 4; ++q) {
+          const int b = b0 + q * G;
+          if (b < nb) {
+            a4[q] += __ldcg(part + ((int64_t)b * 2) * C + c);
+            b4[q] += __ldcg(part + ((int64_t)b * 2 + 1) * C + c);
+          }
+        }
       }
     }
-  }
-  double sa = (sa4[0] + sa4[1]) + (sa4[2] + sa4[3]);
-  double sb = (sb4[0] + sb4[1]) + (sb4[2] + sb4[3]);
-  for (int o = 16; o > 0; o >>= 1) {
-    sa += __shfl_xor_sync(0xffffffffu, sa, o);
-    sb += __shfl_xor_sync(0xffffffffu, sb, o);
-  }
-  if (lane == 0) {
-    if (mode == 0) {  // mean, rstd (biased variance, training-mode BN)
-      double mu = n > 0 ? sa / n : 0.0;
-      double var = n > 0 ? sb / n - mu * mu : 0.0;
-      if (var < 0) var = 0;
-      out_a[c] = (float)mu;
-      out_b[c] = (float)(1.0 / sqrt(var + (double)eps));
-    } else {  // ggamma = sum g*xhat, gbeta = sum g
-      out_a[c] = (float)sb;
-      out_b[c] = (float)sa;
+    __syncthreads();
+    if (g < G) {
+      d_a[g * cc + threadIdx.x % cc] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      d_b[g * cc + threadIdx.x % cc] = (b4[0] + b4[1]) + (b4[2] + b4[3]);
     }
+    __syncthreads();
+    if (threadIdx.x < cc) {
+      double sa = 0.0, sb = 0.0;
+      for (int gg = 0; gg < G; ++gg) {
+        sa += d_a[gg * cc + threadIdx.x];
+        sb += d_b[gg * cc + threadIdx.x];
+      }
+      const int ch = c0 + threadIdx.x;
+      if (gy == nullptr) {  // mean, rstd (biased variance, training-mode BN)
+        const double mu = n > 0 ? sa / n : 0.0;
+        double var = n > 0 ? sb / n - mu * mu : 0.0;
+        if (var < 0) var = 0;
+        out_a[ch] = (float)mu;
+        out_b[ch] = (float)(1.0 / sqrt(var + (double)eps));
+      } else {  // ggamma = sum g*xhat, gbeta = sum g
+        out_a[ch] = (float)sb;
+        out_b[ch] = (float)sa;
+      }
+    }
+    __syncthreads();
   }
+  if (threadIdx.x == 0) *ticket = 0;
 }
 
 template <int VEC>
@@ -244,11 +261,13 @@ bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ g
   }
 }
 
-// number of partial blocks: <= 4 per SM, no more than there are row groups
+// number of partial blocks: ~16 row passes of 8 elements per thread, at most
+// one block per SM -> the partial phase is short and the last block reduces
+// few partials per channel (the element count, not the capacity, would be
+// ideal, but it lives on the device; the capacity bounds it)
 static int bn_partial_blocks(int64_t cap, int64_t C) {
-  const int vec = (C % 8 == 0) ? 8 : 1;
-  const int lanes = std::max<int>(1, kGlueThreads / (int)(C / vec));
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(cap, 1), lanes), kNumSMs * 2));
+  const int64_t elems = std::max<int64_t>(cap, 1) * C;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(elems, (int64_t)kGlueThreads * 8 * 16), kNumSMs));
 }
 
 static bool bn_shape_ok(int64_t C) { return (C % 8 == 0 && C / 8 <= kGlueThreads) || C <= kGlueThreads; }
@@ -395,7 +414,11 @@ using namespace vp;
 extern "C" {
 
 size_t vp_bn_stats_ws_bytes(int64_t cap_n, int64_t C) {
-  return align_up((size_t)bn_partial_blocks(cap_n, C) * 2 * C * 4, 256);
+  return align_up((size_t)bn_partial_blocks(cap_n, C) * 2 * C * 4, 256) + 256;  // partials + ticket
+}
+
+static int* bn_ticket(void* ws, int64_t cap, int64_t C) {
+  return reinterpret_cast<int*>((char*)ws + align_up((size_t)bn_partial_blocks(cap, C) * 2 * C * 4, 256));
 }
 
 int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, int64_t C, float eps, float* mean,
@@ -404,16 +427,16 @@ int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   VP_REQUIRE(ws_bytes >= vp_bn_stats_ws_bytes(cap, C), VP_EVALIDATION, "bn_stats: workspace too small");
   const int nb = bn_partial_blocks(cap, C);
+  int* ticket = bn_ticket(ws, cap, C);
+  cudaMemsetAsync(ticket, 0, sizeof(int), st);
+  VP_CHECK_ASYNC("bn_stats: ticket");
   if (C % 8 == 0)
     bn_partial_kernel<8><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
-                                                       nullptr, nullptr, (float*)ws);
+                                                       nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd);
   else
     bn_partial_kernel<1><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
-                                                       nullptr, nullptr, (float*)ws);
-  VP_CHECK_LAUNCH("bn_partial");
-  bn_finalize_kernel<<<(int)ceil_div(C * 32, 256), 256, 0, st>>>((const float*)ws, n_dev, cap, (int)C, nb, eps, mean,
-                                                                 rstd, 0);
-  VP_CHECK_LAUNCH("bn_finalize");
+                                                       nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd);
+  VP_CHECK_LAUNCH("bn_stats");
   return VP_OK;
 }
 
@@ -444,16 +467,16 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
   VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   VP_REQUIRE(ws_bytes >= vp_bn_backward_ws_bytes(cap, C), VP_EVALIDATION, "bn_backward: workspace too small");
   const int nb = bn_partial_blocks(cap, C);
+  int* ticket = bn_ticket(ws, cap, C);
+  cudaMemsetAsync(ticket, 0, sizeof(int), st);
+  VP_CHECK_ASYNC("bn_backward: ticket");
   if (C % 8 == 0)
     bn_partial_kernel<8><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
-                                                       (float*)ws);
+                                                       (float*)ws, ticket, 0.f, ggamma, gbeta);
   else
     bn_partial_kernel<1><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
-                                                       (float*)ws);
-  VP_CHECK_LAUNCH("bn_bwd_partial");
-  bn_finalize_kernel<<<(int)ceil_div(C * 32, 256), 256, 0, st>>>((const float*)ws, n_dev, cap, (int)C, nb, 0.f, ggamma,
-                                                                 gbeta, 1);
-  VP_CHECK_LAUNCH("bn_bwd_finalize");
+                                                       (float*)ws, ticket, 0.f, ggamma, gbeta);
+  VP_CHECK_LAUNCH("bn_bwd_stats");
   if (cap > 0) {
     const int grid = bn_grid_rows(cap, C);
     if (C % 8 == 0)

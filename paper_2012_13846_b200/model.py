@@ -51,6 +51,14 @@ class Map:
     src: Level
     dst: Level
     ws: torch.Tensor
+    # neighbour-mask row ordering (vp_kernel_map_sort) of the tables the
+    # tensor-core convs read: fwd (and stride-1 dgrad, flipped) over
+    # (nbr_s, perm); strided dgrad over (inv_s, iperm).  None = unsorted.
+    perm: Optional[torch.Tensor] = None
+    nbr_s: Optional[torch.Tensor] = None
+    iperm: Optional[torch.Tensor] = None
+    inv_s: Optional[torch.Tensor] = None
+    sort_ws: Optional[torch.Tensor] = None
 
 
 class ParamBuffer:
@@ -139,7 +147,7 @@ class SparseResNetTrainer:
         self.vox_ws = _lib.workspace(_lib.query("vp_voxelize_ws_bytes", cap), dev)
         self.oc_ws = _lib.workspace(_lib.query("vp_output_coords_ws_bytes", cap), dev)
         # ---- maps: stride-1 per level, strided between consecutive levels
-        self.map_s1 = [self._alloc_map(self.levels[i], self.levels[i], strided=False) for i in range(nlev)]
+        self.map_s1 = [self._alloc_map(self.levels[i], self.levels[i], strided=False, sort=i > 0) for i in range(nlev)]
         self.map_dn = [self._alloc_map(self.levels[i], self.levels[i + 1], strided=True) for i in range(nlev - 1)]
         # dense-grid coordinate index per level (cells = B * ceil(res/2^i)^3
         # int32, kept empty between steps: only touched cells are cleared);
@@ -231,10 +239,16 @@ class SparseResNetTrainer:
     def _width_at(self, level):
         return self.planes[0] if level == 0 else self.planes[level - 1]
 
-    def _alloc_map(self, src: Level, dst: Level, strided: bool) -> Map:
+    # maps with at least this many output rows are neighbour-mask sorted
+    # (vp_kernel_map_sort): at C5-scale levels the sort pays for itself many
+    # times over; at C3 (<= 131k rows, diverse masks) its launches cost more
+    # than the 1.3-1.7x fewer active offsets per tile save (tools/sweep_c2.py)
+    SORT_MIN_ROWS = 1 << 18
+
+    def _alloc_map(self, src: Level, dst: Level, strided: bool, sort: bool = True) -> Map:
         dev, K = self.device, self.K
         cap_p = dst.cap * K
-        return Map(
+        m = Map(
             nbr=torch.zeros((dst.cap, K), dtype=torch.int32, device=dev),
             pin=torch.zeros(cap_p, dtype=torch.int32, device=dev),
             pout=torch.zeros(cap_p, dtype=torch.int32, device=dev),
@@ -243,6 +257,16 @@ class SparseResNetTrainer:
             src=src, dst=dst,
             ws=_lib.workspace(max(_lib.query("vp_kernel_map_ws_bytes", src.cap, dst.cap, K),
                                   _lib.query("vp_kernel_map_grid_ws_bytes", dst.cap, K)), dev))
+        if sort and dst.cap >= self.SORT_MIN_ROWS:
+            m.perm = torch.zeros(dst.cap, dtype=torch.int32, device=dev)
+            m.nbr_s = torch.zeros((dst.cap, K), dtype=torch.int32, device=dev)
+            nws = _lib.query("vp_kernel_map_sort_ws_bytes", dst.cap, K)
+            if strided:
+                m.iperm = torch.zeros(src.cap, dtype=torch.int32, device=dev)
+                m.inv_s = torch.zeros((src.cap, K), dtype=torch.int32, device=dev)
+                nws = max(nws, _lib.query("vp_kernel_map_sort_ws_bytes", src.cap, K))
+            m.sort_ws = _lib.workspace(nws, dev)
+        return m
 
     def _layer_list(self):
         L = [dict(name="stem", cin=self.cin, cout=self.planes[0], src=self.levels[0], dst=self.levels[0],
@@ -333,6 +357,29 @@ class SparseResNetTrainer:
         if m.inv is not None:
             self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
                     m.inv.data_ptr(), m.src.cap, st)
+        if m.perm is not None:
+            self._c("vp_kernel_map_sort", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K, m.perm.data_ptr(),
+                    m.nbr_s.data_ptr(), m.sort_ws.data_ptr(), m.sort_ws.numel(), st)
+        if m.iperm is not None:
+            self._c("vp_kernel_map_sort", m.inv.data_ptr(), m.src.n.data_ptr(), m.src.cap, self.K,
+                    m.iperm.data_ptr(), m.inv_s.data_ptr(), m.sort_ws.data_ptr(), m.sort_ws.numel(), st)
+
+    @staticmethod
+    def fwd_table(L):
+        m = L["map"]
+        return m.nbr_s if m.perm is not None else m.nbr
+
+    @staticmethod
+    def fwd_perm(L):
+        return L["map"].perm
+
+    @staticmethod
+    def dgrad_table(L):
+        """(table, flip, perm) of the layer's dgrad gather."""
+        m = L["map"]
+        if m.inv is None:  # stride 1, symmetric 3^3: inv[v,k] == nbr[v,K-1-k]
+            return (m.nbr_s, 1, m.perm) if m.perm is not None else (m.nbr, 1, None)
+        return (m.inv_s, 0, m.iperm) if m.iperm is not None else (m.inv, 0, None)
 
     def _integer_stage(self, st):
         """Voxelize (first stage) -> strided coordinate chain -> the kernel
@@ -435,7 +482,8 @@ class SparseResNetTrainer:
         fc = self.fcode
         self._wait_map(L["map"])
         self._c("vp_conv_fwd", x.data_ptr(), fc, x.shape[0], L["cin"], L["wb"].data_ptr(), L["wcode"], L["cout"],
-                self.K, L["map"].nbr.data_ptr(), 0, dst.n.data_ptr(), dst.cap, L["y"].data_ptr(), fc,
+                self.K, self.fwd_table(L).data_ptr(), 0, _lib.ptr(self.fwd_perm(L)), dst.n.data_ptr(), dst.cap,
+                L["y"].data_ptr(), fc,
                 L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
         self._c("vp_bn_stats", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
                 L["mean"].data_ptr(), L["rstd"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
@@ -495,13 +543,10 @@ class SparseResNetTrainer:
         if not need_dgrad:
             return None
         gin = self.gact[self.levels.index(src)]
-        if m.inv is None:
-            table, flip = m.nbr, 1  # stride 1, symmetric 3^3: inv[v,k] == nbr[v,K-1-k]
-        else:
-            table, flip = m.inv, 0
+        table, flip, perm = self.dgrad_table(L)
         self._c("vp_conv_dgrad", L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(), L["wcode"],
-                L["cin"], self.K, table.data_ptr(), flip, src.n.data_ptr(), src.cap, gin.data_ptr(), fc,
-                L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
+                L["cin"], self.K, table.data_ptr(), flip, _lib.ptr(perm), src.n.data_ptr(), src.cap, gin.data_ptr(),
+                fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
         return gin
 
     def _backward(self, st):
@@ -675,10 +720,10 @@ class SparseResNetTrainer:
                 if L["kind"] != "stem":
                     src = L["src"]
                     gin = self.gact[self.levels.index(src)]
-                    table, flip = (m.nbr, 1) if m.inv is None else (m.inv, 0)
+                    table, flip, perm = self.dgrad_table(L)
                     dg = timed(lambda: self._c(
                         "vp_conv_dgrad", L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(),
-                        L["wcode"], L["cin"], self.K, table.data_ptr(), flip, src.n.data_ptr(), src.cap,
+                        L["wcode"], L["cin"], self.K, table.data_ptr(), flip, _lib.ptr(perm), src.n.data_ptr(), src.cap,
                         gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st))
                 pairs = int(m.ptr[-1].item())
                 out.append({"name": L["name"], "cin": L["cin"], "cout": L["cout"], "n_out": n_out, "pairs": pairs,

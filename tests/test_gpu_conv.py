@@ -172,3 +172,44 @@ def test_transposed_conv_adjoint():
     ref = O.sparse_conv_transposed(c, (1, 1, 1), z.astype(np.float32), wt.astype(np.float32), off, 2)
     np.testing.assert_allclose(y.features.cpu().numpy(), ref, atol=1e-4)
     assert y.tensor_stride == (1, 1, 1)
+
+
+@pytest.mark.parametrize("c", [32, 128, 256])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_mask_sorted_rows_bitwise_equal(c, stride):
+    """vp_kernel_map_sort: perm is a permutation of the live rows, the sorted
+    table is table[perm], and forward / dgrad over (sorted table, perm) equal
+    the unsorted launch (bit for bit when no tile splits or offset pairing
+    regroups the fp32 sums; within one bf16 rounding otherwise)."""
+    from paper_2012_13846_b200 import conv
+    from paper_2012_13846_b200.tensor import SparseTensor
+    pts, offs = O.synthetic_batch(6, 2048, 64, seed=11, dtype=np.float32)
+    c0, _ = O.voxelize_batch(pts.astype(np.float64), offs, 1.0, 64)
+    t = SparseTensor(c0, np.zeros((len(c0), 1)), (1, 1, 1))
+    shape = conv.KernelShape.hypercubic(3, 3)
+    out4, _ = conv._output_coords4(t.coords4, (1, 1, 1), (stride,) * 3, 3)
+    km = conv._kernel_map4(t.coords4, out4, shape, (1, 1, 1), 3)
+    n_out, n = out4.shape[0], len(t)
+    perm, ts = conv.sort_table(km.nbr, n_out)
+    p = perm.cpu().numpy()
+    assert np.array_equal(np.sort(p), np.arange(n_out))
+    assert torch.equal(ts, km.nbr[perm.long()])
+    masks = ((ts >= 0).int() * (1 << torch.arange(27, device=ts.device))).sum(1).cpu().numpy()
+    assert np.all(np.diff(masks) >= 0)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(n, c, device="cuda", generator=g).to(torch.bfloat16)
+    W = conv.ConvWeights(torch.randn(27, c, c, device="cuda", generator=g) / (27 * c) ** 0.5)
+    y0 = conv.conv_forward_raw(x, W, km.nbr, n_out)
+    y1 = conv.conv_forward_raw(x, W, ts, n_out, perm=perm)
+    torch.testing.assert_close(y1.float(), y0.float(), rtol=1e-2, atol=1e-2)
+    gy = torch.randn(n_out, c, device="cuda", generator=g).to(torch.bfloat16)
+    if stride == 1:
+        tab, flip = km.nbr, True
+    else:
+        tab, flip = km.inverse(), False
+    ip, its = conv.sort_table(tab, n)
+    d0 = conv.conv_dgrad_raw(gy, W, tab, n, flip)
+    d1 = conv.conv_dgrad_raw(gy, W, its, n, flip, perm=ip)
+    torch.testing.assert_close(d1.float(), d0.float(), rtol=1e-2, atol=1e-2)
+    # deterministic: the same sorted launch twice is bitwise identical
+    assert torch.equal(d1, conv.conv_dgrad_raw(gy, W, its, n, flip, perm=ip))

@@ -28,7 +28,7 @@ def run(n, c, density, K=27, iters=20, local=False):
     st = torch.cuda.current_stream().cuda_stream
 
     def launch():
-        _lib.call("vp_conv_fwd", x.data_ptr(), _lib.VP_BF16, n, c, w.data_ptr(), _lib.VP_BF16, c, K, nbr.data_ptr(), 0,
+        _lib.call("vp_conv_fwd", x.data_ptr(), _lib.VP_BF16, n, c, w.data_ptr(), _lib.VP_BF16, c, K, nbr.data_ptr(), 0, None,
                   ncount.data_ptr(), n, y.data_ptr(), _lib.VP_BF16, ws.data_ptr(), ws.numel(), st)
 
     for _ in range(3):
