@@ -51,13 +51,52 @@ __global__ void grid_set_kernel(const int4* __restrict__ c, const int32_t* n_dev
   }
 }
 
+// Internal map hash.  The slot layout of the map's private table is not
+// semantic (only the rows found are), so instead of splitmix64 on the 64-bit
+// key it mixes the two 32-bit halves of the packed key (kernels.py:75-78
+// fields) with 32-bit multiplies: a handful of instructions per probe
+// instead of two emulated 64-bit multiplies.
+__device__ __forceinline__ uint32_t map_slot(uint32_t hi, uint32_t lo, uint32_t mask) {
+  uint32_t h = lo * 0x9E3779B1u ^ (hi * 0x85EBCA77u + 0x165667B1u);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  return h & mask;
+}
+
+// packed key halves: hi = batch << 16 | (x + 32768), lo = (y + 32768) << 16 | (z + 32768)
+__device__ __forceinline__ bool pack_halves(int b, int x, int y, int z, uint32_t& hi, uint32_t& lo) {
+  const uint32_t ux = (uint32_t)(x + kAxisBias), uy = (uint32_t)(y + kAxisBias), uz = (uint32_t)(z + kAxisBias);
+  if ((uint32_t)b > (uint32_t)kBatchMax || ux > 0xFFFFu || uy > 0xFFFFu || uz > 0xFFFFu) return false;
+  hi = ((uint32_t)b << 16) | ux;
+  lo = (uy << 16) | uz;
+  return true;
+}
+
 __global__ void map_insert_kernel(const int4* __restrict__ in, const int32_t* n_dev, int64_t cap_n,
                                   Slot* t, uint64_t cap) {
   int n = load_count(n_dev, cap_n);
+  const uint32_t mask = (uint32_t)(cap - 1);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int4 r = in[i];
-    hash_insert(t, cap, pack_key(r.x, r.y, r.z, r.w), (int)i);
+    const int4 r = in[i];
+    uint32_t hi, lo;
+    if (!pack_halves(r.x, r.y, r.z, r.w, hi, lo)) continue;  // unpackable rows are never found
+    const unsigned long long key = ((unsigned long long)hi << 32) | lo;
+    const unsigned int nrow = ~(unsigned int)i;
+    if (key == kEmptyKey) {
+      atomicMax(&t[cap].nrow, nrow);
+      continue;
+    }
+    uint32_t s = map_slot(hi, lo, mask);
+    while (true) {
+      const unsigned long long prev = atomicCAS(&t[s].key, (unsigned long long)kEmptyKey, key);
+      if (prev == kEmptyKey || prev == key) {
+        atomicMax(&t[s].nrow, nrow);  // rows are unique (SparseTensor), so this is the row
+        break;
+      }
+      s = (s + 1) & mask;
+    }
   }
 }
 
@@ -70,11 +109,10 @@ constexpr int kMapTPR = 8;
 constexpr int kProbeThreads = kMapTile * kMapTPR;  // 1024
 constexpr int kProbeWarps = kProbeThreads / 32;
 
-__global__ void __launch_bounds__(kProbeThreads)
+__global__ void __launch_bounds__(kProbeThreads, 2)
 map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t cap_out,
                  const Slot* __restrict__ t, uint64_t cap, const __grid_constant__ Offsets offs,
-                 int K, int sx, int sy, int sz, int32_t* __restrict__ nbr, int32_t* counts,
-                 int ntiles) {
+                 int K, int32_t* __restrict__ nbr, int32_t* counts, int ntiles) {
   __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
   __shared__ unsigned short s_cnt[kProbeWarps][VP_MAX_OFFSETS];
   const int n_out = load_count(n_out_dev, cap_out);
@@ -90,9 +128,10 @@ map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t
   // Probe kMapBatch offsets at once: the first probe step of every key is
   // issued before any result is inspected (memory-level parallelism); the
   // rare collision chains are finished afterwards.
-  constexpr int kMapBatch = 4;
+  constexpr int kMapBatch = 2;
+  const uint32_t mask = (uint32_t)(cap - 1);
   for (int kb = 0; kb < K; kb += kMapTPR * kMapBatch) {
-    uint64_t key[kMapBatch], slot[kMapBatch];
+    uint32_t khi[kMapBatch], klo[kMapBatch], slot[kMapBatch];
     int v[kMapBatch];
     bool live[kMapBatch];
 #pragma unroll
@@ -100,18 +139,17 @@ map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t
       const int k = kb + b * kMapTPR + j;
       live[b] = false;
       v[b] = -1;
-      key[b] = 0;
-      slot[b] = 0;
-      if (valid && k < K) {
-        const long long qx = (long long)r.y + (long long)offs.d[3 * k] * sx;
-        const long long qy = (long long)r.z + (long long)offs.d[3 * k + 1] * sy;
-        const long long qz = (long long)r.w + (long long)offs.d[3 * k + 2] * sz;
-        if (packable64(r.x, qx, qy, qz)) {
-          // out-of-range queries are plain misses (kernels.py:135-148)
-          key[b] = pack_key(r.x, (int)qx, (int)qy, (int)qz);
-          slot[b] = mix64(key[b]) & (cap - 1);
-          live[b] = key[b] != kEmptyKey;
-          if (!live[b]) v[b] = (int)~t[cap].nrow;
+      khi[b] = klo[b] = slot[b] = 0;
+      // offsets arrive pre-multiplied by the input stride and clamped, so
+      // the query stays in int32; out-of-range queries are plain misses
+      // (kernels.py:135-148)
+      if (valid && k < K && pack_halves(r.x, r.y + offs.d[3 * k], r.z + offs.d[3 * k + 1],
+                                        r.w + offs.d[3 * k + 2], khi[b], klo[b])) {
+        if ((khi[b] & klo[b]) == 0xFFFFFFFFu) {
+          v[b] = (int)~t[cap].nrow;  // the one key equal to the empty marker
+        } else {
+          live[b] = true;
+          slot[b] = map_slot(khi[b], klo[b], mask);
         }
       }
     }
@@ -123,12 +161,11 @@ map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t
     for (int b = 0; b < kMapBatch; ++b) {
       if (!live[b]) continue;
       uint4 s4 = sv[b];
-      uint64_t s = slot[b];
+      uint32_t s = slot[b];
       while (true) {
-        const unsigned long long kk = ((unsigned long long)s4.y << 32) | s4.x;
-        if (kk == key[b]) { v[b] = (int)~s4.z; break; }
-        if (kk == kEmptyKey) break;
-        s = (s + 1) & (cap - 1);
+        if (s4.x == klo[b] && s4.y == khi[b]) { v[b] = (int)~s4.z; break; }
+        if ((s4.x & s4.y) == 0xFFFFFFFFu) break;  // empty slot
+        s = (s + 1) & mask;
         s4 = __ldg(reinterpret_cast<const uint4*>(t + s));
       }
     }
@@ -146,12 +183,10 @@ map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t
     }
   }
   __syncthreads();
-  if (staged) {
+  if (staged) {  // warp per row: K <= 32 contiguous ints, no division
     int32_t* dst = nbr + u0 * K;
-    for (int e = tid; e < rows * K; e += kProbeThreads) {
-      const int rr = e / K, k = e - rr * K;
-      dst[e] = s_nbr[rr * (kMapSmemK + 1) + k];
-    }
+    for (int rr = warp; rr < rows; rr += kProbeWarps)
+      if (lane < K) dst[rr * K + lane] = s_nbr[rr * (kMapSmemK + 1) + lane];
   }
   for (int k = tid; k < K; k += kProbeThreads) {
     int c = 0;
@@ -368,7 +403,12 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "kernel_map: workspace too small");
   Offsets offs;
   memset(&offs, 0, sizeof(offs));
-  memcpy(offs.d, offsets_host, sizeof(int32_t) * 3 * K);
+  for (int k = 0; k < K; ++k)
+    for (int a = 0; a < 3; ++a) {
+      // off * stride, clamped: anything beyond +-2^20 misses like +-2^20 does
+      const int64_t d = (int64_t)offsets_host[3 * k + a] * in_stride[a];
+      offs.d[3 * k + a] = (int32_t)std::max<int64_t>(std::min<int64_t>(d, 1 << 20), -(1 << 20));
+    }
   int r = hash_clear(t, cap, st);
   if (r) return r;
   if (cap_in > 0) {
@@ -382,8 +422,7 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
     return VP_OK;
   }
   map_probe_kernel<<<ntiles, kProbeThreads, 0, st>>>((const int4*)out, n_out_dev, cap_out, t, cap, offs, K,
-                                                   in_stride[0], in_stride[1], in_stride[2], nbr, counts,
-                                                   ntiles);
+                                                   nbr, counts, ntiles);
   VP_CHECK_LAUNCH("map_probe");
   if (pair_in) {
     map_scan_kernel<<<K, 1024, 0, st>>>(counts, n_out_dev, cap_out, ntiles, totals);
