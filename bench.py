@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--blocks", type=int, default=1)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=16, help="clouds per CPU-baseline step")
+    ap.add_argument("--cpu-sample", type=int, default=64,
+                    help="clouds per CPU-baseline step (default: the full 64-cloud C3 batch)")
     ap.add_argument("--profile-only", action="store_true", help="warm-up + a few steps, no JSON (for ncu)")
     ap.add_argument("--plan", default="dp",
                     help="N>1: 'dp' (every GPU a replica, gradient all_reduce), 'auto' (SparsePipe partitioner "
@@ -159,6 +160,12 @@ def run_reference(args, rank):
     import ref_runner
 
     t0 = time.time()
+    # bounded sample: ~0.105 s of reference CPU work per cloud on a 16-thread
+    # host (profiles/r1_bench_reference.json), so size each step's cloud count
+    # for the whole --steps K --warmup W run to take about two minutes
+    per_cloud_s = 0.105
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    args.cpu_sample = int(max(2, min(args.cpu_sample, round(budget / per_cloud_s))))
     r = ref_runner.time_steps(args.cpu_sample, args.points, args.res, max(1, args.steps), max(0, args.warmup))
     value = r["clouds_per_s"]
     cores = os.cpu_count() or 1

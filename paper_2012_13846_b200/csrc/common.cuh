@@ -36,6 +36,36 @@ int check_launch(const char* what, int kernels);
 
 constexpr int kNumSMs = 148;
 
+// ------------------------------------------------------------------ launch
+// Every kernel of the library is launched with Programmatic Dependent Launch
+// (programmatic stream serialization): inside a captured step the next
+// kernel's launch and scheduling overlap the current kernel's tail instead of
+// paying a full launch gap on each of the ~200 dependent kernels.  Each
+// kernel starts with pdl_begin(): griddepcontrol.wait (the previous grid has
+// completed and its writes are visible) and only then launch_dependents, so
+// at most two grids overlap and no kernel reads anything early.
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef VP_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

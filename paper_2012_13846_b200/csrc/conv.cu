@@ -31,6 +31,7 @@ namespace vp {
 // sum the chunk partials of each offset in chunk order (deterministic)
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, const int32_t* __restrict__ pptr,
                                     int K, int chunk, int64_t per, float* __restrict__ gw) {
+  ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -60,6 +61,7 @@ __global__ void conv_fwd_simt_kernel(const void* __restrict__ x, int x_dtype, in
                                      int64_t wci, int cout, int K, const int32_t* __restrict__ table,
                                      int flip, const int32_t* __restrict__ perm, const int32_t* n_out_dev,
                                      int64_t cap_out, void* y, int y_dtype) {
+  ::vp::pdl_begin();
   const int n_out = load_count(n_out_dev, cap_out);
   const int64_t total = (int64_t)n_out * cout;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -85,6 +87,7 @@ wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* 
                   int g_dtype, int cout, int K, const int32_t* __restrict__ pin,
                   const int32_t* __restrict__ pout, const int32_t* __restrict__ pptr, int chunk,
                   float* __restrict__ part) {
+  ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
   __shared__ float s_red[kWgSimtThreads / 32][32];
   if (threadIdx.x == 0) {
@@ -126,6 +129,7 @@ wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* 
 
 __global__ void transpose_w_kernel(const void* __restrict__ w, int w_dtype, int K, int cout, int cin,
                                    bf16* __restrict__ wt) {
+  ::vp::pdl_begin();
   // wt[k, ci, co] = w[k, co, ci]
   const int64_t total = (int64_t)K * cout * cin;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -138,6 +142,7 @@ __global__ void transpose_w_kernel(const void* __restrict__ w, int w_dtype, int 
 }
 
 __global__ void cast_kernel(const void* __restrict__ src, int sd, void* __restrict__ dst, int dd, int64_t n) {
+  ::vp::pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     stf(dst, dd, i, ldf(src, sd, i));
 }
@@ -149,6 +154,7 @@ conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const vo
                       int cout, int K, const int32_t* __restrict__ table, int flip,
                       const int32_t* __restrict__ perm, const int32_t* n_out_dev, int64_t cap_out,
                       void* __restrict__ y, int y_dtype) {
+  ::vp::pdl_begin();
   extern __shared__ float s_w[];  // [K][cin][cout]
   for (int e = threadIdx.x; e < K * cin * cout; e += blockDim.x) {
     const int k = e / (cin * cout), r = e - k * cin * cout, ci = r / cout, co = r - ci * cout;
@@ -221,6 +227,7 @@ __global__ void __launch_bounds__(kStemRows)
 conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict__ w, int w_dtype, int cout,
                  const int32_t* __restrict__ table, int flip, const int32_t* __restrict__ perm,
                  const int32_t* n_out_dev, int64_t cap_out, __nv_bfloat16* __restrict__ y) {
+  ::vp::pdl_begin();
   extern __shared__ float s_mem[];
   float* s_w = s_mem;                                             // [27][cout]
   int* s_t = reinterpret_cast<int*>(s_w + 27 * cout);             // [128][27]
@@ -281,12 +288,12 @@ static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int w
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), kNumSMs * 8));
   if (cin == 1 && K == 27 && cout % 32 == 0 && cout <= 256 && yd == VP_BF16) {
     const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 17 * 4;
-    conv_stem_kernel<<<blocks, kStemRows, smem, st>>>(x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
+    ::vp::launch(conv_stem_kernel, blocks, kStemRows, smem, st, x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
                                                       (__nv_bfloat16*)y);
     VP_CHECK_LAUNCH("conv_stem");
     return VP_OK;
   }
-  conv_fwd_small_kernel<<<blocks, 128, (size_t)K * cin * cout * 4, st>>>(x, xd, cin, w, wd, cout, K, table, flip,
+  ::vp::launch(conv_fwd_small_kernel, blocks, 128, (size_t)K * cin * cout * 4, st, x, xd, cin, w, wd, cout, K, table, flip,
                                                                          perm, n_out_dev, cap_out, y, yd);
   VP_CHECK_LAUNCH("conv_fwd_small");
   return VP_OK;
@@ -318,11 +325,11 @@ static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   p.stage_tbl = tbl;
   static const int dbg = getenv("VP_CONV_DBG") ? atoi(getenv("VP_CONV_DBG")) : 0;
   p.dbg = dbg;
-  kern<<<grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st>>>(p);
+  ::vp::launch(kern, grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st, p);
   VP_CHECK_LAUNCH("conv_tc");
   if (part) {
     const int64_t work = p.cap_out * ND / 4;
-    split_reduce_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), kNumSMs * 8)), 256, 0, st>>>(
+    ::vp::launch(split_reduce_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), kNumSMs * 8)), 256, 0, st, 
         (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.perm, p.y, p.y_dtype);
     VP_CHECK_LAUNCH("split_reduce");
   }
@@ -402,7 +409,7 @@ static int launch_wg_tc(const WgParams& p, int max_items, cudaStream_t st) {
     attr = true;
   }
   const int grid = std::max(1, std::min(max_items, kNumSMs));
-  kern<<<grid, kTcThreads, C::SMEM, st>>>(p);
+  ::vp::launch(kern, grid, kTcThreads, C::SMEM, st, p);
   VP_CHECK_LAUNCH("conv_wgrad_tc");
   return VP_OK;
 }
@@ -466,7 +473,7 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
     char* part = (char*)ws + align_up((size_t)K * cin * cout * 2, 256);
     if (w_dtype != VP_BF16) {
       int64_t cnt = (int64_t)K * cin * cout;
-      cast_kernel<<<(int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st>>>(w, w_dtype, ws, VP_BF16, cnt);
+      ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st, w, w_dtype, ws, VP_BF16, cnt);
       VP_CHECK_LAUNCH("conv_fwd: cast w");
       wb = (const bf16*)ws;
     }
@@ -478,7 +485,7 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
                                                           perm, n_out_dev, cap_out, y, y_dtype, st);
   const int64_t total = cap_out * cout;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
-  conv_fwd_simt_kernel<<<blocks, 256, 0, st>>>(x, x_dtype, (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout,
+  ::vp::launch(conv_fwd_simt_kernel, blocks, 256, 0, st, x, x_dtype, (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout,
                                                 K, table, flip, perm, n_out_dev, cap_out, y, y_dtype);
   VP_CHECK_LAUNCH("conv_fwd_simt");
   return VP_OK;
@@ -501,7 +508,7 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
     char* part = (char*)ws + align_up((size_t)K * cin * cout * 2, 256);
     if (w_dtype != VP_BF16) {
       int64_t cnt = (int64_t)K * cin * cout;
-      cast_kernel<<<(int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st>>>(w, w_dtype, ws, VP_BF16, cnt);
+      ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st, w, w_dtype, ws, VP_BF16, cnt);
       VP_CHECK_LAUNCH("conv_dgrad: cast w");
       wb = (const bf16*)ws;
     }
@@ -513,7 +520,7 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
   const int64_t total = cap_in * cin;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
   // W^T[k, ci, co] = W[k, co, ci]: strides (k: cout*cin, "co"=ci: 1, "ci"=co: cin)
-  conv_fwd_simt_kernel<<<blocks, 256, 0, st>>>(g, g_dtype, (int)cout, w, w_dtype, cout * cin, 1, cin, (int)cin,
+  ::vp::launch(conv_fwd_simt_kernel, blocks, 256, 0, st, g, g_dtype, (int)cout, w, w_dtype, cout * cin, 1, cin, (int)cin,
                                                 K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype);
   VP_CHECK_LAUNCH("conv_dgrad_simt");
   return VP_OK;
@@ -542,7 +549,7 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, part};
     int rc = wg_tc(cin, cout, p, max_items, st);
     if (rc != VP_OK) return rc;
-    wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st>>>(
+    ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st, 
         part, pptr, K, chunk, cin * cout, gw);
     VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
@@ -550,10 +557,10 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
   const int schunk = std::min(chunk, kWgSimtChunk);
   const int sitems = (int)(cap_pairs / schunk + K + 1);
   const int grid = std::max(1, std::min(sitems, kNumSMs * 8));
-  wgrad_simt_kernel<<<grid, kWgSimtThreads, 0, st>>>(x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
+  ::vp::launch(wgrad_simt_kernel, grid, kWgSimtThreads, 0, st, x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
                                                      pptr, schunk, part);
   VP_CHECK_LAUNCH("conv_wgrad_simt");
-  wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st>>>(
+  ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st, 
       part, pptr, K, schunk, cin * cout, gw);
   VP_CHECK_LAUNCH("wgrad_reduce");
   return VP_OK;
@@ -561,7 +568,7 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
 
 int vp_cast(const void* src, int32_t sd, void* dst, int32_t dd, int64_t n, vp_stream_t stream) {
   if (n <= 0) return VP_OK;
-  cast_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8), 256, 0, (cudaStream_t)stream>>>(src, sd, dst,
+  ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8), 256, 0, (cudaStream_t)stream, src, sd, dst,
                                                                                                       dd, n);
   VP_CHECK_LAUNCH("cast");
   return VP_OK;

@@ -97,6 +97,7 @@ __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) 
 
 template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL>
 __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_constant__ FwdParams p) {
+  ::vp::pdl_begin();
   using C = FwdTC<KD, ND, BMN, CPS, RB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_t* n_out_dev, int64_t cap_out, int ND,
                                     int grid, int max_split, const int32_t* __restrict__ perm, void* __restrict__ y,
                                     int y_dtype) {
+  ::vp::pdl_begin();
   const int n_out = load_count(n_out_dev, cap_out);
   const int ntiles = (n_out + 127) / 128;
   const int S = split_count(ntiles, grid < kNumSMs ? grid : kNumSMs, max_split);

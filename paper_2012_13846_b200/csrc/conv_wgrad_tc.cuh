@@ -58,6 +58,7 @@ __device__ __forceinline__ uint32_t wg_off(int c, int kk) {
 
 template <int CIN, int COUT>
 __global__ void __launch_bounds__(kTcThreads, 1) conv_wgrad_tc_kernel(const __grid_constant__ WgParams p) {
+  ::vp::pdl_begin();
   using C = WgTC<CIN, COUT>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);

@@ -61,6 +61,7 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
                   const void* __restrict__ y, int y_dtype, int relu, const float* __restrict__ mean,
                   const float* __restrict__ rstd, float* __restrict__ part /*[blocks][2][C]*/,
                   int* __restrict__ ticket, float eps, float* __restrict__ out_a, float* __restrict__ out_b) {
+  ::vp::pdl_begin();
   __shared__ float s_a[kGlueThreads * VEC], s_b[kGlueThreads * VEC];
   const int n = load_count(n_dev, cap);
   const int tpr = C / VEC;
@@ -191,6 +192,7 @@ bn_apply_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int
                 const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
                 const float* __restrict__ beta, const void* __restrict__ res, int res_dtype, int relu,
                 void* __restrict__ y, int y_dtype) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   const int tpr = C / VEC, lanes = kGlueThreads / tpr;
   const int cv = threadIdx.x % tpr, lr = threadIdx.x / tpr;
@@ -224,6 +226,7 @@ bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ g
                          const float* __restrict__ rstd, const float* __restrict__ gamma, int relu,
                          const float* __restrict__ ggamma, const float* __restrict__ gbeta, void* __restrict__ gx,
                          int gx_dtype, void* __restrict__ gres) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   const int tpr = C / VEC, lanes = kGlueThreads / tpr;
   const int cv = threadIdx.x % tpr, lr = threadIdx.x / tpr;
@@ -281,6 +284,7 @@ static int bn_grid_rows(int64_t cap, int64_t C) {
 // ------------------------------------------------------------------ pooling
 __global__ void batch_count_kernel(const int4* __restrict__ coords, const int32_t* n_dev, int64_t cap, int B,
                                    int32_t* counts) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int b = coords[i].x;
@@ -288,6 +292,7 @@ __global__ void batch_count_kernel(const int4* __restrict__ coords, const int32_
   }
 }
 __global__ void batch_starts_kernel(const int32_t* counts, int B, int32_t* starts) {
+  ::vp::pdl_begin();
   __shared__ int s_warp[1024 / 32 + 1];
   __shared__ int s_carry;
   if (threadIdx.x == 0) s_carry = 0;
@@ -306,6 +311,7 @@ __global__ void batch_starts_kernel(const int32_t* counts, int B, int32_t* start
 // downsampling): segment b = [starts[b], starts[b]+counts[b]).
 __global__ void pool_kernel(const void* __restrict__ x, int dtype, int C, int B, const int32_t* counts,
                             const int32_t* starts, float* out) {
+  ::vp::pdl_begin();
   for (int b = blockIdx.x; b < B; b += gridDim.x) {
     const int s = starts[b], cnt = counts[b];
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -318,6 +324,7 @@ __global__ void pool_kernel(const void* __restrict__ x, int dtype, int C, int B,
 __global__ void pool_backward_kernel(const float* __restrict__ gout, const int4* __restrict__ coords,
                                      const int32_t* __restrict__ counts, const int32_t* n_dev, int64_t cap, int C,
                                      void* gx, int gx_dtype) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   const int64_t total = (int64_t)n * C;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -335,6 +342,7 @@ __global__ void pool_backward_kernel(const float* __restrict__ gout, const int4*
 __global__ void xent_sample_kernel(const float* __restrict__ pooled, int B, int C, const float* __restrict__ w,
                                    const float* __restrict__ bias, int classes, const int32_t* __restrict__ labels,
                                    float* logits, float* g_logits, float* loss_b, float* g_pooled) {
+  ::vp::pdl_begin();
   extern __shared__ float sm[];
   float* s_logit = sm;  // classes
   __shared__ float s_max, s_sum;
@@ -373,6 +381,7 @@ __global__ void xent_sample_kernel(const float* __restrict__ pooled, int B, int 
 __global__ void xent_reduce_kernel(const float* __restrict__ pooled, int B, int C, int classes,
                                    const float* __restrict__ g_logits, const float* __restrict__ loss_b,
                                    float* g_w, float* g_b, float* loss) {
+  ::vp::pdl_begin();
   const int64_t total = (int64_t)classes * (C + 1);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -396,6 +405,7 @@ __global__ void xent_reduce_kernel(const float* __restrict__ pooled, int B, int 
 
 __global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ m, const float* __restrict__ g, int64_t n,
                            float lr, float mom, __nv_bfloat16* __restrict__ pb, int64_t nb) {
+  ::vp::pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float mi = mom * m[i] + g[i];
     float pi = p[i] - lr * mi;
@@ -431,10 +441,10 @@ int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   cudaMemsetAsync(ticket, 0, sizeof(int), st);
   VP_CHECK_ASYNC("bn_stats: ticket");
   if (C % 8 == 0)
-    bn_partial_kernel<8><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
+    ::vp::launch(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
                                                        nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd);
   else
-    bn_partial_kernel<1><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
+    ::vp::launch(bn_partial_kernel<1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
                                                        nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd);
   VP_CHECK_LAUNCH("bn_stats");
   return VP_OK;
@@ -448,10 +458,10 @@ int vp_bn_apply(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = bn_grid_rows(cap, C);
   if (C % 8 == 0)
-    bn_apply_kernel<8><<<grid, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
+    ::vp::launch(bn_apply_kernel<8>, grid, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
                                                        relu, y, yd);
   else
-    bn_apply_kernel<1><<<grid, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
+    ::vp::launch(bn_apply_kernel<1>, grid, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
                                                        relu, y, yd);
   VP_CHECK_LAUNCH("bn_apply");
   return VP_OK;
@@ -471,19 +481,19 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
   cudaMemsetAsync(ticket, 0, sizeof(int), st);
   VP_CHECK_ASYNC("bn_backward: ticket");
   if (C % 8 == 0)
-    bn_partial_kernel<8><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
+    ::vp::launch(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
                                                        (float*)ws, ticket, 0.f, ggamma, gbeta);
   else
-    bn_partial_kernel<1><<<nb, kGlueThreads, 0, st>>>(x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
+    ::vp::launch(bn_partial_kernel<1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
                                                        (float*)ws, ticket, 0.f, ggamma, gbeta);
   VP_CHECK_LAUNCH("bn_bwd_stats");
   if (cap > 0) {
     const int grid = bn_grid_rows(cap, C);
     if (C % 8 == 0)
-      bn_backward_apply_kernel<8><<<grid, kGlueThreads, 0, st>>>(gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
+      ::vp::launch(bn_backward_apply_kernel<8>, grid, kGlueThreads, 0, st, gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
                                                                   rstd, gamma, relu, ggamma, gbeta, gx, gxd, gres);
     else
-      bn_backward_apply_kernel<1><<<grid, kGlueThreads, 0, st>>>(gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
+      ::vp::launch(bn_backward_apply_kernel<1>, grid, kGlueThreads, 0, st, gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
                                                                   rstd, gamma, relu, ggamma, gbeta, gx, gxd, gres);
     VP_CHECK_LAUNCH("bn_bwd_apply");
   }
@@ -499,12 +509,12 @@ int vp_global_pool(const void* x, int32_t xd, const int32_t* coords, const int32
   int32_t* starts = (int32_t*)ws;
   cudaMemsetAsync(counts, 0, sizeof(int32_t) * B, st);
   if (cap > 0) {
-    batch_count_kernel<<<grid_for(cap), 256, 0, st>>>((const int4*)coords, n_dev, cap, B, counts);
+    ::vp::launch(batch_count_kernel, grid_for(cap), 256, 0, st, (const int4*)coords, n_dev, cap, B, counts);
     VP_CHECK_LAUNCH("batch_count");
   }
-  batch_starts_kernel<<<1, 1024, 0, st>>>(counts, B, starts);
+  ::vp::launch(batch_starts_kernel, 1, 1024, 0, st, counts, B, starts);
   VP_CHECK_LAUNCH("batch_starts");
-  pool_kernel<<<std::min(B, kNumSMs * 4), C < 256 ? (int)C : 256, 0, st>>>(x, xd, (int)C, B, counts, starts, out);
+  ::vp::launch(pool_kernel, std::min(B, kNumSMs * 4), C < 256 ? (int)C : 256, 0, st, x, xd, (int)C, B, counts, starts, out);
   VP_CHECK_LAUNCH("pool");
   return VP_OK;
 }
@@ -512,7 +522,7 @@ int vp_global_pool(const void* x, int32_t xd, const int32_t* coords, const int32
 int vp_global_pool_backward(const float* gout, const int32_t* coords, const int32_t* counts, const int32_t* n_dev,
                             int64_t cap, int64_t C, void* gx, int32_t gxd, vp_stream_t stream) {
   if (cap <= 0) return VP_OK;
-  pool_backward_kernel<<<grid_for(cap * C), 256, 0, (cudaStream_t)stream>>>(gout, (const int4*)coords, counts, n_dev,
+  ::vp::launch(pool_backward_kernel, grid_for(cap * C), 256, 0, (cudaStream_t)stream, gout, (const int4*)coords, counts, n_dev,
                                                                            cap, (int)C, gx, gxd);
   VP_CHECK_LAUNCH("pool_backward");
   return VP_OK;
@@ -527,10 +537,10 @@ int vp_linear_xent(const float* pooled, int32_t B, int32_t C, const float* w, co
   VP_REQUIRE(ws_bytes >= vp_linear_xent_ws_bytes(B, classes), VP_EVALIDATION, "linear_xent: workspace too small");
   float* g_logits = (float*)ws;
   float* loss_b = g_logits + (size_t)B * classes;
-  xent_sample_kernel<<<B, 128, classes * sizeof(float), st>>>(pooled, B, C, w, b, classes, labels, logits, g_logits,
+  ::vp::launch(xent_sample_kernel, B, 128, classes * sizeof(float), st, pooled, B, C, w, b, classes, labels, logits, g_logits,
                                                              loss_b, g_pooled);
   VP_CHECK_LAUNCH("xent_sample");
-  xent_reduce_kernel<<<grid_for((int64_t)classes * (C + 1)), 256, 0, st>>>(pooled, B, C, classes, g_logits, loss_b,
+  ::vp::launch(xent_reduce_kernel, grid_for((int64_t)classes * (C + 1)), 256, 0, st, pooled, B, C, classes, g_logits, loss_b,
                                                                           g_w, g_b, loss);
   VP_CHECK_LAUNCH("xent_reduce");
   return VP_OK;
@@ -539,7 +549,7 @@ int vp_linear_xent(const float* pooled, int32_t B, int32_t C, const float* w, co
 int vp_sgd_momentum(float* p, float* m, const float* g, int64_t n, float lr, float momentum, void* pb, int64_t nb,
                     vp_stream_t stream) {
   if (n <= 0) return VP_OK;
-  sgd_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(p, m, g, n, lr, momentum, (__nv_bfloat16*)pb, nb);
+  ::vp::launch(sgd_kernel, grid_for(n), 256, 0, (cudaStream_t)stream, p, m, g, n, lr, momentum, (__nv_bfloat16*)pb, nb);
   VP_CHECK_LAUNCH("sgd");
   return VP_OK;
 }

@@ -42,6 +42,7 @@ uint64_t hash_cap_internal(int64_t n) {
 }
 
 __global__ void hash_clear_kernel(Slot* t, uint64_t cap) {
+  ::vp::pdl_begin();
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (; i <= cap; i += stride) {
@@ -56,7 +57,7 @@ __global__ void hash_clear_kernel(Slot* t, uint64_t cap) {
 
 int hash_clear(Slot* t, uint64_t cap, cudaStream_t st) {
   int blocks = (int)std::min<uint64_t>((cap + 1 + 255) / 256, (uint64_t)kNumSMs * 8);
-  hash_clear_kernel<<<blocks, 256, 0, st>>>(t, cap);
+  ::vp::launch(hash_clear_kernel, blocks, 256, 0, st, t, cap);
   VP_CHECK_LAUNCH("hash_clear");
   return VP_OK;
 }
@@ -64,6 +65,7 @@ int hash_clear(Slot* t, uint64_t cap, cudaStream_t st) {
 // ------------------------------------------------------------------ raw key hash
 __global__ void hash_build_keys_kernel(const int64_t* __restrict__ keys, const int32_t* n_dev,
                                        int64_t cap_n, Slot* t, uint64_t cap) {
+  ::vp::pdl_begin();
   int n = load_count(n_dev, cap_n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -73,6 +75,7 @@ __global__ void hash_build_keys_kernel(const int64_t* __restrict__ keys, const i
 __global__ void hash_lookup_keys_kernel(const Slot* __restrict__ t, uint64_t cap,
                                         const int64_t* __restrict__ q, int64_t m,
                                         int64_t* __restrict__ rows) {
+  ::vp::pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
     rows[i] = hash_find(t, cap, (uint64_t)q[i]);
@@ -81,6 +84,7 @@ __global__ void hash_lookup_keys_kernel(const Slot* __restrict__ t, uint64_t cap
 // ------------------------------------------------------------------ packing
 __global__ void pack_coords_kernel(const int4* __restrict__ c, int64_t n, int64_t* keys,
                                    int32_t* bad) {
+  ::vp::pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int4 r = c[i];
@@ -99,6 +103,7 @@ __global__ void pack_coords_kernel(const int4* __restrict__ c, int64_t n, int64_
 __global__ void validate_insert_kernel(const int4* __restrict__ c, const int32_t* n_dev,
                                        int64_t cap_n, int sx, int sy, int sz, Slot* t,
                                        uint64_t cap, int32_t* flags) {
+  ::vp::pdl_begin();
   int n = load_count(n_dev, cap_n);
   int f = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -118,6 +123,7 @@ __global__ void validate_insert_kernel(const int4* __restrict__ c, const int32_t
 
 __global__ void validate_dup_kernel(const int4* __restrict__ c, const int32_t* n_dev, int64_t cap_n,
                                     const Slot* __restrict__ t, uint64_t cap, int32_t* flags) {
+  ::vp::pdl_begin();
   int n = load_count(n_dev, cap_n);
   int f = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -131,6 +137,7 @@ __global__ void validate_dup_kernel(const int4* __restrict__ c, const int32_t* n
 }
 
 __global__ void finite_kernel(const void* p, int dtype, int64_t count, int32_t* flags) {
+  ::vp::pdl_begin();
   int f = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -159,6 +166,7 @@ __device__ __forceinline__ int floordiv_mul(int a, int s) {
 
 __global__ void oc_insert_kernel(const int4* __restrict__ in, const int32_t* n_dev, int64_t cap_n,
                                  int sx, int sy, int sz, Slot* t, uint64_t cap) {
+  ::vp::pdl_begin();
   int n = load_count(n_dev, cap_n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -176,6 +184,7 @@ constexpr int kCompactTile = kCompactBlock * kCompactItems;
 // i's; one row per thread so every lookup is an independent memory request.
 __global__ void first_of_kernel(const int4* __restrict__ rows, const int32_t* n_dev, int64_t cap_n, int sx, int sy,
                                 int sz, const Slot* __restrict__ t, uint64_t cap, int32_t* __restrict__ first_of) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap_n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -192,6 +201,7 @@ __global__ void __launch_bounds__(kCompactBlock)
 compact_first_kernel(const int4* __restrict__ rows, const int32_t* n_dev, int64_t cap_n, int sx, int sy, int sz,
                      const int32_t* __restrict__ first_of, ScanState ss, int4* __restrict__ out, int32_t* n_out,
                      int32_t* rank_of_first) {
+  ::vp::pdl_begin();
   __shared__ int s_tile;
   __shared__ int s_warp[kCompactBlock / 32 + 1];
   __shared__ long long s_prefix;
@@ -235,6 +245,7 @@ compact_first_kernel(const int4* __restrict__ rows, const int32_t* n_dev, int64_
 // parent[i] = output row of input row i = rank of its first row
 __global__ void oc_parent_kernel(const int32_t* n_dev, int64_t cap_n, const int32_t* first_of,
                                  const int32_t* rank_of_first, int32_t* parent) {
+  ::vp::pdl_begin();
   int n = load_count(n_dev, cap_n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -274,6 +285,7 @@ __device__ __forceinline__ int4 voxel_of(const void* pts, int dtype, int64_t i, 
 __global__ void vox_insert_kernel(const void* pts, int dtype, int64_t n, const int64_t* offs, int nc,
                                   double vs, int rx, int ry, int rz, Slot* t, uint64_t cap,
                                   int4* vox_tmp) {
+  ::vp::pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int b = cloud_of(offs, nc, i);
@@ -284,6 +296,7 @@ __global__ void vox_insert_kernel(const void* pts, int dtype, int64_t n, const i
 }
 
 __global__ void fill_kernel(void* p, int dtype, const int32_t* n_dev, int64_t cap, float v) {
+  ::vp::pdl_begin();
   int n = load_count(n_dev, cap);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -298,12 +311,14 @@ __global__ void fill_kernel(void* p, int dtype, const int32_t* n_dev, int64_t ca
 // voxel sorts its own segment ascending (restoring point order) and sums in
 // f64 in that order — the same summation order as np.add.at.
 __global__ void vm_count_kernel(const int32_t* p2v, int64_t n, int32_t* counts) {
+  ::vp::pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(&counts[p2v[i]], 1);
 }
 __global__ void vm_scan_kernel(const int32_t* counts, const int32_t* n_vox_dev, int64_t cap_vox,
                                int32_t* starts, int32_t* cursor) {
+  ::vp::pdl_begin();
   __shared__ int s_warp[1024 / 32 + 1];
   __shared__ int s_carry;
   int nv = load_count(n_vox_dev, cap_vox);
@@ -323,6 +338,7 @@ __global__ void vm_scan_kernel(const int32_t* counts, const int32_t* n_vox_dev, 
   }
 }
 __global__ void vm_place_kernel(const int32_t* p2v, int64_t n, int32_t* cursor, int32_t* order) {
+  ::vp::pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     order[atomicAdd(&cursor[p2v[i]], 1)] = (int32_t)i;
@@ -330,6 +346,7 @@ __global__ void vm_place_kernel(const int32_t* p2v, int64_t n, int32_t* cursor, 
 __global__ void vm_sum_kernel(const void* f, int dtype, int F, int32_t* order, const int32_t* starts,
                               const int32_t* counts, const int32_t* n_vox_dev, int64_t cap_vox,
                               float* out) {
+  ::vp::pdl_begin();
   int nv = load_count(n_vox_dev, cap_vox);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nv;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -378,7 +395,7 @@ int vp_hash_build(const int64_t* keys, const int32_t* n_dev, int64_t cap_n, void
   if (r) return r;
   if (cap_n > 0) {
     int blocks = (int)std::min<int64_t>(ceil_div(cap_n, 256), kNumSMs * 8);
-    hash_build_keys_kernel<<<blocks, 256, 0, st>>>(keys, n_dev, cap_n, (Slot*)table, table_cap);
+    ::vp::launch(hash_build_keys_kernel, blocks, 256, 0, st, keys, n_dev, cap_n, (Slot*)table, table_cap);
     VP_CHECK_LAUNCH("hash_build");
   }
   return VP_OK;
@@ -388,7 +405,7 @@ int vp_hash_lookup(const void* table, int64_t table_cap, const int64_t* q, int64
                    int64_t* rows, vp_stream_t stream) {
   if (m <= 0) return VP_OK;
   int blocks = (int)std::min<int64_t>(ceil_div(m, 256), kNumSMs * 8);
-  hash_lookup_keys_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const Slot*)table, table_cap, q,
+  ::vp::launch(hash_lookup_keys_kernel, blocks, 256, 0, (cudaStream_t)stream, (const Slot*)table, table_cap, q,
                                                                      m, rows);
   VP_CHECK_LAUNCH("hash_lookup");
   return VP_OK;
@@ -398,7 +415,7 @@ int vp_pack_coords(const int32_t* coords, int64_t n, int64_t* keys, int32_t* bad
                    vp_stream_t stream) {
   if (n <= 0) return VP_OK;
   int blocks = (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8);
-  pack_coords_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const int4*)coords, n, keys, bad_dev);
+  ::vp::launch(pack_coords_kernel, blocks, 256, 0, (cudaStream_t)stream, (const int4*)coords, n, keys, bad_dev);
   VP_CHECK_LAUNCH("pack_coords");
   return VP_OK;
 }
@@ -422,10 +439,10 @@ int vp_validate_coords(const int32_t* coords, const int32_t* n_dev, int64_t cap_
   int r = hash_clear(t, cap, st);
   if (r) return r;
   int blocks = (int)std::min<int64_t>(ceil_div(cap_n, 256), kNumSMs * 8);
-  validate_insert_kernel<<<blocks, 256, 0, st>>>((const int4*)coords, n_dev, cap_n, ts[0], ts[1], ts[2],
+  ::vp::launch(validate_insert_kernel, blocks, 256, 0, st, (const int4*)coords, n_dev, cap_n, ts[0], ts[1], ts[2],
                                                  t, cap, flags);
   VP_CHECK_LAUNCH("validate_insert");
-  validate_dup_kernel<<<blocks, 256, 0, st>>>((const int4*)coords, n_dev, cap_n, t, cap, flags);
+  ::vp::launch(validate_dup_kernel, blocks, 256, 0, st, (const int4*)coords, n_dev, cap_n, t, cap, flags);
   VP_CHECK_LAUNCH("validate_dup");
   return VP_OK;
 }
@@ -434,7 +451,7 @@ int vp_check_finite(const void* feats, int32_t dtype, int64_t count, int32_t* fl
                     vp_stream_t stream) {
   if (count <= 0) return VP_OK;
   int blocks = (int)std::min<int64_t>(ceil_div(count, 256), kNumSMs * 8);
-  finite_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(feats, dtype, count, flags);
+  ::vp::launch(finite_kernel, blocks, 256, 0, (cudaStream_t)stream, feats, dtype, count, flags);
   VP_CHECK_LAUNCH("check_finite");
   return VP_OK;
 }
@@ -478,19 +495,19 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
   if (r) return r;
   cudaMemsetAsync(s1.counter, 0, 256 + tiles * 8, st);
   int blocks = (int)std::min<int64_t>(ceil_div(cap_in, 256), kNumSMs * 8);
-  oc_insert_kernel<<<blocks, 256, 0, st>>>((const int4*)in, n_in_dev, cap_in, step[0], step[1], step[2],
+  ::vp::launch(oc_insert_kernel, blocks, 256, 0, st, (const int4*)in, n_in_dev, cap_in, step[0], step[1], step[2],
                                            t, cap);
   VP_CHECK_LAUNCH("oc_insert");
   (void)s2;
-  first_of_kernel<<<(int)ceil_div(cap_in, 256), 256, 0, st>>>((const int4*)in, n_in_dev, cap_in, step[0], step[1],
+  ::vp::launch(first_of_kernel, (int)ceil_div(cap_in, 256), 256, 0, st, (const int4*)in, n_in_dev, cap_in, step[0], step[1],
                                                                step[2], t, cap, first_of);
   VP_CHECK_LAUNCH("oc_first_of");
-  compact_first_kernel<<<(int)tiles, kCompactBlock, 0, st>>>((const int4*)in, n_in_dev, cap_in, step[0], step[1],
+  ::vp::launch(compact_first_kernel, (int)tiles, kCompactBlock, 0, st, (const int4*)in, n_in_dev, cap_in, step[0], step[1],
                                                              step[2], first_of, s1, (int4*)out, n_out_dev,
                                                              parent ? rank_of_first : nullptr);
   VP_CHECK_LAUNCH("oc_compact");
   if (parent) {
-    oc_parent_kernel<<<blocks, 256, 0, st>>>(n_in_dev, cap_in, first_of, rank_of_first, parent);
+    ::vp::launch(oc_parent_kernel, blocks, 256, 0, st, n_in_dev, cap_in, first_of, rank_of_first, parent);
     VP_CHECK_LAUNCH("oc_parent");
   }
   return VP_OK;
@@ -538,21 +555,21 @@ int vp_voxelize(const void* points, int32_t pts_dtype, int64_t n, const int64_t*
   if (r) return r;
   cudaMemsetAsync(s1.counter, 0, 256 + tiles * 8, st);
   int blocks = (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8);
-  vox_insert_kernel<<<blocks, 256, 0, st>>>(points, pts_dtype, n, offs, nc, vs, res[0], res[1], res[2],
+  ::vp::launch(vox_insert_kernel, blocks, 256, 0, st, points, pts_dtype, n, offs, nc, vs, res[0], res[1], res[2],
                                             t, cap, vox);
   VP_CHECK_LAUNCH("vox_insert");
-  first_of_kernel<<<(int)ceil_div(n, 256), 256, 0, st>>>(vox, nullptr, n, 1, 1, 1, t, cap, first_of);
+  ::vp::launch(first_of_kernel, (int)ceil_div(n, 256), 256, 0, st, vox, nullptr, n, 1, 1, 1, t, cap, first_of);
   VP_CHECK_LAUNCH("vox_first_of");
-  compact_first_kernel<<<(int)tiles, kCompactBlock, 0, st>>>(vox, nullptr, n, 1, 1, 1, first_of, s1,
+  ::vp::launch(compact_first_kernel, (int)tiles, kCompactBlock, 0, st, vox, nullptr, n, 1, 1, 1, first_of, s1,
                                                              (int4*)coords_out, n_out_dev,
                                                              p2v ? rank_of_first : nullptr);
   VP_CHECK_LAUNCH("vox_compact");
   if (p2v) {
-    oc_parent_kernel<<<blocks, 256, 0, st>>>(nullptr, n, first_of, rank_of_first, p2v);
+    ::vp::launch(oc_parent_kernel, blocks, 256, 0, st, nullptr, n, first_of, rank_of_first, p2v);
     VP_CHECK_LAUNCH("vox_p2v");
   }
   if (feats_out) {
-    fill_kernel<<<blocks, 256, 0, st>>>(feats_out, feat_dtype, n_out_dev, n, 1.0f);
+    ::vp::launch(fill_kernel, blocks, 256, 0, st, feats_out, feat_dtype, n_out_dev, n, 1.0f);
     VP_CHECK_LAUNCH("vox_fill");
   }
   return VP_OK;
@@ -581,14 +598,14 @@ int vp_voxel_mean(const void* feats_in, int32_t in_dtype, int64_t n, int32_t F, 
   if (n <= 0 || cap_vox <= 0) return VP_OK;
   cudaMemsetAsync(counts, 0, cap_vox * sizeof(int32_t), st);
   int blocks = (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8);
-  vm_count_kernel<<<blocks, 256, 0, st>>>(p2v, n, counts);
+  ::vp::launch(vm_count_kernel, blocks, 256, 0, st, p2v, n, counts);
   VP_CHECK_LAUNCH("vm_count");
-  vm_scan_kernel<<<1, 1024, 0, st>>>(counts, n_vox_dev, cap_vox, starts, cursor);
+  ::vp::launch(vm_scan_kernel, 1, 1024, 0, st, counts, n_vox_dev, cap_vox, starts, cursor);
   VP_CHECK_LAUNCH("vm_scan");
-  vm_place_kernel<<<blocks, 256, 0, st>>>(p2v, n, cursor, order);
+  ::vp::launch(vm_place_kernel, blocks, 256, 0, st, p2v, n, cursor, order);
   VP_CHECK_LAUNCH("vm_place");
   int vblocks = (int)std::min<int64_t>(ceil_div(cap_vox, 128), kNumSMs * 8);
-  vm_sum_kernel<<<vblocks, 128, 0, st>>>(feats_in, in_dtype, F, order, starts, counts, n_vox_dev,
+  ::vp::launch(vm_sum_kernel, vblocks, 128, 0, st, feats_in, in_dtype, F, order, starts, counts, n_vox_dev,
                                          cap_vox, out);
   VP_CHECK_LAUNCH("vm_sum");
   return VP_OK;

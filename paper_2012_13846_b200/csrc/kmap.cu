@@ -43,6 +43,7 @@ __device__ __forceinline__ int grid_linear(const GridSpec& g, int b, int cx, int
 }
 
 __global__ void grid_set_kernel(const int4* __restrict__ c, const int32_t* n_dev, int64_t cap, GridSpec g, int clear) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int4 r = c[i];
@@ -75,6 +76,7 @@ __device__ __forceinline__ bool pack_halves(int b, int x, int y, int z, uint32_t
 
 __global__ void map_insert_kernel(const int4* __restrict__ in, const int32_t* n_dev, int64_t cap_n,
                                   Slot* t, uint64_t cap) {
+  ::vp::pdl_begin();
   int n = load_count(n_dev, cap_n);
   const uint32_t mask = (uint32_t)(cap - 1);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(kProbeThreads, 2)
 map_probe_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t cap_out,
                  const Slot* __restrict__ t, uint64_t cap, const __grid_constant__ Offsets offs,
                  int K, int32_t* __restrict__ nbr, int32_t* counts, int ntiles) {
+  ::vp::pdl_begin();
   __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
   __shared__ unsigned short s_cnt[kProbeWarps][VP_MAX_OFFSETS];
   const int n_out = load_count(n_out_dev, cap_out);
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(kMapTile)
 map_probe_grid_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t cap_out, GridSpec g,
                       const __grid_constant__ GridOffsets offs, int K, int32_t* __restrict__ nbr, int32_t* counts,
                       int ntiles) {
+  ::vp::pdl_begin();
   __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
   __shared__ int s_cnt[kMapTile / 32][VP_MAX_OFFSETS];
   const int n_out = load_count(n_out_dev, cap_out);
@@ -269,6 +273,7 @@ map_probe_grid_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, in
 __global__ void __launch_bounds__(1024)
 map_scan_kernel(int32_t* counts, const int32_t* n_out_dev, int64_t cap_out, int ntiles_cap,
                 int32_t* totals) {
+  ::vp::pdl_begin();
   __shared__ int s_warp[1024 / 32 + 1];
   __shared__ int s_carry;
   const int n_out = load_count(n_out_dev, cap_out);
@@ -295,6 +300,7 @@ __global__ void __launch_bounds__(kMapTile)
 map_emit_kernel(const int32_t* __restrict__ nbr, const int32_t* n_out_dev, int64_t cap_out, int K,
                 const int32_t* __restrict__ counts, const int32_t* __restrict__ totals, int ntiles_cap,
                 int32_t* __restrict__ pair_in, int32_t* __restrict__ pair_out, int32_t* pair_ptr) {
+  ::vp::pdl_begin();
   __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
   __shared__ int s_w[kMapTile / 32][VP_MAX_OFFSETS];
   __shared__ int s_base[VP_MAX_OFFSETS + 1];
@@ -358,6 +364,7 @@ map_emit_kernel(const int32_t* __restrict__ nbr, const int32_t* n_out_dev, int64
 
 __global__ void map_inverse_kernel(const int32_t* __restrict__ nbr, const int32_t* n_out_dev,
                                    int64_t cap_out, int K, int32_t* __restrict__ inv) {
+  ::vp::pdl_begin();
   const int n_out = load_count(n_out_dev, cap_out);
   const int64_t total = (int64_t)n_out * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -413,7 +420,7 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
   if (r) return r;
   if (cap_in > 0) {
     int blocks = (int)std::min<int64_t>(ceil_div(cap_in, 256), kNumSMs * 8);
-    map_insert_kernel<<<blocks, 256, 0, st>>>((const int4*)in, n_in_dev, cap_in, t, cap);
+    ::vp::launch(map_insert_kernel, blocks, 256, 0, st, (const int4*)in, n_in_dev, cap_in, t, cap);
     VP_CHECK_LAUNCH("map_insert");
   }
   if (cap_out <= 0) {
@@ -421,13 +428,13 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
     VP_CHECK_ASYNC("kernel_map(empty)");
     return VP_OK;
   }
-  map_probe_kernel<<<ntiles, kProbeThreads, 0, st>>>((const int4*)out, n_out_dev, cap_out, t, cap, offs, K,
+  ::vp::launch(map_probe_kernel, ntiles, kProbeThreads, 0, st, (const int4*)out, n_out_dev, cap_out, t, cap, offs, K,
                                                    nbr, counts, ntiles);
   VP_CHECK_LAUNCH("map_probe");
   if (pair_in) {
-    map_scan_kernel<<<K, 1024, 0, st>>>(counts, n_out_dev, cap_out, ntiles, totals);
+    ::vp::launch(map_scan_kernel, K, 1024, 0, st, counts, n_out_dev, cap_out, ntiles, totals);
     VP_CHECK_LAUNCH("map_scan");
-    map_emit_kernel<<<ntiles, kMapTile, 0, st>>>(nbr, n_out_dev, cap_out, K, counts, totals, ntiles,
+    ::vp::launch(map_emit_kernel, ntiles, kMapTile, 0, st, nbr, n_out_dev, cap_out, K, counts, totals, ntiles,
                                                      pair_in, pair_out, pair_ptr);
     VP_CHECK_LAUNCH("map_emit");
   }
@@ -440,7 +447,7 @@ int vp_grid_set(const int32_t* coords, const int32_t* n_dev, int64_t cap, int32_
   VP_REQUIRE((int64_t)B * R * R * R < (1ll << 31), VP_EVALIDATION, "grid: B*R^3 must be < 2^31 cells");
   if (cap <= 0) return VP_OK;
   int blocks = (int)std::min<int64_t>(ceil_div(cap, 256), kNumSMs * 8);
-  grid_set_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const int4*)coords, n_dev, cap, GridSpec{cells, B, R, s},
+  ::vp::launch(grid_set_kernel, blocks, 256, 0, (cudaStream_t)stream, (const int4*)coords, n_dev, cap, GridSpec{cells, B, R, s},
                                                           clear);
   VP_CHECK_LAUNCH("grid_set");
   return VP_OK;
@@ -488,13 +495,13 @@ int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, co
     VP_CHECK_ASYNC("kernel_map_grid(empty)");
     return VP_OK;
   }
-  map_probe_grid_kernel<<<ntiles, kMapTile, 0, st>>>((const int4*)out, n_out_dev, cap_out,
+  ::vp::launch(map_probe_grid_kernel, ntiles, kMapTile, 0, st, (const int4*)out, n_out_dev, cap_out,
                                                      GridSpec{const_cast<int32_t*>(cells), B, R, s}, offs, K, nbr,
                                                      counts, ntiles);
   VP_CHECK_LAUNCH("map_probe_grid");
-  map_scan_kernel<<<K, 1024, 0, st>>>(counts, n_out_dev, cap_out, ntiles, totals);
+  ::vp::launch(map_scan_kernel, K, 1024, 0, st, counts, n_out_dev, cap_out, ntiles, totals);
   VP_CHECK_LAUNCH("map_scan");
-  map_emit_kernel<<<ntiles, kMapTile, 0, st>>>(nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out,
+  ::vp::launch(map_emit_kernel, ntiles, kMapTile, 0, st, nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out,
                                                pair_ptr);
   VP_CHECK_LAUNCH("map_emit");
   return VP_OK;
@@ -507,7 +514,7 @@ int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t 
   VP_CHECK_ASYNC("kernel_map_inverse(memset)");
   if (cap_out > 0) {
     int blocks = (int)std::min<int64_t>(ceil_div(cap_out * K, 256), kNumSMs * 16);
-    map_inverse_kernel<<<blocks, 256, 0, st>>>(nbr, n_out_dev, cap_out, K, inv);
+    ::vp::launch(map_inverse_kernel, blocks, 256, 0, st, nbr, n_out_dev, cap_out, K, inv);
     VP_CHECK_LAUNCH("kernel_map_inverse");
   }
   return VP_OK;

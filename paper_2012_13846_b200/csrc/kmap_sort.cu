@@ -22,6 +22,7 @@ constexpr int kSortMaxK = 30;  // mask + the "empty row" sentinel bit fit a 32-b
 
 __global__ void mask_keys_kernel(const int32_t* __restrict__ table, const int32_t* n_dev, int64_t cap, int K,
                                  uint32_t* __restrict__ keys, int32_t* __restrict__ rows) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t m = 0;
@@ -39,6 +40,7 @@ __global__ void mask_keys_kernel(const int32_t* __restrict__ table, const int32_
 // table_sorted[i, :] = table[perm[i], :] (warp per row group, coalesced writes)
 __global__ void permute_rows_kernel(const int32_t* __restrict__ table, const int32_t* __restrict__ perm,
                                     const int32_t* n_dev, int64_t cap, int K, int32_t* __restrict__ out) {
+  ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   const int64_t total = (int64_t)n * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -87,7 +89,7 @@ int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, 
   char* temp = c.take<char>(tb);
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "kernel_map_sort: workspace too small");
   const int blocks = (int)std::min<int64_t>(ceil_div(cap, 256), kNumSMs * 8);
-  mask_keys_kernel<<<blocks, 256, 0, st>>>(table, n_dev, cap, K, keys, rows);
+  ::vp::launch(mask_keys_kernel, blocks, 256, 0, st, table, n_dev, cap, K, keys, rows);
   VP_CHECK_LAUNCH("map_sort: keys");
   // stable LSD radix sort over the K+1 key bits (deterministic)
   VP_REQUIRE(cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys_out, rows, perm, (int)cap, 0, K + 1, st) ==
@@ -98,7 +100,7 @@ int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, 
     if (_st != VP_OK) return _st;
   }
   const int pblocks = (int)std::min<int64_t>(ceil_div(cap * K, 256), kNumSMs * 16);
-  permute_rows_kernel<<<pblocks, 256, 0, st>>>(table, perm, n_dev, cap, K, table_sorted);
+  ::vp::launch(permute_rows_kernel, pblocks, 256, 0, st, table, perm, n_dev, cap, K, table_sorted);
   VP_CHECK_LAUNCH("map_sort: permute");
   return VP_OK;
 }
