@@ -233,7 +233,11 @@ class SparseResNetTrainer:
         # run off the critical path (parallel branches of the captured graph)
         self.concurrent = True
         self.side = [torch.cuda.Stream(device=dev) for _ in range(4)]
+        self.int_side = self.side[:3]  # the integer stage's chain + two map streams
+        self._all_streams = list(self.side)
         self._forked = set()
+        self.prefetch = False
+        self.states = None
 
     # ------------------------------------------------------------------ setup
     def _width_at(self, level):
@@ -414,7 +418,7 @@ class SparseResNetTrainer:
 
         lev_ev = {}
         if conc:
-            chain = self.side[0]
+            chain = self.int_side[0]
             self._forked.add(id(chain))
             chain.wait_stream(main)
             with torch.cuda.stream(chain):
@@ -452,7 +456,7 @@ class SparseResNetTrainer:
             if not conc:
                 build(i, maps, main, True, True, False)
                 continue
-            side = self.side[1 + (i % 2)]
+            side = self.int_side[1 + (i % 2)]
             self._forked.add(id(side))
             if first_map in maps:
                 # the first layer's map on the critical path; the level's other
@@ -603,7 +607,7 @@ class SparseResNetTrainer:
         may only wait on streams that joined its capture)."""
         if self.concurrent:
             main = torch.cuda.current_stream()
-            for sd in self.side:
+            for sd in self._all_streams:
                 if id(sd) in self._forked:
                     main.wait_stream(sd)
         self._forked = set()
@@ -631,14 +635,113 @@ class SparseResNetTrainer:
         self._c("vp_sgd_momentum", p.data_ptr(), m.data_ptr(), pb.g.data_ptr(), pb.size, float(self.lr),
                 float(self.momentum), pb_shadow.data_ptr(), pb.n_bf16, _lib.stream())
 
+    # ------------------------------------------------------------------ prefetch
+    _STATE_ATTRS = ("points", "labels", "levels", "feat0", "map_s1", "map_dn", "layers_all", "units", "layers")
+
+    def _state(self):
+        return {k: getattr(self, k) for k in self._STATE_ATTRS}
+
+    def _use(self, state):
+        for k, v in state.items():
+            setattr(self, k, v)
+
+    def enable_prefetch(self):
+        """Double-buffer the integer stage: the coordinates and kernel maps of
+        the NEXT batch (which depend only on its points, not on the weights)
+        are built on their own streams while the current batch runs its
+        backward pass, taking voxelization, the strided coordinate chain and
+        the nine maps off the step's critical path.  Two copies of the
+        integer-stage buffers (points, labels, levels, maps); the layer
+        records of the second copy share every activation, gradient and
+        parameter tensor with the first.  Whole-model engines only."""
+        if not (self.first and self.last):
+            raise ValueError("prefetch needs a whole-model engine")
+        if self.states is not None:
+            return
+        a = self._state()
+        dev = self.device
+        levels = [Level(torch.zeros_like(lv.coords), torch.zeros_like(lv.n), lv.cap, lv.stride) for lv in self.levels]
+        lmap = dict(zip(map(id, self.levels), levels))
+
+        def clone_map(m):
+            m2 = self._alloc_map(lmap[id(m.src)], lmap[id(m.dst)], m.inv is not None, sort=m.perm is not None)
+            return m2
+
+        map_s1 = [clone_map(m) for m in self.map_s1]
+        map_dn = [clone_map(m) for m in self.map_dn]
+        mmap = dict(zip(map(id, self.map_s1 + self.map_dn), map_s1 + map_dn))
+        layers_all = []
+        for L in self.layers_all:
+            L2 = dict(L)  # activations / params shared
+            L2["src"], L2["dst"], L2["map"] = lmap[id(L["src"])], lmap[id(L["dst"])], mmap[id(L["map"])]
+            layers_all.append(L2)
+        units = self._unit_list(layers_all)
+        b = dict(points=torch.zeros_like(self.points), labels=torch.zeros_like(self.labels), levels=levels,
+                 feat0=torch.zeros_like(self.feat0), map_s1=map_s1, map_dn=map_dn, layers_all=layers_all,
+                 units=units, layers=[L for u in units for L in u["layers"]])
+        self.states = [a, b]
+        # the prefetched integer stage gets its own streams (the origin P
+        # replaces the step's main stream; chain + two map streams)
+        self.pf_stream = torch.cuda.Stream(device=dev)
+        self.int_side = [torch.cuda.Stream(device=dev) for _ in range(3)]
+        self._all_streams = list(self.side) + [self.pf_stream] + self.int_side
+        self.prefetch = True
+        self._phase = 0  # the state the next step trains on
+        self.graphs = [None, None]
+
+    def prefetch_body(self, cur: int):
+        """One training step on state `cur` (its integer stage was built by
+        the previous step) while the integer stage of state 1-cur is built
+        concurrently with the backward pass."""
+        st = _lib.stream()
+        self.launch_count = 0
+        self._use(self.states[cur])
+        self.map_events = {}  # cur's maps were completed by the previous step
+        self._forward(st)
+        main = torch.cuda.current_stream()
+        P = self.pf_stream
+        P.wait_stream(main)
+        self._forked.add(id(P))
+        self._use(self.states[1 - cur])
+        with torch.cuda.stream(P):
+            self._integer_stage(P.cuda_stream)
+        self._use(self.states[cur])
+        self._backward(st)
+        self._optimizer(st)
+
+    def prefetch_prologue(self):
+        """Build the integer stage of the state the next step trains on."""
+        self._use(self.states[self._phase])
+        self._integer_stage(_lib.stream())
+        self.join_side_streams()
+
+    def prime(self, points: torch.Tensor, labels: torch.Tensor):
+        """Prefetch mode: load the batch the next step trains on and build its
+        integer stage now (the pipeline's fill)."""
+        cur = self.states[self._phase]
+        cur["points"].copy_(points, non_blocking=True)
+        cur["labels"].copy_(labels, non_blocking=True)
+        self.prefetch_prologue()
+
     # ------------------------------------------------------------------ public
     def set_batch(self, points: torch.Tensor, labels: torch.Tensor, non_blocking=True):
+        """Stage a batch.  In prefetch mode it is the batch the NEXT step
+        prefetches (its coordinates / maps are built during that step and it
+        trains on the step after)."""
+        if self.prefetch:
+            nxt = self.states[1 - self._phase]
+            nxt["points"].copy_(points, non_blocking=non_blocking)
+            nxt["labels"].copy_(labels, non_blocking=non_blocking)
+            return
         self.points.copy_(points, non_blocking=non_blocking)
         self.labels.copy_(labels, non_blocking=non_blocking)
 
     def capture(self, warmup: int = 1):
         """Record the step into a CUDA graph (after eager warm-up steps that
-        populate the kernels' one-time attribute caches)."""
+        populate the kernels' one-time attribute caches).  In prefetch mode
+        two graphs (one per buffer phase) are recorded and alternate."""
+        if self.prefetch:
+            return self._capture_prefetch()
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -652,7 +755,39 @@ class SparseResNetTrainer:
         self.graph = g
         return g
 
+    def _capture_prefetch(self):
+        """Warm up and record both phases.  Trains two warm-up steps (on the
+        primed batch, then on the staged one) and leaves the pipeline primed
+        with the staged batch again (phase 0)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self._phase = 0
+            self.prefetch_prologue()
+            for ph in (0, 1):  # eager warm-up of both phases (ends with state 0 prefetched)
+                self.prefetch_body(ph)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        lib = _lib.load()
+        for ph in (0, 1):
+            k0 = lib.vp_kernel_launches()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.prefetch_body(ph)
+            self.graphs[ph] = g
+            self.kernels_per_step = lib.vp_kernel_launches() - k0
+        self._phase = 0
+        self.graph = self.graphs[0]
+        return self.graphs
+
     def step(self):
+        if self.prefetch:
+            if self.graphs[self._phase] is not None:
+                self.graphs[self._phase].replay()
+            else:
+                self.prefetch_body(self._phase)
+            self._phase = 1 - self._phase
+            return
         if self.graph is not None:
             self.graph.replay()
         else:

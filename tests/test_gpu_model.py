@@ -160,3 +160,47 @@ def test_concurrent_streams_equal_serial():
         lb = b.train_step_from_host(pts, offs, labels)
         assert la == lb
     assert torch.equal(a.params.p, b.params.p)
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_prefetch_mode_equals_serial(graphs):
+    """enable_prefetch (the next batch's integer stage built during the
+    current backward, double-buffered, optionally as two alternating CUDA
+    graphs) trains the same batches to bitwise-identical losses and weights
+    as the serial step."""
+    from paper_2012_13846_b200 import model
+    B, P, res = 4, 1500, 48
+    batches = []
+    for i in range(4):
+        pts, _ = O.synthetic_batch(B, P, res, seed=20 + i, dtype=np.float32)
+        batches.append((torch.from_numpy(pts).cuda(), torch.tensor([(i * 3 + b) % 40 for b in range(B)],
+                                                                  dtype=torch.int32).cuda()))
+    ser = model.SparseResNetTrainer(batch=B, points=P, resolution=res, seed=2)
+    ref = []
+    for pts, lab in batches:
+        ser.set_batch(pts, lab)
+        ser.step()
+        ref.append(float(ser.loss.item()))
+    pre = model.SparseResNetTrainer(batch=B, points=P, resolution=res, seed=2)
+    pre.enable_prefetch()
+    if graphs:
+        # capture trains two warm-up steps; restart from the same weights after
+        pre.set_batch(*batches[0])
+        pre.capture()
+        pre.params.p.copy_(ser_init_params(B, P, res))
+        pre.params.m.zero_()
+        pre.params.pb[: pre.params.n_bf16].copy_(pre.params.p[: pre.params.n_bf16].to(torch.bfloat16))
+    pre.prime(*batches[0])
+    got = []
+    for k in range(4):
+        if k + 1 < 4:
+            pre.set_batch(*batches[k + 1])
+        pre.step()
+        got.append(float(pre.loss.item()))
+    assert got == ref
+    assert torch.equal(pre.params.p, ser.params.p)
+
+
+def ser_init_params(B, P, res):
+    from paper_2012_13846_b200 import model
+    return model.SparseResNetTrainer(batch=B, points=P, resolution=res, seed=2).params.p.clone()
