@@ -399,6 +399,8 @@ static int conv_tc(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaS
 
 static size_t split_ws_bytes(int64_t nd) { return align_up((size_t)kNumSMs * 128 * nd * 4, 256); }
 
+constexpr int kWgSms = kNumSMs;
+
 template <int CIN, int COUT>
 static int launch_wg_tc(const WgParams& p, int max_items, cudaStream_t st) {
   using C = WgTC<CIN, COUT>;
@@ -408,7 +410,11 @@ static int launch_wg_tc(const WgParams& p, int max_items, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  const int grid = std::max(1, std::min(max_items, kNumSMs));
+  // persistent, on at most kWgSms SMs: the weight gradient runs on a side
+  // stream next to the critical path (BN / dgrad); leaving SMs free for the
+  // high-priority kernels shortens the step (VP_WGRAD_SMS overrides)
+  static const int wg_sms = getenv("VP_WGRAD_SMS") ? atoi(getenv("VP_WGRAD_SMS")) : kWgSms;
+  const int grid = std::max(1, std::min(max_items, wg_sms));
   ::vp::launch(kern, grid, kTcThreads, C::SMEM, st, p);
   VP_CHECK_LAUNCH("conv_wgrad_tc");
   return VP_OK;

@@ -233,6 +233,11 @@ class SparseResNetTrainer:
         # run off the critical path (parallel branches of the captured graph)
         self.concurrent = True
         self.side = [torch.cuda.Stream(device=dev) for _ in range(4)]
+        # the step's critical path (conv -> BN -> conv ...) is captured on a
+        # HIGH-priority stream; side streams (coordinate chain, maps, weight
+        # gradients, prefetch) keep the default low priority, so when both
+        # have blocks waiting the SMs go to the critical path first
+        self.main_stream = torch.cuda.Stream(device=dev, priority=torch.cuda.Stream.priority_range()[1])
         self.int_side = self.side[:3]  # the integer stage's chain + two map streams
         self._all_streams = list(self.side)
         self._forked = set()
@@ -750,7 +755,7 @@ class SparseResNetTrainer:
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g, stream=self.main_stream):
             self.step_body()
         self.graph = g
         return g
@@ -772,7 +777,7 @@ class SparseResNetTrainer:
         for ph in (0, 1):
             k0 = lib.vp_kernel_launches()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=self.main_stream):
                 self.prefetch_body(ph)
             self.graphs[ph] = g
             self.kernels_per_step = lib.vp_kernel_launches() - k0
