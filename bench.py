@@ -40,11 +40,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
-METRIC = "point clouds/sec train (SparseResNet, 64x2048 pts @ 64^3, bf16)"
-CONFIG = {"workload": "C3: sparse-ResNet classifier, 64 clouds x 2048 pts/cloud at 64^3 voxels per GPU, "
-                      "13 convs (blocks=1), bf16 features, SGD momentum",
-          "global_batch_per_gpu": 64, "points_per_cloud": 2048, "resolution": 64, "planes": [32, 64, 128, 256],
-          "blocks": 1, "classes": 40, "l2": "flushed between timed steps (256 MiB memset, outside the events)"}
+def metric_config(args):
+    """BASELINE.json metric on the workload the flags select: the default is
+    configs[2] ("C3"); --batch 256 --points 16384 --res 128 --blocks 2 is the
+    C5 network on one GPU."""
+    c3 = (args.batch, args.points, args.res, args.blocks) == (64, 2048, 64, 1)
+    c5 = (args.res, args.blocks) == (128, 2)
+    tag = "C3" if c3 else ("C5 (one GPU)" if c5 else "custom")
+    metric = (f"point clouds/sec train (SparseResNet{'' if args.blocks == 1 else f' blocks={args.blocks}'}, "
+              f"{args.batch}x{args.points} pts @ {args.res}^3, bf16)")
+    config = {"workload": f"{tag}: sparse-ResNet classifier, {args.batch} clouds x {args.points} pts/cloud at "
+                          f"{args.res}^3 voxels per GPU, {1 + 4 * (1 + 2 * args.blocks)} convs (blocks={args.blocks}), "
+                          "bf16 features, SGD momentum",
+              "global_batch_per_gpu": args.batch, "points_per_cloud": args.points, "resolution": args.res,
+              "planes": [32, 64, 128, 256], "blocks": args.blocks, "classes": 40,
+              "l2": "flushed between timed steps (256 MiB memset, outside the events)"}
+    return metric, config
 
 
 def parse():
@@ -183,6 +194,8 @@ def run_reference(args, rank):
 
 def main():
     args = parse()
+    global METRIC, CONFIG
+    METRIC, CONFIG = metric_config(args)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))

@@ -12,7 +12,8 @@ from paper_2012_13846_b200 import _lib  # noqa: E402
 
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 d = float(sys.argv[2]) if len(sys.argv) > 2 else 0.25
-n, K = 82000, 27
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 82000
+K = 27
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(0)
 x = torch.randn(n, c, device=dev).to(torch.bfloat16)
