@@ -191,7 +191,12 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t c_in, const void* g, i
 /* ---------------------------------------------------------------- glue
  * Model glue for the SparseResNet training step (no reference
  * implementation: SPEC.md:185 non-goal — parity self-defined). */
-/* per-channel batch statistics over rows: mean/rstd [C] fp32 */
+/* per-channel batch statistics over rows: mean/rstd [C] fp32.  One launch:
+ * the last block to finish reduces every block's partials in block order.
+ * ws (vp_bn_stats_ws_bytes) ends in a ticket word that must be ZERO before
+ * the first call with that workspace; every call leaves it zero again (so a
+ * zero-filled workspace can be reused, also under CUDA-graph replay).  The
+ * same holds for vp_bn_backward's workspace. */
 size_t vp_bn_stats_ws_bytes(int64_t cap_n, int64_t C);
 int vp_bn_stats(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C,
                 float eps, float* mean, float* rstd, void* ws, size_t ws_bytes, vp_stream_t stream);

@@ -4,6 +4,8 @@
 // (SPEC.md:185 lists BN/pool/activation math as a non-goal), so parity is
 // self-defined against oracle/voxpipe_oracle.py.  Every reduction runs in a
 // fixed order (per-block partials, then an ordered sum) -> deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace vp {
@@ -130,11 +132,13 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
   }
   // The LAST block to finish reduces every block's partials in block order
   // (fixed order -> deterministic) and writes the statistics: one launch
-  // instead of partial + finalize.  It re-arms the ticket for the next call.
+  // instead of partial + finalize.
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  // atomicInc wraps to 0 after the last block: the ticket re-arms itself
+  // (and a stale value recovers after one launch)
+  if (threadIdx.x == 0) s_last = atomicInc(reinterpret_cast<unsigned int*>(ticket), gridDim.x - 1) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -183,7 +187,6 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *ticket = 0;
 }
 
 template <int VEC>
@@ -268,9 +271,13 @@ bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ g
 // one block per SM -> the partial phase is short and the last block reduces
 // few partials per channel (the element count, not the capacity, would be
 // ideal, but it lives on the device; the capacity bounds it)
+static int bn_passes() {  // row passes per thread in the partial phase (VP_BN_PASSES overrides, for tuning)
+  static const int v = getenv("VP_BN_PASSES") ? std::max(1, atoi(getenv("VP_BN_PASSES"))) : 32;
+  return v;
+}
 static int bn_partial_blocks(int64_t cap, int64_t C) {
   const int64_t elems = std::max<int64_t>(cap, 1) * C;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(elems, (int64_t)kGlueThreads * 8 * 16), kNumSMs));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(elems, (int64_t)kGlueThreads * 8 * bn_passes()), kNumSMs));
 }
 
 static bool bn_shape_ok(int64_t C) { return (C % 8 == 0 && C / 8 <= kGlueThreads) || C <= kGlueThreads; }
@@ -438,8 +445,6 @@ int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   VP_REQUIRE(ws_bytes >= vp_bn_stats_ws_bytes(cap, C), VP_EVALIDATION, "bn_stats: workspace too small");
   const int nb = bn_partial_blocks(cap, C);
   int* ticket = bn_ticket(ws, cap, C);
-  cudaMemsetAsync(ticket, 0, sizeof(int), st);
-  VP_CHECK_ASYNC("bn_stats: ticket");
   if (C % 8 == 0)
     ::vp::launch(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
                                                        nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd);
@@ -478,8 +483,6 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
   VP_REQUIRE(ws_bytes >= vp_bn_backward_ws_bytes(cap, C), VP_EVALIDATION, "bn_backward: workspace too small");
   const int nb = bn_partial_blocks(cap, C);
   int* ticket = bn_ticket(ws, cap, C);
-  cudaMemsetAsync(ticket, 0, sizeof(int), st);
-  VP_CHECK_ASYNC("bn_backward: ticket");
   if (C % 8 == 0)
     ::vp::launch(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
                                                        (float*)ws, ticket, 0.f, ggamma, gbeta);

@@ -204,7 +204,9 @@ class SparseResNetTrainer:
             L["dg_ws"] = _lib.workspace(_lib.query("vp_conv_dgrad_ws_bytes", L["cin"], L["cout"], self.K), dev)
             L["wg_ws"] = _lib.workspace(_lib.query("vp_conv_wgrad_ws_bytes", L["cin"], L["cout"], self.K,
                                                    L["map"].pin.numel()), dev)
-            L["bn_ws"] = _lib.workspace(_lib.query("vp_bn_stats_ws_bytes", n, L["cout"]), dev)
+            # zero-filled: the fused BN kernels' ticket word starts (and stays) zero
+            L["bn_ws"] = torch.zeros(int(_lib.query("vp_bn_stats_ws_bytes", n, L["cout"])), dtype=torch.uint8,
+                                     device=dev)
         # gradient buffers per level for the activation flowing back
         self.gact = [torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
                      for i, lv in enumerate(self.levels)]
