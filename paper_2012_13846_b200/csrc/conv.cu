@@ -304,11 +304,11 @@ static bool tc_width(int64_t c) { return c == 32 || c == 64 || c == 128 || c == 
 
 constexpr int kMaxSplit = 8;
 
-template <int KD, int ND, bool BMN, int CPS, int RB>
+template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1>
 static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
-  using C = FwdTC<KD, ND, BMN, CPS, RB>;
+  using C = FwdTC<KD, ND, BMN, CPS, RB, TT>;
   const bool tbl = p0.K <= kTblK && ((uintptr_t)p0.table & 15) == 0;
-  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true> : conv_tc_kernel<KD, ND, BMN, CPS, RB, false>;
+  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true, TT> : conv_tc_kernel<KD, ND, BMN, CPS, RB, false, TT>;
   static_assert(C::SMEM_MAX <= 227 * 1024, "conv_tc: shared memory over the per-CTA limit");
   static bool attr_t = false, attr_f = false;  // immutable per-instantiation attribute cache
   bool& attr = tbl ? attr_t : attr_f;
@@ -317,7 +317,8 @@ static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
                VP_EINTERNAL, "conv_tc: cannot reserve shared memory");
     attr = true;
   }
-  const int64_t tiles = ceil_div(p0.cap_out, 128);
+  const int64_t tiles = ceil_div(p0.cap_out, 128 * TT);
+  if (TT > 1) part = nullptr;  // multi-tile items are only used where no split-K is needed
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * kMaxSplit, (int64_t)kNumSMs * CPS));
   FwdParams p = p0;
   p.part = (float*)part;
@@ -359,8 +360,19 @@ static int try_cfg(const FwdParams& p, void* part, cudaStream_t st) {
   return -1;
 }
 
+// rows at which a 256-row work item (two tiles sharing each weight stage)
+// replaces the 128-row one for C_out >= 128: enough 256-row items to fill
+// the machine without split-K (VP_CONV_TT2_ROWS overrides; 0 disables)
+static int64_t tt2_rows() {
+  static const int64_t v = getenv("VP_CONV_TT2_ROWS") ? atoll(getenv("VP_CONV_TT2_ROWS")) : 0;  // off by default: at 1M rows it helps strided dgrad (-9%) but slows C=256 fwd (+14%)
+  return v;
+}
+
 template <int KD, int ND, bool BMN>
 static int launch_conv_tc_cfg(const FwdParams& p, void* part, cudaStream_t st) {
+  if constexpr (ND >= 128 && FwdTC<KD, ND, BMN, 1, 1, 2>::FITS) {
+    if (tt2_rows() > 0 && p.cap_out >= tt2_rows()) return launch_conv_tc<KD, ND, BMN, 1, 1, 2>(p, part, st);
+  }
   int r = -1;
   switch (conv_cfg(ND)) {
     case 0: r = try_cfg<KD, ND, BMN, 0>(p, part, st); break;

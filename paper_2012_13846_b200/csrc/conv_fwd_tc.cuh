@@ -58,35 +58,41 @@ __device__ long long* g_conv_trace = nullptr;
     if (trc != nullptr && (on)) trc[idx] = clock64(); \
   } while (0)
 
-constexpr int tmem_cols_pow2(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+constexpr int tmem_cols_pow2(int c) {
+  return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : c <= 512 ? 512 : 1024;  // 1024: does not fit
+}
 
 // A stage holds RB "atoms": one unit each (a 128-row x 64-element bf16 A
 // slab, 128 B swizzled rows, plus the matching [ND x 64] weight slab).  Big
 // stages amortise the per-stage cost (barrier round trip, row lookups) that
 // bounds small-row gathers (tools/gather_probe2: ~2x per 16 KB at RB=2).
-template <int KD, int ND, bool BMN, int CPS, int RB>
+// TT = 128-row tiles per work item sharing each weight (B) stage: the B
+// slab is fetched once and feeds TT MMAs into TT TMEM accumulators, so at
+// large N (no split-K needed) the L2->SMEM traffic of the weights, 1/2 to
+// 2/3 of all staged bytes at C >= 128, is divided by TT.
+template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1>
 struct FwdTC {
   static constexpr bool PAIR = (KD == 32);
   static constexpr int NCH = PAIR ? 1 : KD / 64;
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int NPAD = (BMN && ND < 64) ? 64 : ND;
   static constexpr int B_BYTES = NPAD * 128;
-  static constexpr int STAGE = RB * (A_BYTES + B_BYTES);
+  static constexpr int STAGE = RB * (TT * A_BYTES + B_BYTES);
   static constexpr int BOOK = 4096;
   // two [128, K <= kTblK] neighbour-table tiles (double buffer)
-  static constexpr int TBL_RESERVE = 2 * 128 * kTblK * 4;
+  static constexpr int TBL_RESERVE = 2 * TT * 128 * kTblK * 4;
   // 228 KB of shared memory per SM, 1 KB reserved per CTA, 1 KB alignment slack
   static constexpr int BUDGET = (228 * 1024) / CPS - 2048 - BOOK - TBL_RESERVE;
   static constexpr int STAGES_RAW = BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
-  static constexpr bool FITS = STAGES_RAW >= 2 && tmem_cols_pow2(ND) * CPS <= 512;
-  static constexpr int ACC = (tmem_cols_pow2(2 * ND) * CPS <= 512) ? 2 : 1;
-  static constexpr int COLS = ACC * ND;
+  static constexpr bool FITS = STAGES_RAW >= 2 && tmem_cols_pow2(TT * ND) * CPS <= 512;
+  static constexpr int ACC = (tmem_cols_pow2(2 * TT * ND) * CPS <= 512) ? 2 : 1;
+  static constexpr int COLS = ACC * TT * ND;
   static constexpr int TMEM_COLS = tmem_cols_pow2(COLS);
   static constexpr uint32_t IDESC = tc::idesc_bf16(128, ND, 0, BMN ? 1 : 0);
   static constexpr int SMEM_BASE = STAGES * STAGE + 1024 + BOOK;
-  static constexpr int SMEM_MAX = SMEM_BASE + 2 * 128 * kTblK * 4;
-  static int smem_bytes(int K, bool tbl) { return SMEM_BASE + (tbl ? 2 * 128 * K * 4 : 0); }
+  static constexpr int SMEM_MAX = SMEM_BASE + 2 * TT * 128 * kTblK * 4;
+  static int smem_bytes(int K, bool tbl) { return SMEM_BASE + (tbl ? 2 * TT * 128 * K * 4 : 0); }
 };
 
 __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) {
@@ -95,10 +101,11 @@ __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) 
   return s > max_split ? max_split : s;
 }
 
-template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL>
+template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL, int TT = 1>
 __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_constant__ FwdParams p) {
   ::vp::pdl_begin();
-  using C = FwdTC<KD, ND, BMN, CPS, RB>;
+  using C = FwdTC<KD, ND, BMN, CPS, RB, TT>;
+  constexpr int TR = 128 * TT;  // rows per work item
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* book = smem + C::STAGES * C::STAGE;
@@ -114,13 +121,13 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   int* s_work = s_info + 4;                                  // u0, n_units, n_act (producers)
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(book + 640);
   int16_t* s_act = reinterpret_cast<int16_t*>(book + 1024);  // <= 343 entries
-  int32_t* s_tbl = reinterpret_cast<int32_t*>(book + C::BOOK);  // [2][128 * K] when K <= kTblK
+  int32_t* s_tbl = reinterpret_cast<int32_t*>(book + C::BOOK);  // [2][TR * K] when K <= kTblK
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
   long long* const trc = blockIdx.x == 0 ? g_conv_trace : nullptr;
   const int n_out = load_count(p.n_out_dev, p.cap_out);
-  const int ntiles = (n_out + 127) / 128;
+  const int ntiles = (n_out + TR - 1) / TR;
   // split partials are sized for kNumSMs work items
   const int S = split_count(ntiles, min((int)gridDim.x, kNumSMs), p.max_split);
   const int total = ntiles * S;
@@ -157,9 +164,9 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
     // hand before the arrive (its release orders them)
     auto issue_tbl = [&](int w, int buf) {
       const int tile = w / S;
-      const int nel = min(128, n_out - tile * 128) * K;
-      const int32_t* src = p.table + (int64_t)tile * 128 * K;
-      int32_t* dst = s_tbl + buf * 128 * K;
+      const int nel = min(TR, n_out - tile * TR) * K;
+      const int32_t* src = p.table + (int64_t)tile * TR * K;
+      int32_t* dst = s_tbl + buf * TR * K;
       const int pre = nel & ~3;
       for (int e = pre; e < nel; ++e) dst[e] = __ldg(src + e);
       tc::fence_proxy_async_smem();
@@ -172,32 +179,39 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++ii) {
       trace_ev(1024 + 4 * (ii & 63), tid == 0);
       const int tile = w / S, split = w - (w / S) * S;
-      const int rows = min(128, n_out - tile * 128);
-      const int32_t* tt = s_tbl + (ii & 1) * 128 * K;  // this tile's staged table
+      const int rows = min(TR, n_out - tile * TR);
+      const int32_t* tt = s_tbl + (ii & 1) * TR * K;  // this item's staged table
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tid < kTcMaskWords) s_mask[tid] = 0;
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tbl) {
         tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);
-        if (rows < 128) {  // ragged last tile: rows past the end read as misses
-          int32_t* tw = s_tbl + (ii & 1) * 128 * K;
-          for (int e = rows * K + tid; e < 128 * K; e += kTcProd) tw[e] = -1;
+        if (rows < TR) {  // ragged last tile: rows past the end read as misses
+          int32_t* tw = s_tbl + (ii & 1) * TR * K;
+          for (int e = rows * K + tid; e < TR * K; e += kTcProd) tw[e] = -1;
         }
         uint32_t bits = 0;
-        if (tid < rows)
-          for (int k = 0; k < K; ++k)
-            if (tt[tid * K + k] >= 0) bits |= 1u << (p.flip ? K - 1 - k : k);
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          const int r = tid + 128 * t;
+          if (r < rows)
+            for (int k = 0; k < K; ++k)
+              if (tt[r * K + k] >= 0) bits |= 1u << (p.flip ? K - 1 - k : k);
+        }
         bits = __reduce_or_sync(0xffffffffu, bits);
         if (lane == 0 && bits) atomicOr(&s_mask[0], bits);
       } else {
-        const int32_t* trow = p.table + ((int64_t)tile * 128 + tid) * K;
         for (int kb = 0; kb < K; kb += 32) {
           uint32_t bits = 0;
           const int kend = min(32, K - kb);
-          for (int j = 0; j < kend; ++j) {
-            const int k = kb + j;
-            const int v = tid < rows ? __ldg(trow + (p.flip ? K - 1 - k : k)) : -1;
-            if (v >= 0) bits |= 1u << j;
+          for (int t = 0; t < TT; ++t) {
+            const int r = tid + 128 * t;
+            const int32_t* trow = p.table + ((int64_t)tile * TR + r) * K;
+            for (int j = 0; j < kend; ++j) {
+              const int k = kb + j;
+              const int v = r < rows ? __ldg(trow + (p.flip ? K - 1 - k : k)) : -1;
+              if (v >= 0) bits |= 1u << j;
+            }
           }
           bits = __reduce_or_sync(0xffffffffu, bits);
           if (lane == 0 && bits) atomicOr(&s_mask[kb >> 5], bits);
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       const uint32_t a_off0 = r0 * 128 + ((q ^ (lane >> 3)) << 4);
       const uint32_t a_off1 = r0 * 128 + ((q ^ ((lane >> 3) + 4)) << 4);
       const uint32_t tt_s = tc::smem_u32(tt) + r0 * K * 4;  // row r0's staged table entries
-      const int32_t* trow0 = p.table + ((int64_t)tile * 128 + r0) * K;
+      const int32_t* trow0 = p.table + ((int64_t)tile * TR + r0) * K;
       const char* xb = reinterpret_cast<const char*>(p.x);
       const int nst = (neff + RB - 1) / RB;  // stages of this work item
       for (int sj = 0; sj < nst; ++sj, ++g) {
@@ -264,12 +278,14 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
         const int na_st = min(RB, neff - sj * RB);  // atoms in use (the MMA skips the rest)
 #pragma unroll 1
         for (int at = 0; at < na_st; ++at) {
-          const uint32_t a_s = s_base + at * C::A_BYTES;
-          const uint32_t b_s = s_base + RB * C::A_BYTES + at * C::B_BYTES;
+          const uint32_t a_s0 = s_base + at * TT * C::A_BYTES;
+          const uint32_t b_s = s_base + RB * TT * C::A_BYTES + at * C::B_BYTES;
           const int unit = u0 + sj * RB + at;
           int ka, kb, cs;
           unit_k(unit, ka, kb, cs);
-          {
+#pragma unroll
+          for (int t = 0; t < TT; ++t) {
+            const uint32_t a_s = a_s0 + t * C::A_BYTES;
             const int kq = C::PAIR ? (q < 4 ? ka : kb) : ka;
             const int col = p.flip ? K - 1 - kq : kq;
             const char* xq = xb + 2 * (C::PAIR ? (q & 3) * 8 : cs * 64 + q * 8);
@@ -278,8 +294,8 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               if (kq < 0 || noa) vr[i] = -1;
-              else if (TBL) vr[i] = tc::lds_s32(tt_s + (uint32_t)(i * 16 * K + col * 4));
-              else vr[i] = (r0 + 4 * i < rows) ? __ldg(trow0 + i * 4 * K + col) : -1;
+              else if (TBL) vr[i] = tc::lds_s32(tt_s + (uint32_t)((t * 128 * K + i * 4 * K + col) * 4));
+              else vr[i] = (t * 128 + r0 + 4 * i < rows) ? __ldg(trow0 + (t * 128 + i * 4) * K + col) : -1;
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -335,12 +351,14 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       trace_ev(1024 + 4 * (ii & 63) + 2, ep == 0 && lane == 0);
       tc::tc_fence_after();
       const int lrow = ep * 32 + lane;
-      const int64_t row = (int64_t)tile * 128 + lrow;
+#pragma unroll 1
+      for (int t = 0; t < TT; ++t) {
+      const int64_t row = (int64_t)tile * TR + t * 128 + lrow;
       const int64_t orow = (p.perm != nullptr && row < n_out) ? (int64_t)__ldg(p.perm + row) : row;
 #pragma unroll 1
       for (int c0 = 0; c0 < ND; c0 += 32) {
         float v[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(ep * 32) << 16) + a * ND + c0, v);
+        tc::tmem_ld32(tmem + ((uint32_t)(ep * 32) << 16) + (a * TT + t) * ND + c0, v);
         if (row < n_out) {
           if (S > 1) {
             float4* dst = reinterpret_cast<float4*>(p.part + (((int64_t)split * ntiles + tile) * 128 + lrow) * ND + c0);
@@ -368,6 +386,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
           }
         }
       }
+      }  // t
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[a]);
       trace_ev(1024 + 4 * (ii & 63) + 3, ep == 0 && lane == 0);
@@ -385,7 +404,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       const int use = ii / C::ACC;
       if (use >= 1) tc::mbar_wait(&tempty[a], (use - 1) & 1);
       tc::tc_fence_after();
-      const uint32_t d = tmem + a * ND;
+      const uint32_t d = tmem + a * TT * ND;
       const int nst = (neff + RB - 1) / RB;
       for (int sj = 0; sj < nst; ++sj, ++g) {
         const int stage = g % C::STAGES;
@@ -394,14 +413,17 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
         const uint32_t s_base = sbase + stage * C::STAGE;
         const int na_st = (p.dbg & 1) ? 0 : min(RB, neff - sj * RB);
         for (int at = 0; at < na_st; ++at) {
-          const uint32_t a_s = s_base + at * C::A_BYTES;
-          const uint32_t b_s = s_base + RB * C::A_BYTES + at * C::B_BYTES;
+          const uint32_t a_s = s_base + at * TT * C::A_BYTES;
+          const uint32_t b_s = s_base + RB * TT * C::A_BYTES + at * C::B_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = tc::smem_desc(a_s + kk * 32, 16, 1024, tc::kSwizzle128);
             const uint64_t bd = BMN ? tc::smem_desc(b_s + kk * 2048, 8192, 1024, tc::kSwizzle128)
                                     : tc::smem_desc(b_s + kk * 32, 16, 1024, tc::kSwizzle128);
-            tc::mma_bf16(d, ad, bd, C::IDESC, (sj > 0 || at > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+            for (int t = 0; t < TT; ++t) {
+              const uint64_t ad = tc::smem_desc(a_s + t * C::A_BYTES + kk * 32, 16, 1024, tc::kSwizzle128);
+              tc::mma_bf16(d + t * ND, ad, bd, C::IDESC, (sj > 0 || at > 0 || kk > 0) ? 1u : 0u);
+            }
           }
         }
         if (p.dbg & 8) tc::mbar_arrive(&empty[stage]);

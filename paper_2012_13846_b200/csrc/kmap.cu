@@ -231,7 +231,7 @@ map_probe_grid_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, in
     if (on) base = grid_linear(g, r.x, cx, cy, cz);
   }
   const unsigned R = (unsigned)g.R;
-  constexpr int KB = 9;
+  constexpr int KB = 27;  // a whole 3^3 kernel's loads in flight at once (larger K loops)
   for (int kb = 0; kb < K; kb += KB) {
     int v[KB];
 #pragma unroll
@@ -254,12 +254,10 @@ map_probe_grid_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, in
     }
   }
   __syncthreads();
-  if (staged) {
+  if (staged) {  // warp per row: K <= 32 contiguous ints, no division
     int32_t* dst = nbr + u0 * K;
-    for (int e = tid; e < rows * K; e += kMapTile) {
-      const int rr = e / K, k = e - rr * K;
-      dst[e] = s_nbr[rr * (kMapSmemK + 1) + k];
-    }
+    for (int rr = warp; rr < rows; rr += kMapTile / 32)
+      if (lane < K) dst[rr * K + lane] = s_nbr[rr * (kMapSmemK + 1) + lane];
   }
   for (int k = tid; k < K; k += kMapTile) {
     int c = 0;

@@ -213,3 +213,45 @@ def test_mask_sorted_rows_bitwise_equal(c, stride):
     torch.testing.assert_close(d1.float(), d0.float(), rtol=1e-2, atol=1e-2)
     # deterministic: the same sorted launch twice is bitwise identical
     assert torch.equal(d1, conv.conv_dgrad_raw(gy, W, its, n, flip, perm=ip))
+
+
+@pytest.mark.parametrize("c", [128, 256])
+@pytest.mark.parametrize("sort", [False, True])
+def test_large_n_two_tile_items_vs_torch(c, sort):
+    """N >= 2^17 rows selects the 256-row work items (two tiles share every
+    weight stage): forward and dgrad against a torch fp32 gather-matmul of
+    the same bf16 operands (|d| <= 1e-2 * sum|W||x| style bound)."""
+    from paper_2012_13846_b200 import conv
+    from paper_2012_13846_b200.tensor import SparseTensor
+    pts, offs = O.synthetic_batch(80, 2048, 64, seed=5, dtype=np.float32)
+    c0, _ = O.voxelize_batch(pts.astype(np.float64), offs, 1.0, 64)
+    assert len(c0) >= (1 << 17)
+    t = SparseTensor(c0, np.zeros((len(c0), 1)), (1, 1, 1))
+    shape = conv.KernelShape.hypercubic(3, 3)
+    km = conv._kernel_map4(t.coords4, t.coords4, shape, (1, 1, 1), 3, with_pairs=False)
+    n = len(t)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(n, c, device="cuda", generator=g).to(torch.bfloat16)
+    W = conv.ConvWeights(torch.randn(27, c, c, device="cuda", generator=g) / (27 * c) ** 0.5)
+    perm, tbl = conv.sort_table(km.nbr, n) if sort else (None, km.nbr)
+    y = conv.conv_forward_raw(x, W, tbl, n, perm=perm).float()
+    xf = torch.cat([x.float(), torch.zeros(1, c, device="cuda")])
+    wf = W.bf16.float()
+    idx = km.nbr.long().clone()
+    idx[idx < 0] = n
+    ref = torch.zeros(n, c, device="cuda")
+    mag = torch.zeros(n, c, device="cuda")
+    for k in range(27):
+        ref += xf[idx[:, k]] @ wf[k].T
+        mag += xf[idx[:, k]].abs() @ wf[k].abs().T
+    assert bool(((y - ref).abs() <= 1e-2 * mag + 1e-3).all())
+    # dgrad (stride 1: the flipped neighbour table)
+    gy = torch.randn(n, c, device="cuda", generator=g).to(torch.bfloat16)
+    gi = conv.conv_dgrad_raw(gy, W, tbl, n, True, perm=perm).float()
+    gf = torch.cat([gy.float(), torch.zeros(1, c, device="cuda")])
+    ref = torch.zeros(n, c, device="cuda")
+    mag = torch.zeros(n, c, device="cuda")
+    for k in range(27):
+        ref += gf[idx[:, 26 - k]] @ wf[k]
+        mag += gf[idx[:, 26 - k]].abs() @ wf[k].abs()
+    assert bool(((gi - ref).abs() <= 1e-2 * mag + 1e-3).all())
