@@ -36,6 +36,17 @@ import time
 
 import numpy as np
 
+# rank 0's stdout carries exactly one JSON line: everything else written to
+# fd 1 (NCCL's version banner, library prints) is sent to stderr, and the
+# JSON line goes to a private duplicate of the original stdout
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -77,6 +88,8 @@ def parse():
                     help="N>1: 'dp' (every GPU a replica, gradient all_reduce), 'auto' (SparsePipe partitioner "
                          "on per-unit GPU profiles -> pipeline stages), or unit cuts like '3' / '1,4,6'")
     ap.add_argument("--p2p-gbs", type=float, default=770.0, help="NVLink P2P GB/s per direction for the planner")
+    ap.add_argument("--dp-allreduce", action="store_true",
+                    help="run the data-parallel gradient all_reduce even at one GPU (tests its graph capture)")
     return ap.parse_args()
 
 
@@ -189,7 +202,7 @@ def run_reference(args, rank):
                              "sample": f"each step {args.cpu_sample} clouds of the C3 workload (bounded sample)"},
             "e2e": {"value": round(value, 3), "unit": "clouds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": round(time.time() - t0, 1)}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -215,10 +228,15 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     allreduce = None
-    if world > 1:
-        def allreduce(flat):  # one NCCL all_reduce of the flat fp32 gradient buffer per step
+    if world > 1 or args.dp_allreduce:
+        if not dist.is_initialized():  # --dp-allreduce at world 1 (capture test of the collective)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+
+        def allreduce(flat):  # one NCCL all_reduce of the flat fp32 gradient buffer per step (graph-captured)
             dist.all_reduce(flat)
-            flat.div_(world)
+            flat.div_(dist.get_world_size())
 
     if world > 1 and args.plan != "dp":
         return run_pipeline(args, rank, world, local, dev)
@@ -238,7 +256,7 @@ def main():
         dev_lab.append(hl.to(dev))
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    use_graph = not args.no_graph and world == 1
+    use_graph = not args.no_graph
     if use_graph:
         # the next batch's coordinates and kernel maps are built while the
         # current batch runs its backward (model.enable_prefetch)
@@ -335,8 +353,8 @@ def main():
                 "gpu_launches": int(kern_per_step * args.steps),
                 "gpu_launches_per_step": int(kern_per_step),
                 "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(), "final_loss": round(loss, 5)}
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        emit(line)
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -421,7 +439,7 @@ def run_pipeline(args, rank, world, local, dev):
                     micro_batch_clouds=args.batch, micro_batches_per_step=world, cuda_graph=not args.no_graph,
                     l2="not flushed: one continuous 1F1B stream (fill + drain inside the timed region)"),
                 "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None}
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.barrier()
     dist.destroy_process_group()
 
