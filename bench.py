@@ -88,6 +88,9 @@ def parse():
                     help="N>1: 'dp' (every GPU a replica, gradient all_reduce), 'auto' (SparsePipe partitioner "
                          "on per-unit GPU profiles -> pipeline stages), or unit cuts like '3' / '1,4,6'")
     ap.add_argument("--p2p-gbs", type=float, default=770.0, help="NVLink P2P GB/s per direction for the planner")
+    ap.add_argument("--pipeline-test", action="store_true",
+                    help="functional test of the multi-process pipeline on ONE GPU: every rank on cuda:0, gloo "
+                         "transport through host memory (not a performance number)")
     ap.add_argument("--dp-allreduce", action="store_true",
                     help="run the data-parallel gradient all_reduce even at one GPU (tests its graph capture)")
     return ap.parse_args()
@@ -222,10 +225,15 @@ def main():
     import voxpipe_oracle as O
     from paper_2012_13846_b200 import _lib, model
 
+    if args.pipeline_test:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.pipeline_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     allreduce = None
     if world > 1 or args.dp_allreduce:
@@ -395,7 +403,7 @@ def run_pipeline(args, rank, world, local, dev):
         split = "-".join("1" for _ in topo.stages)
     del probe
     topo.validate(n_units)
-    tr = PL.DistTransport(dist, topo)  # collective: every rank builds the replica groups
+    tr = PL.DistTransport(dist, topo, host_stage=args.pipeline_test)  # collective: builds the replica groups
     active = topo.locate(rank) is not None  # the plan may leave a GPU idle
     pool = []
     for i in range(4):
@@ -426,7 +434,7 @@ def run_pipeline(args, rank, world, local, dev):
     e1.record(st)
     torch.cuda.synchronize()
     dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cpu" if args.pipeline_test else dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     value = args.steps * world * args.batch / (ms / 1e3)

@@ -464,7 +464,6 @@ class SparseResNetTrainer:
                 build(i, maps, main, True, True, False)
                 continue
             side = self.int_side[1 + (i % 2)]
-            self._forked.add(id(side))
             if first_map in maps:
                 # the first layer's map on the critical path; the level's other
                 # map (and the index clear) on a side stream after it
@@ -474,11 +473,14 @@ class SparseResNetTrainer:
                 if rest:
                     ev0 = torch.cuda.Event()
                     ev0.record(main)
+                    self._forked.add(id(side))  # joined (so joinable) only when it takes work
                     side.wait_event(ev0)
                     needs(side, i, rest)
                     with torch.cuda.stream(side):
                         build(i, rest, side, False, True, True)
             else:
+                self._forked.add(id(side))
+                side.wait_stream(main)  # fork from the origin (a no-op dependency when i > entry)
                 needs(side, i, maps)
                 with torch.cuda.stream(side):
                     build(i, maps, side, True, True, True)

@@ -216,11 +216,14 @@ class DistTransport:
     CPU tests).  One action's communications are one batch_isend_irecv
     (ncclGroupStart/End), enqueued on NCCL's stream before the compute."""
 
-    def __init__(self, dist, topo: Optional["Topology"] = None):
+    def __init__(self, dist, topo: Optional["Topology"] = None, host_stage: bool = False):
         """Creating a process group is collective over the whole world, so
         every rank builds every replica group of `topo` up front, in the
-        same order."""
+        same order.  host_stage: move device tensors through host memory
+        (gloo with several ranks on one GPU — a functional test of the
+        runtime where NCCL cannot run two ranks per device)."""
         self.dist = dist
+        self.host_stage = host_stage
         self._groups = {}
         if topo is not None:
             for st in topo.stages:
@@ -231,12 +234,21 @@ class DistTransport:
         if not comms:
             return
         d = self.dist
-        ops = []
+        ops, back = [], []
         for c in comms:
-            fn = d.isend if c.kind.startswith("send") else d.irecv
-            ops += [d.P2POp(fn, t, c.peer) for t in boundary_tensors(runner.engine_of(c.mb), c.kind)]
+            send = c.kind.startswith("send")
+            fn = d.isend if send else d.irecv
+            for t in boundary_tensors(runner.engine_of(c.mb), c.kind):
+                if self.host_stage and t.is_cuda:
+                    h = t.cpu() if send else torch_empty_like_host(t)
+                    if not send:
+                        back.append((t, h))
+                    t = h
+                ops.append(d.P2POp(fn, t, c.peer))
         for w in d.batch_isend_irecv(ops):
             w.wait()
+        for t, h in back:
+            t.copy_(h)
 
     def group(self, ranks: tuple):
         if len(ranks) <= 1:
@@ -248,8 +260,19 @@ class DistTransport:
     def allreduce_mean(self, t, group) -> None:
         if group is None:
             return
+        if self.host_stage and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=group)
+            t.copy_(h.div_(self.dist.get_world_size(group)))
+            return
         self.dist.all_reduce(t, group=group)
         t.div_(self.dist.get_world_size(group))
+
+
+def torch_empty_like_host(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype, device="cpu")
 
 
 class LocalTransport:

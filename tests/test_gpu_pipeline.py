@@ -119,3 +119,28 @@ def test_pipeline_bf16_graphs_and_replicas():
     pl2 = PL.LocalPipeline(topo2, M, factory(torch.bfloat16), batch_of_factory())
     pl2.run()
     assert torch.equal(pl2.runners[0].master_p, pl2.runners[1].master_p)
+
+
+@pytest.mark.parametrize("n,plan", [(2, "4"), (3, "2,5")])
+def test_multiprocess_pipeline_bench_on_one_gpu(n, plan):
+    """The multi-process SparsePipe runtime end to end (torchrun, one process
+    per stage, StageRunner + DistTransport, bench.py's run_pipeline) with
+    every rank on cuda:0 and gloo moving the stage tensors through host
+    memory — NCCL cannot host two ranks on one device, so this is the
+    functional check of the multi-GPU path available on one B200."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", f"--nproc-per-node={n}",
+           os.path.join(root, "bench.py"), "--gpus", str(n), "--plan", plan, "--pipeline-test", "--steps", "2",
+           "--warmup", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == n and d["value"] > 0
+    assert len(d["config"]["stages"]) == n
