@@ -134,7 +134,7 @@ def test_multiprocess_pipeline_bench_on_one_gpu(n, plan):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", f"--nproc-per-node={n}",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--local-addr", "127.0.0.1", f"--nproc-per-node={n}",
            os.path.join(root, "bench.py"), "--gpus", str(n), "--plan", plan, "--pipeline-test", "--steps", "2",
            "--warmup", "1"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
