@@ -14,7 +14,10 @@
  *     capacities (`cap_*`, host) size grids and buffers;
  *   - no global mutable state: scratch comes from the caller (`ws`, sized by
  *     the matching *_ws_bytes query), so calls are re-entrant across
- *     streams and threads;
+ *     streams and threads (one workspace per concurrent call).  Workspaces
+ *     must be ZERO-FILLED before their first use: the fused BN statistics
+ *     keep a self-re-arming ticket counter in theirs, and every call leaves
+ *     it at zero again;
  *   - status codes mirror voxpipe/errors.py:3-5 exit codes:
  *       VP_OK = 0, VP_EVALIDATION = 2 (ValidationError/StructuralError),
  *       VP_EINTERNAL = 3 (InternalError, e.g. a CUDA launch failure).

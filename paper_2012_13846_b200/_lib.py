@@ -145,6 +145,9 @@ def dtype_code(t) -> int:
 
 
 def workspace(nbytes: int, device):
+    """Caller-owned scratch for a C-ABI call.  Zero-filled: the fused BN
+    statistics keep a self-re-arming ticket in their workspace, which must
+    start at zero (include/voxpipe_b200.h)."""
     import torch
 
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
