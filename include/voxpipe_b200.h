@@ -203,6 +203,15 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t c_in, const void* g, i
 size_t vp_bn_stats_ws_bytes(int64_t cap_n, int64_t C);
 int vp_bn_stats(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C,
                 float eps, float* mean, float* rstd, void* ws, size_t ws_bytes, vp_stream_t stream);
+/* vp_bn_stats + vp_bn_apply in ONE cooperative launch: the blocks reduce
+ * their partial sums, the last one writes mean/rstd, and every block then
+ * normalises its rows when VP_BN_FUSED=1; by default (faster inside the
+ * concurrent training step) it issues the two launches.
+ * ws: vp_bn_stats_ws_bytes, zero-filled before first use. */
+int vp_bn_forward(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C, float eps,
+                  float* mean, float* rstd, const float* gamma, const float* beta, const void* res,
+                  int32_t res_dtype, int32_t relu, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
+                  vp_stream_t stream);
 /* y = act((x - mean) * rstd * gamma + beta [+ res]) ; act = relu if relu */
 int vp_bn_apply(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C,
                 const float* mean, const float* rstd, const float* gamma, const float* beta,

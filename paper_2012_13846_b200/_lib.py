@@ -63,6 +63,7 @@ SIGNATURES = {
     "vp_bn_stats_ws_bytes": (SZ, [I64, I64]),
     "vp_bn_stats": (C.c_int, [P, I32, P, I64, I64, F32, P, P, P, SZ, P]),
     "vp_bn_apply": (C.c_int, [P, I32, P, I64, I64, P, P, P, P, P, I32, I32, P, I32, P]),
+    "vp_bn_forward": (C.c_int, [P, I32, P, I64, I64, F32, P, P, P, P, P, I32, I32, P, I32, P, SZ, P]),
     "vp_bn_backward_ws_bytes": (SZ, [I64, I64]),
     "vp_bn_backward": (C.c_int, [P, P, I32, P, I32, P, I32, P, I64, I64, P, P, P, I32, P, I32, P, P, P, P, SZ, P]),
     "vp_global_pool_ws_bytes": (SZ, [I32]),

@@ -498,11 +498,10 @@ class SparseResNetTrainer:
                 self.K, self.fwd_table(L).data_ptr(), 0, _lib.ptr(self.fwd_perm(L)), dst.n.data_ptr(), dst.cap,
                 L["y"].data_ptr(), fc,
                 L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
-        self._c("vp_bn_stats", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
-                L["mean"].data_ptr(), L["rstd"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
-        self._c("vp_bn_apply", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"],
+        # batch statistics + normalise (+ residual) (+ ReLU): one cooperative launch
+        self._c("vp_bn_forward", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
                 L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(), L["beta"].data_ptr(),
-                _lib.ptr(res), fc, int(relu), L["a"].data_ptr(), fc, st)
+                _lib.ptr(res), fc, int(relu), L["a"].data_ptr(), fc, L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
         L["x"] = x
         return L["a"]
 
