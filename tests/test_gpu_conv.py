@@ -255,3 +255,67 @@ def test_large_n_two_tile_items_vs_torch(c, sort):
         ref += gf[idx[:, 26 - k]] @ wf[k]
         mag += gf[idx[:, 26 - k]].abs() @ wf[k].abs()
     assert bool(((gi - ref).abs() <= 1e-2 * mag + 1e-3).all())
+
+
+SHAPES = {
+    "3d_1": (3, 1, None),                 # 1^3 projection (K = 1)
+    "3d_5": (3, 5, None),                 # 5^3 (K = 125 > 30: no mask sort, unstaged table)
+    "3d_313": (3, (3, 1, 3), None),       # anisotropic extents (K = 9)
+    "2d_3": (2, 3, None),                 # 2-D 3x3 (K = 9)
+    "1d_5": (1, 5, None),                 # 1-D (K = 5)
+    "custom": (3, None, [[0, 0, 0], [1, 0, 0], [0, -1, 0], [0, 0, 2]]),
+}
+
+
+@pytest.mark.parametrize("name", list(SHAPES))
+@pytest.mark.parametrize("stride", [1, 2])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_kernel_shapes_dims_and_strides(name, stride, dtype):
+    """The operator API beyond the 3^3 / 3-D models: 1-D / 2-D tensors,
+    1^3 / 5^3 / anisotropic / custom offset sets, strides 1 and 2 — output
+    coordinates and kernel maps bit-exact with the reference restatement,
+    forward / dgrad / wgrad within the §8(d) tolerance model."""
+    from paper_2012_13846_b200 import conv
+    from paper_2012_13846_b200.tensor import SparseTensor
+    dim, size, custom = SHAPES[name]
+    rng = np.random.default_rng(sum(map(ord, name)) + stride)  # stable across processes
+    n = 700
+    c = np.concatenate([rng.integers(0, 3, (n, 1)), rng.integers(-12, 12, (n, dim))], 1)
+    c = c[np.sort(np.unique(c, axis=0, return_index=True)[1])]  # unique rows, first-seen order
+    shape = conv.KernelShape.custom(dim, custom) if custom else conv.KernelShape.hypercubic(dim, size)
+    off = shape.offsets
+    cin, cout = 32, 64
+    x = rng.normal(size=(len(c), cin)).astype(np.float32)
+    w = (rng.normal(size=(len(off), cout, cin)) / np.sqrt(len(off) * cin)).astype(np.float32)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    rel = 1e-2 if dtype == "bf16" else 1e-5
+    xr = bf16_round(x) if dtype == "bf16" else x.astype(np.float64)
+    wr = bf16_round(w) if dtype == "bf16" else w.astype(np.float64)
+    t = SparseTensor(c, np.zeros((len(c), 1)), (1,) * dim).with_features(torch.from_numpy(x).cuda().to(tdt))
+    W = conv.ConvWeights(torch.from_numpy(w).cuda())
+    st = (stride,) * dim
+    # integer stage: bit-exact
+    oc, _ = conv.generate_output_coords(t, st)
+    roc, _ = O.generate_output_coords(c, (1,) * dim, st)
+    np.testing.assert_array_equal(oc.cpu().numpy(), roc)
+    km = conv.build_kernel_map(t.coords, oc, shape, (1,) * dim)
+    ref = O.build_kernel_map(c, roc, off, (1,) * dim)
+    for (a, b), (ea, eb) in zip(km.pairs, ref):
+        np.testing.assert_array_equal(a.cpu().numpy(), ea)
+        np.testing.assert_array_equal(b.cpu().numpy(), eb)
+    # float stage
+    y = conv.sparse_conv_forward(t, W, shape, st)
+    _, ry, _ = O.sparse_conv_forward(c, xr, (1,) * dim, wr, off, st)
+    _, mag, _ = O.sparse_conv_forward(c, np.abs(xr), (1,) * dim, np.abs(wr), off, st)
+    assert (np.abs(y.features.float().cpu().numpy() - ry) <= rel * mag + 1e-6).all()
+    gy = rng.normal(size=ry.shape).astype(np.float32)
+    gr = bf16_round(gy) if dtype == "bf16" else gy.astype(np.float64)
+    gi, gw = conv.sparse_conv_backward(t, W, shape, st, torch.from_numpy(gy).cuda().to(tdt))
+    rgi, rgw = O.sparse_conv_backward(c, xr, (1,) * dim, wr, off, st, gr)
+    bgi = np.zeros_like(rgi)
+    bgw = np.zeros_like(rgw)
+    for k, (vi, ui) in enumerate(ref):
+        bgi[vi] += np.abs(gr[ui]) @ np.abs(wr[k])
+        bgw[k] = np.abs(gr[ui]).T @ np.abs(xr[vi])
+    assert (np.abs(gi.float().cpu().numpy() - rgi) <= rel * bgi + 1e-6).all()
+    assert (np.abs(gw.cpu().numpy() - rgw) <= 1e-5 * bgw + 1e-6).all()
