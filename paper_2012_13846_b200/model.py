@@ -254,7 +254,8 @@ class SparseResNetTrainer:
     # (vp_kernel_map_sort): at C5-scale levels the sort pays for itself many
     # times over; at C3 (<= 131k rows, diverse masks) its launches cost more
     # than the 1.3-1.7x fewer active offsets per tile save (tools/sweep_c2.py)
-    SORT_MIN_ROWS = 1 << 18
+    SORT_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_MIN_ROWS", 1 << 18))
+    SORT_INV_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_INV_MIN_ROWS", 0))
 
     def _alloc_map(self, src: Level, dst: Level, strided: bool, sort: bool = True) -> Map:
         dev, K = self.device, self.K
@@ -268,14 +269,19 @@ class SparseResNetTrainer:
             src=src, dst=dst,
             ws=_lib.workspace(max(_lib.query("vp_kernel_map_ws_bytes", src.cap, dst.cap, K),
                                   _lib.query("vp_kernel_map_grid_ws_bytes", dst.cap, K)), dev))
+        nws = 0
         if sort and dst.cap >= self.SORT_MIN_ROWS:
             m.perm = torch.zeros(dst.cap, dtype=torch.int32, device=dev)
             m.nbr_s = torch.zeros((dst.cap, K), dtype=torch.int32, device=dev)
             nws = _lib.query("vp_kernel_map_sort_ws_bytes", dst.cap, K)
-            if strided:
-                m.iperm = torch.zeros(src.cap, dtype=torch.int32, device=dev)
-                m.inv_s = torch.zeros((src.cap, K), dtype=torch.int32, device=dev)
-                nws = max(nws, _lib.query("vp_kernel_map_sort_ws_bytes", src.cap, K))
+        if strided and src.cap >= self.SORT_INV_MIN_ROWS:
+            # the inverse table of a strided map is sparse (~2-3 of 27 offsets
+            # per input row): grouped rows cut the strided dgrad 2-2.5x at
+            # every size, and the sort runs in the prefetched integer stage
+            m.iperm = torch.zeros(src.cap, dtype=torch.int32, device=dev)
+            m.inv_s = torch.zeros((src.cap, K), dtype=torch.int32, device=dev)
+            nws = max(nws, _lib.query("vp_kernel_map_sort_ws_bytes", src.cap, K))
+        if nws:
             m.sort_ws = _lib.workspace(nws, dev)
         return m
 
