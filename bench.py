@@ -438,6 +438,13 @@ def run_pipeline(args, rank, world, local, dev):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     value = args.steps * world * args.batch / (ms / 1e3)
+    # PipeDream weight-stashing audit: every (micro-batch,
+    # stage) backward used the weight version its forward used
+    audit = timed.stats.audit if active else []
+    audits = [None] * world
+    dist.all_gather_object(audits, audit)
+    checked = sum(len(a) for a in audits)
+    violations = sum(1 for a in audits for _, _, fv, bv in a if fv != bv)
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "clouds/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
@@ -446,6 +453,7 @@ def run_pipeline(args, rank, world, local, dev):
                     [s.unit_start, s.unit_end, list(s.ranks)] for s in topo.stages],
                     micro_batch_clouds=args.batch, micro_batches_per_step=world, cuda_graph=not args.no_graph,
                     l2="not flushed: one continuous 1F1B stream (fill + drain inside the timed region)"),
+                "weight_version_audit": {"checked": checked, "violations": violations},
                 "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None}
         emit(line)
     dist.barrier()

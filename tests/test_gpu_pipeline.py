@@ -144,3 +144,5 @@ def test_multiprocess_pipeline_bench_on_one_gpu(n, plan):
     d = json.loads(lines[0])
     assert d["n_gpus"] == n and d["value"] > 0
     assert len(d["config"]["stages"]) == n
+    audit = d["weight_version_audit"]
+    assert audit["checked"] == 2 * n * n and audit["violations"] == 0  # steps * world micro-batches x stages
