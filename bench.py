@@ -555,7 +555,8 @@ def roofline(tr, dev, iters=30):
     nm = int(m.src.n.item())
     pm = int(m.ptr[-1].item())
     bm = 16 * nm + 16 * nm + 8 * pm
-    name = "vp_grid_set + vp_kernel_map_grid" if tr.use_grid else "vp_kernel_map"
+    name = {"grid": "vp_grid_set + vp_kernel_map_grid", "brick": "vp_brick_set + vp_kernel_map_brick"}.get(
+        tr.index_kind, "vp_kernel_map")
     out["map"] = {"kernel": f"{name} level0 stride-1 (N={nm}, pairs={pm})", "bound": "hbm",
                   "achieved": round(bm / tm / 1e9, 1), "peak": hbm, "unit": "GB/s",
                   "frac": round(bm / tm / 1e9 / hbm, 4), "us_per_call": round(tm * 1e6, 2), "algorithmic_bytes": bm}

@@ -153,6 +153,23 @@ int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, co
 size_t vp_kernel_map_sort_ws_bytes(int64_t cap, int32_t K);
 int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, int32_t K, int32_t* perm,
                        int32_t* table_sorted, void* ws, size_t ws_bytes, vp_stream_t stream);
+/* Two-level ("brick") index for bounded lattices, the same contract as the
+ * dense grid with ~64x less memory: a coarse table over 4^3 bricks plus a
+ * pool of 256 B bricks allocated only where rows exist (kmap_brick.cu).
+ * `index` (vp_brick_bytes(cap, B, R) bytes) is initialised once with
+ * vp_brick_init; vp_brick_set(clear=0) indexes the rows, vp_brick_set(clear=1)
+ * empties exactly what was set so the index is reusable.  cap <= the cap the
+ * index was sized for.  vp_kernel_map_brick == vp_kernel_map_grid on it. */
+int64_t vp_brick_pool(int64_t cap, int32_t B, int32_t R);
+size_t vp_brick_bytes(int64_t cap, int32_t B, int32_t R);
+int vp_brick_init(void* index, int64_t cap, int32_t B, int32_t R, vp_stream_t stream);
+int vp_brick_set(const int32_t* coords, const int32_t* n_dev, int64_t cap, void* index, int64_t index_cap,
+                 int32_t B, int32_t R, int32_t s, int32_t clear, vp_stream_t stream);
+size_t vp_kernel_map_brick_ws_bytes(int64_t cap_out, int32_t K);
+int vp_kernel_map_brick(const void* index, int64_t index_cap, int32_t B, int32_t R, int32_t s, const int32_t* out,
+                        const int32_t* n_out_dev, int64_t cap_out, const int32_t* offsets_host, int32_t K,
+                        const int32_t* in_stride_host3, int32_t* nbr, int32_t* pair_in, int32_t* pair_out,
+                        int32_t* pair_ptr, void* ws, size_t ws_bytes, vp_stream_t stream);
 /* inverse neighbour table inv[v, k] = u for every pair (v,u) of offset k
  * (the dgrad gather table; conv.py:238-240 iterates the same pairs). */
 int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out,

@@ -378,6 +378,21 @@ __global__ void map_inverse_kernel(const int32_t* __restrict__ nbr, const int32_
 
 }  // namespace vp
 
+namespace vp {
+// per-offset scan of the tile counts + ordered pair emission (shared by the
+// hash, dense-grid and brick probes)
+int map_scan_emit(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out, int K, int32_t* counts,
+                  int32_t* totals, int ntiles, int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr,
+                  cudaStream_t st) {
+  ::vp::launch(map_scan_kernel, K, 1024, 0, st, counts, n_out_dev, cap_out, ntiles, totals);
+  VP_CHECK_LAUNCH("map_scan");
+  ::vp::launch(map_emit_kernel, ntiles, kMapTile, 0, st, nbr, n_out_dev, cap_out, K, (const int32_t*)counts,
+               (const int32_t*)totals, ntiles, pair_in, pair_out, pair_ptr);
+  VP_CHECK_LAUNCH("map_emit");
+  return VP_OK;
+}
+}  // namespace vp
+
 using namespace vp;
 
 extern "C" {
@@ -497,12 +512,7 @@ int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, co
                                                      GridSpec{const_cast<int32_t*>(cells), B, R, s}, offs, K, nbr,
                                                      counts, ntiles);
   VP_CHECK_LAUNCH("map_probe_grid");
-  ::vp::launch(map_scan_kernel, K, 1024, 0, st, counts, n_out_dev, cap_out, ntiles, totals);
-  VP_CHECK_LAUNCH("map_scan");
-  ::vp::launch(map_emit_kernel, ntiles, kMapTile, 0, st, nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out,
-                                               pair_ptr);
-  VP_CHECK_LAUNCH("map_emit");
-  return VP_OK;
+  return map_scan_emit(nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out, pair_ptr, st);
 }
 
 int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out, int32_t K,

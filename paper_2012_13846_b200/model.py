@@ -154,11 +154,22 @@ class SparseResNetTrainer:
         # used instead of a hash table while the lattice stays small
         self.grid_R = [-(-resolution // (2 ** i)) for i in range(nlev)]
         grid_bytes = sum(4 * batch * r ** 3 for r in self.grid_R)
-        if index not in ("auto", "grid", "hash"):
-            raise ValueError(f"index must be auto|grid|hash, got {index!r}")
-        self.use_grid = index == "grid" or (index == "auto" and grid_bytes <= (4 << 30))
-        self.grids = ([torch.full((batch * r ** 3,), 0x7FFFFFFF, dtype=torch.int32, device=dev) for r in self.grid_R]
-                      if self.use_grid else None)
+        if index not in ("auto", "grid", "brick", "hash"):
+            raise ValueError(f"index must be auto|grid|brick|hash, got {index!r}")
+        if index == "auto":
+            index = __import__("os").environ.get("VP_MAP_INDEX", "grid" if grid_bytes <= (4 << 30) else "brick")
+        self.index_kind = index
+        self.use_grid = index in ("grid", "brick")  # a lattice index (dense cells or 4^3 bricks)
+        self.grids = None
+        if index == "grid":
+            self.grids = [torch.full((batch * r ** 3,), 0x7FFFFFFF, dtype=torch.int32, device=dev) for r in self.grid_R]
+        elif index == "brick":
+            self.grids = []
+            for i, r in enumerate(self.grid_R):
+                nb = int(_lib.query("vp_brick_bytes", self.levels[i].cap, batch, r))
+                buf = torch.empty(nb, dtype=torch.uint8, device=dev)
+                _lib.call("vp_brick_init", buf.data_ptr(), self.levels[i].cap, batch, r, _lib.stream())
+                self.grids.append(buf)
         # ---- pipeline units and the layers this engine owns
         self.layers_all = self._layer_list()
         self.units = self._unit_list(self.layers_all)
@@ -357,12 +368,21 @@ class SparseResNetTrainer:
 
     def _grid_set(self, i, st, clear):
         lv = self.levels[i]
+        if self.index_kind == "brick":
+            self._c("vp_brick_set", lv.coords.data_ptr(), lv.n.data_ptr(), lv.cap, self.grids[i].data_ptr(), lv.cap,
+                    self.B, self.grid_R[i], lv.stride, int(clear), st)
+            return
         self._c("vp_grid_set", lv.coords.data_ptr(), lv.n.data_ptr(), lv.cap, self.grids[i].data_ptr(), self.B,
                 self.grid_R[i], lv.stride, int(clear), st)
 
     def _build_map(self, m, st):
         ist = _lib.i32_array((m.src.stride,) * 3)
-        if self.use_grid:
+        if self.index_kind == "brick":
+            i = self.levels.index(m.src)
+            self._c("vp_kernel_map_brick", self.grids[i].data_ptr(), m.src.cap, self.B, self.grid_R[i], m.src.stride,
+                    m.dst.coords.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(),
+                    m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.ws.data_ptr(), m.ws.numel(), st)
+        elif self.use_grid:
             i = self.levels.index(m.src)
             self._c("vp_kernel_map_grid", self.grids[i].data_ptr(), self.B, self.grid_R[i], m.src.stride,
                     m.dst.coords.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.offs3, self.K, ist, m.nbr.data_ptr(),

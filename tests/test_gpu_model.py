@@ -52,13 +52,13 @@ def test_levels_bit_exact():
             c, ts = O.generate_output_coords(c, ts, 2)
 
 
-@pytest.mark.parametrize("index", ["grid", "hash"])
+@pytest.mark.parametrize("index", ["grid", "brick", "hash"])
 def test_trainer_kernel_maps_bit_exact(index):
-    """Every map the engine builds (dense-grid or hash index) equals the
-    oracle's build_kernel_map (conv.py:149-183) pair for pair, nbr included;
-    the grids are empty again after the step."""
+    """Every map the engine builds (dense-grid, brick or hash index) equals
+    the oracle's build_kernel_map (conv.py:149-183) pair for pair, nbr
+    included; the lattice indexes are empty again after the step."""
     tr, pts, offs, labels = make(B=3, P=2500, res=40, index=index)
-    assert tr.use_grid == (index == "grid")
+    assert tr.index_kind == index and tr.use_grid == (index != "hash")
     for rep in range(2):  # the second step checks the grids were cleared
         pts, offs = O.synthetic_batch(3, 2500, 40, seed=11 + rep, dtype=np.float32)
         tr.train_step_from_host(pts, offs, labels)
@@ -77,9 +77,16 @@ def test_trainer_kernel_maps_bit_exact(index):
             col = np.full(nd, -1, np.int64)
             col[eo] = ei
             np.testing.assert_array_equal(nbr[:, k], col)
-    if tr.use_grid:
+    if index == "grid":
         for g in tr.grids:
             assert bool((g == 0x7FFFFFFF).all())
+    if index == "brick":  # coarse table, brick pool and owner list back to their initial state
+        for i, g in enumerate(tr.grids):
+            r = tr.grid_R[i]
+            rc = (r + 3) // 4
+            words = g.view(torch.int32)
+            ncoarse = tr.B * rc ** 3
+            assert bool((words[:ncoarse] == 0x7F7F7F7F).all())
 
 
 @pytest.mark.parametrize("blocks", [1, 2])
