@@ -302,7 +302,7 @@ static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int w
 // ------------------------------------------------------------------ dispatch
 static bool tc_width(int64_t c) { return c == 32 || c == 64 || c == 128 || c == 256; }
 
-constexpr int kMaxSplit = 8;
+constexpr int kMaxSplit = 16;
 
 template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1>
 static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
@@ -409,7 +409,7 @@ static int conv_tc(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaS
   return VP_EINTERNAL;
 }
 
-static size_t split_ws_bytes(int64_t nd) { return align_up((size_t)kNumSMs * 128 * nd * 4, 256); }
+static size_t split_ws_bytes(int64_t nd) { return align_up((size_t)kSplitItems * 128 * nd * 4, 256); }
 
 constexpr int kWgSms = kNumSMs;
 

@@ -95,6 +95,10 @@ struct FwdTC {
   static int smem_bytes(int K, bool tbl) { return SMEM_BASE + (tbl ? 2 * TT * 128 * K * 4 : 0); }
 };
 
+// split-K work items the partial buffer holds (two per SM: the grid of the
+// 2-CTA/SM configurations)
+constexpr int kSplitItems = 2 * kNumSMs;
+
 __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) {
   if (ntiles <= 0 || max_split <= 1 || ntiles * 2 > grid) return 1;
   int s = grid / ntiles;
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   const int n_out = load_count(p.n_out_dev, p.cap_out);
   const int ntiles = (n_out + TR - 1) / TR;
   // split partials are sized for kNumSMs work items
-  const int S = split_count(ntiles, min((int)gridDim.x, kNumSMs), p.max_split);
+  const int S = split_count(ntiles, min((int)gridDim.x, kSplitItems), p.max_split);
   const int total = ntiles * S;
   if ((int)blockIdx.x >= total) return;
 
@@ -443,7 +447,7 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_
   ::vp::pdl_begin();
   const int n_out = load_count(n_out_dev, cap_out);
   const int ntiles = (n_out + 127) / 128;
-  const int S = split_count(ntiles, grid < kNumSMs ? grid : kNumSMs, max_split);
+  const int S = split_count(ntiles, grid < kSplitItems ? grid : kSplitItems, max_split);
   if (S <= 1) return;
   const int64_t total = (int64_t)n_out * ND / 4;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
