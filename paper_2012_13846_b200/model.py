@@ -256,6 +256,7 @@ class SparseResNetTrainer:
         self._forked = set()
         self.prefetch = False
         self.states = None
+        self._sgd_in_backward = False  # set inside step_body / prefetch_body (single-process training)
 
     # ------------------------------------------------------------------ setup
     def _width_at(self, level):
@@ -579,13 +580,39 @@ class SparseResNetTrainer:
                     self.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(),
                     L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st)
         if not need_dgrad:
+            self._layer_sgd(L, ws if self.concurrent else None, None, st)
             return None
         gin = self.gact[self.levels.index(src)]
         table, flip, perm = self.dgrad_table(L)
         self._c("vp_conv_dgrad", L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(), L["wcode"],
                 L["cin"], self.K, table.data_ptr(), flip, _lib.ptr(perm), src.n.data_ptr(), src.cap, gin.data_ptr(),
                 fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
+        if self._sgd_in_backward:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self._layer_sgd(L, ws if self.concurrent else None, ev, st)
         return gin
+
+    def _layer_sgd(self, L, side, after, st):
+        """Momentum SGD of this layer's conv weights as soon as its weight
+        gradient exists and its dgrad (the last reader of W this step) has
+        been issued: on the weight-gradient side stream, off the critical
+        path (single-process training; DP all-reduces first and pipelines
+        update stashed masters, so both keep the one flat update)."""
+        if not self._sgd_in_backward:
+            return
+        pb = self.params
+        off, shape = pb.offsets[L["name"] + ".w"]
+        n = int(np.prod(shape))
+        args = (pb.p.data_ptr() + 4 * off, pb.m.data_ptr() + 4 * off, pb.g.data_ptr() + 4 * off, n, float(self.lr),
+                float(self.momentum), pb.pb.data_ptr() + 2 * off, n)
+        if side is None:
+            self._c("vp_sgd_momentum", *args, st)
+            return
+        if after is not None:
+            side.wait_event(after)
+        with torch.cuda.stream(side):
+            self._c("vp_sgd_momentum", *args, side.cuda_stream)
 
     def _backward(self, st):
         if self.last:
@@ -622,6 +649,11 @@ class SparseResNetTrainer:
     def _optimizer(self, st):
         pb = self.params
         self.join_side_streams()
+        if self._sgd_in_backward:  # conv weights were updated layer by layer; BN + fc here
+            rest = pb.size - pb.n_bf16
+            self._c("vp_sgd_momentum", pb.p.data_ptr() + 4 * pb.n_bf16, pb.m.data_ptr() + 4 * pb.n_bf16,
+                    pb.g.data_ptr() + 4 * pb.n_bf16, rest, float(self.lr), float(self.momentum), None, 0, st)
+            return
         if self.grad_allreduce is not None:
             self.grad_allreduce(pb.g)
         self._c("vp_sgd_momentum", pb.p.data_ptr(), pb.m.data_ptr(), pb.g.data_ptr(), pb.size, float(self.lr),
@@ -631,10 +663,14 @@ class SparseResNetTrainer:
         """One full training step on the current stream (graph-capturable)."""
         st = _lib.stream()
         self.launch_count = 0
-        self._integer_stage(st)
-        self._forward(st)
-        self._backward(st)
-        self._optimizer(st)
+        self._sgd_in_backward = self.grad_allreduce is None
+        try:
+            self._integer_stage(st)
+            self._forward(st)
+            self._backward(st)
+            self._optimizer(st)
+        finally:
+            self._sgd_in_backward = False
 
     def join_side_streams(self):
         """Join the side streams forked since the last join (a captured body
@@ -740,8 +776,12 @@ class SparseResNetTrainer:
         with torch.cuda.stream(P):
             self._integer_stage(P.cuda_stream)
         self._use(self.states[cur])
-        self._backward(st)
-        self._optimizer(st)
+        self._sgd_in_backward = self.grad_allreduce is None
+        try:
+            self._backward(st)
+            self._optimizer(st)
+        finally:
+            self._sgd_in_backward = False
 
     def prefetch_prologue(self):
         """Build the integer stage of the state the next step trains on."""
