@@ -257,6 +257,7 @@ class SparseResNetTrainer:
         self.prefetch = False
         self.states = None
         self._sgd_in_backward = False  # set inside step_body / prefetch_body (single-process training)
+        self.layer_sgd = __import__("os").environ.get("VP_LAYER_SGD", "1") != "0"
 
     # ------------------------------------------------------------------ setup
     def _width_at(self, level):
@@ -663,7 +664,7 @@ class SparseResNetTrainer:
         """One full training step on the current stream (graph-capturable)."""
         st = _lib.stream()
         self.launch_count = 0
-        self._sgd_in_backward = self.grad_allreduce is None
+        self._sgd_in_backward = self.grad_allreduce is None and self.layer_sgd
         try:
             self._integer_stage(st)
             self._forward(st)
@@ -776,7 +777,7 @@ class SparseResNetTrainer:
         with torch.cuda.stream(P):
             self._integer_stage(P.cuda_stream)
         self._use(self.states[cur])
-        self._sgd_in_backward = self.grad_allreduce is None
+        self._sgd_in_backward = self.grad_allreduce is None and self.layer_sgd
         try:
             self._backward(st)
             self._optimizer(st)
