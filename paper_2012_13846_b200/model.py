@@ -598,8 +598,9 @@ class SparseResNetTrainer:
         """Momentum SGD of this layer's conv weights as soon as its weight
         gradient exists and its dgrad (the last reader of W this step) has
         been issued: on the weight-gradient side stream, off the critical
-        path (single-process training; DP all-reduces first and pipelines
-        update stashed masters, so both keep the one flat update)."""
+        path.  Data parallel: the layer's gradient is all-reduced there first
+        (bucket = one layer, overlapping the rest of the backward).  Pipeline
+        stages keep the flat update of their stashed masters (sgd_into)."""
         if not self._sgd_in_backward:
             return
         pb = self.params
@@ -608,11 +609,15 @@ class SparseResNetTrainer:
         args = (pb.p.data_ptr() + 4 * off, pb.m.data_ptr() + 4 * off, pb.g.data_ptr() + 4 * off, n, float(self.lr),
                 float(self.momentum), pb.pb.data_ptr() + 2 * off, n)
         if side is None:
+            if self.grad_allreduce is not None:
+                self.grad_allreduce(pb.g[off:off + n])
             self._c("vp_sgd_momentum", *args, st)
             return
         if after is not None:
             side.wait_event(after)
         with torch.cuda.stream(side):
+            if self.grad_allreduce is not None:
+                self.grad_allreduce(pb.g[off:off + n])
             self._c("vp_sgd_momentum", *args, side.cuda_stream)
 
     def _backward(self, st):
@@ -652,6 +657,8 @@ class SparseResNetTrainer:
         self.join_side_streams()
         if self._sgd_in_backward:  # conv weights were updated layer by layer; BN + fc here
             rest = pb.size - pb.n_bf16
+            if self.grad_allreduce is not None:
+                self.grad_allreduce(pb.g[pb.n_bf16:])
             self._c("vp_sgd_momentum", pb.p.data_ptr() + 4 * pb.n_bf16, pb.m.data_ptr() + 4 * pb.n_bf16,
                     pb.g.data_ptr() + 4 * pb.n_bf16, rest, float(self.lr), float(self.momentum), None, 0, st)
             return
@@ -664,7 +671,7 @@ class SparseResNetTrainer:
         """One full training step on the current stream (graph-capturable)."""
         st = _lib.stream()
         self.launch_count = 0
-        self._sgd_in_backward = self.grad_allreduce is None and self.layer_sgd
+        self._sgd_in_backward = self.layer_sgd
         try:
             self._integer_stage(st)
             self._forward(st)
@@ -777,7 +784,7 @@ class SparseResNetTrainer:
         with torch.cuda.stream(P):
             self._integer_stage(P.cuda_stream)
         self._use(self.states[cur])
-        self._sgd_in_backward = self.grad_allreduce is None and self.layer_sgd
+        self._sgd_in_backward = self.layer_sgd
         try:
             self._backward(st)
             self._optimizer(st)
