@@ -42,7 +42,9 @@ def default_device():
 def pad_coords(coords, device=None) -> tuple[torch.Tensor, int]:
     """(N, 1+D) int rows -> contiguous int32 (N, 4) on the device, and D."""
     if not isinstance(coords, torch.Tensor):
-        coords = torch.as_tensor(np.asarray(coords, dtype=np.int64))
+        a = np.asarray(coords, dtype=np.int64)
+        # read-only arrays (the reference's SparseTensor marks its arrays so) are copied
+        coords = torch.from_numpy(a if a.flags.writeable else a.copy())
     if coords.dim() != 2 or coords.shape[1] < 2:
         raise StructuralError("coords must have shape (N, 1+D) with D >= 1")
     dim = coords.shape[1] - 1
