@@ -324,9 +324,32 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # Each step's pinned-host -> HBM upload runs on a copy stream into a
+    # staging buffer while the previous step computes; the step itself only
+    # waits for its upload and does a 1.5 MB device copy into the engine's
+    # static input buffers.  Every byte still crosses PCIe inside the region.
+    h2d_stream = torch.cuda.Stream(device=dev)
+    stage = [(torch.empty_like(dev_pts[0]), torch.empty_like(dev_lab[0])) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+
+    def upload(i):
+        b = i % 2
+        h2d_stream.wait_event(free[b])
+        with torch.cuda.stream(h2d_stream):
+            stage[b][0].copy_(host_pts[i % pool_n], non_blocking=True)
+            stage[b][1].copy_(host_lab[i % pool_n], non_blocking=True)
+        ready[b].record(h2d_stream)
+
     e0.record(stream)
+    upload(0)
     for i in range(args.steps):
-        tr.set_batch(host_pts[i % pool_n], host_lab[i % pool_n])  # pinned host -> HBM inside the timed region
+        b = i % 2
+        stream.wait_event(ready[b])
+        tr.set_batch(stage[b][0], stage[b][1])
+        free[b].record(stream)
+        if i + 1 < args.steps:
+            upload(i + 1)
         tr.step()
         loss_host.copy_(tr.loss, non_blocking=True)
     e1.record(stream)
