@@ -5,6 +5,7 @@
 // self-defined against oracle/voxpipe_oracle.py.  Every reduction runs in a
 // fixed order (per-block partials, then an ordered sum) -> deterministic.
 #include <cstdlib>
+#include <initializer_list>
 
 #include "common.cuh"
 
@@ -13,9 +14,12 @@ namespace vp {
 constexpr int kGlueThreads = 256;
 
 // 8-wide (16 B for bf16) vector access; VEC == 1 is the scalar fallback for
-// channel counts that are not a multiple of 8.
-template <int VEC>
-__device__ __forceinline__ void ldv(const void* p, int dtype, int64_t i, float* v) {
+// channel counts that are not a multiple of 8.  DT >= 0 fixes the dtype at
+// compile time: with no dtype branch between them the compiler keeps every
+// load of an unrolled row batch in flight (a runtime switch serialised them).
+template <int VEC, int DT = -1>
+__device__ __forceinline__ void ldv(const void* p, int dtype_rt, int64_t i, float* v) {
+  const int dtype = DT >= 0 ? DT : dtype_rt;
   if (VEC == 8 && dtype == VP_BF16) {
     uint4 raw = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p) + i);
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
@@ -34,8 +38,9 @@ __device__ __forceinline__ void ldv(const void* p, int dtype, int64_t i, float* 
     for (int q = 0; q < VEC; ++q) v[q] = ldf(p, dtype, i + q);
   }
 }
-template <int VEC>
-__device__ __forceinline__ void stv(void* p, int dtype, int64_t i, const float* v) {
+template <int VEC, int DT = -1>
+__device__ __forceinline__ void stv(void* p, int dtype_rt, int64_t i, const float* v) {
+  const int dtype = DT >= 0 ? DT : dtype_rt;
   if (VEC == 8 && dtype == VP_BF16) {
     uint4 raw;
     __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
@@ -68,13 +73,13 @@ struct BnFuse {
   void* gres;
 };
 
-template <int VEC>
+template <int VEC, int DT>
 __device__ __forceinline__ void bn_apply_rows(const void* __restrict__ x, int dtype, int n, int C,
                                               const float* __restrict__ mean, const float* __restrict__ rstd,
                                               const float* __restrict__ gamma, const float* __restrict__ beta,
                                               const void* __restrict__ res, int res_dtype, int relu,
                                               void* __restrict__ y, int y_dtype, int blk, int nblk);
-template <int VEC>
+template <int VEC, int DT>
 __device__ __forceinline__ void bn_backward_apply_rows(
     const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype, const void* __restrict__ y, int y_dtype,
     const void* __restrict__ x, int x_dtype, int n, int C, const float* __restrict__ mean,
@@ -90,24 +95,109 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int VEC>
+template <int VEC, int DT>
 __device__ __forceinline__ void bn_fused_apply(const void* x, int dtype, int n, int C, const void* gy, const void* gy2,
                                                int gy_dtype, const void* y, int y_dtype, int relu, const float* mean,
                                                const float* rstd, const float* out_a, const float* out_b,
                                                const BnFuse& F) {
   if (F.mode == 1)  // forward: out_a/out_b = mean/rstd just computed
-    bn_apply_rows<VEC>(x, dtype, n, C, out_a, out_b, F.gamma, F.beta, F.res, F.res_dtype, F.relu, F.out, F.out_dtype,
+    bn_apply_rows<VEC, DT>(x, dtype, n, C, out_a, out_b, F.gamma, F.beta, F.res, F.res_dtype, F.relu, F.out, F.out_dtype,
                        blockIdx.x, gridDim.x);
   else  // backward: out_a/out_b = ggamma/gbeta
-    bn_backward_apply_rows<VEC>(gy, gy2, gy_dtype, y, y_dtype, x, dtype, n, C, mean, rstd, F.gamma, relu, out_a,
+    bn_backward_apply_rows<VEC, DT>(gy, gy2, gy_dtype, y, y_dtype, x, dtype, n, C, mean, rstd, F.gamma, relu, out_a,
                                 out_b, F.out, F.out_dtype, F.gres, blockIdx.x, gridDim.x);
+}
+
+// Reduce the per-block partials [nb][2][C] in a fixed order (same result in
+// every block that calls it) and write (mean, rstd) for stats (gy == null in
+// the producer) or (ggamma, gbeta) = (sum g*xhat, sum g) to out_a / out_b.
+// Called by all threads of a block; ends with a __syncthreads.
+__device__ __noinline__ void bn_finalize(const float* __restrict__ part, int nb, int C, int n, bool stats, float eps,
+                                         float* __restrict__ out_a, float* __restrict__ out_b) {
+  __shared__ double d_a[4 * kGlueThreads], d_b[4 * kGlueThreads];  // [G][cc][4]
+  // channel quads (4 channels as one float4 of a and one of b) when C % 4 == 0,
+  // else single channels; the G thread groups stride over the blocks with 4
+  // block rows (8 loads) in flight, then the groups are summed in order
+  const int W = (C % 4 == 0) ? 4 : 1;
+  const int units = C / W;
+  for (int u0 = 0; u0 < units; u0 += kGlueThreads) {
+    const int cc = min(units - u0, kGlueThreads);
+    const int G = kGlueThreads / cc;  // block groups per unit
+    const int uu = u0 + threadIdx.x % cc, g = threadIdx.x / cc;
+    double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (g < G) {
+      if (W == 4) {
+        for (int b0 = g; b0 < nb; b0 += 4 * G) {
+          float4 ta[4], tb[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int b = b0 + q * G;
+            ta[q] = tb[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (b < nb) {
+              ta[q] = __ldcg(reinterpret_cast<const float4*>(part + ((int64_t)b * 2) * C) + uu);
+              tb[q] = __ldcg(reinterpret_cast<const float4*>(part + ((int64_t)b * 2 + 1) * C) + uu);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            a4[0] += ta[q].x; a4[1] += ta[q].y; a4[2] += ta[q].z; a4[3] += ta[q].w;
+            b4[0] += tb[q].x; b4[1] += tb[q].y; b4[2] += tb[q].z; b4[3] += tb[q].w;
+          }
+        }
+      } else {
+        for (int b0 = g; b0 < nb; b0 += 4 * G) {
+          float ta[4], tb[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int b = b0 + q * G;
+            ta[q] = b < nb ? __ldcg(part + ((int64_t)b * 2) * C + uu) : 0.f;
+            tb[q] = b < nb ? __ldcg(part + ((int64_t)b * 2 + 1) * C + uu) : 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            a4[0] += ta[q];
+            b4[0] += tb[q];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (g < G) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        d_a[(g * cc + threadIdx.x % cc) * 4 + k] = a4[k];
+        d_b[(g * cc + threadIdx.x % cc) * 4 + k] = b4[k];
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < cc * W; e += kGlueThreads) {
+      const int i = e / W, k = e % W;
+      double sa = 0.0, sb = 0.0;
+      for (int gg = 0; gg < G; ++gg) {
+        sa += d_a[(gg * cc + i) * 4 + k];
+        sb += d_b[(gg * cc + i) * 4 + k];
+      }
+      const int ch = (u0 + i) * W + k;
+      if (stats) {  // mean, rstd (biased variance, training-mode BN)
+        const double mu = n > 0 ? sa / n : 0.0;
+        double var = n > 0 ? sb / n - mu * mu : 0.0;
+        if (var < 0) var = 0;
+        out_a[ch] = (float)mu;
+        out_b[ch] = (float)(1.0 / sqrt(var + (double)eps));
+      } else {  // ggamma = sum g*xhat, gbeta = sum g
+        out_a[ch] = (float)sb;
+        out_b[ch] = (float)sa;
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // Per-block per-channel partial sums over `rpb` rows.  Thread layout: tpr =
 // C/VEC threads cover one row (VEC channels each), lanes = 256/tpr rows in
 // flight.  stats mode (gy == null): (sum x, sum x^2); backward mode:
 // (sum g, sum g*xhat) with g = (gy [+ gy2]) masked by (y > 0) when relu.
-template <int VEC>
+template <int VEC, int DT>
 __global__ void __launch_bounds__(kGlueThreads)
 bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int64_t cap, int C,
                   const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype,
@@ -126,19 +216,31 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
   float a[VEC], b[VEC], mu[VEC], rs[VEC];
 #pragma unroll
   for (int q = 0; q < VEC; ++q) a[q] = b[q] = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * lanes;
   if (lr < lanes) {
     if (gy == nullptr) {
       // block b owns row groups b, b+G, b+2G, ... (G = gridDim.x, fixed per
-      // capacity) -> balanced for any live n, fixed summation order
-#pragma unroll 4
-      for (int64_t r = (int64_t)blockIdx.x * lanes + lr; r < n; r += (int64_t)gridDim.x * lanes) {
-        float v[VEC];
-        ldv<VEC>(x, dtype, r * C + c0, v);
+      // capacity) -> balanced for any live n, fixed summation order.  Rows
+      // are loaded in batches of 4 (all loads issued before the first add).
+      for (int64_t r0 = (int64_t)blockIdx.x * lanes + lr; r0 < n; r0 += 4 * stride) {
+        float v[4][VEC];
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) {
-          a[q] += v[q];
-          b[q] += v[q] * v[q];
+        for (int u = 0; u < 4; ++u) {
+          const int64_t r = r0 + u * stride;
+          if (r < n) {
+            ldv<VEC, DT>(x, dtype, r * C + c0, v[u]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) v[u][q] = 0.f;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) {
+            a[q] += v[u][q];
+            b[q] += v[u][q] * v[u][q];
+          }
       }
     } else {
 #pragma unroll
@@ -146,23 +248,29 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
         mu[q] = mean[c0 + q];
         rs[q] = rstd[c0 + q];
       }
-#pragma unroll 2
-      for (int64_t r = (int64_t)blockIdx.x * lanes + lr; r < n; r += (int64_t)gridDim.x * lanes) {
-        float g[VEC], g2[VEC], yy[VEC], xv[VEC];
-        ldv<VEC>(gy, gy_dtype, r * C + c0, g);
-        if (gy2) {
-          ldv<VEC>(gy2, gy_dtype, r * C + c0, g2);
+      for (int64_t r0 = (int64_t)blockIdx.x * lanes + lr; r0 < n; r0 += 2 * stride) {
+        float g[2][VEC], g2[2][VEC], yy[2][VEC], xv[2][VEC];
 #pragma unroll
-          for (int q = 0; q < VEC; ++q) g[q] += g2[q];
-        }
-        if (relu) ldv<VEC>(y, y_dtype, r * C + c0, yy);
-        ldv<VEC>(x, dtype, r * C + c0, xv);
+        for (int u = 0; u < 2; ++u) {
+          const int64_t r = r0 + u * stride;
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) {
-          float gq = (relu && yy[q] <= 0.f) ? 0.f : g[q];
-          a[q] += gq;
-          b[q] += gq * (xv[q] - mu[q]) * rs[q];
+          for (int q = 0; q < VEC; ++q) g[u][q] = g2[u][q] = yy[u][q] = xv[u][q] = 0.f;
+          if (r < n) {
+            ldv<VEC, DT>(gy, gy_dtype, r * C + c0, g[u]);
+            if (gy2) ldv<VEC, DT>(gy2, gy_dtype, r * C + c0, g2[u]);
+            if (relu) ldv<VEC, DT>(y, y_dtype, r * C + c0, yy[u]);
+            ldv<VEC, DT>(x, dtype, r * C + c0, xv[u]);
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) {
+            const float gs = gy2 ? g[u][q] + g2[u][q] : g[u][q];
+            const float gq = (relu && yy[u][q] <= 0.f) ? 0.f : gs;
+            a[q] += gq;
+            b[q] += gq * (xv[u][q] - mu[q]) * rs[q];
+          }
       }
     }
   }
@@ -183,6 +291,9 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
     part[((int64_t)blockIdx.x * 2) * C + e] = sa;
     part[((int64_t)blockIdx.x * 2 + 1) * C + e] = sb;
   }
+  // ticket == null: the consumer kernel reduces the partials (bn_finalize in
+  // every one of its blocks) -> no fence / ticket / serial tail here.
+  if (ticket == nullptr) return;
   // The LAST block to finish reduces every block's partials in block order
   // (fixed order -> deterministic) and writes the statistics: one launch
   // instead of partial + finalize.
@@ -199,64 +310,20 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
     if (threadIdx.x == 0)
       while (ld_acquire(F.epoch) == e0) __nanosleep(32);
     __syncthreads();
-    bn_fused_apply<VEC>(x, dtype, n, C, gy, gy2, gy_dtype, y, y_dtype, relu, mean, rstd, out_a, out_b, F);
+    bn_fused_apply<VEC, DT>(x, dtype, n, C, gy, gy2, gy_dtype, y, y_dtype, relu, mean, rstd, out_a, out_b, F);
     return;
   }
   __threadfence();
-  const int nb = gridDim.x;
-  __shared__ double d_a[kGlueThreads], d_b[kGlueThreads];  // [G][cc]
-  for (int c0 = 0; c0 < C; c0 += kGlueThreads) {
-    const int cc = min(C - c0, kGlueThreads);
-    const int G = kGlueThreads / cc;  // block groups per channel
-    const int c = c0 + threadIdx.x % cc, g = threadIdx.x / cc;
-    double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
-    if (g < G) {
-      for (int b0 = g; b0 < nb; b0 += 4 * G) {  // 4 independent loads in flight, fixed order
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int b = b0 + q * G;
-          if (b < nb) {
-            a4[q] += __ldcg(part + ((int64_t)b * 2) * C + c);
-            b4[q] += __ldcg(part + ((int64_t)b * 2 + 1) * C + c);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (g < G) {
-      d_a[g * cc + threadIdx.x % cc] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-      d_b[g * cc + threadIdx.x % cc] = (b4[0] + b4[1]) + (b4[2] + b4[3]);
-    }
-    __syncthreads();
-    if (threadIdx.x < cc) {
-      double sa = 0.0, sb = 0.0;
-      for (int gg = 0; gg < G; ++gg) {
-        sa += d_a[gg * cc + threadIdx.x];
-        sb += d_b[gg * cc + threadIdx.x];
-      }
-      const int ch = c0 + threadIdx.x;
-      if (gy == nullptr) {  // mean, rstd (biased variance, training-mode BN)
-        const double mu = n > 0 ? sa / n : 0.0;
-        double var = n > 0 ? sb / n - mu * mu : 0.0;
-        if (var < 0) var = 0;
-        out_a[ch] = (float)mu;
-        out_b[ch] = (float)(1.0 / sqrt(var + (double)eps));
-      } else {  // ggamma = sum g*xhat, gbeta = sum g
-        out_a[ch] = (float)sb;
-        out_b[ch] = (float)sa;
-      }
-    }
-    __syncthreads();
-  }
+  bn_finalize(part, gridDim.x, C, n, gy == nullptr, eps, out_a, out_b);
   if (F.mode) {
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release(F.epoch, e0 + 1);
-    bn_fused_apply<VEC>(x, dtype, n, C, gy, gy2, gy_dtype, y, y_dtype, relu, mean, rstd, out_a, out_b, F);
+    bn_fused_apply<VEC, DT>(x, dtype, n, C, gy, gy2, gy_dtype, y, y_dtype, relu, mean, rstd, out_a, out_b, F);
   }
 }
 
-template <int VEC>
+template <int VEC, int DT>
 __device__ __forceinline__ void bn_apply_rows(const void* __restrict__ x, int dtype, int n, int C,
                                               const float* __restrict__ mean, const float* __restrict__ rstd,
                                               const float* __restrict__ gamma, const float* __restrict__ beta,
@@ -272,32 +339,60 @@ __device__ __forceinline__ void bn_apply_rows(const void* __restrict__ x, int dt
     sc[q] = rstd[c0 + q] * gamma[c0 + q];
     sh[q] = beta[c0 + q] - mean[c0 + q] * sc[q];
   }
-  for (int64_t r = (int64_t)blk * lanes + lr; r < n; r += (int64_t)nblk * lanes) {
-    float v[VEC], rv[VEC];
-    ldv<VEC>(x, dtype, r * C + c0, v);
-    if (res) ldv<VEC>(res, res_dtype, r * C + c0, rv);
+  const int64_t stride = (int64_t)nblk * lanes;
+  for (int64_t r0 = (int64_t)blk * lanes + lr; r0 < n; r0 += 2 * stride) {
+    float v[2][VEC], rv[2][VEC];
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      float o = v[q] * sc[q] + sh[q];
-      if (res) o += rv[q];
-      v[q] = relu ? fmaxf(o, 0.f) : o;
+    for (int u = 0; u < 2; ++u) {
+      const int64_t r = r0 + u * stride;
+      if (r < n) {
+        ldv<VEC, DT>(x, dtype, r * C + c0, v[u]);
+        if (res) ldv<VEC, DT>(res, res_dtype, r * C + c0, rv[u]);
+      }
     }
-    stv<VEC>(y, y_dtype, r * C + c0, v);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t r = r0 + u * stride;
+      if (r >= n) break;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        float o = v[u][q] * sc[q] + sh[q];
+        if (res) o += rv[u][q];
+        v[u][q] = relu ? fmaxf(o, 0.f) : o;
+      }
+      stv<VEC, DT>(y, y_dtype, r * C + c0, v[u]);
+    }
   }
 }
 
-template <int VEC>
+// part != null: (mean, rstd) are first reduced from the statistics kernel's
+// per-block partials by every block (bn_finalize into shared memory); block 0
+// also stores them to mean / rstd for the backward pass.
+template <int VEC, int DT>
 __global__ void __launch_bounds__(kGlueThreads)
 bn_apply_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int64_t cap, int C,
                 const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
                 const float* __restrict__ beta, const void* __restrict__ res, int res_dtype, int relu,
-                void* __restrict__ y, int y_dtype) {
+                void* __restrict__ y, int y_dtype, const float* __restrict__ part, int nb, float eps,
+                float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  extern __shared__ float s_stat[];
   ::vp::pdl_begin();
-  bn_apply_rows<VEC>(x, dtype, load_count(n_dev, cap), C, mean, rstd, gamma, beta, res, res_dtype, relu, y, y_dtype,
+  const int n = load_count(n_dev, cap);
+  if (part) {
+    bn_finalize(part, nb, C, n, true, eps, s_stat, s_stat + C);
+    if (blockIdx.x == 0)
+      for (int c = threadIdx.x; c < C; c += kGlueThreads) {
+        mean_out[c] = s_stat[c];
+        rstd_out[c] = s_stat[C + c];
+      }
+    mean = s_stat;
+    rstd = s_stat + C;
+  }
+  bn_apply_rows<VEC, DT>(x, dtype, n, C, mean, rstd, gamma, beta, res, res_dtype, relu, y, y_dtype,
                      blockIdx.x, gridDim.x);
 }
 
-template <int VEC>
+template <int VEC, int DT>
 __device__ __forceinline__ void bn_backward_apply_rows(
     const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype, const void* __restrict__ y, int y_dtype,
     const void* __restrict__ x, int x_dtype, int n, int C, const float* __restrict__ mean,
@@ -318,37 +413,61 @@ __device__ __forceinline__ void bn_backward_apply_rows(
     k2[q] = inv_n * gbeta[c];
     k3[q] = inv_n * ggamma[c];
   }
-  for (int64_t r = (int64_t)blk * lanes + lr; r < n; r += (int64_t)nblk * lanes) {
-    float g[VEC], g2[VEC], yy[VEC], xv[VEC];
-    ldv<VEC>(gy, gy_dtype, r * C + c0, g);
-    if (gy2) {
-      ldv<VEC>(gy2, gy_dtype, r * C + c0, g2);
+  const int64_t stride = (int64_t)nblk * lanes;
+  for (int64_t r0 = (int64_t)blk * lanes + lr; r0 < n; r0 += 2 * stride) {
+    float g[2][VEC], g2[2][VEC], yy[2][VEC], xv[2][VEC];
 #pragma unroll
-      for (int q = 0; q < VEC; ++q) g[q] += g2[q];
+    for (int u = 0; u < 2; ++u) {
+      const int64_t r = r0 + u * stride;
+      if (r < n) {
+        ldv<VEC, DT>(gy, gy_dtype, r * C + c0, g[u]);
+        if (gy2) ldv<VEC, DT>(gy2, gy_dtype, r * C + c0, g2[u]);
+        if (relu) ldv<VEC, DT>(y, y_dtype, r * C + c0, yy[u]);
+        ldv<VEC, DT>(x, x_dtype, r * C + c0, xv[u]);
+      }
     }
-    if (relu) ldv<VEC>(y, y_dtype, r * C + c0, yy);
-    ldv<VEC>(x, x_dtype, r * C + c0, xv);
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      if (relu && yy[q] <= 0.f) g[q] = 0.f;
-      const float xh = (xv[q] - mu[q]) * rs[q];
-      xv[q] = k1[q] * (g[q] - k2[q] - xh * k3[q]);
+    for (int u = 0; u < 2; ++u) {
+      const int64_t r = r0 + u * stride;
+      if (r >= n) break;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        if (gy2) g[u][q] += g2[u][q];
+        if (relu && yy[u][q] <= 0.f) g[u][q] = 0.f;
+        const float xh = (xv[u][q] - mu[q]) * rs[q];
+        xv[u][q] = k1[q] * (g[u][q] - k2[q] - xh * k3[q]);
+      }
+      stv<VEC, DT>(gx, gx_dtype, r * C + c0, xv[u]);
+      if (gres) stv<VEC, DT>(gres, gx_dtype, r * C + c0, g[u]);
     }
-    stv<VEC>(gx, gx_dtype, r * C + c0, xv);
-    if (gres) stv<VEC>(gres, gx_dtype, r * C + c0, g);
   }
 }
 
-template <int VEC>
+// part != null: (ggamma, gbeta) reduced from the partials by every block
+// (block 0 stores them to ggamma_out / gbeta_out), as in bn_apply_kernel.
+template <int VEC, int DT>
 __global__ void __launch_bounds__(kGlueThreads)
 bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ gy2, int gy_dtype,
                          const void* __restrict__ y, int y_dtype, const void* __restrict__ x, int x_dtype,
                          const int32_t* n_dev, int64_t cap, int C, const float* __restrict__ mean,
                          const float* __restrict__ rstd, const float* __restrict__ gamma, int relu,
                          const float* __restrict__ ggamma, const float* __restrict__ gbeta, void* __restrict__ gx,
-                         int gx_dtype, void* __restrict__ gres) {
+                         int gx_dtype, void* __restrict__ gres, const float* __restrict__ part, int nb,
+                         float* __restrict__ ggamma_out, float* __restrict__ gbeta_out) {
+  extern __shared__ float s_stat[];
   ::vp::pdl_begin();
-  bn_backward_apply_rows<VEC>(gy, gy2, gy_dtype, y, y_dtype, x, x_dtype, load_count(n_dev, cap), C, mean, rstd, gamma,
+  const int n = load_count(n_dev, cap);
+  if (part) {
+    bn_finalize(part, nb, C, n, false, 0.f, s_stat, s_stat + C);
+    if (blockIdx.x == 0)
+      for (int c = threadIdx.x; c < C; c += kGlueThreads) {
+        ggamma_out[c] = s_stat[c];
+        gbeta_out[c] = s_stat[C + c];
+      }
+    ggamma = s_stat;
+    gbeta = s_stat + C;
+  }
+  bn_backward_apply_rows<VEC, DT>(gy, gy2, gy_dtype, y, y_dtype, x, x_dtype, n, C, mean, rstd, gamma,
                               relu, ggamma, gbeta, gx, gx_dtype, gres, blockIdx.x, gridDim.x);
 }
 
@@ -357,7 +476,7 @@ bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ g
 // few partials per channel (the element count, not the capacity, would be
 // ideal, but it lives on the device; the capacity bounds it)
 static int bn_passes() {  // row passes per thread in the partial phase (VP_BN_PASSES overrides, for tuning)
-  static const int v = getenv("VP_BN_PASSES") ? std::max(1, atoi(getenv("VP_BN_PASSES"))) : 32;
+  static const int v = getenv("VP_BN_PASSES") ? std::max(1, atoi(getenv("VP_BN_PASSES"))) : 24;
   return v;
 }
 static int bn_partial_blocks(int64_t cap, int64_t C) {
@@ -367,10 +486,15 @@ static int bn_partial_blocks(int64_t cap, int64_t C) {
 
 static bool bn_shape_ok(int64_t C) { return (C % 8 == 0 && C / 8 <= kGlueThreads) || C <= kGlueThreads; }
 
+static int bn_apply_per_sm() {  // apply blocks per SM (VP_BN_APPLY_PER_SM overrides, for tuning)
+  static const int v = getenv("VP_BN_APPLY_PER_SM") ? std::max(1, atoi(getenv("VP_BN_APPLY_PER_SM"))) : 1;
+  return v;
+}
 static int bn_grid_rows(int64_t cap, int64_t C) {
   const int vec = (C % 8 == 0) ? 8 : 1;
   const int lanes = std::max<int>(1, kGlueThreads / (int)(C / vec));
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(cap, 1), lanes), kNumSMs * 8));
+  return (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(std::max<int64_t>(cap, 1), lanes), (int64_t)kNumSMs * bn_apply_per_sm()));
 }
 
 // ------------------------------------------------------------------ pooling
@@ -519,6 +643,21 @@ size_t vp_bn_stats_ws_bytes(int64_t cap_n, int64_t C) {
   return align_up((size_t)bn_partial_blocks(cap_n, C) * 2 * C * 4, 256) + 256;  // partials + ticket
 }
 
+// Launch KERNEL<VEC, DT>: DT fixed at compile time when every tensor the kernel
+// touches has one dtype (f32 or bf16), else the runtime-dtype variant.
+#define VP_BN_LAUNCH(KERNEL, C, DT, ...)                                               \
+  ((C) % 8 != 0          ? ::vp::launch(KERNEL<1, -1>, __VA_ARGS__)                    \
+   : (DT) == VP_BF16 ? ::vp::launch(KERNEL<8, VP_BF16>, __VA_ARGS__)                   \
+   : (DT) == VP_F32  ? ::vp::launch(KERNEL<8, VP_F32>, __VA_ARGS__)                    \
+                     : ::vp::launch(KERNEL<8, -1>, __VA_ARGS__))
+
+static int one_dtype(std::initializer_list<int> ds) {
+  const int d = *ds.begin();
+  for (int v : ds)
+    if (v != d) return -1;
+  return (d == VP_F32 || d == VP_BF16) ? d : -1;
+}
+
 static int* bn_ticket(void* ws, int64_t cap, int64_t C) {
   return reinterpret_cast<int*>((char*)ws + align_up((size_t)bn_partial_blocks(cap, C) * 2 * C * 4, 256));
 }
@@ -531,12 +670,8 @@ int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   const int nb = bn_partial_blocks(cap, C);
   int* ticket = bn_ticket(ws, cap, C);
   const BnFuse F{};
-  if (C % 8 == 0)
-    ::vp::launch(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
-                                                       nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd, F);
-  else
-    ::vp::launch(bn_partial_kernel<1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr, 0, nullptr, 0, 0,
-                                                       nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd, F);
+  VP_BN_LAUNCH(bn_partial_kernel, C, one_dtype({xd}), nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr,
+               nullptr, 0, nullptr, 0, 0, nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd, F);
   VP_CHECK_LAUNCH("bn_stats");
   return VP_OK;
 }
@@ -561,17 +696,26 @@ int vp_bn_forward(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, 
     int* ticket = bn_ticket(ws, cap, C);
     const BnFuse F{1, ticket + 16, gamma, beta, res, rd, relu, y, yd, nullptr};
     cudaError_t e = C % 8 == 0
-        ? ::vp::launch_coop(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr,
+        ? ::vp::launch_coop(bn_partial_kernel<8, -1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr,
                             0, nullptr, 0, 0, nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd, F)
-        : ::vp::launch_coop(bn_partial_kernel<1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr,
+        : ::vp::launch_coop(bn_partial_kernel<1, -1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr, nullptr,
                             0, nullptr, 0, 0, nullptr, nullptr, (float*)ws, ticket, eps, mean, rstd, F);
     VP_REQUIRE(e == cudaSuccess, VP_EINTERNAL, "bn_forward: cooperative launch failed");
     VP_CHECK_LAUNCH("bn_forward");
     return VP_OK;
   }
-  int rc = vp_bn_stats(x, xd, n_dev, cap, C, eps, mean, rstd, ws, ws_bytes, stream);
-  if (rc) return rc;
-  return vp_bn_apply(x, xd, n_dev, cap, C, mean, rstd, gamma, beta, res, rd, relu, y, yd, stream);
+  if (cap <= 0) return vp_bn_stats(x, xd, n_dev, cap, C, eps, mean, rstd, ws, ws_bytes, stream);
+  // partials only (no ticket), then the apply kernel reduces them in every block
+  const int nb = bn_partial_blocks(cap, C);
+  const BnFuse F{};
+  VP_BN_LAUNCH(bn_partial_kernel, C, one_dtype({xd}), nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, nullptr,
+               nullptr, 0, nullptr, 0, 0, nullptr, nullptr, (float*)ws, (int*)nullptr, eps, mean, rstd, F);
+  VP_CHECK_LAUNCH("bn_fwd_stats");
+  VP_BN_LAUNCH(bn_apply_kernel, C, one_dtype({xd, yd, res ? rd : xd}), bn_grid_rows(cap, C), kGlueThreads,
+               2 * C * sizeof(float), st, x, xd, n_dev, cap, (int)C, (const float*)nullptr, (const float*)nullptr,
+               gamma, beta, res, rd, relu, y, yd, (const float*)ws, nb, eps, mean, rstd);
+  VP_CHECK_LAUNCH("bn_fwd_apply");
+  return VP_OK;
 }
 
 int vp_bn_apply(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, int64_t C, const float* mean,
@@ -581,12 +725,9 @@ int vp_bn_apply(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   if (cap <= 0) return VP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = bn_grid_rows(cap, C);
-  if (C % 8 == 0)
-    ::vp::launch(bn_apply_kernel<8>, grid, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
-                                                       relu, y, yd);
-  else
-    ::vp::launch(bn_apply_kernel<1>, grid, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, beta, res, rd,
-                                                       relu, y, yd);
+  VP_BN_LAUNCH(bn_apply_kernel, C, one_dtype({xd, yd, res ? rd : xd}), grid, kGlueThreads, 0, st, x, xd, n_dev, cap,
+               (int)C, mean, rstd, gamma, beta, res, rd, relu, y, yd, (const float*)nullptr, 0, 0.f, (float*)nullptr,
+               (float*)nullptr);
   VP_CHECK_LAUNCH("bn_apply");
   return VP_OK;
 }
@@ -605,30 +746,25 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
   if (bn_fused_enabled() && cap > 0) {
     const BnFuse F{2, ticket + 16, gamma, nullptr, nullptr, 0, relu, gx, gxd, gres};
     cudaError_t e = C % 8 == 0
-        ? ::vp::launch_coop(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y,
+        ? ::vp::launch_coop(bn_partial_kernel<8, -1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y,
                             yd, relu, mean, rstd, (float*)ws, ticket, 0.f, ggamma, gbeta, F)
-        : ::vp::launch_coop(bn_partial_kernel<1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y,
+        : ::vp::launch_coop(bn_partial_kernel<1, -1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y,
                             yd, relu, mean, rstd, (float*)ws, ticket, 0.f, ggamma, gbeta, F);
     VP_REQUIRE(e == cudaSuccess, VP_EINTERNAL, "bn_backward: cooperative launch failed");
     VP_CHECK_LAUNCH("bn_bwd_fused");
     return VP_OK;
   }
   const BnFuse F{};
-  if (C % 8 == 0)
-    ::vp::launch(bn_partial_kernel<8>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
-                                                       (float*)ws, ticket, 0.f, ggamma, gbeta, F);
-  else
-    ::vp::launch(bn_partial_kernel<1>, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd, relu, mean, rstd,
-                                                       (float*)ws, ticket, 0.f, ggamma, gbeta, F);
+  const int dt_stats = one_dtype({xd, gyd, relu ? yd : xd});
+  // cap > 0: partials only, reduced by every block of the apply kernel
+  VP_BN_LAUNCH(bn_partial_kernel, C, dt_stats, nb, kGlueThreads, 0, st, x, xd, n_dev, cap, (int)C, gy, gy2, gyd, y, yd,
+               relu, mean, rstd, (float*)ws, cap > 0 ? (int*)nullptr : ticket, 0.f, ggamma, gbeta, F);
   VP_CHECK_LAUNCH("bn_bwd_stats");
   if (cap > 0) {
     const int grid = bn_grid_rows(cap, C);
-    if (C % 8 == 0)
-      ::vp::launch(bn_backward_apply_kernel<8>, grid, kGlueThreads, 0, st, gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
-                                                                  rstd, gamma, relu, ggamma, gbeta, gx, gxd, gres);
-    else
-      ::vp::launch(bn_backward_apply_kernel<1>, grid, kGlueThreads, 0, st, gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean,
-                                                                  rstd, gamma, relu, ggamma, gbeta, gx, gxd, gres);
+    VP_BN_LAUNCH(bn_backward_apply_kernel, C, one_dtype({xd, gyd, relu ? yd : xd, gxd}), grid, kGlueThreads,
+                 2 * C * sizeof(float), st, gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, relu,
+                 (const float*)nullptr, (const float*)nullptr, gx, gxd, gres, (const float*)ws, nb, ggamma, gbeta);
     VP_CHECK_LAUNCH("bn_bwd_apply");
   }
   return VP_OK;

@@ -11,8 +11,11 @@ from paper_2012_13846_b200 import _lib  # noqa: E402
 
 dev = torch.device("cuda")
 st = torch.cuda.current_stream()
-for n, cap, C in [(115000, 131072, 32), (83000, 131072, 32), (37500, 131072, 64), (10700, 32768, 128),
-                  (2600, 4096, 256)]:
+SHAPES = [(115000, 131072, 32), (83000, 131072, 32), (37500, 131072, 64), (10700, 32768, 128),
+          (2600, 4096, 256)]
+if len(sys.argv) > 1 and sys.argv[1] == "floor":  # fixed cost: almost no rows at the same capacities
+    SHAPES = [(64, cap, C) for _, cap, C in SHAPES]
+for n, cap, C in SHAPES:
     x = torch.randn(cap, C, device=dev).to(torch.bfloat16)
     nd = torch.tensor([n], dtype=torch.int32, device=dev)
     mean = torch.zeros(C, device=dev)
@@ -30,8 +33,27 @@ for n, cap, C in [(115000, 131072, 32), (83000, 131072, 32), (37500, 131072, 64)
         _lib.call("vp_bn_apply", x.data_ptr(), 1, nd.data_ptr(), cap, C, mean.data_ptr(), rstd.data_ptr(),
                   g.data_ptr(), b.data_ptr(), None, 1, 1, y.data_ptr(), 1, torch.cuda.current_stream().cuda_stream)
 
+    gy = torch.randn(cap, C, device=dev).to(torch.bfloat16)
+    gx = torch.empty_like(x)
+    gg = torch.zeros(C, device=dev)
+    gb = torch.zeros(C, device=dev)
+    wsb = torch.zeros(int(_lib.query("vp_bn_backward_ws_bytes", cap, C)), dtype=torch.uint8, device=dev)
+
+    def backward():
+        _lib.call("vp_bn_backward", gy.data_ptr(), None, 1, y.data_ptr(), 1, x.data_ptr(), 1, nd.data_ptr(), cap, C,
+                  mean.data_ptr(), rstd.data_ptr(), g.data_ptr(), 1, gx.data_ptr(), 1, None, gg.data_ptr(),
+                  gb.data_ptr(), wsb.data_ptr(), wsb.numel(), torch.cuda.current_stream().cuda_stream)
+
+    def forward():
+        _lib.call("vp_bn_forward", x.data_ptr(), 1, nd.data_ptr(), cap, C, 1e-5, mean.data_ptr(), rstd.data_ptr(),
+                  g.data_ptr(), b.data_ptr(), None, 1, 1, y.data_ptr(), 1, ws.data_ptr(), ws.numel(),
+                  torch.cuda.current_stream().cuda_stream)
+
+    def tiny():
+        nd.add_(0)
+
     res = []
-    for fn in (stats, apply):
+    for fn in (stats, apply, forward, backward, tiny):
         fn()
         torch.cuda.synchronize()
         s = torch.cuda.Stream()
@@ -49,4 +71,4 @@ for n, cap, C in [(115000, 131072, 32), (83000, 131072, 32), (37500, 131072, 64)
         torch.cuda.synchronize()
         res.append(a.elapsed_time(e) * 1e3 / 100)
     mb = n * C * 2 / 1e6
-    print(f"N={n:6d} C={C:3d} ({mb:5.1f} MB): stats {res[0]:6.2f} us  apply {res[1]:6.2f} us")
+    print(f"N={n:6d} C={C:3d} ({mb:5.1f} MB): stats {res[0]:6.2f} us  apply {res[1]:6.2f} us  forward {res[2]:6.2f} us  backward {res[3]:6.2f} us  (1-elem op {res[4]:5.2f} us)")
