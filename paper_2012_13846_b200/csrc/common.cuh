@@ -1,5 +1,6 @@
 // Shared device helpers for the voxpipe_b200 sm_100a kernels.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -35,6 +36,15 @@ int check_launch(const char* what, int kernels);
   } while (0)
 
 constexpr int kNumSMs = 148;
+
+// Block cap of the grid-stride kernels: per_sm blocks per SM, lowered by
+// VP_GRID_PER_SM (tuning: in the training step these kernels share the GPU
+// with the critical-path stream, where small grids interfere less).
+inline int grid_cap(int per_sm) {
+  static const int lim = getenv("VP_GRID_PER_SM") ? (atoi(getenv("VP_GRID_PER_SM")) > 0 ? atoi(getenv("VP_GRID_PER_SM")) : 1)
+                                                  : (1 << 20);
+  return kNumSMs * (per_sm < lim ? per_sm : lim);
+}
 
 // ------------------------------------------------------------------ launch
 // Every kernel of the library is launched with Programmatic Dependent Launch

@@ -285,7 +285,7 @@ static bool small_fwd_ok(int64_t cin, int64_t cout, int K) { return cin <= 4 && 
 static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int wd, int cout, int K,
                             const int32_t* table, int flip, const int32_t* perm, const int32_t* n_out_dev,
                             int64_t cap_out, void* y, int yd, cudaStream_t st) {
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), kNumSMs * 8));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), grid_cap(8)));
   if (cin == 1 && K == 27 && cout % 32 == 0 && cout <= 256 && yd == VP_BF16) {
     const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 17 * 4;
     ::vp::launch(conv_stem_kernel, blocks, kStemRows, smem, st, x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
@@ -330,7 +330,7 @@ static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   VP_CHECK_LAUNCH("conv_tc");
   if (part) {
     const int64_t work = p.cap_out * ND / 4;
-    ::vp::launch(split_reduce_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), kNumSMs * 8)), 256, 0, st, 
+    ::vp::launch(split_reduce_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), grid_cap(8))), 256, 0, st, 
         (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.perm, p.y, p.y_dtype);
     VP_CHECK_LAUNCH("split_reduce");
   }
@@ -502,7 +502,7 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
   if (small_fwd_ok(cin, cout, K)) return launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip,
                                                           perm, n_out_dev, cap_out, y, y_dtype, st);
   const int64_t total = cap_out * cout;
-  int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
+  int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
   ::vp::launch(conv_fwd_simt_kernel, blocks, 256, 0, st, x, x_dtype, (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout,
                                                 K, table, flip, perm, n_out_dev, cap_out, y, y_dtype);
   VP_CHECK_LAUNCH("conv_fwd_simt");
@@ -536,7 +536,7 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
     return conv_tc<true>(cout, cin, p, part, st);
   }
   const int64_t total = cap_in * cin;
-  int blocks = (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16);
+  int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
   // W^T[k, ci, co] = W[k, co, ci]: strides (k: cout*cin, "co"=ci: 1, "ci"=co: cin)
   ::vp::launch(conv_fwd_simt_kernel, blocks, 256, 0, st, g, g_dtype, (int)cout, w, w_dtype, cout * cin, 1, cin, (int)cin,
                                                 K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype);
@@ -567,18 +567,18 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, part};
     int rc = wg_tc(cin, cout, p, max_items, st);
     if (rc != VP_OK) return rc;
-    ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st, 
+    ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8)), 256, 0, st, 
         part, pptr, K, chunk, cin * cout, gw);
     VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }
   const int schunk = std::min(chunk, kWgSimtChunk);
   const int sitems = (int)(cap_pairs / schunk + K + 1);
-  const int grid = std::max(1, std::min(sitems, kNumSMs * 8));
+  const int grid = std::max(1, std::min(sitems, grid_cap(8)));
   ::vp::launch(wgrad_simt_kernel, grid, kWgSimtThreads, 0, st, x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
                                                      pptr, schunk, part);
   VP_CHECK_LAUNCH("conv_wgrad_simt");
-  ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8), 256, 0, st, 
+  ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8)), 256, 0, st, 
       part, pptr, K, schunk, cin * cout, gw);
   VP_CHECK_LAUNCH("wgrad_reduce");
   return VP_OK;
@@ -586,7 +586,7 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
 
 int vp_cast(const void* src, int32_t sd, void* dst, int32_t dd, int64_t n, vp_stream_t stream) {
   if (n <= 0) return VP_OK;
-  ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8), 256, 0, (cudaStream_t)stream, src, sd, dst,
+  ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(n, 256), grid_cap(8)), 256, 0, (cudaStream_t)stream, src, sd, dst,
                                                                                                       dd, n);
   VP_CHECK_LAUNCH("cast");
   return VP_OK;

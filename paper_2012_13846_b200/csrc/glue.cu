@@ -631,7 +631,7 @@ __global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ m, const f
   }
 }
 
-static int grid_for(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), kNumSMs * 16)); }
+static int grid_for(int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), grid_cap(16))); }
 
 }  // namespace vp
 

@@ -56,7 +56,7 @@ __global__ void hash_clear_kernel(Slot* t, uint64_t cap) {
 }
 
 int hash_clear(Slot* t, uint64_t cap, cudaStream_t st) {
-  int blocks = (int)std::min<uint64_t>((cap + 1 + 255) / 256, (uint64_t)kNumSMs * 8);
+  int blocks = (int)std::min<uint64_t>((cap + 1 + 255) / 256, (uint64_t)grid_cap(8));
   ::vp::launch(hash_clear_kernel, blocks, 256, 0, st, t, cap);
   VP_CHECK_LAUNCH("hash_clear");
   return VP_OK;
@@ -394,7 +394,7 @@ int vp_hash_build(const int64_t* keys, const int32_t* n_dev, int64_t cap_n, void
   int r = hash_clear((Slot*)table, table_cap, st);
   if (r) return r;
   if (cap_n > 0) {
-    int blocks = (int)std::min<int64_t>(ceil_div(cap_n, 256), kNumSMs * 8);
+    int blocks = (int)std::min<int64_t>(ceil_div(cap_n, 256), grid_cap(8));
     ::vp::launch(hash_build_keys_kernel, blocks, 256, 0, st, keys, n_dev, cap_n, (Slot*)table, table_cap);
     VP_CHECK_LAUNCH("hash_build");
   }
@@ -404,7 +404,7 @@ int vp_hash_build(const int64_t* keys, const int32_t* n_dev, int64_t cap_n, void
 int vp_hash_lookup(const void* table, int64_t table_cap, const int64_t* q, int64_t m,
                    int64_t* rows, vp_stream_t stream) {
   if (m <= 0) return VP_OK;
-  int blocks = (int)std::min<int64_t>(ceil_div(m, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(m, 256), grid_cap(8));
   ::vp::launch(hash_lookup_keys_kernel, blocks, 256, 0, (cudaStream_t)stream, (const Slot*)table, table_cap, q,
                                                                      m, rows);
   VP_CHECK_LAUNCH("hash_lookup");
@@ -414,7 +414,7 @@ int vp_hash_lookup(const void* table, int64_t table_cap, const int64_t* q, int64
 int vp_pack_coords(const int32_t* coords, int64_t n, int64_t* keys, int32_t* bad_dev,
                    vp_stream_t stream) {
   if (n <= 0) return VP_OK;
-  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), grid_cap(8));
   ::vp::launch(pack_coords_kernel, blocks, 256, 0, (cudaStream_t)stream, (const int4*)coords, n, keys, bad_dev);
   VP_CHECK_LAUNCH("pack_coords");
   return VP_OK;
@@ -438,7 +438,7 @@ int vp_validate_coords(const int32_t* coords, const int32_t* n_dev, int64_t cap_
   if (cap_n <= 0) return VP_OK;
   int r = hash_clear(t, cap, st);
   if (r) return r;
-  int blocks = (int)std::min<int64_t>(ceil_div(cap_n, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(cap_n, 256), grid_cap(8));
   ::vp::launch(validate_insert_kernel, blocks, 256, 0, st, (const int4*)coords, n_dev, cap_n, ts[0], ts[1], ts[2],
                                                  t, cap, flags);
   VP_CHECK_LAUNCH("validate_insert");
@@ -450,7 +450,7 @@ int vp_validate_coords(const int32_t* coords, const int32_t* n_dev, int64_t cap_
 int vp_check_finite(const void* feats, int32_t dtype, int64_t count, int32_t* flags,
                     vp_stream_t stream) {
   if (count <= 0) return VP_OK;
-  int blocks = (int)std::min<int64_t>(ceil_div(count, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(count, 256), grid_cap(8));
   ::vp::launch(finite_kernel, blocks, 256, 0, (cudaStream_t)stream, feats, dtype, count, flags);
   VP_CHECK_LAUNCH("check_finite");
   return VP_OK;
@@ -494,7 +494,7 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
   int r = hash_clear(t, cap, st);
   if (r) return r;
   cudaMemsetAsync(s1.counter, 0, 256 + tiles * 8, st);
-  int blocks = (int)std::min<int64_t>(ceil_div(cap_in, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(cap_in, 256), grid_cap(8));
   ::vp::launch(oc_insert_kernel, blocks, 256, 0, st, (const int4*)in, n_in_dev, cap_in, step[0], step[1], step[2],
                                            t, cap);
   VP_CHECK_LAUNCH("oc_insert");
@@ -554,7 +554,7 @@ int vp_voxelize(const void* points, int32_t pts_dtype, int64_t n, const int64_t*
   int r = hash_clear(t, cap, st);
   if (r) return r;
   cudaMemsetAsync(s1.counter, 0, 256 + tiles * 8, st);
-  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), grid_cap(8));
   ::vp::launch(vox_insert_kernel, blocks, 256, 0, st, points, pts_dtype, n, offs, nc, vs, res[0], res[1], res[2],
                                             t, cap, vox);
   VP_CHECK_LAUNCH("vox_insert");
@@ -597,14 +597,14 @@ int vp_voxel_mean(const void* feats_in, int32_t in_dtype, int64_t n, int32_t F, 
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "voxel_mean: workspace too small");
   if (n <= 0 || cap_vox <= 0) return VP_OK;
   cudaMemsetAsync(counts, 0, cap_vox * sizeof(int32_t), st);
-  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), grid_cap(8));
   ::vp::launch(vm_count_kernel, blocks, 256, 0, st, p2v, n, counts);
   VP_CHECK_LAUNCH("vm_count");
   ::vp::launch(vm_scan_kernel, 1, 1024, 0, st, counts, n_vox_dev, cap_vox, starts, cursor);
   VP_CHECK_LAUNCH("vm_scan");
   ::vp::launch(vm_place_kernel, blocks, 256, 0, st, p2v, n, cursor, order);
   VP_CHECK_LAUNCH("vm_place");
-  int vblocks = (int)std::min<int64_t>(ceil_div(cap_vox, 128), kNumSMs * 8);
+  int vblocks = (int)std::min<int64_t>(ceil_div(cap_vox, 128), grid_cap(8));
   ::vp::launch(vm_sum_kernel, vblocks, 128, 0, st, feats_in, in_dtype, F, order, starts, counts, n_vox_dev,
                                          cap_vox, out);
   VP_CHECK_LAUNCH("vm_sum");

@@ -432,7 +432,7 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in, co
   int r = hash_clear(t, cap, st);
   if (r) return r;
   if (cap_in > 0) {
-    int blocks = (int)std::min<int64_t>(ceil_div(cap_in, 256), kNumSMs * 8);
+    int blocks = (int)std::min<int64_t>(ceil_div(cap_in, 256), grid_cap(8));
     ::vp::launch(map_insert_kernel, blocks, 256, 0, st, (const int4*)in, n_in_dev, cap_in, t, cap);
     VP_CHECK_LAUNCH("map_insert");
   }
@@ -459,7 +459,7 @@ int vp_grid_set(const int32_t* coords, const int32_t* n_dev, int64_t cap, int32_
   VP_REQUIRE(B >= 1 && R >= 1 && s >= 1, VP_EVALIDATION, "grid: extents must be positive");
   VP_REQUIRE((int64_t)B * R * R * R < (1ll << 31), VP_EVALIDATION, "grid: B*R^3 must be < 2^31 cells");
   if (cap <= 0) return VP_OK;
-  int blocks = (int)std::min<int64_t>(ceil_div(cap, 256), kNumSMs * 8);
+  int blocks = (int)std::min<int64_t>(ceil_div(cap, 256), grid_cap(8));
   ::vp::launch(grid_set_kernel, blocks, 256, 0, (cudaStream_t)stream, (const int4*)coords, n_dev, cap, GridSpec{cells, B, R, s},
                                                           clear);
   VP_CHECK_LAUNCH("grid_set");
@@ -521,7 +521,7 @@ int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t 
   if (cap_in > 0) cudaMemsetAsync(inv, 0xff, sizeof(int32_t) * cap_in * K, st);
   VP_CHECK_ASYNC("kernel_map_inverse(memset)");
   if (cap_out > 0) {
-    int blocks = (int)std::min<int64_t>(ceil_div(cap_out * K, 256), kNumSMs * 16);
+    int blocks = (int)std::min<int64_t>(ceil_div(cap_out * K, 256), grid_cap(16));
     ::vp::launch(map_inverse_kernel, blocks, 256, 0, st, nbr, n_out_dev, cap_out, K, inv);
     VP_CHECK_LAUNCH("kernel_map_inverse");
   }

@@ -239,7 +239,7 @@ int vp_brick_set(const int32_t* coords, const int32_t* n_dev, int64_t cap, void*
   VP_REQUIRE(cap <= index_cap, VP_EVALIDATION, "brick: more rows than the index pool");
   cudaStream_t st = (cudaStream_t)stream;
   BrickSpec g = brick_spec(index, index_cap, B, R, s);
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, 256), kNumSMs * 8));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap, 256), grid_cap(8)));
   if (clear) {
     ::vp::launch(brick_clear_kernel, kNumSMs * 4, 256, 0, st, g);
     VP_CHECK_LAUNCH("brick_clear");

@@ -88,7 +88,7 @@ int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, 
   size_t tb = cub_temp_bytes(cap, K);
   char* temp = c.take<char>(tb);
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "kernel_map_sort: workspace too small");
-  const int blocks = (int)std::min<int64_t>(ceil_div(cap, 256), kNumSMs * 8);
+  const int blocks = (int)std::min<int64_t>(ceil_div(cap, 256), grid_cap(8));
   ::vp::launch(mask_keys_kernel, blocks, 256, 0, st, table, n_dev, cap, K, keys, rows);
   VP_CHECK_LAUNCH("map_sort: keys");
   // stable LSD radix sort over the K+1 key bits (deterministic)
@@ -99,7 +99,7 @@ int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, 
     int _st = ::vp::check_launch("map_sort: radix", 6);  // cub onesweep: histogram, scan, 4 digit passes
     if (_st != VP_OK) return _st;
   }
-  const int pblocks = (int)std::min<int64_t>(ceil_div(cap * K, 256), kNumSMs * 16);
+  const int pblocks = (int)std::min<int64_t>(ceil_div(cap * K, 256), grid_cap(16));
   ::vp::launch(permute_rows_kernel, pblocks, 256, 0, st, table, perm, n_dev, cap, K, table_sorted);
   VP_CHECK_LAUNCH("map_sort: permute");
   return VP_OK;
