@@ -127,6 +127,84 @@ wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* 
   }
 }
 
+// Stem weight gradient (cin = 1, bf16): gw[k][co] = sum_q g[pout[q]][co] * x[pin[q]].
+// The generic SIMT kernel walks pairs per warp with one dependent load chain
+// per channel; here every thread owns whole pairs (the COUT-wide g row in
+// registers, kWgStemPairs pairs in flight), then a fixed-order shuffle tree
+// and an ordered sum over the warps give each item's partial (deterministic).
+constexpr int kWgStemThreads = 256, kWgStemPairs = 4, kWgStemChunk = kWgStemThreads * kWgStemPairs;
+template <int COUT>
+__global__ void __launch_bounds__(kWgStemThreads)
+wgrad_stem_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gy, int K, const int32_t* __restrict__ pin,
+                  const int32_t* __restrict__ pout, const int32_t* __restrict__ pptr, float* __restrict__ part) {
+  ::vp::pdl_begin();
+  __shared__ int s_pref[VP_MAX_OFFSETS + 1];
+  __shared__ float s_red[kWgStemThreads / 32][COUT];
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < K; ++k) {
+      s_pref[k] = acc;
+      acc += (pptr[k + 1] - pptr[k] + kWgStemChunk - 1) / kWgStemChunk;
+    }
+    s_pref[K] = acc;
+  }
+  __syncthreads();
+  const int n_items = s_pref[K];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    int k = 0;
+    while (s_pref[k + 1] <= item) ++k;
+    const int p0 = pptr[k] + (item - s_pref[k]) * kWgStemChunk;
+    const int p1 = min(pptr[k + 1], p0 + kWgStemChunk);
+    float acc[COUT];
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) acc[c] = 0.f;
+    uint4 row[kWgStemPairs][COUT / 8];
+    float xv[kWgStemPairs];
+#pragma unroll
+    for (int j = 0; j < kWgStemPairs; ++j) {
+      const int q = p0 + j * kWgStemThreads + threadIdx.x;
+      xv[j] = 0.f;
+#pragma unroll
+      for (int t = 0; t < COUT / 8; ++t) row[j][t] = make_uint4(0u, 0u, 0u, 0u);
+      if (q < p1) {
+        const int64_t o = pout[q];
+        xv[j] = __bfloat162float(x[pin[q]]);
+        const uint4* src = reinterpret_cast<const uint4*>(gy + o * COUT);
+#pragma unroll
+        for (int t = 0; t < COUT / 8; ++t) row[j][t] = __ldg(src + t);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kWgStemPairs; ++j)
+#pragma unroll
+      for (int t = 0; t < COUT / 8; ++t) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&row[j][t]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = __bfloat1622float2(h[u]);
+          acc[t * 8 + 2 * u] += f.x * xv[j];
+          acc[t * 8 + 2 * u + 1] += f.y * xv[j];
+        }
+      }
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) {
+      float v = acc[c];
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+      if (lane == 0) s_red[warp][c] = v;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < COUT; c += kWgStemThreads) {
+      float v = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < kWgStemThreads / 32; ++w2) v += s_red[w2][c];
+      part[(int64_t)item * COUT + c] = v;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void transpose_w_kernel(const void* __restrict__ w, int w_dtype, int K, int cout, int cin,
                                    bf16* __restrict__ wt) {
   ::vp::pdl_begin();
@@ -569,6 +647,23 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     if (rc != VP_OK) return rc;
     ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8)), 256, 0, st, 
         part, pptr, K, chunk, cin * cout, gw);
+    VP_CHECK_LAUNCH("wgrad_reduce");
+    return VP_OK;
+  }
+  if (cin == 1 && (cout == 16 || cout == 32 || cout == 64) && x_dtype == VP_BF16 && g_dtype == VP_BF16) {
+    // kWgStemChunk >= kWgSimtChunk: fewer items than the workspace is sized for
+    const int items = (int)(cap_pairs / kWgStemChunk + K + 1);
+    const int grid = std::max(1, std::min(items, grid_cap(8)));
+    const bf16 *xb = (const bf16*)x, *gb = (const bf16*)g;
+    if (cout == 16)
+      ::vp::launch(wgrad_stem_kernel<16>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
+    else if (cout == 32)
+      ::vp::launch(wgrad_stem_kernel<32>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
+    else
+      ::vp::launch(wgrad_stem_kernel<64>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
+    VP_CHECK_LAUNCH("conv_wgrad_stem");
+    ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8)), 256, 0, st, part, pptr,
+                 K, kWgStemChunk, cin * cout, gw);
     VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }

@@ -107,13 +107,15 @@ def test_tc_widths(cin, cout, stride):
     assert np.abs(gw.cpu().numpy() - rgw).max() <= 1e-4 * scale_w
 
 
-def test_stem_cin1_simt():
-    """C_in = 1 (occupancy stem) goes through the SIMT kernels."""
+@pytest.mark.parametrize("cout,clouds,npts", [(32, 2, 500), (16, 2, 500), (64, 2, 500), (32, 6, 3000)])
+def test_stem_cin1_simt(cout, clouds, npts):
+    """C_in = 1 (occupancy stem) goes through the SIMT kernels (wgrad: the
+    stem kernel, several pair chunks per offset in the large case)."""
     from paper_2012_13846_b200 import conv
-    pts, offs = O.synthetic_batch(2, 500, 32, seed=9, dtype=np.float64)
-    coords, feats = O.voxelize_batch(pts, offs, 1.0, 32)
+    pts, offs = O.synthetic_batch(clouds, npts, 32 if clouds == 2 else 48, seed=9, dtype=np.float64)
+    coords, feats = O.voxelize_batch(pts, offs, 1.0, 32 if clouds == 2 else 48)
     rng = np.random.default_rng(5)
-    w = (rng.normal(size=(27, 32, 1)) / np.sqrt(27)).astype(np.float32)
+    w = (rng.normal(size=(27, cout, 1)) / np.sqrt(27)).astype(np.float32)
     for dt, rel in ((torch.float32, 1e-5), (torch.bfloat16, 1e-2)):
         t, W, shape, y = run_layer(coords, feats, w, 1, dt)
         wr = w.astype(np.float64) if dt == torch.float32 else bf16_round(w)
