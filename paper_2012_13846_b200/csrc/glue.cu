@@ -57,6 +57,47 @@ __device__ __forceinline__ void stv(void* p, int dtype_rt, int64_t i, const floa
   }
 }
 
+// Raw row vectors: a batch of loads is issued into these before any of it is
+// converted (bf16 rows stay packed: 4 registers per 8 channels), so deep
+// batches fit in registers.  Generic dtypes convert at load.
+template <int VEC, int DT>
+struct RawVec {
+  float v[VEC];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) v[q] = 0.f;
+  }
+  __device__ __forceinline__ void load(const void* p, int dt, int64_t i) { ldv<VEC, DT>(p, dt, i, v); }
+  __device__ __forceinline__ void get(float* o) const {
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) o[q] = v[q];
+  }
+};
+template <>
+struct RawVec<8, VP_BF16> {
+  uint4 r;
+  __device__ __forceinline__ void zero() { r = make_uint4(0u, 0u, 0u, 0u); }
+  __device__ __forceinline__ void load(const void* p, int, int64_t i) {
+    r = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p) + i);
+  }
+  __device__ __forceinline__ void get(float* o) const {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h[q]);
+      o[2 * q] = f.x;
+      o[2 * q + 1] = f.y;
+    }
+  }
+};
+// rows per batch: deeper for the packed bf16 rows
+template <int VEC, int DT>
+struct BnDepth {
+  static constexpr int stats = (VEC == 8 && DT == VP_BF16) ? 8 : 4;
+  static constexpr int bwd = (VEC == 8 && DT == VP_BF16) ? 4 : 2;
+  static constexpr int apply = (VEC == 8 && DT == VP_BF16) ? 4 : 2;
+};
+
 // Fused BN (one cooperative launch): after the statistics, every block waits
 // for the last block's result (epoch flag) and applies the normalisation to
 // its rows.  mode 0 = statistics only, 1 = forward apply, 2 = backward apply.
@@ -222,25 +263,25 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
       // block b owns row groups b, b+G, b+2G, ... (G = gridDim.x, fixed per
       // capacity) -> balanced for any live n, fixed summation order.  Rows
       // are loaded in batches of 4 (all loads issued before the first add).
-      for (int64_t r0 = (int64_t)blockIdx.x * lanes + lr; r0 < n; r0 += 4 * stride) {
-        float v[4][VEC];
+      constexpr int U = BnDepth<VEC, DT>::stats;
+      for (int64_t r0 = (int64_t)blockIdx.x * lanes + lr; r0 < n; r0 += U * stride) {
+        RawVec<VEC, DT> rv[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int64_t r = r0 + u * stride;
-          if (r < n) {
-            ldv<VEC, DT>(x, dtype, r * C + c0, v[u]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) v[u][q] = 0.f;
-          }
+          rv[u].zero();
+          if (r < n) rv[u].load(x, dtype, r * C + c0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < U; ++u) {
+          float v[VEC];
+          rv[u].get(v);
 #pragma unroll
           for (int q = 0; q < VEC; ++q) {
-            a[q] += v[u][q];
-            b[q] += v[u][q] * v[u][q];
+            a[q] += v[q];
+            b[q] += v[q] * v[q];
           }
+        }
       }
     } else {
 #pragma unroll
@@ -248,32 +289,70 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
         mu[q] = mean[c0 + q];
         rs[q] = rstd[c0 + q];
       }
-      for (int64_t r0 = (int64_t)blockIdx.x * lanes + lr; r0 < n; r0 += 2 * stride) {
-        float g[2][VEC], g2[2][VEC], yy[2][VEC], xv[2][VEC];
+      constexpr int U = BnDepth<VEC, DT>::bwd;
+      for (int64_t r0 = (int64_t)blockIdx.x * lanes + lr; r0 < n; r0 += U * stride) {
+        RawVec<VEC, DT> rg[U], rg2[U], ry[U], rx[U];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int64_t r = r0 + u * stride;
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) g[u][q] = g2[u][q] = yy[u][q] = xv[u][q] = 0.f;
+          rg[u].zero();
+          rg2[u].zero();
+          ry[u].zero();
+          rx[u].zero();
           if (r < n) {
-            ldv<VEC, DT>(gy, gy_dtype, r * C + c0, g[u]);
-            if (gy2) ldv<VEC, DT>(gy2, gy_dtype, r * C + c0, g2[u]);
-            if (relu) ldv<VEC, DT>(y, y_dtype, r * C + c0, yy[u]);
-            ldv<VEC, DT>(x, dtype, r * C + c0, xv[u]);
+            rg[u].load(gy, gy_dtype, r * C + c0);
+            if (gy2) rg2[u].load(gy2, gy_dtype, r * C + c0);
+            if (relu) ry[u].load(y, y_dtype, r * C + c0);
+            rx[u].load(x, dtype, r * C + c0);
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < U; ++u) {
+          float g[VEC], g2[VEC], yy[VEC], xv[VEC];
+          rg[u].get(g);
+          rg2[u].get(g2);
+          ry[u].get(yy);
+          rx[u].get(xv);
 #pragma unroll
           for (int q = 0; q < VEC; ++q) {
-            const float gs = gy2 ? g[u][q] + g2[u][q] : g[u][q];
-            const float gq = (relu && yy[u][q] <= 0.f) ? 0.f : gs;
+            const float gs = gy2 ? g[q] + g2[q] : g[q];
+            const float gq = (relu && yy[q] <= 0.f) ? 0.f : gs;
             a[q] += gq;
-            b[q] += gq * (xv[u][q] - mu[q]) * rs[q];
+            b[q] += gq * (xv[q] - mu[q]) * rs[q];
           }
+        }
       }
     }
   }
+  if (tpr <= 32 && 32 % tpr == 0) {
+    // whole rows per warp: fixed xor tree over the warp's rows, then the 8
+    // warps' sums in order (all threads busy instead of C serial sums)
+#pragma unroll
+    for (int q = 0; q < VEC; ++q)
+      for (int m = tpr; m < 32; m <<= 1) {
+        a[q] += __shfl_xor_sync(0xffffffffu, a[q], m);
+        b[q] += __shfl_xor_sync(0xffffffffu, b[q], m);
+      }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane < tpr) {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        s_a[warp * C + lane * VEC + q] = a[q];
+        s_b[warp * C + lane * VEC + q] = b[q];
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < C; e += kGlueThreads) {
+      float sa = 0.f, sb = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < kGlueThreads / 32; ++w2) {
+        sa += s_a[w2 * C + e];
+        sb += s_b[w2 * C + e];
+      }
+      part[((int64_t)blockIdx.x * 2) * C + e] = sa;
+      part[((int64_t)blockIdx.x * 2 + 1) * C + e] = sb;
+    }
+  } else {
 #pragma unroll
   for (int q = 0; q < VEC; ++q) {
     s_a[threadIdx.x * VEC + q] = a[q];
@@ -290,6 +369,7 @@ bn_partial_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, i
     }
     part[((int64_t)blockIdx.x * 2) * C + e] = sa;
     part[((int64_t)blockIdx.x * 2 + 1) * C + e] = sb;
+  }
   }
   // ticket == null: the consumer kernel reduces the partials (bn_finalize in
   // every one of its blocks) -> no fence / ticket / serial tail here.
@@ -340,27 +420,33 @@ __device__ __forceinline__ void bn_apply_rows(const void* __restrict__ x, int dt
     sh[q] = beta[c0 + q] - mean[c0 + q] * sc[q];
   }
   const int64_t stride = (int64_t)nblk * lanes;
-  for (int64_t r0 = (int64_t)blk * lanes + lr; r0 < n; r0 += 2 * stride) {
-    float v[2][VEC], rv[2][VEC];
+  constexpr int U = BnDepth<VEC, DT>::apply;
+  for (int64_t r0 = (int64_t)blk * lanes + lr; r0 < n; r0 += U * stride) {
+    RawVec<VEC, DT> rx[U], rr[U];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * stride;
+      rx[u].zero();
+      rr[u].zero();
       if (r < n) {
-        ldv<VEC, DT>(x, dtype, r * C + c0, v[u]);
-        if (res) ldv<VEC, DT>(res, res_dtype, r * C + c0, rv[u]);
+        rx[u].load(x, dtype, r * C + c0);
+        if (res) rr[u].load(res, res_dtype, r * C + c0);
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * stride;
       if (r >= n) break;
+      float v[VEC], rv[VEC];
+      rx[u].get(v);
+      rr[u].get(rv);
 #pragma unroll
       for (int q = 0; q < VEC; ++q) {
-        float o = v[u][q] * sc[q] + sh[q];
-        if (res) o += rv[u][q];
-        v[u][q] = relu ? fmaxf(o, 0.f) : o;
+        float o = v[q] * sc[q] + sh[q];
+        if (res) o += rv[q];
+        v[q] = relu ? fmaxf(o, 0.f) : o;
       }
-      stv<VEC, DT>(y, y_dtype, r * C + c0, v[u]);
+      stv<VEC, DT>(y, y_dtype, r * C + c0, v);
     }
   }
 }
@@ -414,31 +500,41 @@ __device__ __forceinline__ void bn_backward_apply_rows(
     k3[q] = inv_n * ggamma[c];
   }
   const int64_t stride = (int64_t)nblk * lanes;
-  for (int64_t r0 = (int64_t)blk * lanes + lr; r0 < n; r0 += 2 * stride) {
-    float g[2][VEC], g2[2][VEC], yy[2][VEC], xv[2][VEC];
+  constexpr int U = BnDepth<VEC, DT>::apply;
+  for (int64_t r0 = (int64_t)blk * lanes + lr; r0 < n; r0 += U * stride) {
+    RawVec<VEC, DT> rg[U], rg2[U], ry[U], rx[U];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * stride;
+      rg[u].zero();
+      rg2[u].zero();
+      ry[u].zero();
+      rx[u].zero();
       if (r < n) {
-        ldv<VEC, DT>(gy, gy_dtype, r * C + c0, g[u]);
-        if (gy2) ldv<VEC, DT>(gy2, gy_dtype, r * C + c0, g2[u]);
-        if (relu) ldv<VEC, DT>(y, y_dtype, r * C + c0, yy[u]);
-        ldv<VEC, DT>(x, x_dtype, r * C + c0, xv[u]);
+        rg[u].load(gy, gy_dtype, r * C + c0);
+        if (gy2) rg2[u].load(gy2, gy_dtype, r * C + c0);
+        if (relu) ry[u].load(y, y_dtype, r * C + c0);
+        rx[u].load(x, x_dtype, r * C + c0);
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * stride;
       if (r >= n) break;
+      float g[VEC], g2[VEC], yy[VEC], xv[VEC];
+      rg[u].get(g);
+      rg2[u].get(g2);
+      ry[u].get(yy);
+      rx[u].get(xv);
 #pragma unroll
       for (int q = 0; q < VEC; ++q) {
-        if (gy2) g[u][q] += g2[u][q];
-        if (relu && yy[u][q] <= 0.f) g[u][q] = 0.f;
-        const float xh = (xv[u][q] - mu[q]) * rs[q];
-        xv[u][q] = k1[q] * (g[u][q] - k2[q] - xh * k3[q]);
+        if (gy2) g[q] += g2[q];
+        if (relu && yy[q] <= 0.f) g[q] = 0.f;
+        const float xh = (xv[q] - mu[q]) * rs[q];
+        xv[q] = k1[q] * (g[q] - k2[q] - xh * k3[q]);
       }
-      stv<VEC, DT>(gx, gx_dtype, r * C + c0, xv[u]);
-      if (gres) stv<VEC, DT>(gres, gx_dtype, r * C + c0, g[u]);
+      stv<VEC, DT>(gx, gx_dtype, r * C + c0, xv);
+      if (gres) stv<VEC, DT>(gres, gx_dtype, r * C + c0, g);
     }
   }
 }
