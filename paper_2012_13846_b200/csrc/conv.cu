@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "conv_fwd_tc.cuh"
+#include "conv_rows.cuh"
 #include "conv_wgrad_tc.cuh"
 #include "tc.cuh"
 
@@ -358,6 +359,33 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
   }
 }
 
+// 32-wide sparse levels: the row-compacted mma.sync kernel (conv_rows.cuh)
+// instead of the tcgen05 tile.  Opt-in (VP_CONV_ROWS=1): measured 2.1-2.3x
+// slower at C3 (8 warps/SM with ~100-instruction dependent chains per offset;
+// DESIGN.md §10), kept as the starting point for a compacted path.
+static bool rows32_ok(int64_t cin, int64_t cout, int K) {
+  static const bool on = getenv("VP_CONV_ROWS") && atoi(getenv("VP_CONV_ROWS")) == 1;
+  return on && cin == 32 && cout == 32 && K <= 27;
+}
+
+template <bool WT>
+static int launch_rows32(const bf16* x, const bf16* w, int K, const int32_t* table, int flip, const int32_t* perm,
+                         const int32_t* n_out_dev, int64_t cap_out, void* y, int yd, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    VP_REQUIRE(cudaFuncSetAttribute(conv_rows32_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    RowsSmem::TOTAL) == cudaSuccess,
+               VP_EINTERNAL, "conv_rows32: cannot reserve shared memory");
+    attr = true;
+  }
+  const int64_t slices = ceil_div(cap_out, 32);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(slices, kRowsWarps), kNumSMs));
+  ::vp::launch(conv_rows32_kernel<WT>, grid, kRowsWarps * 32, RowsSmem::TOTAL, st, x, w, K, table, flip, perm,
+               n_out_dev, cap_out, y, yd);
+  VP_CHECK_LAUNCH("conv_rows32");
+  return VP_OK;
+}
+
 static bool small_fwd_ok(int64_t cin, int64_t cout, int K) { return cin <= 4 && (int64_t)K * cin * cout <= 12288; }
 
 static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int wd, int cout, int K,
@@ -586,6 +614,8 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
       wb = (const bf16*)ws;
     }
     (void)x_rows;  // the cp.async gather zero-fills missing neighbours itself
+    if (rows32_ok(cin, cout, K))
+      return launch_rows32<false>((const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, st);
     FwdParams p{(const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
     return conv_tc<false>(cin, cout, p, part, st);
   }
@@ -622,6 +652,8 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
     }
     // grad_in = sum_k W_k^T g[table]: GEMM K-dim = C_out, N = C_in, W read as MN-major B
     (void)g_rows;
+    if (rows32_ok(cout, cin, K))
+      return launch_rows32<true>((const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, st);
     FwdParams p{(const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1, 0, 0};
     return conv_tc<true>(cout, cin, p, part, st);
   }

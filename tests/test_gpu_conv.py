@@ -321,3 +321,20 @@ def test_kernel_shapes_dims_and_strides(name, stride, dtype):
         bgw[k] = np.abs(gr[ui]).T @ np.abs(xr[vi])
     assert (np.abs(gi.float().cpu().numpy() - rgi) <= rel * bgi + 1e-6).all()
     assert (np.abs(gw.cpu().numpy() - rgw) <= 1e-5 * bgw + 1e-6).all()
+
+
+def test_rows32_kernel_opt_in():
+    """The opt-in row-compacted 32-wide kernel (VP_CONV_ROWS=1, read once per
+    process -> a child pytest) passes the same fwd/dgrad/wgrad checks as the
+    tcgen05 path for C_in = C_out = 32 at stride 1 and 2."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VP_CONV_ROWS="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(root, "tests", "test_gpu_conv.py"),
+                        "-k", "test_tc_widths and 32-32"], capture_output=True, text=True, timeout=600, cwd=root,
+                       env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "2 passed" in r.stdout
