@@ -302,7 +302,14 @@ conv_fwd_small_kernel(const void* __restrict__ x, int x_dtype, int cin, const vo
 // accumulates 32 outputs per pass against broadcast weights, and the bf16
 // output tile is written back through shared memory with coalesced stores.
 constexpr int kStemRows = 128;
-__global__ void __launch_bounds__(kStemRows)
+// XT: input and weight dtype fixed at compile time (-1 = runtime), so the 27
+// gathers of a row are independent loads in flight rather than a chain of
+// dtype branches
+// 16 output channels per pass keeps a thread at <= 64 registers: 8 CTAs per
+// SM, so C3's ~900 tiles run as one wave (at 128 registers they took two).
+constexpr int kStemPass = 16;
+template <int XT>
+__global__ void __launch_bounds__(kStemRows, 8)
 conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict__ w, int w_dtype, int cout,
                  const int32_t* __restrict__ table, int flip, const int32_t* __restrict__ perm,
                  const int32_t* n_out_dev, int64_t cap_out, __nv_bfloat16* __restrict__ y) {
@@ -310,10 +317,15 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
   extern __shared__ float s_mem[];
   float* s_w = s_mem;                                             // [27][cout]
   int* s_t = reinterpret_cast<int*>(s_w + 27 * cout);             // [128][27]
-  uint32_t* s_o = reinterpret_cast<uint32_t*>(s_t + kStemRows * 27);  // [128][16 + 1] packed bf16 pairs
+  uint32_t* s_o = reinterpret_cast<uint32_t*>(s_t + kStemRows * 27);  // [128][8 + 1] packed bf16 pairs
+#pragma unroll 8
   for (int e = threadIdx.x; e < 27 * cout; e += kStemRows) {
-    const int k = e / cout, co = e - k * cout;
-    s_w[e] = ldf(w, w_dtype, (int64_t)k * cout + co);
+    if (XT == VP_BF16)
+      s_w[e] = __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(w) + e));
+    else if (XT == VP_F32)
+      s_w[e] = __ldg(reinterpret_cast<const float*>(w) + e);
+    else
+      s_w[e] = ldf(w, w_dtype, e);
   }
   const int n_out = load_count(n_out_dev, cap_out);
   const int ntiles = (n_out + kStemRows - 1) / kStemRows;
@@ -322,37 +334,59 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
     const int rows = min(kStemRows, (int)(n_out - u0));
     __syncthreads();
     const int32_t* tb = table + u0 * 27;
+    if ((reinterpret_cast<uintptr_t>(table) & 15) == 0) {
+      // 16 B loads, all in flight (a tile's table is 864 int4)
+      const int n4 = rows * 27 / 4;
+#pragma unroll
+      for (int j = 0; j < (kStemRows * 27 / 4 + kStemRows - 1) / kStemRows; ++j) {
+        const int e = threadIdx.x + j * kStemRows;
+        if (e < n4) reinterpret_cast<int4*>(s_t)[e] = __ldg(reinterpret_cast<const int4*>(tb) + e);
+      }
+      for (int e = n4 * 4 + threadIdx.x; e < rows * 27; e += kStemRows) s_t[e] = __ldg(tb + e);
+    } else {
 #pragma unroll 4
-    for (int e = threadIdx.x; e < rows * 27; e += kStemRows) s_t[e] = __ldg(tb + e);
+      for (int e = threadIdx.x; e < rows * 27; e += kStemRows) s_t[e] = __ldg(tb + e);
+    }
     __syncthreads();
     float xk[27];
     const bool valid = threadIdx.x < rows;
 #pragma unroll
     for (int k = 0; k < 27; ++k) {
       const int v = valid ? s_t[threadIdx.x * 27 + (flip ? 26 - k : k)] : -1;
-      xk[k] = v >= 0 ? ldf(x, x_dtype, v) : 0.f;
+      if (XT == VP_BF16)
+        xk[k] = v >= 0 ? __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(x) + v)) : 0.f;
+      else if (XT == VP_F32)
+        xk[k] = v >= 0 ? __ldg(reinterpret_cast<const float*>(x) + v) : 0.f;
+      else
+        xk[k] = v >= 0 ? ldf(x, x_dtype, v) : 0.f;
     }
-    for (int c0 = 0; c0 < cout; c0 += 32) {
-      float acc[32];
+    for (int c0 = 0; c0 < cout; c0 += kStemPass) {
+      float acc[kStemPass];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+      for (int c = 0; c < kStemPass; ++c) acc[c] = 0.f;
 #pragma unroll
       for (int k = 0; k < 27; ++k) {
-        const float* wr = s_w + k * cout + c0;
+        const float4* wr = reinterpret_cast<const float4*>(s_w + k * cout + c0);  // broadcast, 16 B aligned
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] += wr[c] * xk[k];
+        for (int q = 0; q < kStemPass / 4; ++q) {
+          const float4 w4 = wr[q];
+          acc[4 * q] += w4.x * xk[k];
+          acc[4 * q + 1] += w4.y * xk[k];
+          acc[4 * q + 2] += w4.z * xk[k];
+          acc[4 * q + 3] += w4.w * xk[k];
+        }
       }
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < kStemPass / 2; ++c) {
         __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * c], acc[2 * c + 1]);
-        s_o[threadIdx.x * 17 + c] = *reinterpret_cast<uint32_t*>(&h);
+        s_o[threadIdx.x * 9 + c] = *reinterpret_cast<uint32_t*>(&h);
       }
       __syncthreads();
-      // coalesced: word e of the tile -> row e / 16, pair e % 16
-      for (int e = threadIdx.x; e < rows * 16; e += kStemRows) {
-        const int rr = e >> 4, c = e & 15;
+      // coalesced: word e of the tile -> row e / 8, pair e % 8
+      for (int e = threadIdx.x; e < rows * 8; e += kStemRows) {
+        const int rr = e >> 3, c = e & 7;
         const int64_t orow = perm ? (int64_t)__ldg(perm + u0 + rr) : u0 + rr;
-        reinterpret_cast<uint32_t*>(y + orow * cout + c0)[c] = s_o[rr * 17 + c];
+        reinterpret_cast<uint32_t*>(y + orow * cout + c0)[c] = s_o[rr * 9 + c];
       }
       __syncthreads();
     }
@@ -393,9 +427,11 @@ static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int w
                             int64_t cap_out, void* y, int yd, cudaStream_t st) {
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), grid_cap(8)));
   if (cin == 1 && K == 27 && cout % 32 == 0 && cout <= 256 && yd == VP_BF16) {
-    const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 17 * 4;
-    ::vp::launch(conv_stem_kernel, blocks, kStemRows, smem, st, x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
-                                                      (__nv_bfloat16*)y);
+    const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 9 * 4;
+    const int dt = xd == wd ? xd : -1;
+    auto kern = dt == VP_BF16 ? conv_stem_kernel<VP_BF16> : dt == VP_F32 ? conv_stem_kernel<VP_F32> : conv_stem_kernel<-1>;
+    ::vp::launch(kern, blocks, kStemRows, smem, st, x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
+                 (__nv_bfloat16*)y);
     VP_CHECK_LAUNCH("conv_stem");
     return VP_OK;
   }
