@@ -456,7 +456,8 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_
     const int n = (int)(idx - r * ND);
     const int tile = (int)(r >> 7), lr = (int)(r & 127);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < S; ++s) {
+#pragma unroll 4
+    for (int s = 0; s < S; ++s) {  // loads batched, sums stay in split order
       const float4 v = *reinterpret_cast<const float4*>(part + (((int64_t)s * ntiles + tile) * 128 + lr) * ND + n);
       acc.x += v.x;
       acc.y += v.y;
