@@ -621,6 +621,7 @@ __global__ void batch_starts_kernel(const int32_t* counts, int B, int32_t* start
 }
 // rows are batch-contiguous (voxelize+batch order, preserved by first-seen
 // downsampling): segment b = [starts[b], starts[b]+counts[b]).
+template <int DT>  // x dtype at compile time (-1: runtime) so the row loads batch
 __global__ void pool_kernel(const void* __restrict__ x, int dtype, int C, int B, const int32_t* counts,
                             const int32_t* starts, float* out) {
   ::vp::pdl_begin();
@@ -628,7 +629,13 @@ __global__ void pool_kernel(const void* __restrict__ x, int dtype, int C, int B,
     const int s = starts[b], cnt = counts[b];
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
       float acc = 0.f;
-      for (int r = 0; r < cnt; ++r) acc += ldf(x, dtype, (int64_t)(s + r) * C + c);
+#pragma unroll 8
+      for (int r = 0; r < cnt; ++r) {
+        const int64_t i = (int64_t)(s + r) * C + c;
+        acc += DT == VP_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(x)[i])
+               : DT == VP_F32 ? reinterpret_cast<const float*>(x)[i]
+                              : ldf(x, dtype, i);
+      }
       out[(int64_t)b * C + c] = cnt > 0 ? acc / (float)cnt : 0.f;
     }
   }
@@ -656,14 +663,27 @@ __global__ void xent_sample_kernel(const float* __restrict__ pooled, int B, int 
                                    float* logits, float* g_logits, float* loss_b, float* g_pooled) {
   ::vp::pdl_begin();
   extern __shared__ float sm[];
-  float* s_logit = sm;  // classes
+  float* s_logit = sm;            // classes
+  float* s_g = sm + classes;      // classes: this sample's g_logits
+  float* s_x = sm + 2 * classes;  // C: this sample's pooled row
   __shared__ float s_max, s_sum;
   const int b = blockIdx.x;
-  for (int j = threadIdx.x; j < classes; j += blockDim.x) {
-    float acc = bias[j];
-    for (int c = 0; c < C; ++c) acc += w[(int64_t)j * C + c] * pooled[(int64_t)b * C + c];
-    s_logit[j] = acc;
-    logits[(int64_t)b * classes + j] = acc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) s_x[c] = pooled[(int64_t)b * C + c];
+  __syncthreads();
+  // logits: a warp per class, lanes stride the channels (coalesced W row),
+  // fixed xor tree -> deterministic
+  for (int j = warp; j < classes; j += nw) {
+    float acc = 0.f;
+#pragma unroll 4
+    for (int c = lane; c < C; c += 32) acc += w[(int64_t)j * C + c] * s_x[c];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (lane == 0) {
+      const float v = acc + bias[j];
+      s_logit[j] = v;
+      logits[(int64_t)b * classes + j] = v;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -679,13 +699,16 @@ __global__ void xent_sample_kernel(const float* __restrict__ pooled, int B, int 
   __syncthreads();
   const int lab = labels[b];
   for (int j = threadIdx.x; j < classes; j += blockDim.x) {
-    float p = expf(s_logit[j] - s_max) / s_sum;
-    g_logits[(int64_t)b * classes + j] = (p - (j == lab ? 1.f : 0.f)) / (float)B;
+    const float p = expf(s_logit[j] - s_max) / s_sum;
+    const float gj = (p - (j == lab ? 1.f : 0.f)) / (float)B;
+    s_g[j] = gj;
+    g_logits[(int64_t)b * classes + j] = gj;
   }
   __syncthreads();
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float acc = 0.f;
-    for (int j = 0; j < classes; ++j) acc += g_logits[(int64_t)b * classes + j] * w[(int64_t)j * C + c];
+#pragma unroll 8
+    for (int j = 0; j < classes; ++j) acc += s_g[j] * w[(int64_t)j * C + c];
     g_pooled[(int64_t)b * C + c] = acc;
   }
 }
@@ -701,6 +724,7 @@ __global__ void xent_reduce_kernel(const float* __restrict__ pooled, int B, int 
     const int c = (int)(e - (int64_t)j * (C + 1));
     float acc = 0.f;
     if (c < C) {
+#pragma unroll 8
       for (int b = 0; b < B; ++b) acc += g_logits[(int64_t)b * classes + j] * pooled[(int64_t)b * C + c];
       g_w[(int64_t)j * C + c] = acc;
     } else {
@@ -880,7 +904,8 @@ int vp_global_pool(const void* x, int32_t xd, const int32_t* coords, const int32
   }
   ::vp::launch(batch_starts_kernel, 1, 1024, 0, st, counts, B, starts);
   VP_CHECK_LAUNCH("batch_starts");
-  ::vp::launch(pool_kernel, std::min(B, kNumSMs * 4), C < 256 ? (int)C : 256, 0, st, x, xd, (int)C, B, counts, starts, out);
+  auto pk = xd == VP_BF16 ? pool_kernel<VP_BF16> : xd == VP_F32 ? pool_kernel<VP_F32> : pool_kernel<-1>;
+  ::vp::launch(pk, std::min(B, kNumSMs * 4), C < 256 ? (int)C : 256, 0, st, x, xd, (int)C, B, counts, starts, out);
   VP_CHECK_LAUNCH("pool");
   return VP_OK;
 }
@@ -903,7 +928,7 @@ int vp_linear_xent(const float* pooled, int32_t B, int32_t C, const float* w, co
   VP_REQUIRE(ws_bytes >= vp_linear_xent_ws_bytes(B, classes), VP_EVALIDATION, "linear_xent: workspace too small");
   float* g_logits = (float*)ws;
   float* loss_b = g_logits + (size_t)B * classes;
-  ::vp::launch(xent_sample_kernel, B, 128, classes * sizeof(float), st, pooled, B, C, w, b, classes, labels, logits, g_logits,
+  ::vp::launch(xent_sample_kernel, B, 256, (2 * classes + C) * sizeof(float), st, pooled, B, C, w, b, classes, labels, logits, g_logits,
                                                              loss_b, g_pooled);
   VP_CHECK_LAUNCH("xent_sample");
   ::vp::launch(xent_reduce_kernel, grid_for((int64_t)classes * (C + 1)), 256, 0, st, pooled, B, C, classes, g_logits, loss_b,
