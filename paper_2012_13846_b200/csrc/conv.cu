@@ -465,7 +465,9 @@ static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * kMaxSplit, (int64_t)kNumSMs * CPS));
   FwdParams p = p0;
   p.part = (float*)part;
-  p.max_split = part ? kMaxSplit : 1;
+  static const int max_split = getenv("VP_CONV_MAX_SPLIT") ? std::max(1, std::min(kMaxSplit, atoi(getenv("VP_CONV_MAX_SPLIT"))))
+                                                          : kMaxSplit;  // tuning
+  p.max_split = part ? max_split : 1;
   p.stage_tbl = tbl;
   static const int dbg = getenv("VP_CONV_DBG") ? atoi(getenv("VP_CONV_DBG")) : 0;
   p.dbg = dbg;
