@@ -507,14 +507,16 @@ def _time_launch(launch, iters):
     return a.elapsed_time(b) / iters / 1e3
 
 
-def _ncu_traffic(kernel_key):
-    """dram read+write bytes per launch of `kernel_key` from the committed ncu
-    --set full summary (profiles/ncu_traffic.json), else None."""
+def _ncu_traffic(kernel_key, layer=None):
+    """dram read+write bytes per launch of `kernel_key` (for `layer` when that
+    layer was captured) from the committed ncu --set full summaries
+    (profiles/ncu_traffic.json), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel_key)
+            t = json.load(f)
     except (OSError, ValueError):
         return None
+    return t.get(f"{kernel_key} {layer}", t.get(kernel_key))
 
 
 def roofline(tr, dev, iters=30):
@@ -560,7 +562,7 @@ def roofline(tr, dev, iters=30):
     key = f"conv_fwd_tc<{L['cin']},{L['cout']}>"
     out = {"kernel": f"{key} layer {L['name']} (N_out={n_out}, pairs={P})", "bound": bound,
            "achieved": round(ach, 2), "peak": peak, "unit": unit, "frac": round(ach / peak, 4),
-           "traffic": _ncu_traffic(key), "peak_source": src, "us_per_launch": round(t * 1e6, 2),
+           "traffic": _ncu_traffic(key, L["name"]), "peak_source": src, "us_per_launch": round(t * 1e6, 2),
            "algorithmic_flops": fl, "algorithmic_bytes": byts, "tflops": round(tflops, 2), "gbs": round(gbs, 1),
            "per_layer_fwd_us": {l["name"]: round(tt * 1e6, 1) for tt, l in rows}}
     # kernel-map builder as the step runs it, level 0 stride-1: index insert
