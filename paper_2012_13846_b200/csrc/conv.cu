@@ -49,8 +49,7 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, const int32_
     const int k = (int)(e / per);
     const int64_t o = e - (int64_t)k * per;
     float acc = 0.f;
-#pragma unroll 4
-    for (int it = s_pref[k]; it < s_pref[k + 1]; ++it) acc += part[(int64_t)it * per + o];  // loads batched, order kept
+    for (int it = s_pref[k]; it < s_pref[k + 1]; ++it) acc += part[(int64_t)it * per + o];
     gw[e] = acc;
   }
 }
