@@ -40,7 +40,7 @@ struct FwdParams {
   float* part;    // split-K partials (grid * 128 * ND floats), may be null if max_split == 1
   int max_split;  // >= 1
   int stage_tbl;  // stage table tiles in smem (K <= kTblK, 16 B-aligned table); set by the launcher
-  int dbg;        // experiments only: bit0 no MMA, bit1 no B copies, bit2 no A copies, bit3 plain arrive for empty
+  int dbg;        // experiments only: bit0 no MMA, bit1 no B copies, bit2 no A copies, bit3 plain arrive for empty, bit4 every offset active (no mask scan)
 };
 
 constexpr int kTcProd = 128, kTcEpi = 128, kTcThreads = kTcProd + kTcEpi + 32;
@@ -188,7 +188,14 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (tid < kTcMaskWords) s_mask[tid] = 0;
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tbl) {
+      if (tbl && (p.dbg & 16)) {  // experiment: every offset active, no scan
+        tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);
+        if (rows < TR) {
+          int32_t* tw = s_tbl + (ii & 1) * TR * K;
+          for (int e = rows * K + tid; e < TR * K; e += kTcProd) tw[e] = -1;
+        }
+        if (tid == 0) s_mask[0] = K >= 32 ? 0xffffffffu : (1u << K) - 1u;
+      } else if (tbl) {
         tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);
         if (rows < TR) {  // ragged last tile: rows past the end read as misses
           int32_t* tw = s_tbl + (ii & 1) * TR * K;
@@ -198,9 +205,17 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
           const int r = tid + 128 * t;
-          if (r < rows)
-            for (int k = 0; k < K; ++k)
-              if (tt[r * K + k] >= 0) bits |= 1u << (p.flip ? K - 1 - k : k);
+          if (r < rows) {
+            if (K == 27) {  // 3^3: all 27 shared-memory loads in flight
+              uint32_t m = 0;
+#pragma unroll
+              for (int k = 0; k < 27; ++k) m |= (tt[r * 27 + k] >= 0 ? 1u : 0u) << k;
+              bits |= p.flip ? (__brev(m) >> 5) : m;
+            } else {
+              for (int k = 0; k < K; ++k)
+                if (tt[r * K + k] >= 0) bits |= 1u << (p.flip ? K - 1 - k : k);
+            }
+          }
         }
         bits = __reduce_or_sync(0xffffffffu, bits);
         if (lane == 0 && bits) atomicOr(&s_mask[0], bits);
