@@ -13,6 +13,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv
   -o gpurun_out/prof_fwd -f python bench.py --profile-only --no-graph > gpurun_out/ncu_f.log 2>&1; echo "ncu fwd rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_tc_kernel -s 1 -c 1 \
   -o gpurun_out/prof_fwd32 -f python bench.py --profile-only --no-graph > gpurun_out/ncu_f32.log 2>&1; echo "ncu fwd32 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_tc_kernel -s 0 -c 1 \
+  -o gpurun_out/prof_fwd32d -f python bench.py --profile-only --no-graph > gpurun_out/ncu_f32d.log 2>&1; echo "ncu fwd32d rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"map_probe_grid|map_emit|grid_set" -s 0 -c 3 \
   -o gpurun_out/prof_map -f python bench.py --profile-only --no-graph > gpurun_out/ncu_m.log 2>&1; echo "ncu map rc=$?"
 timeout 300 python tools/timeline.py > gpurun_out/timeline.txt 2>&1; echo "timeline rc=$?"
