@@ -19,3 +19,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"map
   -o gpurun_out/prof_map -f python bench.py --profile-only --no-graph > gpurun_out/ncu_m.log 2>&1; echo "ncu map rc=$?"
 timeout 300 python tools/timeline.py > gpurun_out/timeline.txt 2>&1; echo "timeline rc=$?"
 timeout 300 python tools/step_breakdown.py > gpurun_out/step_breakdown.txt 2>&1; echo "breakdown rc=$?"
+# keep what comes back under gpurun's 64 MiB: raw csv exports of the captures
+for r in gpurun_out/prof_*.ncu-rep; do
+  [ -f "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  [ -n "${KEEP_REPS:-}" ] || rm -f "$r"
+done
