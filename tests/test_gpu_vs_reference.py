@@ -73,7 +73,7 @@ def test_conv_forward_backward_vs_reference(ref, stride, dtype):
     ry = R.sparse_conv_forward(rt, R.ConvWeights(w), rshape, stride)
     shape = conv.KernelShape.hypercubic(3, 3)
     t = SparseTensor(c, np.zeros((len(c), 1)), (1, 1, 1)).with_features(torch.tensor(x).cuda().to(tdt))
-    W = conv.ConvWeights(torch.from_numpy(w).cuda())
+    W = conv.ConvWeights(torch.tensor(w).cuda())
     y = conv.sparse_conv_forward(t, W, shape, stride)
     # integer stage: output coordinates and kernel map bit-exact with the reference
     np.testing.assert_array_equal(y.coords.cpu().numpy(), ry.coords)
