@@ -92,7 +92,7 @@ def test_conv_forward_backward_vs_reference(ref, stride, dtype):
     if dtype == "bf16":
         g = bf16_round(g)
     rgi, rgw = R.sparse_conv_backward(rt, R.ConvWeights(w), rshape, stride, g)
-    gi, gw = conv.sparse_conv_backward(t, W, shape, stride, torch.from_numpy(g).cuda().to(tdt))
+    gi, gw = conv.sparse_conv_backward(t, W, shape, stride, torch.tensor(g).cuda().to(tdt))
     bgi = np.zeros_like(rgi)
     bgw = np.zeros_like(rgw)
     for k, (vi, ui) in enumerate(rkm.pairs):
