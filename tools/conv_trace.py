@@ -51,7 +51,8 @@ ghz = 1.965
 print(f"C={c} density={d} kernel {e0.elapsed_time(e1) * 1e3:.1f} us")
 for i in range(int(valid.sum())):
     a = (tl_ev[i] - t0) / ghz / 1e3
-    print(f" tile {i}: prologue {a[0]:7.2f} -> published {a[1]:7.2f}   epi got acc {a[2]:7.2f} done {a[3]:7.2f} us")
+    b = (st_ev[i] - t0) / ghz / 1e3
+    print(f" tile {i}: prologue {a[0]:7.2f} -> all in {b[0]:7.2f} scan {b[1]:7.2f} mask {b[2]:7.2f} -> published {a[1]:7.2f}  mma saw {b[3]:7.2f}  epi got acc {a[2]:7.2f} done {a[3]:7.2f} us")
 ns = int((st_ev[:, 0] > 0).sum())
 for gg in range(min(ns, 60)):
     a = (st_ev[gg] - t0) / ghz / 1e3
