@@ -15,6 +15,9 @@
 // (128-row tile, split) pairs; when the tile count cannot fill the grid the
 // active offsets of a tile are split across CTAs (fp32 partials, reduced in a
 // fixed order afterwards) -> deterministic with no atomics on the output.
+// Each item's offset-activity scan (which offsets any of its rows hits) runs
+// in the epilogue warps one item ahead, so the producers only publish at a
+// tile boundary.
 // C_in = 32 packs two offsets into one 64-wide K stage.  CPS CTAs share an SM
 // (smem ring and TMEM sized to fit): random-row gather throughput scales with
 // independent CTAs per SM far more than with ring depth (tools/gather_probe2).
@@ -123,8 +126,10 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   uint64_t* tbar = reinterpret_cast<uint64_t*>(book + 256);   // [2] table-tile arrivals
   int* s_info = reinterpret_cast<int*>(book + 512);          // [2] units per work item (for MMA)
   int* s_work = s_info + 4;                                  // u0, n_units, n_act (producers)
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(book + 640);
-  int16_t* s_act = reinterpret_cast<int16_t*>(book + 1024);  // <= 343 entries
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(book + 640);  // [2][16] per item parity
+  int* s_na = reinterpret_cast<int*>(book + 800);              // [2] active offsets per parity
+  uint64_t* sready = reinterpret_cast<uint64_t*>(book + 272);  // [2] item scan done (epilogue -> producers)
+  int16_t* s_act = reinterpret_cast<int16_t*>(book + 1024);  // [2][512]: <= 343 entries per parity
   int32_t* s_tbl = reinterpret_cast<int32_t*>(book + C::BOOK);  // [2][TR * K] when K <= kTblK
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -150,6 +155,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       tc::mbar_init(&ifull[i], 1);
       tc::mbar_init(&iempty[i], 1);
       tc::mbar_init(&tbar[i], 1);
+      tc::mbar_init(&sready[i], 1);
     }
     tc::fence_mbar_init();
   }
@@ -185,87 +191,30 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       const int tile = w / S, split = w - (w / S) * S;
       const int rows = min(TR, n_out - tile * TR);
       const int32_t* tt = s_tbl + (ii & 1) * TR * K;  // this item's staged table
+      if (tbl) tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);  // landed (the scan waited too): makes it visible here
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tid < kTcMaskWords) s_mask[tid] = 0;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tbl && (p.dbg & 16)) {  // experiment: every offset active, no scan
-        tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);
-        if (rows < TR) {
-          int32_t* tw = s_tbl + (ii & 1) * TR * K;
-          for (int e = rows * K + tid; e < TR * K; e += kTcProd) tw[e] = -1;
-        }
-        if (tid == 0) s_mask[0] = K >= 32 ? 0xffffffffu : (1u << K) - 1u;
-      } else if (tbl) {
-        tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);
-        if (rows < TR) {  // ragged last tile: rows past the end read as misses
-          int32_t* tw = s_tbl + (ii & 1) * TR * K;
-          for (int e = rows * K + tid; e < TR * K; e += kTcProd) tw[e] = -1;
-        }
-        uint32_t bits = 0;
-#pragma unroll
-        for (int t = 0; t < TT; ++t) {
-          const int r = tid + 128 * t;
-          if (r < rows) {
-            if (K == 27) {  // 3^3: all 27 shared-memory loads in flight
-              uint32_t m = 0;
-#pragma unroll
-              for (int k = 0; k < 27; ++k) m |= (tt[r * 27 + k] >= 0 ? 1u : 0u) << k;
-              bits |= p.flip ? (__brev(m) >> 5) : m;
-            } else {
-              for (int k = 0; k < K; ++k)
-                if (tt[r * K + k] >= 0) bits |= 1u << (p.flip ? K - 1 - k : k);
-            }
-          }
-        }
-        bits = __reduce_or_sync(0xffffffffu, bits);
-        if (lane == 0 && bits) atomicOr(&s_mask[0], bits);
-      } else {
-        for (int kb = 0; kb < K; kb += 32) {
-          uint32_t bits = 0;
-          const int kend = min(32, K - kb);
-          for (int t = 0; t < TT; ++t) {
-            const int r = tid + 128 * t;
-            const int32_t* trow = p.table + ((int64_t)tile * TR + r) * K;
-            for (int j = 0; j < kend; ++j) {
-              const int k = kb + j;
-              const int v = r < rows ? __ldg(trow + (p.flip ? K - 1 - k : k)) : -1;
-              if (v >= 0) bits |= 1u << j;
-            }
-          }
-          bits = __reduce_or_sync(0xffffffffu, bits);
-          if (lane == 0 && bits) atomicOr(&s_mask[kb >> 5], bits);
-        }
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 0) {
-        // active offsets in ascending order (ballot prefix per 32-offset word)
-        int na = 0;
-        for (int kb = 0; kb < K; kb += 32) {
-          const uint32_t m = s_mask[kb >> 5];
-          if (m & (1u << lane)) s_act[na + __popc(m & ((1u << lane) - 1u))] = (int16_t)(kb + lane);
-          na += __popc(m);
-        }
-        __syncwarp();
-        if (lane == 0) {
-          const int nu = C::PAIR ? (na + 1) / 2 : na * C::NCH;
-          const int u0 = (int)((int64_t)nu * split / S), u1 = (int)((int64_t)nu * (split + 1) / S);
-          s_work[0] = u0;
-          s_work[1] = u1 - u0;
-          s_work[2] = na;
-          const int slot = ii & 1;
-          if (ii >= 2) tc::mbar_wait(&iempty[slot], ((ii >> 1) - 1) & 1);
-          s_info[slot] = max(u1 - u0, 1);
-          trace_ev(1024 + 4 * (ii & 63) + 1, true);
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&ifull[slot])) : "memory");
-          // every producer is past tile ii-1 (barrier above): its buffer is free
-          if (tbl && w + (int)gridDim.x < total) issue_tbl(w + gridDim.x, (ii + 1) & 1);
-        }
+      // the epilogue warps scanned this item's offset activity (scan_item)
+      if (warp == 0 && lane == 0) {
+        tc::mbar_wait(&sready[ii & 1], (ii >> 1) & 1);
+        const int na = s_na[ii & 1];
+        const int nu = C::PAIR ? (na + 1) / 2 : na * C::NCH;
+        const int u0 = (int)((int64_t)nu * split / S), u1 = (int)((int64_t)nu * (split + 1) / S);
+        s_work[0] = u0;
+        s_work[1] = u1 - u0;
+        s_work[2] = na;
+        const int slot = ii & 1;
+        if (ii >= 2) tc::mbar_wait(&iempty[slot], ((ii >> 1) - 1) & 1);
+        s_info[slot] = max(u1 - u0, 1);
+        trace_ev(1024 + 4 * (ii & 63) + 1, true);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&ifull[slot])) : "memory");
+        // every producer is past tile ii-1 (barrier below at ii-1's end): its buffer is free
+        if (tbl && w + (int)gridDim.x < total) issue_tbl(w + gridDim.x, (ii + 1) & 1);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const int u0 = s_work[0], nun = s_work[1], na = s_work[2];
       const int neff = nun > 0 ? nun : 1;
       // unit -> (offset of A's first half / whole row, second half, 64-col slice)
-      const uint32_t s_act_s = tc::smem_u32(s_act);
+      const uint32_t s_act_s = tc::smem_u32(s_act + (ii & 1) * 512);
       auto unit_k = [&](int unit, int& ka, int& kb, int& cs) {
         kb = -1;
         cs = 0;
@@ -362,9 +311,88 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   } else if (warp < 8) {
     // ============================ epilogue ============================
     const int ep = warp - 4;
+    const int etid = tid - 128;
+    // Offset-activity scan of the CTA's iiw-th item (work item wi) into buffer
+    // iiw & 1: OR of the rows' neighbour-hit masks -> ascending active-offset
+    // list + count, then sready.  Run here, in the epilogue warps' slack, so
+    // the producers only publish at a tile boundary.
+    auto scan_item = [&](int wi, int iiw) {
+      const int b = iiw & 1;
+      const int tile_w = wi / S;
+      const int rows_w = min(TR, n_out - tile_w * TR);
+      uint32_t* msk = s_mask + b * 16;
+      if (etid < kTcMaskWords) msk[etid] = 0;
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (TBL) {
+        tc::mbar_wait(&tbar[b], (iiw >> 1) & 1);
+        int32_t* tw = s_tbl + b * TR * K;
+        if (rows_w < TR)  // ragged last tile: rows past the end read as misses
+          for (int e = rows_w * K + etid; e < TR * K; e += kTcEpi) tw[e] = -1;
+        if (p.dbg & 16) {  // experiment: every offset active, no scan
+          if (etid == 0) msk[0] = K >= 32 ? 0xffffffffu : (1u << K) - 1u;
+        } else {
+          uint32_t bits = 0;
+#pragma unroll
+          for (int t = 0; t < TT; ++t) {
+            const int r = etid + 128 * t;
+            if (r < rows_w) {
+              if (K == 27) {  // 3^3: all 27 shared-memory loads in flight
+                uint32_t m = 0;
+#pragma unroll
+                for (int k = 0; k < 27; ++k) m |= (tw[r * 27 + k] >= 0 ? 1u : 0u) << k;
+                bits |= p.flip ? (__brev(m) >> 5) : m;
+              } else {
+                for (int k = 0; k < K; ++k)
+                  if (tw[r * K + k] >= 0) bits |= 1u << (p.flip ? K - 1 - k : k);
+              }
+            }
+          }
+          bits = __reduce_or_sync(0xffffffffu, bits);
+          if (lane == 0 && bits) atomicOr(&msk[0], bits);
+        }
+      } else {
+        for (int kb = 0; kb < K; kb += 32) {
+          uint32_t bits = 0;
+          const int kend = min(32, K - kb);
+          for (int t = 0; t < TT; ++t) {
+            const int r = etid + 128 * t;
+            const int32_t* trow = p.table + ((int64_t)tile_w * TR + r) * K;
+            for (int j = 0; j < kend; ++j) {
+              const int k = kb + j;
+              const int v = r < rows_w ? __ldg(trow + (p.flip ? K - 1 - k : k)) : -1;
+              if (v >= 0) bits |= 1u << j;
+            }
+          }
+          bits = __reduce_or_sync(0xffffffffu, bits);
+          if (lane == 0 && bits) atomicOr(&msk[kb >> 5], bits);
+        }
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (ep == 0) {
+        int16_t* act = s_act + b * 512;
+        int na = 0;
+        for (int kb = 0; kb < K; kb += 32) {
+          const uint32_t m = msk[kb >> 5];
+          if (m & (1u << lane)) act[na + __popc(m & ((1u << lane) - 1u))] = (int16_t)(kb + lane);
+          na += __popc(m);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          s_na[b] = na;
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&sready[b])) : "memory");
+        }
+      }
+    };
+    if ((int)blockIdx.x < total) scan_item(blockIdx.x, 0);
     int ii = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++ii) {
       const int tile = w / S, split = w - (w / S) * S;
+      // next item's scan: once item ii is published its producers are past
+      // item ii-1, whose mask / list / table buffers the scan reuses
+      if (w + (int)gridDim.x < total) {
+        tc::mbar_wait(&ifull[ii & 1], (ii >> 1) & 1);
+        scan_item(w + gridDim.x, ii + 1);
+      }
       const int a = ii % C::ACC;
       tc::mbar_wait(&tfull[a], (ii / C::ACC) & 1);
       trace_ev(1024 + 4 * (ii & 63) + 2, ep == 0 && lane == 0);
