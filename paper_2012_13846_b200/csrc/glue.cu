@@ -575,9 +575,18 @@ static int bn_passes() {  // row passes per thread in the partial phase (VP_BN_P
   static const int v = getenv("VP_BN_PASSES") ? std::max(1, atoi(getenv("VP_BN_PASSES"))) : 24;
   return v;
 }
-static int bn_partial_blocks(int64_t cap, int64_t C) {
+static int bn_bwd_passes() {  // the backward partials read 3-4 tensors: own pass count (VP_BN_BWD_PASSES)
+  static const int v = getenv("VP_BN_BWD_PASSES") ? std::max(1, atoi(getenv("VP_BN_BWD_PASSES"))) : bn_passes();
+  return v;
+}
+static int bn_partial_blocks(int64_t cap, int64_t C, bool bwd = false) {
   const int64_t elems = std::max<int64_t>(cap, 1) * C;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(elems, (int64_t)kGlueThreads * 8 * bn_passes()), kNumSMs));
+  const int passes = bwd ? bn_bwd_passes() : bn_passes();
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(elems, (int64_t)kGlueThreads * 8 * passes), kNumSMs));
+}
+// partial rows reserved in the (shared forward/backward) workspace
+static int bn_partial_slots(int64_t cap, int64_t C) {
+  return std::max(bn_partial_blocks(cap, C, false), bn_partial_blocks(cap, C, true));
 }
 
 static bool bn_shape_ok(int64_t C) { return (C % 8 == 0 && C / 8 <= kGlueThreads) || C <= kGlueThreads; }
@@ -760,7 +769,7 @@ using namespace vp;
 extern "C" {
 
 size_t vp_bn_stats_ws_bytes(int64_t cap_n, int64_t C) {
-  return align_up((size_t)bn_partial_blocks(cap_n, C) * 2 * C * 4, 256) + 256;  // partials + ticket
+  return align_up((size_t)bn_partial_slots(cap_n, C) * 2 * C * 4, 256) + 256;  // partials + ticket
 }
 
 // Launch KERNEL<VEC, DT>: DT fixed at compile time when every tensor the kernel
@@ -779,7 +788,7 @@ static int one_dtype(std::initializer_list<int> ds) {
 }
 
 static int* bn_ticket(void* ws, int64_t cap, int64_t C) {
-  return reinterpret_cast<int*>((char*)ws + align_up((size_t)bn_partial_blocks(cap, C) * 2 * C * 4, 256));
+  return reinterpret_cast<int*>((char*)ws + align_up((size_t)bn_partial_slots(cap, C) * 2 * C * 4, 256));
 }
 
 int vp_bn_stats(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, int64_t C, float eps, float* mean,
@@ -861,7 +870,7 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   VP_REQUIRE(ws_bytes >= vp_bn_backward_ws_bytes(cap, C), VP_EVALIDATION, "bn_backward: workspace too small");
-  const int nb = bn_partial_blocks(cap, C);
+  const int nb = bn_partial_blocks(cap, C, true);
   int* ticket = bn_ticket(ws, cap, C);
   if (bn_fused_enabled() && cap > 0) {
     const BnFuse F{2, ticket + 16, gamma, nullptr, nullptr, 0, relu, gx, gxd, gres};
