@@ -205,7 +205,7 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t c_out,
 size_t vp_conv_wgrad_ws_bytes(int64_t c_in, int64_t c_out, int32_t K, int64_t cap_pairs);
 int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t c_in, const void* g, int32_t g_dtype,
                   int64_t c_out, int32_t K, const int32_t* pair_in, const int32_t* pair_out,
-                  const int32_t* pair_ptr, int64_t cap_pairs, float* grad_w,
+                  const int32_t* pair_ptr, int64_t cap_pairs, void* grad_w,
                   void* ws, size_t ws_bytes, vp_stream_t stream);
 
 /* ---------------------------------------------------------------- glue

@@ -65,7 +65,7 @@ SIGNATURES = {
     "vp_conv_dgrad_ws_bytes": (SZ, [I64, I64, I32]),
     "vp_conv_dgrad": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, P, I64, P, I32, P, SZ, P]),
     "vp_conv_wgrad_ws_bytes": (SZ, [I64, I64, I32, I64]),
-    "vp_conv_wgrad": (C.c_int, [P, I32, I64, P, I32, I64, I32, P, P, P, I64, P, P, SZ, P]),
+    "vp_conv_wgrad": (C.c_int, [P, I32, I64, P, I32, I64, I32, P, P, P, I64, P, P, SZ, P]),  # grad_w: fp32 (f64 for f64 operands)
     "vp_bn_stats_ws_bytes": (SZ, [I64, I64]),
     "vp_bn_stats": (C.c_int, [P, I32, P, I64, I64, F32, P, P, P, SZ, P]),
     "vp_bn_apply": (C.c_int, [P, I32, P, I64, I64, P, P, P, P, P, I32, I32, P, I32, P]),
@@ -151,10 +151,15 @@ def dtype_code(t) -> int:
     raise StructuralError(f"unsupported feature dtype {t.dtype}")
 
 
-def workspace(nbytes: int, device):
-    """Caller-owned scratch for a C-ABI call.  Zero-filled: the fused BN
-    statistics keep a self-re-arming ticket in their workspace, which must
-    start at zero (include/voxpipe_b200.h)."""
+def workspace(nbytes: int, device, zero: bool = False):
+    """Caller-owned scratch for a C-ABI call, from torch's stream-ordered
+    caching allocator.  Uninitialised: every entry point initialises the
+    scratch it reads.  zero=True for the BN statistics, whose workspace ends
+    in a self-re-arming ticket word that must start at zero
+    (include/voxpipe_b200.h)."""
     import torch
 
-    return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    n = max(int(nbytes), 256)
+    if zero:
+        return torch.zeros(n, dtype=torch.uint8, device=device)
+    return torch.empty(n, dtype=torch.uint8, device=device)

@@ -299,9 +299,11 @@ def conv_dgrad_raw(g: torch.Tensor, w: ConvWeights, table: torch.Tensor, n_in: i
 
 
 def conv_wgrad_raw(x: torch.Tensor, g: torch.Tensor, w_shape: tuple, kmap: KernelMap) -> torch.Tensor:
-    """grad_w[k] = sum over pairs (v, u) of offset k of g[u] x[v]^T (conv.py:241), fp32."""
+    """grad_w[k] = sum over pairs (v, u) of offset k of g[u] x[v]^T (conv.py:241),
+    fp32 (f64 for f64 features)."""
     K, n_out_c, n_in_c = w_shape
-    gw = torch.empty((K, n_out_c, n_in_c), dtype=torch.float32, device=x.device)
+    gdt = torch.float64 if x.dtype == torch.float64 else torch.float32
+    gw = torch.empty((K, n_out_c, n_in_c), dtype=gdt, device=x.device)
     cap_pairs = max(int(kmap.pair_in.numel()), 1)
     ws = _lib.workspace(_lib.query("vp_conv_wgrad_ws_bytes", n_in_c, n_out_c, K, cap_pairs), x.device)
     _lib.call("vp_conv_wgrad", x.data_ptr(), _lib.dtype_code(x), n_in_c, g.data_ptr(), _lib.dtype_code(g), n_out_c,

@@ -29,9 +29,42 @@
 namespace vp {
 
 
-// sum the chunk partials of each offset in chunk order (deterministic)
-__global__ void wgrad_reduce_kernel(const float* __restrict__ part, const int32_t* __restrict__ pptr,
-                                    int K, int chunk, int64_t per, float* __restrict__ gw) {
+// Pairwise (binary-counter) summation of n values p[0], p[stride], ... in a
+// fixed order: after element i the stack holds the partial sums of blocks
+// whose sizes are the binary digits of i+1, merged as soon as two equal
+// blocks meet — a balanced tree, so the rounding error grows with log2(n)
+// rather than n (the stride-1 centre offset of a C5 stem layer
+// reduces ~1,600 chunk partials).  Deterministic: the order depends on n only.
+template <typename T>
+__device__ __forceinline__ T tree_sum(const T* __restrict__ p, int64_t stride, int n) {
+  T stack[32];
+  int top = 0;
+  int i = 0;
+  for (; i + 4 <= n; i += 4) {  // four loads in flight, merged in order
+    T v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = p[(int64_t)(i + j) * stride];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      T s = v[j];
+      for (unsigned c = (unsigned)(i + j) + 1u; (c & 1u) == 0u; c >>= 1) s = stack[--top] + s;
+      stack[top++] = s;
+    }
+  }
+  for (; i < n; ++i) {
+    T s = p[(int64_t)i * stride];
+    for (unsigned c = (unsigned)i + 1u; (c & 1u) == 0u; c >>= 1) s = stack[--top] + s;
+    stack[top++] = s;
+  }
+  T acc = T(0);
+  while (top > 0) acc = stack[--top] + acc;
+  return acc;
+}
+
+// sum the chunk partials of each offset, pairwise in chunk order (deterministic)
+template <typename T>
+__global__ void wgrad_reduce_kernel(const T* __restrict__ part, const int32_t* __restrict__ pptr,
+                                    int K, int chunk, int64_t per, T* __restrict__ gw) {
   ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
   if (threadIdx.x == 0) {
@@ -48,15 +81,34 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, const int32_
        e += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(e / per);
     const int64_t o = e - (int64_t)k * per;
-    float acc = 0.f;
-    for (int it = s_pref[k]; it < s_pref[k + 1]; ++it) acc += part[(int64_t)it * per + o];
-    gw[e] = acc;
+    gw[e] = tree_sum(part + (int64_t)s_pref[k] * per + o, per, s_pref[k + 1] - s_pref[k]);
   }
 }
 
 // ------------------------------------------------------------------ SIMT paths
-// Generic widths / fp32 features: y[u, co] = sum_k sum_ci W[k, co, ci] x[t[u,k], ci].
+// Generic widths, fp32 and f64 features.  T is the accumulation type: fp32
+// for bf16/fp32 features, f64 when any operand is f64 (the reference's own
+// precision, conv.py:77-105 — parity to ~1e-12 and a finite-difference
+// gradient check are possible in that mode).
+template <typename T>
+__device__ __forceinline__ T ldv(const void* p, int dtype, int64_t i) {
+  if (dtype == VP_F64) return (T)reinterpret_cast<const double*>(p)[i];
+  if (dtype == VP_BF16) return (T)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+  return (T)reinterpret_cast<const float*>(p)[i];
+}
+template <typename T>
+__device__ __forceinline__ void stv(void* p, int dtype, int64_t i, T v) {
+  if (dtype == VP_F64)
+    reinterpret_cast<double*>(p)[i] = (double)v;
+  else if (dtype == VP_BF16)
+    reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn((float)v);
+  else
+    reinterpret_cast<float*>(p)[i] = (float)v;
+}
+
+// y[u, co] = sum_k sum_ci W[k, co, ci] x[t[u,k], ci].
 // W is addressed as W[k*wk + co*wco + ci*wci] so dgrad passes W^T by strides.
+template <typename T>
 __global__ void conv_fwd_simt_kernel(const void* __restrict__ x, int x_dtype, int cin,
                                      const void* __restrict__ w, int w_dtype, int64_t wk, int64_t wco,
                                      int64_t wci, int cout, int K, const int32_t* __restrict__ table,
@@ -69,28 +121,29 @@ __global__ void conv_fwd_simt_kernel(const void* __restrict__ x, int x_dtype, in
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t u = e / cout;
     const int co = (int)(e - u * cout);
-    float acc = 0.f;
+    T acc = T(0);
     for (int k = 0; k < K; ++k) {
       const int v = table[u * K + (flip ? K - 1 - k : k)];
       if (v < 0) continue;
       for (int ci = 0; ci < cin; ++ci)
-        acc += ldf(w, w_dtype, k * wk + co * wco + ci * wci) * ldf(x, x_dtype, (int64_t)v * cin + ci);
+        acc += ldv<T>(w, w_dtype, k * wk + co * wco + ci * wci) * ldv<T>(x, x_dtype, (int64_t)v * cin + ci);
     }
-    stf(y, y_dtype, perm ? (int64_t)perm[u] * cout + co : e, acc);
+    stv<T>(y, y_dtype, perm ? (int64_t)perm[u] * cout + co : e, acc);
   }
 }
 
 // wgrad partials: block per (chunk item); warps stride over the chunk's pairs,
 // lanes over output elements; fixed-order cross-warp sum.
 constexpr int kWgSimtThreads = 256;
+template <typename T>
 __global__ void __launch_bounds__(kWgSimtThreads)
 wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* __restrict__ gy,
                   int g_dtype, int cout, int K, const int32_t* __restrict__ pin,
                   const int32_t* __restrict__ pout, const int32_t* __restrict__ pptr, int chunk,
-                  float* __restrict__ part) {
+                  T* __restrict__ part) {
   ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
-  __shared__ float s_red[kWgSimtThreads / 32][32];
+  __shared__ T s_red[kWgSimtThreads / 32][32];
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int k = 0; k < K; ++k) {
@@ -111,15 +164,15 @@ wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* 
     for (int e0 = 0; e0 < per; e0 += 32) {
       const int e = e0 + lane;
       const int co = e / cin, ci = e - (e / cin) * cin;
-      float acc = 0.f;
+      T acc = T(0);
       if (e < per)
 #pragma unroll 8
         for (int q = p0 + warp; q < p1; q += kWgSimtThreads / 32)
-          acc += ldf(gy, g_dtype, (int64_t)pout[q] * cout + co) * ldf(x, x_dtype, (int64_t)pin[q] * cin + ci);
+          acc += ldv<T>(gy, g_dtype, (int64_t)pout[q] * cout + co) * ldv<T>(x, x_dtype, (int64_t)pin[q] * cin + ci);
       s_red[warp][lane] = acc;
       __syncthreads();
       if (warp == 0 && e < per) {
-        float s = 0.f;
+        T s = T(0);
         for (int w2 = 0; w2 < kWgSimtThreads / 32; ++w2) s += s_red[w2][lane];
         part[(int64_t)item * per + e] = s;
       }
@@ -639,9 +692,11 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(cin >= 1 && cout >= 1, VP_EVALIDATION, "channel widths must be positive");
-  VP_REQUIRE(y_dtype == VP_F32 || y_dtype == VP_BF16, VP_EVALIDATION, "output dtype must be f32 or bf16");
+  VP_REQUIRE(y_dtype == VP_F32 || y_dtype == VP_BF16 || y_dtype == VP_F64, VP_EVALIDATION,
+             "output dtype must be f32, bf16 or f64");
   if (cap_out <= 0) return VP_OK;
-  if (x_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
+  const bool f64 = x_dtype == VP_F64 || w_dtype == VP_F64 || y_dtype == VP_F64;
+  if (!f64 && x_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
     VP_REQUIRE(ws && ws_bytes >= vp_conv_fwd_ws_bytes(cin, cout, K), VP_EVALIDATION, "conv_fwd: workspace too small");
     const bf16* wb = (const bf16*)w;
     char* part = (char*)ws + align_up((size_t)K * cin * cout * 2, 256);
@@ -657,12 +712,14 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
     FwdParams p{(const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
     return conv_tc<false>(cin, cout, p, part, st);
   }
-  if (small_fwd_ok(cin, cout, K)) return launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip,
-                                                          perm, n_out_dev, cap_out, y, y_dtype, st);
+  if (!f64 && small_fwd_ok(cin, cout, K))
+    return launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip, perm, n_out_dev, cap_out, y,
+                            y_dtype, st);
   const int64_t total = cap_out * cout;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
-  ::vp::launch(conv_fwd_simt_kernel, blocks, 256, 0, st, x, x_dtype, (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout,
-                                                K, table, flip, perm, n_out_dev, cap_out, y, y_dtype);
+  ::vp::launch(f64 ? conv_fwd_simt_kernel<double> : conv_fwd_simt_kernel<float>, blocks, 256, 0, st, x, x_dtype,
+               (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout, K, table, flip, perm, n_out_dev, cap_out, y,
+               y_dtype);
   VP_CHECK_LAUNCH("conv_fwd_simt");
   return VP_OK;
 }
@@ -676,8 +733,11 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
                   int64_t cap_in, void* gi, int32_t gi_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
+  VP_REQUIRE(gi_dtype == VP_F32 || gi_dtype == VP_BF16 || gi_dtype == VP_F64, VP_EVALIDATION,
+             "grad_in dtype must be f32, bf16 or f64");
   if (cap_in <= 0) return VP_OK;
-  if (g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
+  const bool f64 = g_dtype == VP_F64 || w_dtype == VP_F64 || gi_dtype == VP_F64;
+  if (!f64 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
     VP_REQUIRE(ws && ws_bytes >= vp_conv_dgrad_ws_bytes(cin, cout, K), VP_EVALIDATION,
                "conv_dgrad: workspace too small");
     const bf16* wb = (const bf16*)w;
@@ -698,23 +758,27 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
   const int64_t total = cap_in * cin;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
   // W^T[k, ci, co] = W[k, co, ci]: strides (k: cout*cin, "co"=ci: 1, "ci"=co: cin)
-  ::vp::launch(conv_fwd_simt_kernel, blocks, 256, 0, st, g, g_dtype, (int)cout, w, w_dtype, cout * cin, 1, cin, (int)cin,
-                                                K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype);
+  ::vp::launch(f64 ? conv_fwd_simt_kernel<double> : conv_fwd_simt_kernel<float>, blocks, 256, 0, st, g, g_dtype,
+               (int)cout, w, w_dtype, cout * cin, 1, cin, (int)cin, K, table, flip, perm, n_in_dev, cap_in, gi,
+               gi_dtype);
   VP_CHECK_LAUNCH("conv_dgrad_simt");
   return VP_OK;
 }
 
 constexpr int kWgSimtChunk = 512;  // SIMT path: short chunks, many CTAs
 
+// fp32 partials of the SIMT chunk size; the f64 path runs chunks twice as
+// long, so 8-byte partials of (cap/2chunk + K + 1) items fit the same
+// budget with 2(K+1) slack items
 size_t vp_conv_wgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K, int64_t cap_pairs) {
   const int chunk = std::min(wgrad_chunk(cap_pairs), kWgSimtChunk);
-  const int64_t items = cap_pairs / chunk + K + 1;
+  const int64_t items = cap_pairs / chunk + 2 * ((int64_t)K + 1);
   return align_up((size_t)items * cin * cout * 4, 256);
 }
 
 int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
                   int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
-                  float* gw, void* ws, size_t ws_bytes, vp_stream_t stream) {
+                  void* gw_out, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(ws && ws_bytes >= vp_conv_wgrad_ws_bytes(cin, cout, K, cap_pairs), VP_EVALIDATION,
@@ -722,13 +786,27 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
   const int chunk = wgrad_chunk(cap_pairs);
   const int max_items = (int)(cap_pairs / chunk + K + 1);
   float* part = (float*)ws;
+  float* gw = (float*)gw_out;
   const int64_t total = (int64_t)K * cin * cout;
+  const int rblocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8));
+  if (x_dtype == VP_F64 || g_dtype == VP_F64) {  // the reference's precision: f64 partials, f64 grad_w
+    const int dchunk = 2 * std::min(chunk, kWgSimtChunk);
+    const int ditems = (int)(cap_pairs / dchunk + K + 1);
+    double* dpart = (double*)ws;
+    ::vp::launch(wgrad_simt_kernel<double>, std::max(1, std::min(ditems, grid_cap(8))), kWgSimtThreads, 0, st, x,
+                 x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout, pptr, dchunk, dpart);
+    VP_CHECK_LAUNCH("conv_wgrad_simt_f64");
+    ::vp::launch(wgrad_reduce_kernel<double>, rblocks, 256, 0, st, (const double*)dpart, pptr, K, dchunk,
+                 (int64_t)cin * cout, (double*)gw_out);
+    VP_CHECK_LAUNCH("wgrad_reduce_f64");
+    return VP_OK;
+  }
   if (x_dtype == VP_BF16 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, part};
     int rc = wg_tc(cin, cout, p, max_items, st);
     if (rc != VP_OK) return rc;
-    ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8)), 256, 0, st, 
-        part, pptr, K, chunk, cin * cout, gw);
+    ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, chunk,
+                 (int64_t)cin * cout, gw);
     VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }
@@ -744,19 +822,19 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     else
       ::vp::launch(wgrad_stem_kernel<64>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
     VP_CHECK_LAUNCH("conv_wgrad_stem");
-    ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8)), 256, 0, st, part, pptr,
-                 K, kWgStemChunk, cin * cout, gw);
+    ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, kWgStemChunk,
+                 (int64_t)cin * cout, gw);
     VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }
   const int schunk = std::min(chunk, kWgSimtChunk);
   const int sitems = (int)(cap_pairs / schunk + K + 1);
   const int grid = std::max(1, std::min(sitems, grid_cap(8)));
-  ::vp::launch(wgrad_simt_kernel, grid, kWgSimtThreads, 0, st, x, x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout,
-                                                     pptr, schunk, part);
+  ::vp::launch(wgrad_simt_kernel<float>, grid, kWgSimtThreads, 0, st, x, x_dtype, (int)cin, g, g_dtype, (int)cout, K,
+               pin, pout, pptr, schunk, part);
   VP_CHECK_LAUNCH("conv_wgrad_simt");
-  ::vp::launch(wgrad_reduce_kernel, (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8)), 256, 0, st, 
-      part, pptr, K, schunk, cin * cout, gw);
+  ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, schunk,
+               (int64_t)cin * cout, gw);
   VP_CHECK_LAUNCH("wgrad_reduce");
   return VP_OK;
 }

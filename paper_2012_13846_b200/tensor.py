@@ -66,7 +66,7 @@ def pad_coords(coords, device=None) -> tuple[torch.Tensor, int]:
 def _to_features(features, device) -> torch.Tensor:
     if not isinstance(features, torch.Tensor):
         features = torch.as_tensor(np.asarray(features, dtype=np.float64)).to(torch.float32)
-    if features.dtype not in (torch.float32, torch.bfloat16):
+    if features.dtype not in (torch.float32, torch.bfloat16, torch.float64):
         features = features.to(torch.float32)
     return features.to(device).contiguous()
 
@@ -101,9 +101,15 @@ class SparseTensor:
     """Immutable (coords, features) pair with tensor-stride bookkeeping
     (tensor.py:36-100), device resident."""
 
-    __slots__ = ("coords4", "features", "tensor_stride", "dim")
+    __slots__ = ("coords4", "features", "tensor_stride", "dim", "plans")
 
-    def __init__(self, coords, features, tensor_stride, *, _trusted: bool = False, _dim: Optional[int] = None):
+    def __init__(self, coords, features, tensor_stride, *, _trusted: bool = False, _dim: Optional[int] = None,
+                 _plans: Optional[dict] = None):
+        # plans: the coordinate bookkeeping derived from these rows (output
+        # coordinates, kernel maps, sorted tables per (stride, kernel shape)),
+        # shared by every tensor on the same coordinates (nn.py) — the role
+        # of MinkowskiEngine's coordinate manager
+        self.plans = {} if _plans is None else _plans
         if _trusted:
             self.coords4 = coords
             self.dim = _dim if _dim is not None else 3
@@ -156,7 +162,8 @@ class SparseTensor:
     def with_features(self, features: torch.Tensor) -> "SparseTensor":
         if features.shape[0] != len(self):
             raise StructuralError("coords and features row counts differ")
-        return SparseTensor(self.coords4, features.contiguous(), self.tensor_stride, _trusted=True, _dim=self.dim)
+        return SparseTensor(self.coords4, features.contiguous(), self.tensor_stride, _trusted=True, _dim=self.dim,
+                            _plans=self.plans)
 
     def to_numpy(self) -> tuple[np.ndarray, np.ndarray]:
         """(coords int64 (N, 1+D), features float64) as the reference stores them."""

@@ -5,17 +5,19 @@ with `act_round` rounding every tensor the engine stores in bf16).
 Tolerances:
   fp32 engine (SIMT kernels): loss rel 1e-5, every gradient rel-L2 <= 1e-3 —
       pins the engine's dataflow (wiring, BN, residual, pool, SGD) exactly;
-  bf16 engine (tcgen05 path): loss rel 2e-3; gradients cosine >= 0.97 and
-      rel-L2 <= 0.25 (blocks=1; cos >= 0.92 / rel-L2 <= 0.4 at blocks=2) vs the
-      bf16-emulating oracle — bf16 roundings of nearly
-      equal values diverge layer by layer (forward activations drift ~1e-3 per
-      layer), and training-mode BN over few rows amplifies the drift in the
-      backward pass;
+  bf16 engine (tcgen05 path): loss rel 1e-3; every gradient's
+      rel-L2 vs the bf16-emulating oracle <= 2 x the oracle's OWN sensitivity
+      to accumulation order (the same oracle with fp32 conv accumulation) +
+      0.02 (tests/parity_util.py): bf16 roundings of nearly equal values flip
+      under any change of summation order and training-mode BN amplifies the
+      flips layer by layer, so the bound is calibrated on that noise rather
+      than fixed — a defect of a few % in one layer still fails;
   level coordinates bit-exact."""
 import numpy as np
 import pytest
 
 import voxpipe_oracle as O
+from parity_util import noise_calibrated_grad_check
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -95,17 +97,9 @@ def test_train_step_matches_oracle(blocks):
     p0 = tr.state_numpy()
     loss = tr.train_step_from_host(pts, offs, labels)
     c, f = O.voxelize_batch(pts.astype(np.float64), offs, 1.0, 48)
-    pr = {k: (bf16_round(v) if k.endswith(".w") and not k.startswith("fc") else v) for k, v in p0.items()}
-    rloss, rgrads, _, _ = O.resnet_train_step(pr, c, f, labels, 4, blocks=blocks, wdtype=bf16_round,
-                                              act_round=bf16_round)
-    assert abs(loss - rloss) <= 2e-3 * abs(rloss), (loss, rloss)
     g = tr.grads_numpy()
-    errs = {k: np.linalg.norm(g[k] - rg) / (np.linalg.norm(rg) + 1e-12) for k, rg in rgrads.items()}
-    cos = {k: float((g[k] * rg).sum() / (np.linalg.norm(g[k]) * np.linalg.norm(rg) + 1e-30)) for k, rg in rgrads.items()}
-    # deeper nets accumulate more bf16 drift (the fp32 test pins the dataflow)
-    tol_rel, tol_cos = (0.25, 0.97) if blocks == 1 else (0.4, 0.92)
-    bad = {k: (errs[k], cos[k]) for k in errs if errs[k] > tol_rel or cos[k] < tol_cos}
-    assert not bad, sorted(bad.items(), key=lambda kv: -kv[1][0])[:8]
+    rloss, _ = noise_calibrated_grad_check(g, p0, c, f, labels, 4, blocks)
+    assert abs(loss - rloss) <= 1e-3 * abs(rloss), (loss, rloss)
     # SGD momentum update (first step: m = g, p -= lr*g)
     p1 = tr.state_numpy()
     for k in ("fc.w", "stem.w", "s3.down.gamma"):
