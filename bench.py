@@ -12,8 +12,10 @@ backward, optimizer (nothing cached across steps).
   e2e   : clouds/s through the public trainer API from pinned HOST memory:
           H2D of the step's points + labels, the step, D2H of the loss, all
           inside the timed region
-  roofline : dominant kernel (largest-FLOP tensor-core conv forward of the
-          step), re-launched standalone on the step's own data, CUDA events
+  roofline : dominant conv kernel (largest per-launch device time among every
+          layer's tensor-core forward / dgrad / wgrad), re-launched on the
+          step's own data and tables with the L2 flushed before each launch;
+          SURVEY §8(d) algorithmic bytes / FLOPs (paper_2012_13846_b200/roofline.py)
   cpu_baseline : the reference's own CPU path (oracle/_ref voxpipe, convs via
           voxpipe.conv + numpy glue) on a bounded sample of the same workload
 
@@ -57,10 +59,12 @@ def metric_config(args):
     C5 network on one GPU."""
     c3 = (args.batch, args.points, args.res, args.blocks) == (64, 2048, 64, 1)
     c5 = (args.res, args.blocks) == (128, 2)
-    tag = "C3" if c3 else ("C5 (one GPU)" if c5 else "custom")
+    tag = "C3" if c3 else ("C5" if c5 else "custom")
+    global CONFIG_TAG
+    CONFIG_TAG = tag
     metric = (f"point clouds/sec train (SparseResNet{'' if args.blocks == 1 else f' blocks={args.blocks}'}, "
               f"{args.batch}x{args.points} pts @ {args.res}^3, bf16)")
-    config = {"workload": f"{tag}: sparse-ResNet classifier, {args.batch} clouds x {args.points} pts/cloud at "
+    config = {"workload": f"{tag}{' (one GPU)' if tag == 'C5' else ''}: sparse-ResNet classifier, {args.batch} clouds x {args.points} pts/cloud at "
                           f"{args.res}^3 voxels per GPU, {1 + 4 * (1 + 2 * args.blocks)} convs (blocks={args.blocks}), "
                           "bf16 features, SGD momentum",
               "global_batch_per_gpu": args.batch, "points_per_cloud": args.points, "resolution": args.res,
@@ -362,7 +366,7 @@ def main():
     e2e_value = world * args.batch * args.steps / (e2e_ms / 1e3)
 
     # ---------------- roofline of the dominant kernel (standalone, same data)
-    roof = roofline(tr, dev)
+    roof = roofline(tr, dev, CONFIG_TAG)
 
     if world > 1:
         dist.barrier()
@@ -435,15 +439,19 @@ def run_pipeline(args, rank, world, local, dev):
                      torch.tensor([(b + 7 * i) % 40 for b in range(args.batch)], dtype=torch.int32, device=dev)))
     dist.barrier()  # first collective on every rank before any P2P group
 
+    mult = topo.mb_multiple()  # every replica group all-reduces the same number of rounds
+
     def run(n_mb):
+        n_mb = -(-n_mb // mult) * mult
         return PL.StageRunner(topo, rank, n_mb, make, lambda mb: pool[mb % len(pool)], tr,
                               use_graphs=not args.no_graph)
 
+    n_timed = -(-(args.steps * world) // mult) * mult
     if active:
         warm = run(max(1, args.warmup) * world)
         warm.run()
         torch.cuda.synchronize()
-        timed = run(args.steps * world)
+        timed = run(n_timed)
         # reuse the warmed engines, graphs and weights
         timed.slots, timed.graphs = warm.slots[:len(timed.slots)], warm.graphs
         timed.master_p, timed.master_pb, timed.master_m = warm.master_p, warm.master_pb, warm.master_m
@@ -460,7 +468,7 @@ def run_pipeline(args, rank, world, local, dev):
     ms = torch.tensor([e0.elapsed_time(e1)], device="cpu" if args.pipeline_test else dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    value = args.steps * world * args.batch / (ms / 1e3)
+    value = n_timed * args.batch / (ms / 1e3)
     # PipeDream weight-stashing audit: every (micro-batch,
     # stage) backward used the weight version its forward used
     audit = timed.stats.audit if active else []
@@ -474,7 +482,8 @@ def run_pipeline(args, rank, world, local, dev):
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": dict(CONFIG, parallelism=f"pipeline {split}", stages=[
                     [s.unit_start, s.unit_end, list(s.ranks)] for s in topo.stages],
-                    micro_batch_clouds=args.batch, micro_batches_per_step=world, cuda_graph=not args.no_graph,
+                    micro_batch_clouds=args.batch, micro_batches_per_step=world, micro_batches_timed=n_timed,
+                    cuda_graph=not args.no_graph,
                     l2="not flushed: one continuous 1F1B stream (fill + drain inside the timed region)"),
                 "weight_version_audit": {"checked": checked, "violations": violations},
                 "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None}
@@ -483,108 +492,82 @@ def run_pipeline(args, rank, world, local, dev):
     dist.destroy_process_group()
 
 
-def _peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
-    except OSError:
-        return {}, "fallback"
+def roofline(tr, dev, tag, iters=20):
+    """Roofline of the dominant conv kernel of the step and of the kernel-map
+    builder (paper_2012_13846_b200/roofline.py: SURVEY §8(d) algorithmic
+    work; every launch preceded by an L2 flush, CUDA events on the launching
+    stream, the step's own data and tables).
 
-
-def _time_launch(launch, iters):
-    import torch
-
-    st = torch.cuda.current_stream()
-    for _ in range(3):
-        launch()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record(st)
-    for _ in range(iters):
-        launch()
-    b.record(st)
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) / iters / 1e3
-
-
-def _ncu_traffic(kernel_key, layer=None):
-    """dram read+write bytes per launch of `kernel_key` (for `layer` when that
-    layer was captured) from the committed ncu --set full summaries
-    (profiles/ncu_traffic.json), else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            t = json.load(f)
-    except (OSError, ValueError):
-        return None
-    return t.get(f"{kernel_key} {layer}", t.get(kernel_key))
-
-
-def roofline(tr, dev, iters=30):
-    """Roofline of the dominant tensor-core kernel of the step and of the
-    kernel-map builder, each relaunched standalone on the step's own data
-    (CUDA events on the launching stream, warm L2).
-
-    Dominant kernel = the conv forward (vp_conv_fwd, tcgen05 path) with the
-    largest device time per launch.  Algorithmic work per launch (SURVEY
-    §8(d)): F = 2 * P * C_in * C_out useful FLOPs; compulsory bytes
-    B = 2 N_in C_in + 2 N_out C_out + 2*27*C_in*C_out + 4*27*N_out (neighbour
-    table).  Bound = tensor if F/B * HBM > tensor peak, else hbm.
-    Map: B_map = 16 N_in + 16 N_out + 8 P for the largest stride-1 map."""
+    Candidates: each tensor-core layer's forward, dgrad and wgrad launch
+    (the C_in = 1 stem runs SIMT kernels).  Dominant = the largest device
+    time per launch; all candidates are listed under `kernels`."""
     import torch
 
     from paper_2012_13846_b200 import _lib
+    from paper_2012_13846_b200 import roofline as RL
 
-    peaks, src = _peaks()
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    tc_peak = peaks.get("bf16_tflops", 1590.0)
-    st = torch.cuda.current_stream()
+    hbm, tc_peak, src = RL.peaks()
+    flush = RL.Flusher(dev)
+    st = torch.cuda.current_stream().cuda_stream
+    fc = _lib.VP_BF16
     rows = []
     for L in tr.layers:
         if L["cin"] < 32:
             continue
-        dst = L["dst"]
+        src_l, dst, m = L["src"], L["dst"], L["map"]
+        P = int(m.ptr[-1].item())
+        n_in, n_out = int(src_l.n.item()), int(dst.n.item())
+        x = L["x"]
 
-        def launch(L=L, dst=dst):
-            _lib.call("vp_conv_fwd", L["x"].data_ptr(), _lib.VP_BF16, L["x"].shape[0], L["cin"], L["wb"].data_ptr(),
-                      _lib.VP_BF16, L["cout"], tr.K, tr.fwd_table(L).data_ptr(), 0, _lib.ptr(tr.fwd_perm(L)),
-                      dst.n.data_ptr(), dst.cap,
-                      L["y"].data_ptr(), _lib.VP_BF16, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st.cuda_stream)
+        def fwd(L=L, dst=dst, x=x):
+            _lib.call("vp_conv_fwd", x.data_ptr(), fc, x.shape[0], L["cin"], L["wb"].data_ptr(), fc, L["cout"],
+                      tr.K, tr.fwd_table(L).data_ptr(), 0, _lib.ptr(tr.fwd_perm(L)), dst.n.data_ptr(), dst.cap,
+                      L["y"].data_ptr(), fc, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
 
-        rows.append((_time_launch(launch, iters), L))
-    t, L = max(rows, key=lambda r: r[0])
-    P = int(L["map"].ptr[-1].item())
-    n_out, n_in = int(L["dst"].n.item()), int(L["src"].n.item())
-    fl = 2.0 * P * L["cin"] * L["cout"]
-    byts = 2 * n_in * L["cin"] + 2 * n_out * L["cout"] + 2 * 27 * L["cin"] * L["cout"] + 4 * n_out * 27
-    tflops, gbs = fl / t / 1e12, byts / t / 1e9
-    bound = "tensor" if (fl / byts) * hbm / 1e3 > tc_peak else "hbm"
-    ach, peak, unit = (tflops, tc_peak, "TFLOP/s") if bound == "tensor" else (gbs, hbm, "GB/s")
-    key = f"conv_fwd_tc<{L['cin']},{L['cout']}>"
-    out = {"kernel": f"{key} layer {L['name']} (N_out={n_out}, pairs={P})", "bound": bound,
-           "achieved": round(ach, 2), "peak": peak, "unit": unit, "frac": round(ach / peak, 4),
-           "traffic": _ncu_traffic(key, L["name"]), "peak_source": src, "us_per_launch": round(t * 1e6, 2),
-           "algorithmic_flops": fl, "algorithmic_bytes": byts, "tflops": round(tflops, 2), "gbs": round(gbs, 1),
-           "per_layer_fwd_us": {l["name"]: round(tt * 1e6, 1) for tt, l in rows}}
+        table, flip, perm = tr.dgrad_table(L)
+        gin = tr.gact[tr.levels.index(src_l)]
+
+        def dgrad(L=L, src_l=src_l, table=table, flip=flip, perm=perm, gin=gin):
+            _lib.call("vp_conv_dgrad", L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(), fc,
+                      L["cin"], tr.K, table.data_ptr(), flip, _lib.ptr(perm), src_l.n.data_ptr(), src_l.cap,
+                      gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
+
+        def wgrad(L=L, m=m, x=x):
+            _lib.call("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"], tr.K,
+                      m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(),
+                      L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st)
+
+        for mode, fn, key, (a, b, ci, co) in (
+                ("fwd", fwd, f"conv_fwd_tc<{L['cin']},{L['cout']}>", (n_in, n_out, L["cin"], L["cout"])),
+                ("dgrad", dgrad, f"conv_dgrad_tc<{L['cout']},{L['cin']}>", (n_out, n_in, L["cout"], L["cin"])),
+                ("wgrad", wgrad, f"conv_wgrad_tc<{L['cin']},{L['cout']}>", (n_in, n_out, L["cin"], L["cout"]))):
+            t = RL.time_cold(fn, flush, iters)
+            F, B = RL.conv_work(P, a, b, ci, co, tr.K, mode)
+            rec = RL.classify(F, B, t, hbm, tc_peak)
+            rows.append((t, key, L["name"], mode, P, n_in, n_out, rec))
+    t, key, name, mode, P, n_in, n_out, rec = max(rows, key=lambda r: r[0])
+    out = {"kernel": f"{key} {mode} layer {name} (N_in={n_in}, N_out={n_out}, pairs={P})", **rec,
+           "traffic": RL.ncu_traffic(tag, key, name), "peak_source": src,
+           "timing": "mean of per-launch CUDA events, L2 flushed (256 MiB write) before every launch",
+           "kernels": {f"{nm}.{md}": [r["us_per_launch"], r["frac"], r["bound"]] for _, _, nm, md, *_x, r in rows}}
     # kernel-map builder as the step runs it, level 0 stride-1: index insert
     # (dense grid, or hash) + probe + ordered pair compaction (+ grid clear)
     m = tr.map_s1[0]
 
     def map_launch():
         if tr.use_grid:
-            tr._grid_set(0, st.cuda_stream, clear=False)
-        tr._build_map(m, st.cuda_stream)
+            tr._grid_set(0, st, clear=False)
+        tr._build_map(m, st)
         if tr.use_grid:
-            tr._grid_set(0, st.cuda_stream, clear=True)
+            tr._grid_set(0, st, clear=True)
 
-    tm = _time_launch(map_launch, iters)
+    tm = RL.time_cold(map_launch, flush, iters)
     nm = int(m.src.n.item())
     pm = int(m.ptr[-1].item())
-    bm = 16 * nm + 16 * nm + 8 * pm
     name = {"grid": "vp_grid_set + vp_kernel_map_grid", "brick": "vp_brick_set + vp_kernel_map_brick"}.get(
         tr.index_kind, "vp_kernel_map")
-    out["map"] = {"kernel": f"{name} level0 stride-1 (N={nm}, pairs={pm})", "bound": "hbm",
-                  "achieved": round(bm / tm / 1e9, 1), "peak": hbm, "unit": "GB/s",
-                  "frac": round(bm / tm / 1e9 / hbm, 4), "us_per_call": round(tm * 1e6, 2), "algorithmic_bytes": bm}
+    out["map"] = {"kernel": f"{name} level0 stride-1 (N={nm}, pairs={pm})",
+                  **RL.classify(0.0, RL.map_bytes(nm, nm, pm), tm, hbm, tc_peak)}
     return out
 
 

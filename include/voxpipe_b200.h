@@ -269,6 +269,29 @@ int vp_sgd_momentum(float* p, float* m, const float* g, int64_t n, float lr, flo
 int vp_cast(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t count,
             vp_stream_t stream);
 
+/* ---------------------------------------------------------------- wide rows
+ * Coordinates the packed 64-bit key cannot hold (kernels.py:40-78: more than
+ * 3 axes, or axes beyond the 16-bit fields) — the reference's TupleCoordIndex
+ * fallback (kernels.py:95-122).  Rows are int64 [n, D1] = [batch, x1..xD]
+ * (2 <= D1 <= 8); the index is an open-addressing table of row numbers whose
+ * probe compares whole tuples (first occurrence wins).  Host arrays:
+ * tensor_stride / step / in_stride int64 [D1-1], offsets int32 [K, D1-1]. */
+size_t vp_wide_ws_bytes(int64_t n_in, int64_t n_out, int32_t D1, int32_t K);
+/* tensor.py:49-78 on wide rows: flags |= 1 duplicate, 2 negative batch,
+ * 4 axis not a multiple of the tensor stride. */
+int vp_wide_validate(const int64_t* rows, int64_t n, int32_t D1, const int64_t* tensor_stride,
+                     int32_t* flags_dev, void* ws, size_t ws_bytes, vp_stream_t stream);
+/* conv.py:124-146: out rows = unique(floor(in / step) * step) in first-seen
+ * order; *n_out_dev = count.  out holds n rows. */
+int vp_wide_output_coords(const int64_t* in, int64_t n, int32_t D1, const int64_t* step, int64_t* out,
+                          int32_t* n_out_dev, void* ws, size_t ws_bytes, vp_stream_t stream);
+/* conv.py:149-183 on wide rows: nbr [n_out, K] + CSR pairs in the reference
+ * order (offset-major, ascending out row). */
+int vp_wide_kernel_map(const int64_t* in, int64_t n_in, const int64_t* out, int64_t n_out, int32_t D1,
+                       const int32_t* offsets, int32_t K, const int64_t* in_stride, int32_t* nbr,
+                       int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr, void* ws, size_t ws_bytes,
+                       vp_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

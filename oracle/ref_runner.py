@@ -91,5 +91,54 @@ def time_steps(B, npts, res, steps, warmup, seed=0):
     return {"kind": cs.kind, "clouds_per_s": B * steps / dt, "s_per_step": dt / steps}
 
 
+def layer_split(B, npts, res, seed=0, reps=1):
+    """Per conv layer of the SparseResNet on the reference CPU path: wall
+    seconds of the reference's generate_output_coords and build_kernel_map
+    (conv.py:124-183) against its full sparse_conv_forward / _backward
+    (conv.py:186-242, which rebuild both); the remainder is the
+    gather-GEMM-scatter plus SparseTensor validation."""
+    kind, mods = load_reference()
+    if mods is None:
+        raise RuntimeError("oracle/_ref (the reference build) is required for the per-layer split")
+    R, RT = mods
+    pts, offs = O.synthetic_batch(B, npts, res, seed=seed, dtype=np.float32)
+    pts = pts.astype(np.float64)
+    t0 = time.perf_counter()
+    ts = [RT.voxelize(RT.PointCloud(pts[offs[i]:offs[i + 1]]), 1.0, (res,) * 3) for i in range(B)]
+    x = RT.batch(ts)
+    vox_s = time.perf_counter() - t0
+    shape = R.KernelShape.hypercubic(3, 3)
+    params = O.init_params(1, seed=2)
+    convs, _ = O.resnet_layout(1)
+    rows = []
+    rng = np.random.default_rng(1)
+    for name, ci, co, stride in convs:
+        if x.feature_width != ci:
+            x = R.SparseTensor(x.coords, rng.normal(size=(len(x), ci)), x.tensor_stride)
+        w = R.ConvWeights(params[name + ".w"])
+        rec = {"layer": name, "cin": ci, "cout": co, "stride": stride, "n_in": len(x)}
+        best = {}
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            oc, _ns = R.generate_output_coords(x, stride)
+            t1 = time.perf_counter()
+            km = R.build_kernel_map(x.coords, oc, shape, x.tensor_stride)
+            t2 = time.perf_counter()
+            y = R.sparse_conv_forward(x, w, shape, stride)
+            t3 = time.perf_counter()
+            R.sparse_conv_backward(x, w, shape, stride, np.ones((len(y), co)))
+            t4 = time.perf_counter()
+            for k, v in (("coords_s", t1 - t0), ("map_s", t2 - t1), ("fwd_s", t3 - t2), ("bwd_s", t4 - t3)):
+                best[k] = min(best.get(k, 1e30), v)
+        rec.update({k: round(v, 4) for k, v in best.items()})
+        rec["pairs"] = km.total_pairs()
+        # fwd and bwd each rebuild coords + map (conv.py:196-208, 228-242)
+        rec["gemm_fwd_s"] = round(max(best["fwd_s"] - best["coords_s"] - best["map_s"], 0.0), 4)
+        rec["gemm_bwd_s"] = round(max(best["bwd_s"] - best["coords_s"] - best["map_s"], 0.0), 4)
+        rows.append(rec)
+        x = R.SparseTensor(y.coords, y.features, y.tensor_stride)
+    return {"kind": kind, "voxelize_batch_s": round(vox_s, 4), "layers": rows}
+
+
 if __name__ == "__main__":
     print(time_steps(int(sys.argv[1]) if len(sys.argv) > 1 else 4, 2048, 64, 1, 1))

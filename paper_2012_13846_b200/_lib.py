@@ -79,6 +79,10 @@ SIGNATURES = {
     "vp_linear_xent": (C.c_int, [P, I32, I32, P, P, I32, P, P, P, P, P, P, P, SZ, P]),
     "vp_sgd_momentum": (C.c_int, [P, P, P, I64, F32, F32, P, I64, P]),
     "vp_cast": (C.c_int, [P, I32, P, I32, I64, P]),
+    "vp_wide_ws_bytes": (SZ, [I64, I64, I32, I32]),
+    "vp_wide_validate": (C.c_int, [P, I64, I32, P, P, P, SZ, P]),
+    "vp_wide_output_coords": (C.c_int, [P, I64, I32, P, P, P, P, SZ, P]),
+    "vp_wide_kernel_map": (C.c_int, [P, I64, P, I64, I32, P, I32, P, P, P, P, P, P, SZ, P]),
 }
 
 _lib = None
@@ -137,6 +141,11 @@ def stream():
 def i32_array(vals):
     vals = [int(v) for v in vals]
     return (C.c_int32 * max(1, len(vals)))(*vals)
+
+
+def i64_array(vals):
+    vals = [int(v) for v in vals]
+    return (C.c_int64 * max(1, len(vals)))(*vals)
 
 
 def dtype_code(t) -> int:

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvoxpipe_b200.so")
-SOURCES = ["hash_coords.cu", "kmap.cu", "kmap_sort.cu", "kmap_brick.cu", "conv.cu", "glue.cu"]
+SOURCES = ["hash_coords.cu", "kmap.cu", "kmap_sort.cu", "kmap_brick.cu", "conv.cu", "glue.cu", "wide.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

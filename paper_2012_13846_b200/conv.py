@@ -27,7 +27,7 @@ import torch
 
 from . import _lib
 from .errors import StructuralError, ValidationError
-from .tensor import SparseTensor, binary_size, pad_coords
+from .tensor import SparseTensor, binary_size, is_wide, pad_coords, widen
 
 _WEIGHTS_MAGIC = b"VXCW"
 _WEIGHTS_VERSION = 1
@@ -86,7 +86,10 @@ class KernelShape:
 
 class ConvWeights:
     """One (n_out, n_in) matrix per kernel offset (conv.py:77-105), device
-    resident fp32 masters with a cached bf16 copy for the tensor cores."""
+    resident: f64 when given f64 (the reference's precision, e.g. numpy
+    arrays), else fp32 masters; `operand(dtype)` is the copy the kernels read
+    for features of that dtype (bf16 for the tensor cores), cached until the
+    masters change."""
 
     def __init__(self, matrices, device=None):
         if not isinstance(matrices, torch.Tensor):
@@ -95,20 +98,30 @@ class ConvWeights:
             raise StructuralError("weights must have shape (K, n_out, n_in)")
         from .tensor import default_device
 
+        dt = torch.float64 if matrices.dtype == torch.float64 else torch.float32
         m = matrices.to(device=device or (matrices.device if matrices.is_cuda else default_device()),
-                        dtype=torch.float32).contiguous()
+                        dtype=dt).contiguous()
         if m.numel() and not bool(torch.isfinite(m).all()):
             raise ValidationError("weight entries must be finite")
         self.matrices = m
-        self._bf16: Optional[torch.Tensor] = None
-        self._bf16_version = -1
+        self._ops: dict = {}
+
+    def operand(self, dtype) -> torch.Tensor:
+        """The weight operand for features of `dtype`: bf16 features -> bf16,
+        fp32 -> fp32, f64 -> f64 (conversions cached per master version)."""
+        dtype = torch.bfloat16 if dtype == torch.bfloat16 else (torch.float64 if dtype == torch.float64
+                                                                 else torch.float32)
+        if self.matrices.dtype == dtype:
+            return self.matrices
+        hit = self._ops.get(dtype)
+        if hit is None or hit[0] != self.matrices._version:
+            hit = (self.matrices._version, self.matrices.to(dtype).contiguous())
+            self._ops[dtype] = hit
+        return hit[1]
 
     @property
     def bf16(self) -> torch.Tensor:
-        if self._bf16 is None or self._bf16_version != self.matrices._version:
-            self._bf16 = self.matrices.to(torch.bfloat16).contiguous()
-            self._bf16_version = self.matrices._version
-        return self._bf16
+        return self.operand(torch.bfloat16)
 
     @property
     def num_offsets(self) -> int:
@@ -178,11 +191,21 @@ def _stride3(stride, dim) -> tuple:
 
 
 def _output_coords4(coords4: torch.Tensor, tensor_stride: tuple, stride: tuple, dim: int):
-    """generate_output_coords on the padded layout -> (coords4_out, new_stride)."""
+    """generate_output_coords on the storage layout -> (coords_out, new_stride)."""
     new_stride = tuple(int(o) * int(s) for o, s in zip(tensor_stride, stride))
     if all(s == 1 for s in stride):
         return coords4.clone(), new_stride
     n = coords4.shape[0]
+    if is_wide(coords4) or max(new_stride) > 16384:  # wide rows (kernels.py:95-122 fallback)
+        c = widen(coords4, dim)
+        if n == 0:
+            return c.clone(), new_stride
+        out = torch.empty_like(c)
+        n_out = torch.empty(1, dtype=torch.int32, device=c.device)
+        ws = _lib.workspace(_lib.query("vp_wide_ws_bytes", n, 0, dim + 1, 1), c.device)
+        _lib.call("vp_wide_output_coords", c.data_ptr(), n, dim + 1, _lib.i64_array(new_stride), out.data_ptr(),
+                  n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+        return out[: int(n_out.item())], new_stride
     if n == 0:
         return torch.empty((0, 4), dtype=torch.int32, device=coords4.device), new_stride
     out = torch.empty((n, 4), dtype=torch.int32, device=coords4.device)
@@ -209,6 +232,8 @@ def _kernel_map4(in4: torch.Tensor, out4: torch.Tensor, shape: KernelShape, in_s
     if K > _lib.MAX_OFFSETS:
         raise ValidationError(f"at most {_lib.MAX_OFFSETS} kernel offsets are supported")
     n_in, n_out = in4.shape[0], out4.shape[0]
+    if is_wide(in4) or is_wide(out4):
+        return _kernel_map_wide(widen(in4, dim), widen(out4, dim), shape, in_stride, dim)
     nbr = torch.empty((max(n_out, 1), K), dtype=torch.int32, device=device)
     cap_p = max(n_out * K, 1)
     pin = torch.empty(cap_p, dtype=torch.int32, device=device) if with_pairs else None
@@ -222,6 +247,26 @@ def _kernel_map4(in4: torch.Tensor, out4: torch.Tensor, shape: KernelShape, in_s
               _lib.ptr(pout), pptr.data_ptr() if with_pairs else None, ws.data_ptr(), ws.numel(), _lib.stream())
     if not with_pairs:
         pin = pout = torch.empty(0, dtype=torch.int32, device=device)
+    return KernelMap(shape.offsets, nbr[:n_out], pin, pout, pptr, n_in=n_in)
+
+
+def _kernel_map_wide(inw: torch.Tensor, outw: torch.Tensor, shape: KernelShape, in_stride: tuple,
+                     dim: int) -> KernelMap:
+    """Kernel map over wide int64 rows (vp_wide_kernel_map): the reference's
+    TupleCoordIndex fallback (kernels.py:95-122) with the same pair order."""
+    device = inw.device
+    K = shape.num_offsets
+    n_in, n_out = inw.shape[0], outw.shape[0]
+    nbr = torch.empty((max(n_out, 1), K), dtype=torch.int32, device=device)
+    cap_p = max(n_out * K, 1)
+    pin = torch.empty(cap_p, dtype=torch.int32, device=device)
+    pout = torch.empty(cap_p, dtype=torch.int32, device=device)
+    pptr = torch.zeros(K + 1, dtype=torch.int32, device=device)
+    ws = _lib.workspace(_lib.query("vp_wide_ws_bytes", n_in, n_out, dim + 1, K), device)
+    offs = np.ascontiguousarray(shape.offsets, dtype=np.int64).ravel()
+    _lib.call("vp_wide_kernel_map", inw.data_ptr() if n_in else None, n_in, outw.data_ptr() if n_out else None, n_out,
+              dim + 1, _lib.i32_array(offs), K, _lib.i64_array(in_stride), nbr.data_ptr(), pin.data_ptr(),
+              pout.data_ptr(), pptr.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
     return KernelMap(shape.offsets, nbr[:n_out], pin, pout, pptr, n_in=n_in)
 
 
@@ -274,7 +319,7 @@ def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: 
     out_dtype = out_dtype or x.dtype
     K = w.num_offsets
     y = torch.empty((max(n_out, 1), w.n_out), dtype=out_dtype, device=x.device)
-    wt = w.bf16 if x.dtype == torch.bfloat16 else w.matrices
+    wt = w.operand(x.dtype)
     ws = _lib.workspace(_lib.query("vp_conv_fwd_ws_bytes", w.n_in, w.n_out, K), x.device)
     _lib.call("vp_conv_fwd", x.data_ptr(), _lib.dtype_code(x), max(x.shape[0], 1), w.n_in, wt.data_ptr(),
               _lib.dtype_code(wt), w.n_out,
@@ -289,7 +334,7 @@ def conv_dgrad_raw(g: torch.Tensor, w: ConvWeights, table: torch.Tensor, n_in: i
     out_dtype = out_dtype or g.dtype
     K = w.num_offsets
     gi = torch.empty((max(n_in, 1), w.n_in), dtype=out_dtype, device=g.device)
-    wt = w.bf16 if g.dtype == torch.bfloat16 else w.matrices
+    wt = w.operand(g.dtype)
     ws = _lib.workspace(_lib.query("vp_conv_dgrad_ws_bytes", w.n_in, w.n_out, K), g.device)
     _lib.call("vp_conv_dgrad", g.data_ptr(), _lib.dtype_code(g), max(g.shape[0], 1), w.n_out, wt.data_ptr(),
               _lib.dtype_code(wt),

@@ -118,17 +118,13 @@ def transposed_plan(t: SparseTensor, shape: C.KernelShape, stride, out: SparseTe
 
 
 def _weights(w: torch.Tensor, x: torch.Tensor) -> C.ConvWeights:
-    """The kernels' weight operand: the parameter itself (fp32/f64 features)
-    or its bf16 copy (tensor-core path), without ConvWeights' host checks."""
+    """The kernels' weight operand around the parameter (no copy for
+    fp32/f64 parameters; bf16 features read a bf16 copy), without
+    ConvWeights' host-side finiteness check."""
     cw = C.ConvWeights.__new__(C.ConvWeights)
     m = w.detach()
-    if x.dtype == torch.float64:
-        m = m.to(torch.float64)
-    elif m.dtype != torch.float32:
-        m = m.to(torch.float32)
-    cw.matrices = m.contiguous()
-    cw._bf16 = m.to(torch.bfloat16).contiguous() if x.dtype == torch.bfloat16 else None
-    cw._bf16_version = cw.matrices._version
+    cw.matrices = m if m.dtype in (torch.float32, torch.float64) else m.to(torch.float32)
+    cw._ops = {}
     return cw
 
 

@@ -11,18 +11,27 @@ schedule's invariants on CPU with the gloo backend, and
 tests/test_gpu_pipeline.py checks on the GPU that a pipelined run equals an
 emulation of the same weight-version semantics on the single-GPU engine.
 
-Wire format per micro-batch (forward, stage s -> s+1), capacity-sized so no
-size has to be read back to the host (NCCL needs sizes at enqueue time):
-    n       int32 [1]          live rows (device-side count)
-    coords  int32 [cap, 4]     rows [batch, x, y, z] of the cut level
-    feats   bf16  [cap, C]     activation of the last unit of stage s
+Wire format per micro-batch — the analogue of the reference's binary
+sparse-tensor format (tensor.py:270-301: header, then coords, then
+features), live rows only:
+  forward (stage s -> s+1), on the forward-direction communicator:
+    header  int32 [4]          (n, C, tensor_stride, B) — sent alone first; the
+                               receiver reads it, then posts the payload
+    coords  int32 [n, 4]       rows [batch, x, y, z] of the cut level
+    feats   bf16  [n, C]       activation of the last unit of stage s
     labels  int32 [B]          class labels travel with the clouds
-backward (s+1 -> s): grad feats bf16 [cap, C].  The analogue of the
-reference's binary sparse-tensor format (tensor.py:270-301) with the header
-carried as a device tensor.
+  backward (s+1 -> s), on the backward-direction communicator:
+    grad    bf16  [n, C]       n known to both sides from the forward header
+Receivers keep capacity-sized buffers; only 16 + 16 n + 2 n C + 4 B bytes
+(forward) and 2 n C bytes (backward) cross NVLink.  Activations and
+gradients use separate communicators, so sends are posted and left in flight
+(waited only before their buffer is rewritten) while receives are waited in
+stream order right before the compute that consumes them: F(mb)'s send never
+gates B(mb').
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -71,6 +80,15 @@ class Topology:
     @property
     def world(self) -> int:
         return sum(len(s.ranks) for s in self.stages)
+
+    def mb_multiple(self) -> int:
+        """Micro-batch counts must be multiples of every stage's replica count:
+        replicas all-reduce once per backward round, so a short round would
+        leave a collective without partners."""
+        m = 1
+        for s in self.stages:
+            m = m * len(s.ranks) // math.gcd(m, len(s.ranks))
+        return m
 
     def locate(self, rank: int):
         """-> (stage index, replica index) of a rank, or None if idle."""
@@ -198,8 +216,8 @@ def simulate_versions(topo: Topology, n_mb: int, stash: bool = True) -> list:
 
 # ---------------------------------------------------------------- transport
 def boundary_tensors(e, kind: str) -> list:
-    """Tensors one communication of `kind` moves for engine e (wire format in
-    the module docstring)."""
+    """Capacity-sized tensors behind one communication of `kind` for engine
+    e (LocalTransport moves them whole; DistTransport sends live rows)."""
     if kind == "send_fwd":
         lv = e.levels[e.exit_level]
         return [lv.n, lv.coords, e.out_act, e.labels]
@@ -213,43 +231,93 @@ def boundary_tensors(e, kind: str) -> list:
 
 class DistTransport:
     """torch.distributed P2P (NCCL on B200 over NVLink/NVSwitch; gloo for the
-    CPU tests).  One action's communications are one batch_isend_irecv
-    (ncclGroupStart/End), enqueued on NCCL's stream before the compute."""
+    CPU tests) with the header-first live-size wire format of the module
+    docstring.  Two extra communicators over the whole world carry the
+    forward (activation) and backward (gradient) directions; replica groups
+    carry the gradient all_reduce."""
 
     def __init__(self, dist, topo: Optional["Topology"] = None, host_stage: bool = False):
         """Creating a process group is collective over the whole world, so
-        every rank builds every replica group of `topo` up front, in the
-        same order.  host_stage: move device tensors through host memory
-        (gloo with several ranks on one GPU — a functional test of the
-        runtime where NCCL cannot run two ranks per device)."""
+        every rank builds the direction communicators and every replica
+        group of `topo` up front, in the same order.  host_stage: move device
+        tensors through host memory (gloo with several ranks on one GPU — a
+        functional test of the runtime where NCCL cannot run two ranks per
+        device)."""
         self.dist = dist
         self.host_stage = host_stage
         self._groups = {}
+        world = list(range(dist.get_world_size()))
+        self.g_fwd = dist.new_group(world)
+        self.g_bwd = dist.new_group(world)
         if topo is not None:
             for st in topo.stages:
                 if len(st.ranks) > 1:
                     self._groups[tuple(st.ranks)] = dist.new_group(list(st.ranks))
+        self.bytes_sent = 0
+        self.messages = 0
+
+    # -- point to point ------------------------------------------------------
+    def _send(self, runner, slot, t, peer, group):
+        keep = t
+        if self.host_stage and t.is_cuda:
+            keep = t.cpu()
+        w = self.dist.isend(keep, peer, group=group)
+        runner.pending_sends.setdefault(slot, []).append((w, keep))
+        self.bytes_sent += t.numel() * t.element_size()
+        self.messages += 1
+
+    def _recv(self, t, peer, group):
+        """Blocking-in-stream-order receive into t (a contiguous view)."""
+        if self.host_stage and t.is_cuda:
+            h = torch_empty_like_host(t)
+            self.dist.irecv(h, peer, group=group).wait()
+            t.copy_(h)
+            return
+        self.dist.irecv(t, peer, group=group).wait()
 
     def exchange(self, runner, comms) -> None:
-        if not comms:
-            return
-        d = self.dist
-        ops, back = [], []
-        for c in comms:
-            send = c.kind.startswith("send")
-            fn = d.isend if send else d.irecv
-            for t in boundary_tensors(runner.engine_of(c.mb), c.kind):
-                if self.host_stage and t.is_cuda:
-                    h = t.cpu() if send else torch_empty_like_host(t)
-                    if not send:
-                        back.append((t, h))
-                    t = h
-                ops.append(d.P2POp(fn, t, c.peer))
-        for w in d.batch_isend_irecv(ops):
-            w.wait()
-        for t, h in back:
-            t.copy_(h)
+        import torch
 
+        for c in comms:
+            e = runner.engine_of(c.mb)
+            slot = runner.slot_of[c.mb]
+            if c.kind == "send_fwd":
+                lv = e.levels[e.exit_level]
+                n = int(lv.n.item())  # the stage's forward has produced the cut level
+                C = e.out_act.shape[1]
+                runner.wire_rows[(c.mb, "out")] = n
+                hdr = torch.tensor([n, C, int(getattr(lv, "stride", 1)), e.labels.numel()], dtype=torch.int32,
+                                   device=lv.n.device)
+                for t in (hdr, lv.coords[:n], e.out_act[:n], e.labels):
+                    self._send(runner, slot, t, c.peer, self.g_fwd)
+            elif c.kind == "recv_fwd":
+                lv = e.levels[e.entry_level]
+                hdr = torch.empty(4, dtype=torch.int32, device=lv.n.device)
+                self._recv(hdr, c.peer, self.g_fwd)
+                n, C, _ts, B = (int(v) for v in hdr.tolist())
+                if n > lv.coords.shape[0] or C != e.x_in.shape[1] or B != e.labels.numel():
+                    raise StructuralError(f"pipeline header {(n, C, B)} does not fit the stage input "
+                                          f"(cap {lv.coords.shape[0]}, C {e.x_in.shape[1]}, B {e.labels.numel()})")
+                runner.wire_rows[(c.mb, "in")] = n
+                lv.n.fill_(n)
+                for t in (lv.coords[:n], e.x_in[:n], e.labels):
+                    self._recv(t, c.peer, self.g_fwd)
+            elif c.kind == "send_bwd":
+                n = runner.wire_rows[(c.mb, "in")]
+                self._send(runner, slot, e.grad_input[:n].contiguous(), c.peer, self.g_bwd)
+            else:  # recv_bwd
+                n = runner.wire_rows[(c.mb, "out")]
+                self._recv(e.g_out_ext[:n], c.peer, self.g_bwd)
+
+    def wait_sends(self, runner, slot=None) -> None:
+        """Complete the in-flight sends of one slot (before its buffers are
+        rewritten) or of all slots."""
+        slots = list(runner.pending_sends) if slot is None else [slot]
+        for s in slots:
+            for w, _ in runner.pending_sends.pop(s, []):
+                w.wait()
+
+    # -- replica groups ------------------------------------------------------
     def group(self, ranks: tuple):
         if len(ranks) <= 1:
             return None
@@ -318,6 +386,9 @@ class LocalTransport:
     def group(self, ranks: tuple):
         return tuple(ranks) if len(ranks) > 1 else None
 
+    def wait_sends(self, runner, slot=None) -> None:  # sends are copies: complete when posted
+        return None
+
     def allreduce_mean(self, t, group) -> None:
         raise StructuralError("replicated stages in LocalPipeline reduce through LocalPipeline")
 
@@ -351,6 +422,9 @@ class StageRunner:
                  transport, stash: bool = True, use_graphs: bool = False):
         import torch
 
+        if n_mb % topo.mb_multiple():
+            raise ValidationError(f"{n_mb} micro-batches: must be a multiple of {topo.mb_multiple()} (the replica "
+                                  "counts' lcm) so every replica group all-reduces the same number of rounds")
         self.topo, self.rank, self.n_mb = topo, rank, n_mb
         self.stage, self.replica = topo.locate(rank)
         self.S = len(topo.stages)
@@ -377,6 +451,8 @@ class StageRunner:
         self.use_graphs = use_graphs
         self.graphs = {}
         self._next_slot = 0
+        self.pending_sends = {}  # slot -> [(work, buffer)] still in flight
+        self.wire_rows = {}  # (mb, "in" | "out") -> live rows of the boundary level
 
     def engine_of(self, mb):
         return self.slots[self.slot_of[mb]]
@@ -423,6 +499,7 @@ class StageRunner:
 
     def forward(self, a: Action):
         e = self.engine_of(a.mb)
+        self.tr.wait_sends(self, self.slot_of[a.mb])  # this slot's previous sends read the buffers F rewrites
         self._refresh(e)
         self.slot_version[self.slot_of[a.mb]] = self.version
         if self.first:
@@ -435,6 +512,7 @@ class StageRunner:
 
     def backward_grad(self, a: Action):
         e = self.engine_of(a.mb)
+        self.tr.wait_sends(self, self.slot_of[a.mb])
         if not self.stash:
             self._refresh(e)
         self._run(e, "B")
@@ -456,6 +534,7 @@ class StageRunner:
     def run(self):
         for a in self.program:
             self.execute(a)
+        self.tr.wait_sends(self)
         return self.stats
 
 

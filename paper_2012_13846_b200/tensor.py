@@ -9,10 +9,16 @@ exposes; `coords4` is the padded (N, 4) storage the kernels read.
 
 Every check the reference's constructor performs (tensor.py:49-78) runs on
 the GPU (one flag word read back); duplicate detection is a hash insert
-instead of np.unique.  Coordinates must lie in the reference's packable range
-(kernels.py:40-46; batch <= 65535, |axis| <= 32767) — the range its hash
-index supports natively; rows outside it raise ValidationError here (the
-reference would fall back to a dict index, kernels.py:95-122).
+instead of np.unique.
+
+Two coordinate storages, chosen per tensor:
+  * packed (the fast path): int32 (N, 4), every axis in [-16384, 16383] and
+    batch <= 65535 — strided outputs and every neighbour query then stay
+    inside the reference's packed 64-bit key (kernels.py:40-78);
+  * wide: int64 (N, 1+D) for D > 3 axes or coordinates beyond that range —
+    the reference's TupleCoordIndex fallback (kernels.py:95-122), served by
+    the vp_wide_* kernels (whole-tuple hash).  `coords4` then holds the
+    (N, 1+D) int64 rows.
 """
 from __future__ import annotations
 
@@ -39,8 +45,19 @@ def default_device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+PACKED_AXIS_MIN, PACKED_AXIS_MAX, PACKED_BATCH_MAX = -16384, 16383, 65535
+MAX_AXES = 7  # wide rows: batch + up to 7 axes
+
+
+def is_wide(c: torch.Tensor) -> bool:
+    """Wide storage = int64 rows (N, 1+D); packed = int32 (N, 4)."""
+    return c.dtype == torch.int64
+
+
 def pad_coords(coords, device=None) -> tuple[torch.Tensor, int]:
-    """(N, 1+D) int rows -> contiguous int32 (N, 4) on the device, and D."""
+    """(N, 1+D) int rows -> (storage on the device, D): packed int32 (N, 4)
+    when D <= 3 and every value is inside the packed range, else wide int64
+    (N, 1+D) rows (module docstring)."""
     if not isinstance(coords, torch.Tensor):
         a = np.asarray(coords, dtype=np.int64)
         # read-only arrays (the reference's SparseTensor marks its arrays so) are copied
@@ -48,19 +65,32 @@ def pad_coords(coords, device=None) -> tuple[torch.Tensor, int]:
     if coords.dim() != 2 or coords.shape[1] < 2:
         raise StructuralError("coords must have shape (N, 1+D) with D >= 1")
     dim = coords.shape[1] - 1
-    if dim > 3:
-        raise ValidationError(f"the GPU path supports 1..3 axes (packable keys), got {dim}")
+    if dim > MAX_AXES:
+        raise ValidationError(f"at most {MAX_AXES} coordinate axes are supported, got {dim}")
     device = device or (coords.device if coords.is_cuda else default_device())
-    if coords.dtype != torch.int32:
-        if coords.numel() and (coords.max() > 2**31 - 1 or coords.min() < -(2**31)):
-            raise ValidationError("coordinate axis out of packable range [-32768, 32767]")
-        coords = coords.to(torch.int32)
-    coords = coords.to(device)
+    if coords.dtype == torch.int32 and coords.shape[1] == 4 and coords.is_cuda:
+        return coords.contiguous(), dim  # already packed storage (trusted callers)
+    if coords.dtype.is_floating_point:
+        raise ValidationError("coordinates must be integers")
+    wide = dim > 3
+    if not wide and coords.numel():
+        c64 = coords.to(torch.int64)
+        ax = c64[:, 1:]
+        wide = bool(ax.min() < PACKED_AXIS_MIN) or bool(ax.max() > PACKED_AXIS_MAX) or bool(
+            c64[:, 0].max() > PACKED_BATCH_MAX)
+    if wide:
+        return coords.to(device=device, dtype=torch.int64).contiguous(), dim
+    coords = coords.to(device=device, dtype=torch.int32)
     if dim == 3:
         return coords.contiguous(), dim
     c4 = torch.zeros((coords.shape[0], 4), dtype=torch.int32, device=device)
     c4[:, : 1 + dim] = coords
     return c4, dim
+
+
+def widen(c: torch.Tensor, dim: int) -> torch.Tensor:
+    """Packed (N, 4) int32 -> wide (N, 1+D) int64 (identity on wide rows)."""
+    return c if is_wide(c) else c[:, : 1 + dim].to(torch.int64).contiguous()
 
 
 def _to_features(features, device) -> torch.Tensor:
@@ -76,8 +106,12 @@ def validate(coords4: torch.Tensor, features: Optional[torch.Tensor], stride: tu
     n = coords4.shape[0]
     flags = torch.zeros(1, dtype=torch.int32, device=coords4.device)
     st = _lib.stream()
-    ts = tuple(stride) + (1,) * (3 - dim)
-    if n:
+    if n and is_wide(coords4):
+        ws = _lib.workspace(_lib.query("vp_wide_ws_bytes", n, 0, dim + 1, 1), coords4.device)
+        _lib.call("vp_wide_validate", coords4.data_ptr(), n, dim + 1, _lib.i64_array(stride), flags.data_ptr(),
+                  ws.data_ptr(), ws.numel(), st)
+    elif n:
+        ts = tuple(stride) + (1,) * (3 - dim)
         ws = _lib.workspace(_lib.query("vp_validate_coords_ws_bytes", n), coords4.device)
         _lib.call("vp_validate_coords", coords4.data_ptr(), None, n, _lib.i32_array(ts), flags.data_ptr(),
                   ws.data_ptr(), ws.numel(), st)
@@ -132,7 +166,11 @@ class SparseTensor:
 
     @property
     def coords(self) -> torch.Tensor:
-        return self.coords4[:, : 1 + self.dim]
+        return self.coords4 if is_wide(self.coords4) else self.coords4[:, : 1 + self.dim]
+
+    @property
+    def wide(self) -> bool:
+        return is_wide(self.coords4)
 
     @property
     def feature_width(self) -> int:
@@ -302,9 +340,10 @@ def batch(tensors: Sequence[SparseTensor]) -> SparseTensor:
     for t in tensors[1:]:
         if t.dim != t0.dim or t.feature_width != t0.feature_width or t.tensor_stride != t0.tensor_stride:
             raise StructuralError("batched tensors must share D, D_f and stride")
+    wide = any(t.wide for t in tensors) or len(tensors) - 1 > PACKED_BATCH_MAX
     cs = []
     for i, t in enumerate(tensors):
-        c = t.coords4.clone()
+        c = widen(t.coords4, t.dim).clone() if wide else t.coords4.clone()
         c[:, 0] = i
         cs.append(c)
     coords = torch.cat(cs, 0)

@@ -3,11 +3,13 @@ active voxels (6 / 55 / 552 synthetic ModelNet40-shaped clouds x 2048 pts at
 64^3), C_in = C_out in {32, 64, 128, 256}, kernel 3^3, stride 1 / 2 and the
 transposed (stride-2 adjoint) conv, forward + dgrad + wgrad.
 
-Every kernel is timed alone with CUDA events on its launch stream (warm L2,
-iters back to back) and reported against SURVEY §8(d)'s algorithmic work:
+Every kernel is timed alone with CUDA events on its launch stream, the L2
+flushed before every launch (paper_2012_13846_b200/roofline.py), and reported
+against SURVEY §8(d)'s algorithmic work:
   map  : B = 16 N_in + 16 N_out + 8 P                      (HBM bound)
   conv : F = 2 P C_in C_out ; B = 2 N_in C_in + 2 N_out C_out + 2*27*C_in*C_out
-         + 4*27*N_out (neighbour table)  -> bound = tensor if F/B*HBM > TC
+         + 8 P (wgrad: + 4*27*C_in*C_out fp32 instead of the bf16 weights)
+         -> bound = tensor if F/B*HBM > TC
 Prints one JSON line per (N, C, mode) and writes them to --out."""
 import argparse
 import json
@@ -23,33 +25,23 @@ import torch  # noqa: E402
 
 import voxpipe_oracle as O  # noqa: E402
 from paper_2012_13846_b200 import _lib, conv, tensor  # noqa: E402
+from paper_2012_13846_b200 import roofline as RL  # noqa: E402
 
-PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-    os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
-HBM, TC = PEAKS["hbm_gbs"], PEAKS["bf16_tflops"]
+HBM, TC, _ = RL.peaks()
+_FLUSH = []
 
 
 def timeit(fn, iters):
-    for _ in range(3):
-        fn()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record()
-    for _ in range(iters):
-        fn()
-    b.record()
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) / iters * 1e-3  # seconds
+    if not _FLUSH:
+        _FLUSH.append(RL.Flusher(torch.device("cuda")))
+    return RL.time_cold(fn, _FLUSH[0], iters)
 
 
-def conv_roof(P, n_in, n_out, cin, cout, t):
-    F = 2.0 * P * cin * cout
-    B = 2 * n_in * cin + 2 * n_out * cout + 2 * 27 * cin * cout + 4 * 27 * n_out
-    tf, gbs = F / t / 1e12, B / t / 1e9
-    tensor_bound = (F / B) * HBM / 1e3 > TC
-    frac = tf / TC if tensor_bound else gbs / HBM
-    return {"us": round(t * 1e6, 2), "tflops": round(tf, 1), "gbs": round(gbs, 1),
-            "bound": "tensor" if tensor_bound else "hbm", "frac": round(frac, 4), "F": F, "B": B}
+def conv_roof(P, n_in, n_out, cin, cout, t, mode="fwd"):
+    F, B = RL.conv_work(P, n_in, n_out, cin, cout, 27, mode)
+    r = RL.classify(F, B, t, HBM, TC)
+    return {"us": r["us_per_launch"], "tflops": r["tflops"], "gbs": r["gbs"], "bound": r["bound"],
+            "frac": r["frac"], "F": F, "B": B}
 
 
 def main():
@@ -126,7 +118,7 @@ def main():
                               wsw.data_ptr(), wsw.numel(), st)
 
                 for mode, fn, ni, no in (("fwd", fwd, n, n_out), ("dgrad", dgrad, n_out, n), ("wgrad", wgrad, n, n_out)):
-                    r = conv_roof(P, ni, no, c, c, timeit(fn, a.iters))
+                    r = conv_roof(P, ni, no, c, c, timeit(fn, a.iters), mode)
                     rec = {"mode": f"{mode}_s{stride}", "N_in": n, "N_out": n_out, "C": c, "pairs": P, **r}
                     if stride == 2 and mode == "dgrad":
                         rec["note"] = "= transposed conv (coarse->fine) over the inverse map"
