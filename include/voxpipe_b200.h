@@ -185,9 +185,12 @@ int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t 
  *   perm   : nullable; table row i holds the neighbours of output row
  *            perm[i] (vp_kernel_map_sort), which is where its result goes.
  *   w      : [K, c_out, c_in] in w_dtype.
- *   x_rows : rows allocated in x (every table entry is < x_rows); the
- *            tensor-core path gathers rows with TMA tile::gather4 and
- *            encodes a missing neighbour as row x_rows (zero fill). */
+ *   x_rows : rows allocated in x (every table entry is < x_rows); checked
+ *            by the shim only.  The tensor-core path gathers rows with
+ *            16-byte cp.async (8 lanes per 128 B row) and zero-fills a
+ *            missing neighbour (table entry -1) with a 0-byte source; the
+ *            per-tile [128, K] table slab is staged with one bulk copy
+ *            (cp.async.bulk, SASS UBLKCP), not TMA tensor maps. */
 int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t c_in, const void* w, int32_t w_dtype,
                 int64_t c_out, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
                 const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype,

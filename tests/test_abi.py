@@ -61,6 +61,9 @@ def test_library_is_sm100a_and_uses_tcgen05(lib):
     out = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "UTCHMMA" in out and "LDTM" in out  # tcgen05.mma / tcgen05.ld in SASS
+    # gathered rows move by cp.async (LDGSTS), the per-tile
+    # neighbour-table slab by a bulk copy (UBLKCP)
+    assert "LDGSTS" in out and "UBLKCP" in out
 
 
 def test_product_has_no_oracle_import():
