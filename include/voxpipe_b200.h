@@ -246,6 +246,43 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gy_dtype, const void
                    const float* mean, const float* rstd, const float* gamma, int32_t relu,
                    void* grad_x, int32_t gx_dtype, void* grad_res, float* ggamma, float* gbeta,
                    void* ws, size_t ws_bytes, vp_stream_t stream);
+/* ---- BN statistics fused into the producing conv (no reference code:
+ * SPEC.md:184-185 non-goal).  The conv forward (or the dgrad of the NEXT
+ * conv) writes per-CTA fp32 partial sums of the BN statistics from its
+ * epilogue, so the critical path runs conv -> apply instead of conv ->
+ * statistics pass -> apply.
+ *   bn_part : vp_bn_part_bytes(C) bytes, device; int header (rows written,
+ *             set on the device by the producer) + [rows][2][C] fp32.
+ *   bn_mode : 0 off (plain vp_conv_fwd / vp_conv_dgrad);
+ *             1 forward: partials (sum y, sum y^2) of the stored output;
+ *             2 backward: the output becomes g = round(y) [+ bn_add],
+ *               zeroed where bn_act <= 0 (ReLU mask; bn_act nullable),
+ *               stored rounded; partials (sum g, sum g*(bn_pre - bn_mean)).
+ *   bn_add/bn_act/bn_pre: same dtype and shape as the conv output.
+ * A bf16 tensor-core conv fuses it into its epilogue (or its split-K
+ * reduction); every other path runs one extra pass over the output. */
+size_t vp_bn_part_bytes(int64_t C);
+int vp_conv_fwd_bn(const void* x, int32_t x_dtype, int64_t x_rows, int64_t c_in, const void* w, int32_t w_dtype,
+                   int64_t c_out, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                   const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
+                   int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act, const void* bn_pre,
+                   const float* bn_mean, vp_stream_t stream);
+int vp_conv_dgrad_bn(const void* g, int32_t g_dtype, int64_t g_rows, int64_t c_out, const void* w, int32_t w_dtype,
+                     int64_t c_in, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                     const int32_t* n_in_dev, int64_t cap_in, void* grad_in, int32_t gi_dtype, void* ws,
+                     size_t ws_bytes, int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act,
+                     const void* bn_pre, const float* bn_mean, vp_stream_t stream);
+/* vp_bn_apply with the statistics reduced from a mode-1 bn_part (fixed
+ * order); also stores mean/rstd for the backward. */
+int vp_bn_apply_part(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C, float eps,
+                     const void* bn_part, float* mean, float* rstd, const float* gamma, const float* beta,
+                     const void* res, int32_t res_dtype, int32_t relu, void* y, int32_t y_dtype, vp_stream_t stream);
+/* BN backward from a mode-2 bn_part: gm is the masked gradient the producer
+ * stored; writes grad_x and ggamma/gbeta [C]. */
+int vp_bn_backward_part(const void* gm, int32_t gm_dtype, const void* x, int32_t x_dtype, const int32_t* n_dev,
+                        int64_t cap_n, int64_t C, const float* mean, const float* rstd, const float* gamma,
+                        const void* bn_part, void* grad_x, int32_t gx_dtype, float* ggamma, float* gbeta,
+                        vp_stream_t stream);
 /* global average pool per batch index (rows batch-contiguous):
  * out [B, C] fp32, counts [B] int32 */
 int vp_global_pool(const void* x, int32_t x_dtype, const int32_t* coords, const int32_t* n_dev,

@@ -19,6 +19,7 @@
 // workspace and a second kernel sums the chunks of each offset in a fixed
 // order -> deterministic.
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "conv_fwd_tc.cuh"
@@ -361,16 +362,26 @@ constexpr int kStemRows = 128;
 // 16 output channels per pass keeps a thread at <= 64 registers: 8 CTAs per
 // SM, so C3's ~900 tiles run as one wave (at 128 registers they took two).
 constexpr int kStemPass = 16;
+constexpr int kStemCluster = 4;  // CTAs per cluster when the stem also writes BN statistics
 template <int XT>
 __global__ void __launch_bounds__(kStemRows, 8)
 conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict__ w, int w_dtype, int cout,
                  const int32_t* __restrict__ table, int flip, const int32_t* __restrict__ perm,
-                 const int32_t* n_out_dev, int64_t cap_out, __nv_bfloat16* __restrict__ y) {
+                 const int32_t* n_out_dev, int64_t cap_out, __nv_bfloat16* __restrict__ y, const BnEpi bn) {
   ::vp::pdl_begin();
   extern __shared__ float s_mem[];
   float* s_w = s_mem;                                             // [27][cout]
   int* s_t = reinterpret_cast<int*>(s_w + 27 * cout);             // [128][27]
   uint32_t* s_o = reinterpret_cast<uint32_t*>(s_t + kStemRows * 27);  // [128][8 + 1] packed bf16 pairs
+  // BN statistics (e.mode == 1): this CTA's per-channel (sum, sum^2) of the
+  // stored bf16 outputs, accumulated tile by tile by a fixed owner thread
+  float* s_acc = reinterpret_cast<float*>(s_o + kStemRows * 9);   // [2][cout]
+  float* s_wp = s_acc + 2 * cout;                                 // [4 warps][8 pairs][4]
+  const bool stats = bn.mode == 1;
+  if (stats) {
+    for (int c = threadIdx.x; c < 2 * cout; c += kStemRows) s_acc[c] = 0.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *bn.nb = gridDim.x / kStemCluster;
+  }
 #pragma unroll 8
   for (int e = threadIdx.x; e < 27 * cout; e += kStemRows) {
     if (XT == VP_BF16)
@@ -436,13 +447,73 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
       }
       __syncthreads();
       // coalesced: word e of the tile -> row e / 8, pair e % 8
-      for (int e = threadIdx.x; e < rows * 8; e += kStemRows) {
-        const int rr = e >> 3, c = e & 7;
+      for (int el = threadIdx.x; el < rows * 8; el += kStemRows) {
+        const int rr = el >> 3, c = el & 7;
         const int64_t orow = perm ? (int64_t)__ldg(perm + u0 + rr) : u0 + rr;
         reinterpret_cast<uint32_t*>(y + orow * cout + c0)[c] = s_o[rr * 9 + c];
       }
+      if (stats) {
+        // thread t: channel pair t & 7 over rows 8*(t>>3) .. +8, then an xor
+        // tree over the warp's 4 row groups, then the 4 warps in order
+        const int cp = threadIdx.x & 7, rg = threadIdx.x >> 3;
+        float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int rr = rg * 8 + r;
+          if (rr < rows) {
+            const uint32_t pk = s_o[rr * 9 + cp];
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk));
+            a0 += f.x;
+            a1 += f.y;
+            b0 += f.x * f.x;
+            b1 += f.y * f.y;
+          }
+        }
+#pragma unroll
+        for (int m = 8; m < 32; m <<= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, m);
+          a1 += __shfl_xor_sync(0xffffffffu, a1, m);
+          b0 += __shfl_xor_sync(0xffffffffu, b0, m);
+          b1 += __shfl_xor_sync(0xffffffffu, b1, m);
+        }
+        const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+        if (lane < 8) {
+          float* d = s_wp + (wp * 8 + lane) * 4;
+          d[0] = a0;
+          d[1] = a1;
+          d[2] = b0;
+          d[3] = b1;
+        }
+        __syncthreads();
+        if (threadIdx.x < kStemPass) {  // channel c0 + t: pair t/2, half t&1
+          const int t = threadIdx.x, pr = t >> 1, hf = t & 1;
+          float sa = 0.f, sb = 0.f;
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) {
+            sa += s_wp[(w4 * 8 + pr) * 4 + hf];
+            sb += s_wp[(w4 * 8 + pr) * 4 + 2 + hf];
+          }
+          s_acc[c0 + t] += sa;
+          s_acc[cout + c0 + t] += sb;
+        }
+      }
       __syncthreads();
     }
+  }
+  if (stats) {
+    // the cluster's CTAs in rank order -> one partial row per cluster
+    // (launched with kStemCluster-CTA clusters: a full one-wave grid, few rows)
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (cl.block_rank() == 0) {
+      for (int c = threadIdx.x; c < 2 * cout; c += kStemRows) {
+        float acc = 0.f;
+        for (int r = 0; r < kStemCluster; ++r) acc += cl.map_shared_rank(s_acc, r)[c];
+        bn.part[(int64_t)(blockIdx.x / kStemCluster) * 2 * cout + c] = acc;
+      }
+    }
+    cl.sync();  // remote shared memory stays alive until rank 0 has read it
   }
 }
 
@@ -475,16 +546,28 @@ static int launch_rows32(const bf16* x, const bf16* w, int K, const int32_t* tab
 
 static bool small_fwd_ok(int64_t cin, int64_t cout, int K) { return cin <= 4 && (int64_t)K * cin * cout <= 12288; }
 
+// epi: BN statistics from the stem kernel (mode 1) when it runs; the caller
+// runs the generic pass otherwise (*fused reports which)
 static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int wd, int cout, int K,
                             const int32_t* table, int flip, const int32_t* perm, const int32_t* n_out_dev,
-                            int64_t cap_out, void* y, int yd, cudaStream_t st) {
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), grid_cap(8)));
+                            int64_t cap_out, void* y, int yd, cudaStream_t st, const BnEpi& epi = BnEpi{},
+                            bool* fused = nullptr) {
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cap_out, 128), grid_cap(8)));
+  if (fused) *fused = false;
   if (cin == 1 && K == 27 && cout % 32 == 0 && cout <= 256 && yd == VP_BF16) {
-    const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 9 * 4;
+    const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 9 * 4 + 2 * cout * 4 + 4 * 8 * 4 * 4;
     const int dt = xd == wd ? xd : -1;
     auto kern = dt == VP_BF16 ? conv_stem_kernel<VP_BF16> : dt == VP_F32 ? conv_stem_kernel<VP_F32> : conv_stem_kernel<-1>;
-    ::vp::launch(kern, blocks, kStemRows, smem, st, x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
-                 (__nv_bfloat16*)y);
+    BnEpi e = epi.mode == 1 ? epi : BnEpi{};
+    if (e.mode == 1) {  // clusters of kStemCluster CTAs, one partial row each
+      blocks = (int)std::min<int64_t>(ceil_div(blocks, kStemCluster) * kStemCluster, (int64_t)kBnPartRows * kStemCluster);
+      if (fused) *fused = true;
+      ::vp::launch_cluster(kern, kStemCluster, blocks, kStemRows, smem, st, x, xd, w, wd, cout, table, flip, perm,
+                           n_out_dev, cap_out, (__nv_bfloat16*)y, e);
+    } else {
+      ::vp::launch(kern, blocks, kStemRows, smem, st, x, xd, w, wd, cout, table, flip, perm, n_out_dev, cap_out,
+                   (__nv_bfloat16*)y, e);
+    }
     VP_CHECK_LAUNCH("conv_stem");
     return VP_OK;
   }
@@ -492,6 +575,80 @@ static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int w
                                                                          perm, n_out_dev, cap_out, y, yd);
   VP_CHECK_LAUNCH("conv_fwd_small");
   return VP_OK;
+}
+
+// ------------------------------------------------------------------ BN epilogue (generic)
+// The bn_epi.cuh transform for the paths without a fused epilogue (SIMT,
+// stem, fp32/f64 outputs, the row-compacted kernel): one pass over the
+// conv's output rows in place after the conv.  Block b owns rows b, b+G, ...
+// (lanes rows at a time); per-channel sums in a fixed order.
+__device__ __forceinline__ float round_to(int dtype, float v) { return dtype == VP_BF16 ? bf16_round(v) : v; }
+
+__global__ void __launch_bounds__(256)
+bn_epi_rows_kernel(void* __restrict__ y, int yd, const int32_t* n_dev, int64_t cap, int C, const BnEpi e) {
+  ::vp::pdl_begin();
+  __shared__ float s_a[256], s_b[256];
+  const int n = load_count(n_dev, cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *e.nb = gridDim.x;
+  for (int c0 = 0; c0 < C; c0 += 256) {
+    const int cc = min(256, C - c0);
+    const int lanes = 256 / cc;
+    const int c = c0 + (int)threadIdx.x % cc, lr = (int)threadIdx.x / cc;
+    float a = 0.f, b = 0.f;
+    if (lr < lanes) {
+      const float mu = e.mode == 2 ? e.mean[c] : 0.f;
+      for (int64_t r = (int64_t)blockIdx.x * lanes + lr; r < n; r += (int64_t)gridDim.x * lanes) {
+        const int64_t i = r * C + c;
+        const float v = ldf(y, yd, i);
+        if (e.mode == 2) {
+          float g = v + (e.add ? ldf(e.add, yd, i) : 0.f);
+          g = (e.act == nullptr || ldf(e.act, yd, i) > 0.f) ? round_to(yd, g) : 0.f;
+          stf(y, yd, i, g);
+          a += g;
+          b += g * (ldf(e.pre, yd, i) - mu);
+        } else {
+          a += v;
+          b += v * v;
+        }
+      }
+    }
+    s_a[threadIdx.x] = a;
+    s_b[threadIdx.x] = b;
+    __syncthreads();
+    if ((int)threadIdx.x < cc) {
+      float sa = 0.f, sb = 0.f;
+      for (int l = 0; l < lanes; ++l) {
+        sa += s_a[l * cc + threadIdx.x];
+        sb += s_b[l * cc + threadIdx.x];
+      }
+      e.part[((int64_t)blockIdx.x * 2) * C + c0 + threadIdx.x] = sa;
+      e.part[((int64_t)blockIdx.x * 2 + 1) * C + c0 + threadIdx.x] = sb;
+    }
+    __syncthreads();
+  }
+}
+
+static int launch_bn_epi_rows(void* y, int yd, const int32_t* n_dev, int64_t cap, int64_t C, const BnEpi& e,
+                              cudaStream_t st) {
+  const int64_t lanes = std::max<int64_t>(1, 256 / std::min<int64_t>(C, 256));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(cap, 1), lanes * 8), kNumSMs));
+  ::vp::launch(bn_epi_rows_kernel, grid, 256, 0, st, y, yd, n_dev, cap, (int)C, e);
+  VP_CHECK_LAUNCH("bn_epi_rows");
+  return VP_OK;
+}
+
+// caller buffer -> BnEpi (header int nb, partial rows after kBnPartHeader bytes)
+static BnEpi make_epi(int32_t mode, void* bn_part, const void* add, const void* act, const void* pre,
+                      const float* mean) {
+  BnEpi e{};
+  e.mode = bn_part ? mode : 0;
+  e.nb = (int*)bn_part;
+  e.part = bn_part ? (float*)((char*)bn_part + kBnPartHeader) : nullptr;
+  e.add = add;
+  e.act = act;
+  e.pre = pre;
+  e.mean = mean;
+  return e;
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -525,7 +682,13 @@ static int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   p.dbg = dbg;
   ::vp::launch(kern, grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st, p);
   VP_CHECK_LAUNCH("conv_tc");
-  if (part) {
+  if (part && p.epi.mode != 0) {  // bf16 output + BN statistics: at most one partial row per SM
+    const int64_t work = p.cap_out * ND / 4;
+    ::vp::launch(split_reduce_epi_kernel<ND>,
+                 (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, kSplitEpiThreads), kNumSMs)),
+                 kSplitEpiThreads, 0, st, (const float*)part, p.n_out_dev, p.cap_out, grid, p.max_split, p.perm, (bf16*)p.y, p.epi);
+    VP_CHECK_LAUNCH("split_reduce_epi");
+  } else if (part) {
     const int64_t work = p.cap_out * ND / 4;
     ::vp::launch(split_reduce_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), grid_cap(8))), 256, 0, st, 
         (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.perm, p.y, p.y_dtype);
@@ -686,15 +849,45 @@ size_t vp_conv_fwd_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
   return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cout);
 }
 
+static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype,
+                         int64_t cout, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                         const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
+                         const BnEpi& epi, cudaStream_t st);
+
 int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype, int64_t cout,
                 int32_t K, const int32_t* table, int32_t flip, const int32_t* perm, const int32_t* n_out_dev,
                 int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return conv_fwd_impl(x, x_dtype, x_rows, cin, w, w_dtype, cout, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype,
+                       ws, ws_bytes, BnEpi{}, (cudaStream_t)stream);
+}
+
+size_t vp_bn_part_bytes(int64_t C) { return kBnPartHeader + (size_t)kBnPartRows * 2 * std::max<int64_t>(C, 1) * 4; }
+
+int vp_conv_fwd_bn(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype,
+                   int64_t cout, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                   const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
+                   int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act, const void* bn_pre,
+                   const float* bn_mean, vp_stream_t stream) {
+  VP_REQUIRE(bn_mode >= 0 && bn_mode <= 2 && (bn_mode == 0 || bn_part), VP_EVALIDATION, "conv_fwd_bn: bad bn mode");
+  VP_REQUIRE(bn_mode != 2 || (bn_pre && bn_mean), VP_EVALIDATION, "conv_fwd_bn: mode 2 needs pre and mean");
+  return conv_fwd_impl(x, x_dtype, x_rows, cin, w, w_dtype, cout, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype,
+                       ws, ws_bytes, make_epi(bn_mode, bn_part, bn_add, bn_act, bn_pre, bn_mean), (cudaStream_t)stream);
+}
+
+static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype,
+                         int64_t cout, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                         const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
+                         const BnEpi& epi, cudaStream_t st) {
+  // the generic BN pass after any conv path without a fused epilogue
+  auto epi_after = [&](int rc) -> int {
+    if (rc != VP_OK || epi.mode == 0) return rc;
+    return launch_bn_epi_rows(y, y_dtype, n_out_dev, cap_out, cout, epi, st);
+  };
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(cin >= 1 && cout >= 1, VP_EVALIDATION, "channel widths must be positive");
   VP_REQUIRE(y_dtype == VP_F32 || y_dtype == VP_BF16 || y_dtype == VP_F64, VP_EVALIDATION,
              "output dtype must be f32, bf16 or f64");
-  if (cap_out <= 0) return VP_OK;
+  if (cap_out <= 0) return epi_after(VP_OK);
   const bool f64 = x_dtype == VP_F64 || w_dtype == VP_F64 || y_dtype == VP_F64;
   if (!f64 && x_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
     VP_REQUIRE(ws && ws_bytes >= vp_conv_fwd_ws_bytes(cin, cout, K), VP_EVALIDATION, "conv_fwd: workspace too small");
@@ -708,34 +901,70 @@ int vp_conv_fwd(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, con
     }
     (void)x_rows;  // the cp.async gather zero-fills missing neighbours itself
     if (rows32_ok(cin, cout, K))
-      return launch_rows32<false>((const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, st);
+      return epi_after(
+          launch_rows32<false>((const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, st));
     FwdParams p{(const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
-    return conv_tc<false>(cin, cout, p, part, st);
+    if (y_dtype == VP_BF16) {
+      p.epi = epi;  // fused into the epilogue / split-K reduction
+      return conv_tc<false>(cin, cout, p, part, st);
+    }
+    return epi_after(conv_tc<false>(cin, cout, p, part, st));
   }
-  if (!f64 && small_fwd_ok(cin, cout, K))
-    return launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip, perm, n_out_dev, cap_out, y,
-                            y_dtype, st);
+  if (!f64 && small_fwd_ok(cin, cout, K)) {
+    bool fused = false;
+    const int rc = launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip, perm, n_out_dev,
+                                    cap_out, y, y_dtype, st, epi, &fused);
+    return fused ? rc : epi_after(rc);
+  }
   const int64_t total = cap_out * cout;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
   ::vp::launch(f64 ? conv_fwd_simt_kernel<double> : conv_fwd_simt_kernel<float>, blocks, 256, 0, st, x, x_dtype,
                (int)cin, w, w_dtype, cout * cin, cin, 1, (int)cout, K, table, flip, perm, n_out_dev, cap_out, y,
                y_dtype);
   VP_CHECK_LAUNCH("conv_fwd_simt");
-  return VP_OK;
+  return epi_after(VP_OK);
 }
 
 size_t vp_conv_dgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
   return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cin);
 }
 
+static int conv_dgrad_impl(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, const void* w, int32_t w_dtype,
+                           int64_t cin, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                           const int32_t* n_in_dev, int64_t cap_in, void* gi, int32_t gi_dtype, void* ws,
+                           size_t ws_bytes, const BnEpi& epi, cudaStream_t st);
+
 int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, const void* w, int32_t w_dtype, int64_t cin,
                   int32_t K, const int32_t* table, int32_t flip, const int32_t* perm, const int32_t* n_in_dev,
                   int64_t cap_in, void* gi, int32_t gi_dtype, void* ws, size_t ws_bytes, vp_stream_t stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return conv_dgrad_impl(g, g_dtype, g_rows, cout, w, w_dtype, cin, K, table, flip, perm, n_in_dev, cap_in, gi,
+                         gi_dtype, ws, ws_bytes, BnEpi{}, (cudaStream_t)stream);
+}
+
+int vp_conv_dgrad_bn(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, const void* w, int32_t w_dtype,
+                     int64_t cin, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                     const int32_t* n_in_dev, int64_t cap_in, void* gi, int32_t gi_dtype, void* ws, size_t ws_bytes,
+                     int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act, const void* bn_pre,
+                     const float* bn_mean, vp_stream_t stream) {
+  VP_REQUIRE(bn_mode >= 0 && bn_mode <= 2 && (bn_mode == 0 || bn_part), VP_EVALIDATION, "conv_dgrad_bn: bad bn mode");
+  VP_REQUIRE(bn_mode != 2 || (bn_pre && bn_mean), VP_EVALIDATION, "conv_dgrad_bn: mode 2 needs pre and mean");
+  return conv_dgrad_impl(g, g_dtype, g_rows, cout, w, w_dtype, cin, K, table, flip, perm, n_in_dev, cap_in, gi,
+                         gi_dtype, ws, ws_bytes, make_epi(bn_mode, bn_part, bn_add, bn_act, bn_pre, bn_mean),
+                         (cudaStream_t)stream);
+}
+
+static int conv_dgrad_impl(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, const void* w, int32_t w_dtype,
+                           int64_t cin, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
+                           const int32_t* n_in_dev, int64_t cap_in, void* gi, int32_t gi_dtype, void* ws,
+                           size_t ws_bytes, const BnEpi& epi, cudaStream_t st) {
+  auto epi_after = [&](int rc) -> int {
+    if (rc != VP_OK || epi.mode == 0) return rc;
+    return launch_bn_epi_rows(gi, gi_dtype, n_in_dev, cap_in, cin, epi, st);
+  };
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(gi_dtype == VP_F32 || gi_dtype == VP_BF16 || gi_dtype == VP_F64, VP_EVALIDATION,
              "grad_in dtype must be f32, bf16 or f64");
-  if (cap_in <= 0) return VP_OK;
+  if (cap_in <= 0) return epi_after(VP_OK);
   const bool f64 = g_dtype == VP_F64 || w_dtype == VP_F64 || gi_dtype == VP_F64;
   if (!f64 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
     VP_REQUIRE(ws && ws_bytes >= vp_conv_dgrad_ws_bytes(cin, cout, K), VP_EVALIDATION,
@@ -751,9 +980,14 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
     // grad_in = sum_k W_k^T g[table]: GEMM K-dim = C_out, N = C_in, W read as MN-major B
     (void)g_rows;
     if (rows32_ok(cout, cin, K))
-      return launch_rows32<true>((const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, st);
+      return epi_after(
+          launch_rows32<true>((const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, st));
     FwdParams p{(const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1, 0, 0};
-    return conv_tc<true>(cout, cin, p, part, st);
+    if (gi_dtype == VP_BF16) {
+      p.epi = epi;
+      return conv_tc<true>(cout, cin, p, part, st);
+    }
+    return epi_after(conv_tc<true>(cout, cin, p, part, st));
   }
   const int64_t total = cap_in * cin;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
@@ -762,7 +996,7 @@ int vp_conv_dgrad(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, 
                (int)cout, w, w_dtype, cout * cin, 1, cin, (int)cin, K, table, flip, perm, n_in_dev, cap_in, gi,
                gi_dtype);
   VP_CHECK_LAUNCH("conv_dgrad_simt");
-  return VP_OK;
+  return epi_after(VP_OK);
 }
 
 constexpr int kWgSimtChunk = 512;  // SIMT path: short chunks, many CTAs

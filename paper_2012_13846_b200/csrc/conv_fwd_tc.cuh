@@ -22,6 +22,7 @@
 // (smem ring and TMEM sized to fit): random-row gather throughput scales with
 // independent CTAs per SM far more than with ring depth (tools/gather_probe2).
 #pragma once
+#include "bn_epi.cuh"
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -44,6 +45,7 @@ struct FwdParams {
   int max_split;  // >= 1
   int stage_tbl;  // stage table tiles in smem (K <= kTblK, 16 B-aligned table); set by the launcher
   int dbg;        // experiments only: bit0 no MMA, bit1 no B copies, bit2 no A copies, bit3 plain arrive for empty, bit4 every offset active (no mask scan)
+  BnEpi epi;      // BN statistics of the output (bn_epi.cuh); mode 0 = off.  Needs a bf16 output.
 };
 
 constexpr int kTcProd = 128, kTcEpi = 128, kTcThreads = kTcProd + kTcEpi + 32;
@@ -140,6 +142,10 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   // split partials are sized for kNumSMs work items
   const int S = split_count(ntiles, min((int)gridDim.x, kSplitItems), p.max_split);
   const int total = ntiles * S;
+  // BN partial rows: one per CTA that owns work (the split-K reduction
+  // writes them instead when the tiles are split)
+  const bool epi = p.epi.mode != 0 && S == 1;
+  if (epi && blockIdx.x == 0 && tid == 0) *p.epi.nb = min((int)gridDim.x, total);
   if ((int)blockIdx.x >= total) return;
 
   if (tid == 0) {
@@ -166,6 +172,11 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   const uint32_t tmem = *s_tmem;
   const uint32_t sbase = tc::smem_u32(smem);
 
+  // BN statistics (epi): lane l of each epilogue warp accumulates channel
+  // 32*j + l over the warp's rows of every item, in item order
+  float bs1[ND / 32], bs2[ND / 32];
+#pragma unroll
+  for (int j = 0; j < ND / 32; ++j) bs1[j] = bs2[j] = 0.f;
   if (warp < 4) {
     // ============================ producers ============================
     constexpr bool tbl = TBL;
@@ -394,6 +405,31 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
         scan_item(w + gridDim.x, ii + 1);
       }
       const int a = ii % C::ACC;
+      if (epi && p.epi.mode == 2 && (p.dbg & 96)) {
+        // experiment (VP_CONV_DBG bit 5: bulk, bit 6: per-line): this item's
+        // rows of the BN operands (add / act / pre) head for L2 while the
+        // accumulator is still being produced
+#pragma unroll 1
+        for (int t = 0; t < TT; ++t) {
+          const int64_t row = (int64_t)tile * TR + t * 128 + ep * 32 + lane;
+          if (row < n_out) {
+            const int64_t orow = p.perm != nullptr ? (int64_t)__ldg(p.perm + row) : row;
+            const int64_t off = orow * ND * 2;
+            const char* srcs[3] = {reinterpret_cast<const char*>(p.epi.add), reinterpret_cast<const char*>(p.epi.act),
+                                   reinterpret_cast<const char*>(p.epi.pre)};
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              if (srcs[q] == nullptr) continue;
+              if (p.dbg & 32) {
+                tc::prefetch_l2(srcs[q] + off, ND * 2);
+              } else {
+#pragma unroll
+                for (int l = 0; l < ND * 2; l += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(srcs[q] + off + l));
+              }
+            }
+          }
+        }
+      }
       tc::mbar_wait(&tfull[a], (ii / C::ACC) & 1);
       trace_ev(1024 + 4 * (ii & 63) + 2, ep == 0 && lane == 0);
       tc::tc_fence_after();
@@ -402,6 +438,22 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       for (int t = 0; t < TT; ++t) {
       const int64_t row = (int64_t)tile * TR + t * 128 + lrow;
       const int64_t orow = (p.perm != nullptr && row < n_out) ? (int64_t)__ldg(p.perm + row) : row;
+      if (epi) {  // bf16 output + BN statistics (all lanes: the sums are warp-collective)
+#pragma unroll 1
+        for (int j = 0; j < ND / 32; ++j) {
+          float v[32];
+          tc::tmem_ld32(tmem + ((uint32_t)(ep * 32) << 16) + (a * TT + t) * ND + 32 * j, v);
+          float s1, s2;
+          bn_epi_chunk32<ND>(p.epi, v, row < n_out, orow, 32 * j, reinterpret_cast<bf16*>(p.y), s1, s2);
+#pragma unroll
+          for (int jj = 0; jj < ND / 32; ++jj)  // register-resident accumulators (no dynamic index)
+            if (jj == j) {
+              bs1[jj] += s1;
+              bs2[jj] += s2;
+            }
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < ND; c0 += 32) {
         float v[32];
@@ -481,6 +533,26 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   }
   __syncthreads();
   if (warp == 8) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+  if (epi && warp >= 4 && warp < 8) {
+    // the 4 warps' sums in warp order -> this CTA's partial row (the stage
+    // ring is free: every copy and MMA has completed)
+    float* red = reinterpret_cast<float*>(smem);  // [4][2][ND]
+    const int ep = warp - 4, etid = tid - 128;
+#pragma unroll
+    for (int j = 0; j < ND / 32; ++j) {
+      red[(ep * 2 + 0) * ND + 32 * j + lane] = bs1[j];
+      red[(ep * 2 + 1) * ND + 32 * j + lane] = bs2[j];
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    float* dst = p.epi.part + (int64_t)blockIdx.x * 2 * ND;
+    for (int e = etid; e < 2 * ND; e += kTcEpi) {
+      const int h = e / ND, c = e - h * ND;
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) acc += red[(w * 2 + h) * ND + c];
+      dst[e] = acc;
+    }
+  }
 }
 
 // out[r, n] = sum over splits of the fp32 partials, in split order.
@@ -515,6 +587,92 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_
     } else {
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + oidx) = acc;
     }
+  }
+}
+
+// split_reduce_kernel + the BN epilogue (bn_epi.cuh) for a bf16 output:
+// thread t always owns channels [(4t) % ND, +4) (ND divides 4096), so its
+// statistics accumulate in registers; the block then sums its threads in a
+// fixed order into partial row blockIdx.x.
+constexpr int kSplitEpiThreads = 1024;  // wide blocks: <= 148 partial rows, as many threads as the plain reduction
+template <int ND>
+__global__ void __launch_bounds__(kSplitEpiThreads)
+split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev, int64_t cap_out, int grid,
+                        int max_split, const int32_t* __restrict__ perm, bf16* __restrict__ y, const BnEpi e) {
+  ::vp::pdl_begin();
+  __shared__ float s_red[2][kSplitEpiThreads][4];
+  const int n_out = load_count(n_out_dev, cap_out);
+  const int ntiles = (n_out + 127) / 128;
+  const int S = split_count(ntiles, grid < kSplitItems ? grid : kSplitItems, max_split);
+  if (S <= 1) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *e.nb = gridDim.x;
+  const int n = (threadIdx.x * 4) % ND;
+  float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+  const int64_t total = (int64_t)n_out * ND / 4;
+  for (int64_t el = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; el < total; el += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = el * 4 / ND;
+    const int tile = (int)(r >> 7), lr = (int)(r & 127);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int s = 0; s < S; ++s) {  // loads batched, sums stay in split order
+      const float4 v = *reinterpret_cast<const float4*>(part + (((int64_t)s * ntiles + tile) * 128 + lr) * ND + n);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    const int64_t oidx = (perm ? (int64_t)__ldg(perm + r) : r) * ND + n;
+    float v[4] = {acc.x, acc.y, acc.z, acc.w}, o[4], h[4];
+    if (e.mode == 2) {
+      uint2 ra = e.add ? __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(e.add) + oidx))
+                       : make_uint2(0u, 0u);
+      uint2 rc = e.act ? __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(e.act) + oidx))
+                       : make_uint2(0x3f803f80u, 0x3f803f80u);
+      uint2 rp = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(e.pre) + oidx));
+      const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&ra);
+      const __nv_bfloat162* hc = reinterpret_cast<const __nv_bfloat162*>(&rc);
+      const __nv_bfloat162* hp = reinterpret_cast<const __nv_bfloat162*>(&rp);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float2 fa = __bfloat1622float2(ha[q]), fc = __bfloat1622float2(hc[q]), fp = __bfloat1622float2(hp[q]);
+        const float fa2[2] = {fa.x, fa.y}, fc2[2] = {fc.x, fc.y}, fp2[2] = {fp.x, fp.y};
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c = 2 * q + j;
+          const float g = bf16_round(v[c]) + fa2[j];
+          o[c] = fc2[j] > 0.f ? bf16_round(g) : 0.f;
+          h[c] = o[c] * (fp2[j] - __ldg(e.mean + n + c));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        o[c] = bf16_round(v[c]);
+        h[c] = o[c] * o[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      a[c] += o[c];
+      b[c] += h[c];
+    }
+    __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(y + oidx);
+    d[0] = __floats2bfloat162_rn(o[0], o[1]);
+    d[1] = __floats2bfloat162_rn(o[2], o[3]);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    s_red[0][threadIdx.x][c] = a[c];
+    s_red[1][threadIdx.x][c] = b[c];
+  }
+  __syncthreads();
+  constexpr int G = ND / 4, M = kSplitEpiThreads * 4 / ND;  // channel quads, threads per quad
+  for (int idx = threadIdx.x; idx < 2 * ND; idx += blockDim.x) {
+    const int hh = idx / ND, c = idx - hh * ND;
+    float acc = 0.f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc += s_red[hh][c / 4 + m * G][c % 4];
+    e.part[((int64_t)blockIdx.x * 2 + hh) * ND + c] = acc;
   }
 }
 

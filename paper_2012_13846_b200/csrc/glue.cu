@@ -460,11 +460,12 @@ bn_apply_kernel(const void* __restrict__ x, int dtype, const int32_t* n_dev, int
                 const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
                 const float* __restrict__ beta, const void* __restrict__ res, int res_dtype, int relu,
                 void* __restrict__ y, int y_dtype, const float* __restrict__ part, int nb, float eps,
-                float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+                float* __restrict__ mean_out, float* __restrict__ rstd_out, const int* __restrict__ nb_dev) {
   extern __shared__ float s_stat[];
   ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   if (part) {
+    if (nb_dev) nb = *nb_dev;  // written by the producer (bn_epi.cuh)
     bn_finalize(part, nb, C, n, true, eps, s_stat, s_stat + C);
     if (blockIdx.x == 0)
       for (int c = threadIdx.x; c < C; c += kGlueThreads) {
@@ -549,12 +550,21 @@ bn_backward_apply_kernel(const void* __restrict__ gy, const void* __restrict__ g
                          const float* __restrict__ rstd, const float* __restrict__ gamma, int relu,
                          const float* __restrict__ ggamma, const float* __restrict__ gbeta, void* __restrict__ gx,
                          int gx_dtype, void* __restrict__ gres, const float* __restrict__ part, int nb,
-                         float* __restrict__ ggamma_out, float* __restrict__ gbeta_out) {
+                         float* __restrict__ ggamma_out, float* __restrict__ gbeta_out, const int* __restrict__ nb_dev) {
   extern __shared__ float s_stat[];
   ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
   if (part) {
-    bn_finalize(part, nb, C, n, false, 0.f, s_stat, s_stat + C);
+    if (nb_dev) {
+      // producer partials (bn_epi.cuh): [0] = sum g, [1] = sum g*(x - mean);
+      // ggamma = rstd * [1]
+      nb = *nb_dev;
+      bn_finalize(part, nb, C, n, false, 0.f, s_stat, s_stat + C);
+      for (int c = threadIdx.x; c < C; c += kGlueThreads) s_stat[c] *= rstd[c];
+      __syncthreads();
+    } else {
+      bn_finalize(part, nb, C, n, false, 0.f, s_stat, s_stat + C);
+    }
     if (blockIdx.x == 0)
       for (int c = threadIdx.x; c < C; c += kGlueThreads) {
         ggamma_out[c] = s_stat[c];
@@ -842,7 +852,7 @@ int vp_bn_forward(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, 
   VP_CHECK_LAUNCH("bn_fwd_stats");
   VP_BN_LAUNCH(bn_apply_kernel, C, one_dtype({xd, yd, res ? rd : xd}), bn_grid_rows(cap, C), kGlueThreads,
                2 * C * sizeof(float), st, x, xd, n_dev, cap, (int)C, (const float*)nullptr, (const float*)nullptr,
-               gamma, beta, res, rd, relu, y, yd, (const float*)ws, nb, eps, mean, rstd);
+               gamma, beta, res, rd, relu, y, yd, (const float*)ws, nb, eps, mean, rstd, (const int*)nullptr);
   VP_CHECK_LAUNCH("bn_fwd_apply");
   return VP_OK;
 }
@@ -856,7 +866,7 @@ int vp_bn_apply(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, in
   const int grid = bn_grid_rows(cap, C);
   VP_BN_LAUNCH(bn_apply_kernel, C, one_dtype({xd, yd, res ? rd : xd}), grid, kGlueThreads, 0, st, x, xd, n_dev, cap,
                (int)C, mean, rstd, gamma, beta, res, rd, relu, y, yd, (const float*)nullptr, 0, 0.f, (float*)nullptr,
-               (float*)nullptr);
+               (float*)nullptr, (const int*)nullptr);
   VP_CHECK_LAUNCH("bn_apply");
   return VP_OK;
 }
@@ -893,9 +903,101 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
     const int grid = bn_grid_rows(cap, C);
     VP_BN_LAUNCH(bn_backward_apply_kernel, C, one_dtype({xd, gyd, relu ? yd : xd, gxd}), grid, kGlueThreads,
                  2 * C * sizeof(float), st, gy, gy2, gyd, y, yd, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, relu,
-                 (const float*)nullptr, (const float*)nullptr, gx, gxd, gres, (const float*)ws, nb, ggamma, gbeta);
+                 (const float*)nullptr, (const float*)nullptr, gx, gxd, gres, (const float*)ws, nb, ggamma, gbeta,
+                 (const int*)nullptr);
     VP_CHECK_LAUNCH("bn_bwd_apply");
   }
+  return VP_OK;
+}
+
+// Reduce a producer's partial rows (bn_epi.cuh layout) to the BN
+// statistics once: block = 32 channels x 32 warps; warps 0-15 sum column 0
+// (sum y | sum g), warps 16-31 column 1, each warp over rows w, w+16, ...
+// (8 loads in flight), in double; then the 16 warps in order.  mode 1:
+// mean / rstd (biased variance, training BN); mode 2: ggamma = rstd * sum
+// g*(x-mean), gbeta = sum g.  A few blocks of L2 reads instead of every
+// apply block re-reducing up to 444 rows.
+__global__ void __launch_bounds__(1024)
+bn_part_finalize_kernel(const void* __restrict__ bn_part, int C, const int32_t* n_dev, int64_t cap, float eps, int mode,
+                        const float* __restrict__ rstd_in, float* __restrict__ out_a, float* __restrict__ out_b) {
+  ::vp::pdl_begin();
+  __shared__ double s[32][33];
+  const int nb = *reinterpret_cast<const int*>(bn_part);
+  const float* part = reinterpret_cast<const float*>(reinterpret_cast<const char*>(bn_part) + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = warp >> 4, wg = warp & 15;
+  const int c = blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (c < C) {
+    for (int b0 = wg; b0 < nb; b0 += 16 * 8) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int b = b0 + 16 * q;
+        v[q] = b < nb ? __ldcg(part + ((int64_t)b * 2 + h) * C + c) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v[q];
+    }
+  }
+  s[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && c < C) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) {
+      s0 += s[w][lane];
+      s1 += s[16 + w][lane];
+    }
+    if (mode == 1) {
+      const int n = load_count(n_dev, cap);
+      const double mu = n > 0 ? s0 / n : 0.0;
+      double var = n > 0 ? s1 / n - mu * mu : 0.0;
+      if (var < 0) var = 0;
+      out_a[c] = (float)mu;
+      out_b[c] = (float)(1.0 / sqrt(var + (double)eps));
+    } else {
+      out_a[c] = (float)(s1 * (double)rstd_in[c]);
+      out_b[c] = (float)s0;
+    }
+  }
+}
+
+// The apply halves of the forward / backward BN whose statistics partials a
+// producer wrote (vp_conv_fwd_bn / vp_conv_dgrad_bn, bn_epi.cuh): one launch
+// each on the critical path instead of a statistics pass plus an apply.
+int vp_bn_apply_part(const void* x, int32_t xd, const int32_t* n_dev, int64_t cap, int64_t C, float eps,
+                     const void* bn_part, float* mean, float* rstd, const float* gamma, const float* beta,
+                     const void* res, int32_t rd, int32_t relu, void* y, int32_t yd, vp_stream_t stream) {
+  VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
+  VP_REQUIRE(bn_part, VP_EVALIDATION, "bn_apply_part: partials required");
+  cudaStream_t st = (cudaStream_t)stream;
+  ::vp::launch(bn_part_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, bn_part, (int)C, n_dev, cap, eps, 1,
+               (const float*)nullptr, mean, rstd);
+  VP_CHECK_LAUNCH("bn_part_finalize");
+  if (cap <= 0) return VP_OK;
+  VP_BN_LAUNCH(bn_apply_kernel, C, one_dtype({xd, yd, res ? rd : xd}), bn_grid_rows(cap, C), kGlueThreads, 0, st, x,
+               xd, n_dev, cap, (int)C, (const float*)mean, (const float*)rstd, gamma, beta, res, rd, relu, y, yd,
+               (const float*)nullptr, 0, 0.f, (float*)nullptr, (float*)nullptr, (const int*)nullptr);
+  VP_CHECK_LAUNCH("bn_apply_part");
+  return VP_OK;
+}
+
+int vp_bn_backward_part(const void* gm, int32_t gmd, const void* x, int32_t xd, const int32_t* n_dev, int64_t cap,
+                        int64_t C, const float* mean, const float* rstd, const float* gamma, const void* bn_part,
+                        void* gx, int32_t gxd, float* ggamma, float* gbeta, vp_stream_t stream) {
+  VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
+  VP_REQUIRE(bn_part, VP_EVALIDATION, "bn_backward_part: partials required");
+  cudaStream_t st = (cudaStream_t)stream;
+  ::vp::launch(bn_part_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, bn_part, (int)C, n_dev, cap, 0.f, 2, rstd,
+               ggamma, gbeta);
+  VP_CHECK_LAUNCH("bn_part_finalize");
+  if (cap <= 0) return VP_OK;
+  VP_BN_LAUNCH(bn_backward_apply_kernel, C, one_dtype({xd, gmd, gxd}), bn_grid_rows(cap, C), kGlueThreads, 0, st, gm,
+               (const void*)nullptr, gmd, (const void*)nullptr, gmd, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, 0,
+               (const float*)ggamma, (const float*)gbeta, gx, gxd, (void*)nullptr, (const float*)nullptr, 0,
+               (float*)nullptr, (float*)nullptr, (const int*)nullptr);
+  VP_CHECK_LAUNCH("bn_backward_part");
   return VP_OK;
 }
 

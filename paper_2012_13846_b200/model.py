@@ -218,11 +218,18 @@ class SparseResNetTrainer:
             # zero-filled: the fused BN kernels' ticket word starts (and stays) zero
             L["bn_ws"] = torch.zeros(int(_lib.query("vp_bn_stats_ws_bytes", n, L["cout"])), dtype=torch.uint8,
                                      device=dev)
+            # BN statistics partials written by the producing conv's epilogue
+            # (forward: this conv; backward: the dgrad of the next conv)
+            L["fpart"] = _lib.workspace(_lib.query("vp_bn_part_bytes", L["cout"]), dev)
+            L["bpart"] = _lib.workspace(_lib.query("vp_bn_part_bytes", L["cout"]), dev)
         # gradient buffers per level for the activation flowing back
         self.gact = [torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
                      for i, lv in enumerate(self.levels)]
-        self.gid = [torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
-                    for i, lv in enumerate(self.levels)]
+        # identity (skip-path) gradients per level, two per level so that
+        # consecutive BasicBlocks of one level (blocks >= 2) never read and
+        # write the same buffer in one launch (_gid)
+        self.gid = [[torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
+                     for i, lv in enumerate(self.levels)] for _ in range(2 if blocks > 1 else 1)]
         # stage boundary buffers (pipeline): input features of a non-first
         # stage, gradient of the output of a non-last stage
         ent, ext = self.entry_level, self.exit_level
@@ -258,6 +265,9 @@ class SparseResNetTrainer:
         self.states = None
         self._sgd_in_backward = False  # set inside step_body / prefetch_body (single-process training)
         self.layer_sgd = __import__("os").environ.get("VP_LAYER_SGD", "1") != "0"
+        # BN statistics from the producing conv's epilogue (vp_conv_fwd_bn /
+        # vp_conv_dgrad_bn) instead of a separate statistics pass
+        self.bn_fuse = __import__("os").environ.get("VP_BN_EPI", "1") != "0"
 
     # ------------------------------------------------------------------ setup
     def _width_at(self, level):
@@ -311,9 +321,9 @@ class SparseResNetTrainer:
                           map=self.map_dn[s], kind="down"))
             for b in range(self.blocks):
                 L.append(dict(name=f"s{s}.b{b}.c1", cin=p, cout=p, src=self.levels[s + 1], dst=self.levels[s + 1],
-                              map=self.map_s1[s + 1], kind="c1"))
+                              map=self.map_s1[s + 1], kind="c1", block=b))
                 L.append(dict(name=f"s{s}.b{b}.c2", cin=p, cout=p, src=self.levels[s + 1], dst=self.levels[s + 1],
-                              map=self.map_s1[s + 1], kind="c2"))
+                              map=self.map_s1[s + 1], kind="c2", block=b))
             prev = p
         for i, l in enumerate(L):
             l["index"] = i
@@ -526,14 +536,23 @@ class SparseResNetTrainer:
         dst = L["dst"]
         fc = self.fcode
         self._wait_map(L["map"])
-        self._c("vp_conv_fwd", x.data_ptr(), fc, x.shape[0], L["cin"], L["wb"].data_ptr(), L["wcode"], L["cout"],
-                self.K, self.fwd_table(L).data_ptr(), 0, _lib.ptr(self.fwd_perm(L)), dst.n.data_ptr(), dst.cap,
-                L["y"].data_ptr(), fc,
-                L["fwd_ws"].data_ptr(), L["fwd_ws"].numel(), st)
-        # batch statistics + normalise (+ residual) (+ ReLU): one cooperative launch
-        self._c("vp_bn_forward", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
-                L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(), L["beta"].data_ptr(),
-                _lib.ptr(res), fc, int(relu), L["a"].data_ptr(), fc, L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
+        conv = (x.data_ptr(), fc, x.shape[0], L["cin"], L["wb"].data_ptr(), L["wcode"], L["cout"], self.K,
+                self.fwd_table(L).data_ptr(), 0, _lib.ptr(self.fwd_perm(L)), dst.n.data_ptr(), dst.cap,
+                L["y"].data_ptr(), fc, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel())
+        if self.bn_fuse:
+            # conv with the BN statistics from its epilogue, then normalise
+            # (+ residual) (+ ReLU) from those partials: two launches
+            self._c("vp_conv_fwd_bn", *conv, 1, L["fpart"].data_ptr(), None, None, None, None, st)
+            self._c("vp_bn_apply_part", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
+                    L["fpart"].data_ptr(), L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(),
+                    L["beta"].data_ptr(), _lib.ptr(res), fc, int(relu), L["a"].data_ptr(), fc, st)
+        else:
+            self._c("vp_conv_fwd", *conv, st)
+            # batch statistics + normalise (+ residual) (+ ReLU)
+            self._c("vp_bn_forward", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
+                    L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(), L["beta"].data_ptr(),
+                    _lib.ptr(res), fc, int(relu), L["a"].data_ptr(), fc, L["bn_ws"].data_ptr(),
+                    L["bn_ws"].numel(), st)
         L["x"] = x
         return L["a"]
 
@@ -562,15 +581,40 @@ class SparseResNetTrainer:
                 pb.view(pb.g, "fc.b").data_ptr(), self.xent_ws.data_ptr(), self.xent_ws.numel(), st)
         return x
 
-    def _bn_conv_backward(self, L, g_out, g_out2, g_res, st, need_dgrad=True):
+    def _gid(self, c2):
+        """The skip-path gradient buffer of the BasicBlock ending in c2."""
+        return self.gid[c2["block"] % len(self.gid)][c2["level"]]
+
+    def _gm_buf(self, P):
+        """Where the producer stores layer P's masked BN gradient: the
+        identity-gradient buffer of P's level when P ends a BasicBlock (that
+        gradient is also the block's skip-path gradient), else the level's
+        activation-gradient buffer."""
+        return self._gid(P) if P["kind"] == "c2" else self.gact[P["level"]]
+
+    def _bn_conv_backward(self, L, g_out, g_out2, g_res, st, need_dgrad=True, prepared=False, prev=None,
+                          prev_add=None):
         """BN(+ReLU) backward then conv dgrad/wgrad.  g_out (+g_out2) is the
-        gradient wrt L['a']; returns the gradient wrt the conv input."""
+        gradient wrt L['a']; returns the gradient wrt the conv input.
+
+        prepared: the producer of g_out (the next conv's dgrad epilogue)
+        already stored L's masked gradient in g_out and wrote L's BN partials
+        (L['bpart']), so only the apply runs here.  prev: the layer whose
+        activation is L's input; with BN fusion on, this dgrad's epilogue
+        prepares prev's BN backward the same way (prev_add = the skip-path
+        gradient that joins prev's output) and the result is prev's masked
+        gradient."""
         dst, src, m = L["dst"], L["src"], L["map"]
         fc = self.fcode
-        self._c("vp_bn_backward", g_out.data_ptr(), _lib.ptr(g_out2), fc, L["a"].data_ptr(), fc,
-                L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], L["mean"].data_ptr(),
-                L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(), fc, _lib.ptr(g_res),
-                L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
+        if prepared:
+            self._c("vp_bn_backward_part", g_out.data_ptr(), fc, L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap,
+                    L["cout"], L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(),
+                    L["bpart"].data_ptr(), L["gy"].data_ptr(), fc, L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), st)
+        else:
+            self._c("vp_bn_backward", g_out.data_ptr(), _lib.ptr(g_out2), fc, L["a"].data_ptr(), fc,
+                    L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], L["mean"].data_ptr(),
+                    L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(), fc, _lib.ptr(g_res),
+                    L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
         x = L["x"]
         if self.concurrent:  # weight gradient off the critical path
             ws = self.side[3 - (L["index"] % 2)]
@@ -587,11 +631,17 @@ class SparseResNetTrainer:
         if not need_dgrad:
             self._layer_sgd(L, ws if self.concurrent else None, None, st)
             return None
-        gin = self.gact[self.levels.index(src)]
         table, flip, perm = self.dgrad_table(L)
-        self._c("vp_conv_dgrad", L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(), L["wcode"],
-                L["cin"], self.K, table.data_ptr(), flip, _lib.ptr(perm), src.n.data_ptr(), src.cap, gin.data_ptr(),
-                fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
+        dgrad = (L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(), L["wcode"], L["cin"],
+                 self.K, table.data_ptr(), flip, _lib.ptr(perm), src.n.data_ptr(), src.cap)
+        if prev is not None and self.bn_fuse:
+            gin = self._gm_buf(prev)
+            self._c("vp_conv_dgrad_bn", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), 2,
+                    prev["bpart"].data_ptr(), _lib.ptr(prev_add), prev["a"].data_ptr(), prev["y"].data_ptr(),
+                    prev["mean"].data_ptr(), st)
+        else:
+            gin = self.gact[self.levels.index(src)]
+            self._c("vp_conv_dgrad", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
         if self._sgd_in_backward:
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
@@ -635,22 +685,34 @@ class SparseResNetTrainer:
             g = self.g_out_ext  # gradient of this stage's output, received from the next stage
         g2 = None  # pending identity-branch gradient for the current activation
         units = self.units[self.unit_range[0]:self.unit_range[1] + 1]
+        # the layer whose activation feeds each layer (None: the engine's input)
+        prev_of = {id(L): (self.layers[i - 1] if i > 0 else None) for i, L in enumerate(self.layers)}
+        prepared = False  # g already holds the masked gradient + BN partials (fused producer)
         for u in reversed(units):
             Ls = u["layers"]
             if u["kind"] == "block":
                 c1, c2 = Ls
-                gid = self.gid[c2["level"]]
-                # out = relu(bn2(conv2(h)) + idn): mask by out, identity grad -> gid;
-                # gh lives in gact[lvl] and c1's dgrad overwrites it after use
-                gh = self._bn_conv_backward(c2, g, g2, gid, st)
-                gx = self._bn_conv_backward(c1, gh, None, None, st)
+                gid = self._gid(c2)
+                # out = relu(bn2(conv2(h)) + idn): mask by out, identity grad -> gid
+                # (prepared: the producer stored it there already); gh lives in
+                # gact[lvl] and c1's dgrad overwrites it after use.  c2's dgrad
+                # prepares c1's BN; c1's prepares the previous unit's output
+                # layer, whose gradient joins this block's identity gradient.
+                gh = self._bn_conv_backward(c2, g, g2, gid, st, prepared=prepared, prev=c1)
+                gx = self._bn_conv_backward(c1, gh, None, None, st, prepared=self.bn_fuse, prev=prev_of[id(c1)],
+                                            prev_add=gid)
                 g, g2 = gx, gid
             elif u["kind"] == "down":
-                g = self._bn_conv_backward(Ls[0], g, g2, None, st)
+                g = self._bn_conv_backward(Ls[0], g, g2, None, st, prepared=prepared, prev=prev_of[id(Ls[0])])
                 g2 = None
             else:  # stem: no input gradient
-                self._bn_conv_backward(Ls[0], g, g2, None, st, need_dgrad=False)
+                self._bn_conv_backward(Ls[0], g, g2, None, st, need_dgrad=False, prepared=prepared)
                 g = g2 = None
+            # the next (earlier) unit's output layer was prepared by this unit's
+            # first dgrad when that layer is inside this engine
+            prepared = self.bn_fuse and prev_of[id(Ls[0])] is not None
+            if prepared:
+                g2 = None  # already folded into the prepared gradient
         if not self.first:
             if g2 is not None:
                 g.add_(g2)  # the stage input fed both branches of its first block
