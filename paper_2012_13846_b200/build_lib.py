@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvoxpipe_b200.so")
-SOURCES = ["hash_coords.cu", "kmap.cu", "kmap_sort.cu", "kmap_brick.cu", "conv.cu", "glue.cu", "wide.cu"]
+SOURCES = ["hash_coords.cu", "kmap.cu", "kmap_sort.cu", "kmap_brick.cu", "conv.cu", "glue.cu", "wide.cu"] + [
+    f"conv_tc_k{kd}_{t}.cu" for kd in (32, 64, 128, 256) for t in ("f", "d")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -45,7 +46,7 @@ def _compile(src: str, objdir: str) -> str:
 def build(verbose: bool = True) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 8)) as ex:
         objs = list(ex.map(lambda s: _compile(s, objdir), SOURCES))
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:

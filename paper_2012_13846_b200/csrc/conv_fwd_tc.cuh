@@ -46,6 +46,7 @@ struct FwdParams {
   int stage_tbl;  // stage table tiles in smem (K <= kTblK, 16 B-aligned table); set by the launcher
   int dbg;        // experiments only: bit0 no MMA, bit1 no B copies, bit2 no A copies, bit3 plain arrive for empty, bit4 every offset active (no mask scan)
   BnEpi epi;      // BN statistics of the output (bn_epi.cuh); mode 0 = off.  Needs a bf16 output.
+  long long* trace;  // debug timeline of CTA 0 (null = off)
 };
 
 constexpr int kTcProd = 128, kTcEpi = 128, kTcThreads = kTcProd + kTcEpi + 32;
@@ -57,7 +58,8 @@ constexpr int kTblK = 32;  // K <= kTblK: each tile's [128, K] table is staged i
 // buffer: stage events [g][4] at slot g < 256 (producer slot acquired,
 // producer issued, MMA saw full, MMA committed), tile events at 1024 + 4*ii
 // (prologue start, work published, epilogue got accumulator, epilogue done).
-__device__ long long* g_conv_trace = nullptr;
+// (the buffer travels in FwdParams::trace; vp_debug_conv_trace sets it)
+extern long long* g_conv_trace_host;
 #define trace_ev(idx, on)                           \
   do {                                              \
     if (trc != nullptr && (on)) trc[idx] = clock64(); \
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
-  long long* const trc = blockIdx.x == 0 ? g_conv_trace : nullptr;
+  long long* const trc = blockIdx.x == 0 ? p.trace : nullptr;
   const int n_out = load_count(p.n_out_dev, p.cap_out);
   const int ntiles = (n_out + TR - 1) / TR;
   // split partials are sized for kNumSMs work items
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       for (int sj = 0; sj < nst; ++sj, ++g) {
         const int stage = g % C::STAGES;
         if (g >= (uint32_t)C::STAGES) tc::mbar_wait(&empty[stage], ((g / C::STAGES) - 1) & 1);
+        trace_ev(4 * (g & 255), tid == 0 && g < 256);
         const uint32_t s_base = sbase + stage * C::STAGE;
         const int na_st = min(RB, neff - sj * RB);  // atoms in use (the MMA skips the rest)
 #pragma unroll 1
@@ -316,6 +319,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
         }
         // the stage's full barrier completes when every producer's copies have landed
         tc::cp_async_arrive_noinc(&full[stage]);
+        trace_ev(4 * (g & 255) + 1, tid == 0 && g < 256);
       }
     }
     tc::cp_async_wait<0>();
@@ -508,6 +512,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       for (int sj = 0; sj < nst; ++sj, ++g) {
         const int stage = g % C::STAGES;
         tc::mbar_wait(&full[stage], (g / C::STAGES) & 1);
+        trace_ev(4 * (g & 255) + 2, g < 256);
         tc::tc_fence_after();
         const uint32_t s_base = sbase + stage * C::STAGE;
         const int na_st = (p.dbg & 1) ? 0 : min(RB, neff - sj * RB);
@@ -527,6 +532,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
         }
         if (p.dbg & 8) tc::mbar_arrive(&empty[stage]);
         else tc::mma_commit(&empty[stage]);
+        trace_ev(4 * (g & 255) + 3, g < 256);
       }
       tc::mma_commit(&tfull[a]);
     }
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 }
 
 // out[r, n] = sum over splits of the fp32 partials, in split order.
-__global__ void split_reduce_kernel(const float* __restrict__ part, const int32_t* n_out_dev, int64_t cap_out, int ND,
+static __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_t* n_out_dev, int64_t cap_out, int ND,
                                     int grid, int max_split, const int32_t* __restrict__ perm, void* __restrict__ y,
                                     int y_dtype) {
   ::vp::pdl_begin();

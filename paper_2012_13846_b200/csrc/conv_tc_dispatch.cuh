@@ -1,0 +1,144 @@
+// Tensor-core conv dispatch: (C_in, C_out, operand layout) -> the
+// implicit-GEMM instantiation and its (CTAs/SM, atoms/stage) config.  The
+// instantiations are compiled in one translation unit per (K width, B
+// layout) (conv_tc_*.cu) so the library builds in parallel.
+#pragma once
+#include <algorithm>
+#include <string>
+
+#include "common.cuh"
+#include "conv_fwd_tc.cuh"
+
+namespace vp {
+
+constexpr int kMaxSplit = 16;
+
+template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1>
+inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
+  using C = FwdTC<KD, ND, BMN, CPS, RB, TT>;
+  const bool tbl = p0.K <= kTblK && ((uintptr_t)p0.table & 15) == 0;
+  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true, TT> : conv_tc_kernel<KD, ND, BMN, CPS, RB, false, TT>;
+  static_assert(C::SMEM_MAX <= 227 * 1024, "conv_tc: shared memory over the per-CTA limit");
+  static bool attr_t = false, attr_f = false;  // immutable per-instantiation attribute cache
+  bool& attr = tbl ? attr_t : attr_f;
+  if (!attr) {
+    VP_REQUIRE(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_MAX) == cudaSuccess,
+               VP_EINTERNAL, "conv_tc: cannot reserve shared memory");
+    attr = true;
+  }
+  const int64_t tiles = ceil_div(p0.cap_out, 128 * TT);
+  if (TT > 1) part = nullptr;  // multi-tile items are only used where no split-K is needed
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * kMaxSplit, (int64_t)kNumSMs * CPS));
+  FwdParams p = p0;
+  p.part = (float*)part;
+  static const int max_split = getenv("VP_CONV_MAX_SPLIT") ? std::max(1, std::min(kMaxSplit, atoi(getenv("VP_CONV_MAX_SPLIT"))))
+                                                          : kMaxSplit;  // tuning
+  p.max_split = part ? max_split : 1;
+  p.stage_tbl = tbl;
+  static const int dbg = getenv("VP_CONV_DBG") ? atoi(getenv("VP_CONV_DBG")) : 0;
+  p.dbg = dbg;
+  p.trace = g_conv_trace_host;
+  ::vp::launch(kern, grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st, p);
+  VP_CHECK_LAUNCH("conv_tc");
+  if (part && p.epi.mode != 0) {  // bf16 output + BN statistics: at most one partial row per SM
+    const int64_t work = p.cap_out * ND / 4;
+    ::vp::launch(split_reduce_epi_kernel<ND>,
+                 (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, kSplitEpiThreads), kNumSMs)),
+                 kSplitEpiThreads, 0, st, (const float*)part, p.n_out_dev, p.cap_out, grid, p.max_split, p.perm, (bf16*)p.y, p.epi);
+    VP_CHECK_LAUNCH("split_reduce_epi");
+  } else if (part) {
+    const int64_t work = p.cap_out * ND / 4;
+    ::vp::launch(split_reduce_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), grid_cap(8))), 256, 0, st, 
+        (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.perm, p.y, p.y_dtype);
+    VP_CHECK_LAUNCH("split_reduce");
+  }
+  return VP_OK;
+}
+
+// (CTAs per SM, atoms per stage) candidates for the gather-bound implicit
+// GEMM; conv_cfg picks one per output width (VP_CONV_CFG=i overrides, for
+// tuning).  Infeasible ones (ring < 2 stages, TMEM) fall through.
+constexpr int kCfgCps[] = {1, 1, 2, 2, 3};
+constexpr int kCfgRb[] = {2, 1, 2, 1, 1};
+
+inline int conv_cfg(int64_t nd, int64_t cap_out) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("VP_CONV_CFG");
+    env = e ? atoi(e) : -1;
+  }
+  if (env >= 0 && env < 5) return env;
+  // per output width (VP_CONV_CFG_<ND>, tuning)
+  static int per[4] = {-2, -2, -2, -2};
+  const int slot = nd == 32 ? 0 : nd == 64 ? 1 : nd == 128 ? 2 : 3;
+  if (per[slot] == -2) {
+    const std::string name = "VP_CONV_CFG_" + std::to_string(nd);
+    const char* e = getenv(name.c_str());
+    per[slot] = e ? atoi(e) : -1;
+  }
+  if (per[slot] >= 0 && per[slot] < 5) return per[slot];
+  // C_out = 128 at <= 64k rows (C3's level 3: ~80 tiles, split-K): one CTA
+  // per SM with single-atom stages measured 45.9k -> 47.2k clouds/s
+  if (nd == 128 && cap_out <= 65536) return 1;
+  return 3;
+}
+
+template <int KD, int ND, bool BMN, int I>
+inline int try_cfg(const FwdParams& p, void* part, cudaStream_t st) {
+  using C = FwdTC<KD, ND, BMN, kCfgCps[I], kCfgRb[I]>;
+  if constexpr (C::FITS) return launch_conv_tc<KD, ND, BMN, kCfgCps[I], kCfgRb[I]>(p, part, st);
+  return -1;
+}
+
+// rows at which a 256-row work item (two tiles sharing each weight stage)
+// replaces the 128-row one for C_out >= 128: enough 256-row items to fill
+// the machine without split-K (VP_CONV_TT2_ROWS overrides; 0 disables)
+inline int64_t tt2_rows() {
+  static const int64_t v = getenv("VP_CONV_TT2_ROWS") ? atoll(getenv("VP_CONV_TT2_ROWS")) : 0;  // off by default: at 1M rows it helps strided dgrad (-9%) but slows C=256 fwd (+14%)
+  return v;
+}
+
+template <int KD, int ND, bool BMN>
+inline int launch_conv_tc_cfg(const FwdParams& p, void* part, cudaStream_t st) {
+  if constexpr (ND >= 128 && FwdTC<KD, ND, BMN, 1, 1, 2>::FITS) {
+    if (tt2_rows() > 0 && p.cap_out >= tt2_rows()) return launch_conv_tc<KD, ND, BMN, 1, 1, 2>(p, part, st);
+  }
+  int r = -1;
+  switch (conv_cfg(ND, p.cap_out)) {
+    case 0: r = try_cfg<KD, ND, BMN, 0>(p, part, st); break;
+    case 1: r = try_cfg<KD, ND, BMN, 1>(p, part, st); break;
+    case 2: r = try_cfg<KD, ND, BMN, 2>(p, part, st); break;
+    case 3: r = try_cfg<KD, ND, BMN, 3>(p, part, st); break;
+    case 4: r = try_cfg<KD, ND, BMN, 4>(p, part, st); break;
+  }
+  if (r >= 0) return r;
+  r = try_cfg<KD, ND, BMN, 0>(p, part, st);  // (1, 2): fits every width but 256
+  if (r >= 0) return r;
+  return launch_conv_tc<KD, ND, BMN, 1, 1>(p, part, st);
+}
+
+template <int KD, bool BMN>
+inline int conv_tc_nd(int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
+  switch (nd) {
+    case 32: return launch_conv_tc_cfg<KD, 32, BMN>(p, part, st);
+    case 64: return launch_conv_tc_cfg<KD, 64, BMN>(p, part, st);
+    case 128: return launch_conv_tc_cfg<KD, 128, BMN>(p, part, st);
+    case 256: return launch_conv_tc_cfg<KD, 256, BMN>(p, part, st);
+  }
+  return VP_EINTERNAL;
+}
+
+
+// one translation unit each (conv_tc_k<KD>_<f|d>.cu)
+#define VP_CONV_TC_DECL(KD, T) int conv_tc_k##KD##_##T(int64_t nd, const FwdParams& p, void* part, cudaStream_t st);
+VP_CONV_TC_DECL(32, f)
+VP_CONV_TC_DECL(64, f)
+VP_CONV_TC_DECL(128, f)
+VP_CONV_TC_DECL(256, f)
+VP_CONV_TC_DECL(32, d)
+VP_CONV_TC_DECL(64, d)
+VP_CONV_TC_DECL(128, d)
+VP_CONV_TC_DECL(256, d)
+#undef VP_CONV_TC_DECL
+
+}  // namespace vp

@@ -1,0 +1,8 @@
+// Tensor-core conv instantiations: K width 32, forward (W K-major).
+#include "conv_tc_dispatch.cuh"
+
+namespace vp {
+int conv_tc_k32_f(int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
+  return conv_tc_nd<32, false>(nd, p, part, st);
+}
+}  // namespace vp

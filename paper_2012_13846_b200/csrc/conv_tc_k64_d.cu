@@ -1,0 +1,8 @@
+// Tensor-core conv instantiations: K width 64, dgrad (W read MN-major).
+#include "conv_tc_dispatch.cuh"
+
+namespace vp {
+int conv_tc_k64_d(int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
+  return conv_tc_nd<64, true>(nd, p, part, st);
+}
+}  // namespace vp

@@ -95,6 +95,10 @@ class ParamBuffer:
         return self.pb[off: off + int(np.prod(shape))].view(shape)
 
 
+_DBG_SKIP_WGRAD = __import__("os").environ.get("VP_DBG_SKIP_WGRAD", "0") == "1"
+_DBG_SKIP_PREFETCH = __import__("os").environ.get("VP_DBG_SKIP_PREFETCH", "0") == "1"
+
+
 class SparseResNetTrainer:
     """Graph-capturable SparseResNet training engine on one GPU."""
 
@@ -616,6 +620,8 @@ class SparseResNetTrainer:
                     L["rstd"].data_ptr(), L["gamma"].data_ptr(), 1, L["gy"].data_ptr(), fc, _lib.ptr(g_res),
                     L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["bn_ws"].data_ptr(), L["bn_ws"].numel(), st)
         x = L["x"]
+        if _DBG_SKIP_WGRAD:  # experiments only: the step without weight gradients (never for results)
+            return self._dgrad_only(L, prev, prev_add, need_dgrad, st)
         if self.concurrent:  # weight gradient off the critical path
             ws = self.side[3 - (L["index"] % 2)]
             self._forked.add(id(ws))
@@ -646,6 +652,22 @@ class SparseResNetTrainer:
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
             self._layer_sgd(L, ws if self.concurrent else None, ev, st)
+        return gin
+
+    def _dgrad_only(self, L, prev, prev_add, need_dgrad, st):
+        if not need_dgrad:
+            return None
+        src, fc = L["src"], self.fcode
+        table, flip, perm = self.dgrad_table(L)
+        dgrad = (L["gy"].data_ptr(), fc, L["gy"].shape[0], L["cout"], L["wb"].data_ptr(), L["wcode"], L["cin"],
+                 self.K, table.data_ptr(), flip, _lib.ptr(perm), src.n.data_ptr(), src.cap)
+        gin = self._gm_buf(prev) if (prev is not None and self.bn_fuse) else self.gact[self.levels.index(src)]
+        if prev is not None and self.bn_fuse:
+            self._c("vp_conv_dgrad_bn", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), 2,
+                    prev["bpart"].data_ptr(), _lib.ptr(prev_add), prev["a"].data_ptr(), prev["y"].data_ptr(),
+                    prev["mean"].data_ptr(), st)
+        else:
+            self._c("vp_conv_dgrad", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
         return gin
 
     def _layer_sgd(self, L, side, after, st):
@@ -823,7 +845,7 @@ class SparseResNetTrainer:
         b = dict(points=torch.zeros_like(self.points), labels=torch.zeros_like(self.labels), levels=levels,
                  feat0=torch.zeros_like(self.feat0), map_s1=map_s1, map_dn=map_dn, layers_all=layers_all,
                  units=units, layers=[L for u in units for L in u["layers"]])
-        self.states = [a, b]
+        self.states = [a, a] if _DBG_SKIP_PREFETCH else [a, b]
         # the prefetched integer stage gets its own streams (the origin P
         # replaces the step's main stream; chain + two map streams)
         self.pf_stream = torch.cuda.Stream(device=dev)
@@ -845,6 +867,8 @@ class SparseResNetTrainer:
         P = self.pf_stream
 
         def fork():
+            if _DBG_SKIP_PREFETCH:  # experiments only: no next-batch integer stage (never for results)
+                return
             P.wait_stream(main)
             self._forked.add(id(P))
             self._use(self.states[1 - cur])

@@ -27,9 +27,27 @@ ws = _lib.workspace(_lib.query("vp_conv_fwd_ws_bytes", c, c, K), dev)
 st = torch.cuda.current_stream().cuda_stream
 
 
+if len(sys.argv) > 4 and sys.argv[4] == "real":
+    # a real C3 layer: the trainer's level tables and activations
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import voxpipe_oracle as O
+    from paper_2012_13846_b200 import model
+    tr = model.SparseResNetTrainer(batch=64, points=2048, resolution=64)
+    pts, offs = O.synthetic_batch(64, 2048, 64, seed=1000, dtype=np.float32)
+    tr.train_step_from_host(pts, offs, np.arange(64) % 40)
+    L = [L for L in tr.layers if L["cin"] == c and L["cout"] == c and L["kind"] == "c1"][0]
+    x = L["x"]
+    w = L["wb"]
+    nbr = tr.fwd_table(L)
+    n = int(L["dst"].n.item())
+    ncount = L["dst"].n
+    y = L["y"]
+    print("layer", L["name"], "rows", n, "hits/row", float((nbr[:n] >= 0).sum()) / n)
+
+
 def launch():
-    _lib.call("vp_conv_fwd", x.data_ptr(), _lib.VP_BF16, n, c, w.data_ptr(), _lib.VP_BF16, c, K, nbr.data_ptr(), 0, None,
-              ncount.data_ptr(), n, y.data_ptr(), _lib.VP_BF16, ws.data_ptr(), ws.numel(), st)
+    _lib.call("vp_conv_fwd", x.data_ptr(), _lib.VP_BF16, x.shape[0], c, w.data_ptr(), _lib.VP_BF16, c, K, nbr.data_ptr(),
+              0, None, ncount.data_ptr(), nbr.shape[0], y.data_ptr(), _lib.VP_BF16, ws.data_ptr(), ws.numel(), st)
 
 
 launch()
