@@ -68,9 +68,10 @@ __device__ __forceinline__ T tree_sum(const T* __restrict__ p, int64_t stride, i
 // sum the chunk partials of each offset, pairwise in chunk order (deterministic)
 template <typename T>
 __global__ void wgrad_reduce_kernel(const T* __restrict__ part, const int32_t* __restrict__ pptr,
-                                    int K, int chunk, int64_t per, T* __restrict__ gw) {
+                                    int K, int chunk, int64_t per, T* __restrict__ gw, const int* chunk_dev) {
   ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
+  if (chunk_dev) chunk = *chunk_dev;  // chosen on the device by the partial kernel
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int k = 0; k < K; ++k) {
@@ -672,10 +673,15 @@ static size_t split_ws_bytes(int64_t nd) { return align_up((size_t)kSplitItems *
 
 constexpr int kWgSms = kNumSMs;
 
-template <int CIN, int COUT>
-static int launch_wg_tc(const WgParams& p, int max_items, cudaStream_t st) {
-  using C = WgTC<CIN, COUT>;
-  auto kern = conv_wgrad_tc_kernel<CIN, COUT>;
+static int wgrad_cps() {  // CTAs per SM of the weight-gradient kernel where two fit (VP_WGRAD_CPS overrides)
+  static const int v = getenv("VP_WGRAD_CPS") ? atoi(getenv("VP_WGRAD_CPS")) : 2;
+  return v;
+}
+
+template <int CIN, int COUT, int CPS>
+static int launch_wg_tc_cps(const WgParams& p, int max_items, cudaStream_t st) {
+  using C = WgTC<CIN, COUT, CPS>;
+  auto kern = conv_wgrad_tc_kernel<CIN, COUT, CPS>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -685,10 +691,18 @@ static int launch_wg_tc(const WgParams& p, int max_items, cudaStream_t st) {
   // stream next to the critical path (BN / dgrad); leaving SMs free for the
   // high-priority kernels shortens the step (VP_WGRAD_SMS overrides)
   static const int wg_sms = getenv("VP_WGRAD_SMS") ? atoi(getenv("VP_WGRAD_SMS")) : kWgSms;
-  const int grid = std::max(1, std::min(max_items, wg_sms));
+  const int grid = std::max(1, std::min(max_items, wg_sms * CPS));
   ::vp::launch(kern, grid, kTcThreads, C::SMEM, st, p);
   VP_CHECK_LAUNCH("conv_wgrad_tc");
   return VP_OK;
+}
+
+template <int CIN, int COUT>
+static int launch_wg_tc(const WgParams& p, int max_items, cudaStream_t st) {
+  if constexpr (WgTC<CIN, COUT, 2>::FITS) {
+    if (wgrad_cps() == 2) return launch_wg_tc_cps<CIN, COUT, 2>(p, max_items, st);
+  }
+  return launch_wg_tc_cps<CIN, COUT, 1>(p, max_items, st);
 }
 
 template <int CIN>
@@ -886,6 +900,7 @@ static int conv_dgrad_impl(const void* g, int32_t g_dtype, int64_t g_rows, int64
 }
 
 constexpr int kWgSimtChunk = 512;  // SIMT path: short chunks, many CTAs
+constexpr size_t kWgHeader = 256;  // tail of the wgrad workspace: the device-chosen chunk
 
 // fp32 partials of the SIMT chunk size; the f64 path runs chunks twice as
 // long, so 8-byte partials of (cap/2chunk + K + 1) items fit the same
@@ -893,7 +908,7 @@ constexpr int kWgSimtChunk = 512;  // SIMT path: short chunks, many CTAs
 size_t vp_conv_wgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K, int64_t cap_pairs) {
   const int chunk = std::min(wgrad_chunk(cap_pairs), kWgSimtChunk);
   const int64_t items = cap_pairs / chunk + 2 * ((int64_t)K + 1);
-  return align_up((size_t)items * cin * cout * 4, 256);
+  return align_up((size_t)items * cin * cout * 4, 256) + kWgHeader;  // + the device-chosen chunk word
 }
 
 int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
@@ -917,16 +932,30 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
                  x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout, pptr, dchunk, dpart);
     VP_CHECK_LAUNCH("conv_wgrad_simt_f64");
     ::vp::launch(wgrad_reduce_kernel<double>, rblocks, 256, 0, st, (const double*)dpart, pptr, K, dchunk,
-                 (int64_t)cin * cout, (double*)gw_out);
+                 (int64_t)cin * cout, (double*)gw_out, (const int*)nullptr);
     VP_CHECK_LAUNCH("wgrad_reduce_f64");
     return VP_OK;
   }
   if (x_dtype == VP_BF16 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
-    WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, chunk, part};
-    int rc = wg_tc(cin, cout, p, max_items, st);
+    // pairs per item: from the static pair capacity, or chosen on the device
+    // from the live pair count (bounded by the partials the workspace holds)
+    // default: the capacity rule — in the concurrent training step fewer,
+    // longer items leave more SMs to the critical path (C3: 1.309 vs 1.319
+    // ms/step), although the live-count chunk runs the 128-wide layers
+    // standalone 25% faster (VP_WGRAD_DEVICE_CHUNK=1)
+    static const bool static_chunk = !(getenv("VP_WGRAD_DEVICE_CHUNK") && atoi(getenv("VP_WGRAD_DEVICE_CHUNK")) == 1);
+    const int64_t ws_items = (int64_t)((ws_bytes - kWgHeader) / ((size_t)cin * cout * 4));
+    int* chunk_dev = (int*)((char*)ws + ws_bytes - kWgHeader);
+    // floor: gathered bytes per item >= f/2 x its C_out x C_in fp32 partial (VP_WGRAD_MIN_F, default 1)
+    static const int min_f = getenv("VP_WGRAD_MIN_F") ? std::max(0, atoi(getenv("VP_WGRAD_MIN_F"))) : 1;
+    const int chunk_min = (int)std::min<int64_t>(2 * cin * cout / (cin + cout) * min_f, kWgMaxChunk);
+    WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, static_chunk ? chunk : 0, part,
+               (int)std::min<int64_t>(ws_items, 1 << 30), chunk_dev, chunk_min};
+    const int grid_items = static_chunk ? max_items : (int)std::min<int64_t>(ws_items, 1 << 30);
+    int rc = wg_tc(cin, cout, p, grid_items, st);
     if (rc != VP_OK) return rc;
     ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, chunk,
-                 (int64_t)cin * cout, gw);
+                 (int64_t)cin * cout, gw, static_chunk ? (const int*)nullptr : (const int*)chunk_dev);
     VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }
@@ -943,7 +972,7 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
       ::vp::launch(wgrad_stem_kernel<64>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
     VP_CHECK_LAUNCH("conv_wgrad_stem");
     ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, kWgStemChunk,
-                 (int64_t)cin * cout, gw);
+                 (int64_t)cin * cout, gw, (const int*)nullptr);
     VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }
@@ -954,7 +983,7 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
                pin, pout, pptr, schunk, part);
   VP_CHECK_LAUNCH("conv_wgrad_simt");
   ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, schunk,
-               (int64_t)cin * cout, gw);
+               (int64_t)cin * cout, gw, (const int*)nullptr);
   VP_CHECK_LAUNCH("wgrad_reduce");
   return VP_OK;
 }

@@ -14,6 +14,8 @@
 
 namespace vp {
 
+constexpr int kWgMaxChunk = 2048;
+
 struct WgParams {
   const __nv_bfloat16* x;
   const __nv_bfloat16* g;
@@ -21,15 +23,34 @@ struct WgParams {
   const int32_t* pin;
   const int32_t* pout;
   const int32_t* pptr;
-  int chunk;        // pairs per item (multiple of 64, <= kWgMaxChunk)
+  int chunk;        // pairs per item (multiple of 64, <= kWgMaxChunk); 0 = chosen on the device
   float* part;      // partials, items * C_out * C_in
+  int max_items;    // partials the workspace holds (device-chosen chunk)
+  int* chunk_out;   // device-chosen chunk, for wgrad_reduce_kernel
+  int chunk_min;    // device-chosen chunk floor (keeps C_out x C_in partials small next to the gathers)
 };
 
-constexpr int kWgMaxChunk = 2048;
+// Pairs per work item from the LIVE pair count (pptr[K], on the device):
+// about one item per CTA so every SM works and the chains stay short, but
+// long enough that the partials fit the workspace.  Depends only on the
+// pair count and the launch shape -> deterministic.
+__device__ __forceinline__ int wg_device_chunk(int total, int K, int grid, int max_items, int chunk_min) {
+  // items <= total / c + K (one partial chunk per offset): aim at <= grid
+  const int slots = max(grid - K - 1, grid / 2);
+  int c = max((total + slots - 1) / slots, chunk_min);
+  const int room = max_items - K - 1;
+  if (room > 0) c = max(c, (total + room - 1) / room);
+  c = (c + 63) / 64 * 64;
+  return min(max(c, 64), kWgMaxChunk);
+}
+
 // (kTcProd / kTcEpi / kTcThreads from conv_fwd_tc.cuh: warps 0-3 produce,
 // 4-7 drain TMEM, 8 issues the MMAs)
 
-template <int CIN, int COUT>
+// CPS CTAs per SM: the gathers are bound by the producers' cp.async issue
+// rate, so two independent CTAs per SM (half the ring each) move more pairs
+// per microsecond where two rings of >= 4 stages fit (C_in, C_out <= 128).
+template <int CIN, int COUT, int CPS = 1>
 struct WgTC {
   static constexpr int PK = 64;
   static constexpr int MPAD = COUT < 64 ? 64 : COUT;
@@ -41,8 +62,9 @@ struct WgTC {
   static constexpr int B_BYTES = NPAD * PK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int IDX_BYTES = kWgMaxChunk * 8;
-  static constexpr int STAGES_RAW = (196 * 1024 - IDX_BYTES) / STAGE;
+  static constexpr int STAGES_RAW = ((CPS == 1 ? 196 : 104) * 1024 - IDX_BYTES) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 3 ? 3 : STAGES_RAW);
+  static constexpr bool FITS = STAGES_RAW >= (CPS == 1 ? 3 : 4);
   static constexpr int COLS = MT * N;
   static constexpr int ACC = 2 * COLS <= 512 ? 2 : 1;
   static constexpr int TCOLS = ACC * COLS <= 32 ? 32 : ACC * COLS <= 64 ? 64 : ACC * COLS <= 128 ? 128
@@ -56,10 +78,10 @@ __device__ __forceinline__ uint32_t wg_off(int c, int kk) {
   return (uint32_t)((c >> 3) * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + (((c & 7) ^ (kk & 7)) << 4));
 }
 
-template <int CIN, int COUT>
-__global__ void __launch_bounds__(kTcThreads, 1) conv_wgrad_tc_kernel(const __grid_constant__ WgParams p) {
+template <int CIN, int COUT, int CPS = 1>
+__global__ void __launch_bounds__(kTcThreads, CPS) conv_wgrad_tc_kernel(const __grid_constant__ WgParams p) {
   ::vp::pdl_begin();
-  using C = WgTC<CIN, COUT>;
+  using C = WgTC<CIN, COUT, CPS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   int32_t* s_pin = reinterpret_cast<int32_t*>(smem + C::STAGES * C::STAGE);
@@ -73,7 +95,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) conv_wgrad_tc_kernel(const __gr
   int* s_pref = reinterpret_cast<int*>(book + 512);  // K+1 <= 344 ints
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int K = p.K, chunk = p.chunk;
+  const int K = p.K;
+  __shared__ int s_chunk;
+  if (tid == 0) {
+    s_chunk = p.chunk > 0 ? p.chunk : wg_device_chunk(p.pptr[K] - p.pptr[0], K, gridDim.x, p.max_items, p.chunk_min);
+    if (blockIdx.x == 0 && p.chunk_out) *p.chunk_out = s_chunk;
+  }
+  __syncthreads();
+  const int chunk = s_chunk;
   if (tid == 0) {
     int acc = 0;
     for (int k = 0; k < K; ++k) {

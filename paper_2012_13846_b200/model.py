@@ -283,6 +283,8 @@ class SparseResNetTrainer:
     # than the 1.3-1.7x fewer active offsets per tile save (tools/sweep_c2.py)
     SORT_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_MIN_ROWS", 1 << 18))
     SORT_INV_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_INV_MIN_ROWS", 0))
+    # levels whose forward tables are sorted regardless of size
+    SORT_LEVELS = tuple(int(v) for v in __import__("os").environ.get("VP_SORT_LEVELS", "1").split(",") if v)
     # prefetch mode: fork the next batch's integer stage at the start of the
     # step, concurrent with the forward too (VP_PREFETCH_EARLY=0: after the
     # forward; measured 42.5k -> 43.8k clouds/s at C3 with the early fork)
@@ -301,7 +303,8 @@ class SparseResNetTrainer:
             ws=_lib.workspace(max(_lib.query("vp_kernel_map_ws_bytes", src.cap, dst.cap, K),
                                   _lib.query("vp_kernel_map_grid_ws_bytes", dst.cap, K)), dev))
         nws = 0
-        if sort and dst.cap >= self.SORT_MIN_ROWS:
+        lvl = int(dst.stride).bit_length() - 1  # level i has tensor stride 2^i
+        if sort and (dst.cap >= self.SORT_MIN_ROWS or lvl in self.SORT_LEVELS):
             m.perm = torch.zeros(dst.cap, dtype=torch.int32, device=dev)
             m.nbr_s = torch.zeros((dst.cap, K), dtype=torch.int32, device=dev)
             nws = _lib.query("vp_kernel_map_sort_ws_bytes", dst.cap, K)
