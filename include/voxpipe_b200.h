@@ -89,8 +89,10 @@ int vp_check_finite(const void* feats, int32_t dtype, int64_t count, int32_t* fl
 /* generate_output_coords (conv.py:124-146) for stride > 1: floor-div by
  * the NEW tensor stride `step` (= tensor_stride * stride), rescale, unique
  * rows in FIRST-SEEN order.  out needs cap_in rows; *n_out_dev receives
- * N_out.  parent (nullable, int32 [cap_in]) receives the output row of each
- * input row (used by pooling/unpooling glue). */
+ * N_out, or -1 when a downsampled row leaves the packed 16-bit axis range
+ * (e.g. -32768 floored to a multiple of 3): such rows cannot be keyed, so
+ * the caller uses vp_wide_output_coords instead.  parent (nullable, int32
+ * [cap_in]) receives the output row of each input row (pooling glue). */
 size_t vp_output_coords_ws_bytes(int64_t cap_in);
 int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
                      const int32_t* step_host3, int32_t* out, int32_t* n_out_dev,

@@ -197,15 +197,7 @@ def _output_coords4(coords4: torch.Tensor, tensor_stride: tuple, stride: tuple, 
         return coords4.clone(), new_stride
     n = coords4.shape[0]
     if is_wide(coords4) or max(new_stride) > 16384:  # wide rows (kernels.py:95-122 fallback)
-        c = widen(coords4, dim)
-        if n == 0:
-            return c.clone(), new_stride
-        out = torch.empty_like(c)
-        n_out = torch.empty(1, dtype=torch.int32, device=c.device)
-        ws = _lib.workspace(_lib.query("vp_wide_ws_bytes", n, 0, dim + 1, 1), c.device)
-        _lib.call("vp_wide_output_coords", c.data_ptr(), n, dim + 1, _lib.i64_array(new_stride), out.data_ptr(),
-                  n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
-        return out[: int(n_out.item())], new_stride
+        return _output_coords_wide(coords4, new_stride, dim)
     if n == 0:
         return torch.empty((0, 4), dtype=torch.int32, device=coords4.device), new_stride
     out = torch.empty((n, 4), dtype=torch.int32, device=coords4.device)
@@ -214,6 +206,23 @@ def _output_coords4(coords4: torch.Tensor, tensor_stride: tuple, stride: tuple, 
     step = tuple(new_stride) + (1,) * (3 - dim)
     _lib.call("vp_output_coords", coords4.data_ptr(), None, n, _lib.i32_array(step), out.data_ptr(),
               n_out.data_ptr(), None, ws.data_ptr(), ws.numel(), _lib.stream())
+    n_o = int(n_out.item())
+    if n_o < 0:  # a floored row left the 16-bit packed range: the wide-row path
+        return _output_coords_wide(coords4, new_stride, dim)
+    return out[:n_o], new_stride
+
+
+def _output_coords_wide(coords4: torch.Tensor, new_stride: tuple, dim: int):
+    """generate_output_coords over wide int64 rows (vp_wide_output_coords)."""
+    n = coords4.shape[0]
+    c = widen(coords4, dim)
+    if n == 0:
+        return c.clone(), new_stride
+    out = torch.empty_like(c)
+    n_out = torch.empty(1, dtype=torch.int32, device=c.device)
+    ws = _lib.workspace(_lib.query("vp_wide_ws_bytes", n, 0, dim + 1, 1), c.device)
+    _lib.call("vp_wide_output_coords", c.data_ptr(), n, dim + 1, _lib.i64_array(new_stride), out.data_ptr(),
+              n_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
     return out[: int(n_out.item())], new_stride
 
 
@@ -238,7 +247,7 @@ def _kernel_map4(in4: torch.Tensor, out4: torch.Tensor, shape: KernelShape, in_s
     cap_p = max(n_out * K, 1)
     pin = torch.empty(cap_p, dtype=torch.int32, device=device) if with_pairs else None
     pout = torch.empty(cap_p, dtype=torch.int32, device=device) if with_pairs else None
-    pptr = torch.zeros(K + 1, dtype=torch.int32, device=device)
+    pptr = torch.empty(K + 1, dtype=torch.int32, device=device)  # written by the map (0s when empty)
     ws = _lib.workspace(_lib.query("vp_kernel_map_ws_bytes", n_in, n_out, K), device)
     st3 = tuple(in_stride) + (1,) * (3 - dim)
     offs = shape.offsets3()
@@ -261,7 +270,7 @@ def _kernel_map_wide(inw: torch.Tensor, outw: torch.Tensor, shape: KernelShape, 
     cap_p = max(n_out * K, 1)
     pin = torch.empty(cap_p, dtype=torch.int32, device=device)
     pout = torch.empty(cap_p, dtype=torch.int32, device=device)
-    pptr = torch.zeros(K + 1, dtype=torch.int32, device=device)
+    pptr = torch.empty(K + 1, dtype=torch.int32, device=device)  # written by the map (0s when empty)
     ws = _lib.workspace(_lib.query("vp_wide_ws_bytes", n_in, n_out, dim + 1, K), device)
     offs = np.ascontiguousarray(shape.offsets, dtype=np.int64).ravel()
     _lib.call("vp_wide_kernel_map", inw.data_ptr() if n_in else None, n_in, outw.data_ptr() if n_out else None, n_out,

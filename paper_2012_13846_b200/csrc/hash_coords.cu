@@ -164,15 +164,22 @@ __device__ __forceinline__ int floordiv_mul(int a, int s) {
   return q * s;
 }
 
+// a downsampled row that leaves the 16-bit packed range (e.g. x = -32768
+// floored to a multiple of 3) cannot be keyed: flag it, and the compaction
+// reports n_out = -1 so the caller takes the wide-row path (vp_wide_*),
+// instead of merging rows whose packed keys collide
+__device__ __forceinline__ bool axis_packable(int v) { return v >= kAxisMin && v <= kAxisMax; }
+
 __global__ void oc_insert_kernel(const int4* __restrict__ in, const int32_t* n_dev, int64_t cap_n,
-                                 int sx, int sy, int sz, Slot* t, uint64_t cap) {
+                                 int sx, int sy, int sz, Slot* t, uint64_t cap, unsigned int* unpackable) {
   ::vp::pdl_begin();
   int n = load_count(n_dev, cap_n);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int4 r = in[i];
-    hash_insert(t, cap, pack_key(r.x, floordiv_mul(r.y, sx), floordiv_mul(r.z, sy), floordiv_mul(r.w, sz)),
-                (int)i);
+    const int x = floordiv_mul(r.y, sx), y = floordiv_mul(r.z, sy), z = floordiv_mul(r.w, sz);
+    if (!(axis_packable(x) && axis_packable(y) && axis_packable(z))) *unpackable = 1u;
+    hash_insert(t, cap, pack_key(r.x, x, y, z), (int)i);
   }
 }
 
@@ -200,7 +207,7 @@ __global__ void first_of_kernel(const int4* __restrict__ rows, const int32_t* n_
 __global__ void __launch_bounds__(kCompactBlock)
 compact_first_kernel(const int4* __restrict__ rows, const int32_t* n_dev, int64_t cap_n, int sx, int sy, int sz,
                      const int32_t* __restrict__ first_of, ScanState ss, int4* __restrict__ out, int32_t* n_out,
-                     int32_t* rank_of_first) {
+                     int32_t* rank_of_first, const unsigned int* unpackable) {
   ::vp::pdl_begin();
   __shared__ int s_tile;
   __shared__ int s_warp[kCompactBlock / 32 + 1];
@@ -239,7 +246,8 @@ compact_first_kernel(const int4* __restrict__ rows, const int32_t* n_dev, int64_
   }
   if (n == 0 && tile == 0 && threadIdx.x == 0) *n_out = 0;
   const int64_t last = (int64_t)n - 1;
-  if (last >= base && last < base + kCompactTile && threadIdx.x == 0) *n_out = (int)(s_prefix + total);
+  if (last >= base && last < base + kCompactTile && threadIdx.x == 0)
+    *n_out = (unpackable && *unpackable) ? -1 : (int)(s_prefix + total);
 }
 
 // parent[i] = output row of input row i = rank of its first row
@@ -352,14 +360,39 @@ __global__ void vm_sum_kernel(const void* f, int dtype, int F, int32_t* order, c
        g += (int64_t)gridDim.x * blockDim.x) {
     int s = starts[g], c = counts[g];
     int32_t* seg = order + s;
-    for (int a = 1; a < c; ++a) {  // insertion sort: segments are tiny
-      int32_t key = seg[a];
-      int b = a - 1;
-      while (b >= 0 && seg[b] > key) {
-        seg[b + 1] = seg[b];
-        --b;
+    // restore point order inside the voxel (the sums run in point order,
+    // tensor.py:171-184): insertion sort for the usual handful of points,
+    // in-place heapsort (O(c log c)) when clipping piles many points into
+    // one boundary voxel
+    if (c <= 32) {
+      for (int a = 1; a < c; ++a) {
+        int32_t key = seg[a];
+        int b = a - 1;
+        while (b >= 0 && seg[b] > key) {
+          seg[b + 1] = seg[b];
+          --b;
+        }
+        seg[b + 1] = key;
       }
-      seg[b + 1] = key;
+    } else {
+      auto sift = [&](int root, int end) {
+        while (2 * root + 1 < end) {
+          int ch = 2 * root + 1;
+          if (ch + 1 < end && seg[ch + 1] > seg[ch]) ++ch;
+          if (seg[root] >= seg[ch]) break;
+          const int32_t tmp = seg[root];
+          seg[root] = seg[ch];
+          seg[ch] = tmp;
+          root = ch;
+        }
+      };
+      for (int r = c / 2 - 1; r >= 0; --r) sift(r, c);
+      for (int end = c - 1; end > 0; --end) {
+        const int32_t tmp = seg[0];
+        seg[0] = seg[end];
+        seg[end] = tmp;
+        sift(0, end);
+      }
     }
     for (int j = 0; j < F; ++j) {
       double acc = 0.0;
@@ -495,8 +528,9 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
   if (r) return r;
   cudaMemsetAsync(s1.counter, 0, 256 + tiles * 8, st);
   int blocks = (int)std::min<int64_t>(ceil_div(cap_in, 256), grid_cap(8));
+  unsigned int* unpackable = s1.counter + 2;  // zeroed with the scan state above
   ::vp::launch(oc_insert_kernel, blocks, 256, 0, st, (const int4*)in, n_in_dev, cap_in, step[0], step[1], step[2],
-                                           t, cap);
+                                           t, cap, unpackable);
   VP_CHECK_LAUNCH("oc_insert");
   (void)s2;
   ::vp::launch(first_of_kernel, (int)ceil_div(cap_in, 256), 256, 0, st, (const int4*)in, n_in_dev, cap_in, step[0], step[1],
@@ -504,7 +538,8 @@ int vp_output_coords(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
   VP_CHECK_LAUNCH("oc_first_of");
   ::vp::launch(compact_first_kernel, (int)tiles, kCompactBlock, 0, st, (const int4*)in, n_in_dev, cap_in, step[0], step[1],
                                                              step[2], first_of, s1, (int4*)out, n_out_dev,
-                                                             parent ? rank_of_first : nullptr);
+                                                             parent ? rank_of_first : nullptr,
+                                                             (const unsigned int*)unpackable);
   VP_CHECK_LAUNCH("oc_compact");
   if (parent) {
     ::vp::launch(oc_parent_kernel, blocks, 256, 0, st, n_in_dev, cap_in, first_of, rank_of_first, parent);
@@ -562,7 +597,7 @@ int vp_voxelize(const void* points, int32_t pts_dtype, int64_t n, const int64_t*
   VP_CHECK_LAUNCH("vox_first_of");
   ::vp::launch(compact_first_kernel, (int)tiles, kCompactBlock, 0, st, vox, nullptr, n, 1, 1, 1, first_of, s1,
                                                              (int4*)coords_out, n_out_dev,
-                                                             p2v ? rank_of_first : nullptr);
+                                                             p2v ? rank_of_first : nullptr, (const unsigned int*)nullptr);
   VP_CHECK_LAUNCH("vox_compact");
   if (p2v) {
     ::vp::launch(oc_parent_kernel, blocks, 256, 0, st, nullptr, n, first_of, rank_of_first, p2v);

@@ -159,6 +159,12 @@ class ClusterSpec:
 
     processors: list
     bandwidth_bytes_per_sec: float
+    # optional per-pair overrides {(a, b) sorted: bytes/s} and per-type
+    # metadata {type: {field: value}}, kept and round-tripped as the
+    # reference's ClusterSpec does (profiling.py:242-323); the planner, like
+    # the reference's, uses the single bandwidth
+    pair_bandwidth: dict = field(default_factory=dict)
+    processor_types: dict = field(default_factory=dict)
 
     def __post_init__(self):
         if not self.processors:
@@ -168,6 +174,10 @@ class ClusterSpec:
         ids = [p.instance_id for p in self.processors]
         if len(set(ids)) != len(ids):
             raise StructuralError("duplicate processor instance ids")
+
+    def bandwidth_between(self, a: str, b: str) -> float:
+        key = (a, b) if a <= b else (b, a)
+        return self.pair_bandwidth.get(key, self.bandwidth_bytes_per_sec)
 
     def type_of(self, instance_id: str) -> str:
         for p in self.processors:
@@ -181,9 +191,15 @@ class ClusterSpec:
 
 
 def cluster_to_json(c: ClusterSpec) -> str:
-    return json.dumps({"format_version": FORMAT_VERSION,
-                       "processors": [{"id": p.instance_id, "type": p.type_name} for p in c.processors],
-                       "bandwidth_bytes_per_sec": c.bandwidth_bytes_per_sec}, indent=2, sort_keys=True)
+    obj = {"format_version": FORMAT_VERSION,
+           "processors": [{"id": p.instance_id, "type": p.type_name} for p in c.processors],
+           "bandwidth_bytes_per_sec": c.bandwidth_bytes_per_sec}
+    if c.pair_bandwidth:
+        obj["pair_bandwidth"] = [{"a": a, "b": b, "bandwidth_bytes_per_sec": v}
+                                 for (a, b), v in sorted(c.pair_bandwidth.items())]
+    if c.processor_types:
+        obj["processor_types"] = {k: dict(v) for k, v in sorted(c.processor_types.items())}
+    return json.dumps(obj, indent=2, sort_keys=True)
 
 
 def cluster_from_json(text: str) -> ClusterSpec:
@@ -191,8 +207,16 @@ def cluster_from_json(text: str) -> ClusterSpec:
         obj = json.loads(text)
         if int(obj.get("format_version", -1)) != FORMAT_VERSION:
             raise ValidationError("unsupported or missing cluster format_version")
+        pair = {}
+        for rec in obj.get("pair_bandwidth", []):
+            a, b = str(rec["a"]), str(rec["b"])
+            bw = float(rec["bandwidth_bytes_per_sec"])
+            if not bw > 0:
+                raise ValidationError("pair bandwidth must be positive")
+            pair[(a, b) if a <= b else (b, a)] = bw
+        types = {str(k): dict(v) for k, v in obj.get("processor_types", {}).items()}
         return ClusterSpec([Processor(str(r["id"]), str(r["type"])) for r in obj["processors"]],
-                           float(obj["bandwidth_bytes_per_sec"]))
+                           float(obj["bandwidth_bytes_per_sec"]), pair, types)
     except (json.JSONDecodeError, KeyError, TypeError, ValueError) as exc:
         raise ValidationError(f"malformed cluster file: {exc}") from exc
 

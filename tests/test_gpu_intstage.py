@@ -187,3 +187,22 @@ def test_validation_errors():
     two = SparseTensor([[0, 0, 0, 0], [1, 0, 0, 0]], np.zeros((2, 1)), (1, 1, 1))
     with pytest.raises(StructuralError):  # flattening batch indices collides (tensor.py:224-229)
         batch([two])
+
+
+def test_voxel_mean_many_points_in_one_voxel():
+    """clipping can pile a large share of a cloud into one boundary
+    voxel; the point-order mean must stay exact and fast (heapsort path for
+    segments > 32 points)."""
+    import time
+    from paper_2012_13846_b200 import tensor as T
+    rng = np.random.default_rng(4)
+    n = 60000
+    pts = rng.uniform(-50.0, 60.0, (n, 3))  # most points clip into the corner/edge voxels of a 4^3 grid
+    feats = rng.normal(size=(n, 2))
+    t0 = time.time()
+    m = T.voxelize(T.PointCloud(pts, feats), 1.0, (4, 4, 4))
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 20.0
+    rc, rf = O.voxelize(pts, 1.0, (4, 4, 4), features=feats)
+    np.testing.assert_array_equal(m.coords.cpu().numpy(), rc)
+    np.testing.assert_allclose(m.features.cpu().numpy(), rf, rtol=1e-6, atol=1e-6)

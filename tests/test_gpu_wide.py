@@ -108,3 +108,20 @@ def test_wide_validation_errors():
         SparseTensor([[0, 100001, 0, 0]], np.zeros((1, 1)), (2, 2, 2))
     t = SparseTensor([[0, 100000, 0, 0], [1, 100000, 0, 0]], np.zeros((2, 1)), (2, 2, 2))
     assert t.wide and len(t) == 2
+
+
+def test_abi_output_coords_flags_unpackable_rows():
+    """at the C-ABI, a row that is packable before downsampling
+    but not after (x = -32768 floored to a multiple of 3 = -32769) is not
+    merged silently: vp_output_coords reports n_out = -1 (use the wide path)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2012_13846_b200 import _lib
+    c = torch.tensor([[0, -32768, 0, 0], [0, -32767, 5, 0], [1, 3, 3, 3]], dtype=torch.int32, device="cuda")
+    out = torch.empty_like(c)
+    n_out = torch.empty(1, dtype=torch.int32, device="cuda")
+    ws = _lib.workspace(_lib.query("vp_output_coords_ws_bytes", 3), c.device)
+    for step, expect in (((3, 3, 3), -1), ((2, 2, 2), 3)):
+        _lib.call("vp_output_coords", c.data_ptr(), None, 3, _lib.i32_array(step), out.data_ptr(), n_out.data_ptr(),
+                  None, ws.data_ptr(), ws.numel(), _lib.stream())
+        assert int(n_out.item()) == expect, (step, int(n_out.item()))

@@ -242,3 +242,21 @@ def test_acceptance_7_table_iii_shape():
     mp = P.evaluate(P.plan_with_types_as(ps, c, "TitanXP"), ps, c)
     hete = P.plan(ps, c).objective
     assert hete <= mp * (1 + 1e-12) <= dp * (1 + 1e-12)
+
+
+def test_cluster_pair_bandwidth_and_types_round_trip():
+    """The reference ClusterSpec's optional pair_bandwidth / processor_types
+    (profiling.py:242-323) are kept and round-tripped."""
+    import json
+    c = P.ClusterSpec.homogeneous(3, "b200", 9e11)
+    obj = json.loads(P.cluster_to_json(c))
+    obj["pair_bandwidth"] = [{"a": "b2002", "b": "b2000", "bandwidth_bytes_per_sec": 4e11}]
+    obj["processor_types"] = {"b200": {"memory_bytes": 180e9}}
+    c2 = P.cluster_from_json(json.dumps(obj))
+    assert c2.bandwidth_between("b2000", "b2002") == 4e11 == c2.bandwidth_between("b2002", "b2000")
+    assert c2.bandwidth_between("b2000", "b2001") == 9e11
+    c3 = P.cluster_from_json(P.cluster_to_json(c2))
+    assert c3.pair_bandwidth == c2.pair_bandwidth and c3.processor_types == c2.processor_types
+    obj["pair_bandwidth"][0]["bandwidth_bytes_per_sec"] = 0
+    with pytest.raises(P.ValidationError):
+        P.cluster_from_json(json.dumps(obj))
