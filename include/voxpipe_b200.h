@@ -42,7 +42,10 @@ extern "C" {
 typedef struct CUstream_st* vp_stream_t; /* == cudaStream_t */
 
 enum { VP_OK = 0, VP_EVALIDATION = 2, VP_EINTERNAL = 3 };
-enum { VP_F32 = 0, VP_BF16 = 1, VP_F64 = 2 };
+/* VP_TF32: fp32 storage with tf32 tensor-core math — accepted as the
+ * feature dtype of vp_conv_fwd / vp_conv_dgrad (fp32 accumulation, error
+ * <= 2e-3 * sum|W||x|); everywhere else it means VP_F32. */
+enum { VP_F32 = 0, VP_BF16 = 1, VP_F64 = 2, VP_TF32 = 3 };
 #define VP_MAX_OFFSETS 343 /* 7^3 */
 
 const char* vp_last_error(void);
@@ -180,8 +183,11 @@ int vp_kernel_map_inverse(const int32_t* nbr, const int32_t* n_out_dev, int64_t 
 /* ---------------------------------------------------------------- sparse conv
  * Forward (conv.py:186-208, Eq. 3): y[u] = sum_k W_k x[nbr[u,k]], summed per
  * output row in offset order; output-stationary implicit GEMM on tcgen05
- * (bf16 in, fp32 TMEM accumulate) when x is bf16 and C_in, C_out are in
- * {32,64,128,256}; a SIMT kernel otherwise.  Deterministic, no atomics.
+ * (bf16 in, fp32 TMEM accumulate) when x is bf16 and C_in, C_out are
+ * multiples of 8 up to 256 (tiles of 32/64/128/256, the padding zero-filled
+ * on load and never stored); tf32 math on the same tiles when x_dtype is
+ * VP_TF32 (C_in <= 128); a SIMT kernel otherwise (exact fp32 / f64).
+ * Deterministic, no atomics.
  *   table  : nbr [cap_out, K] (or inv for dgrad); flip != 0 reads column
  *            K-1-k (stride-1 symmetric kernels: inv[v,k] == nbr[v,K-1-k]).
  *   perm   : nullable; table row i holds the neighbours of output row

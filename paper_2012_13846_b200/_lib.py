@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvoxpipe_b200.so")
 
 VP_OK, VP_EVALIDATION, VP_EINTERNAL = 0, 2, 3
-VP_F32, VP_BF16, VP_F64 = 0, 1, 2
+VP_F32, VP_BF16, VP_F64, VP_TF32 = 0, 1, 2, 3
 MAX_OFFSETS = 343
 
 P = C.c_void_p

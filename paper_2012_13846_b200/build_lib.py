@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvoxpipe_b200.so")
 SOURCES = ["hash_coords.cu", "kmap.cu", "kmap_sort.cu", "kmap_brick.cu", "conv.cu", "glue.cu", "wide.cu"] + [
-    f"conv_tc_k{kd}_{t}.cu" for kd in (32, 64, 128, 256) for t in ("f", "d")]
+    f"conv_tc_k{kd}_{t}.cu" for kd in (32, 64, 128, 256) for t in ("f", "d")] + ["conv_tc_tf32.cu", "conv_tc_pad.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -321,8 +321,18 @@ def _sortable(table: torch.Tensor) -> bool:
     return table.dim() == 2 and 1 <= table.shape[1] <= 30 and table.shape[0] >= SORT_MIN_ROWS
 
 
+def _math_code(t: torch.Tensor, math: str) -> int:
+    """Feature dtype code for the C-ABI: math="tf32" runs fp32 features on
+    the tensor cores with tf32 multiplies (VP_TF32); "exact" keeps fp32 SIMT."""
+    if math not in ("exact", "tf32"):
+        raise ValidationError(f"math must be 'exact' or 'tf32', got {math!r}")
+    if math == "tf32" and t.dtype == torch.float32:
+        return _lib.VP_TF32
+    return _lib.dtype_code(t)
+
+
 def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: int, out_dtype=None,
-                     flip: bool = False, perm: Optional[torch.Tensor] = None) -> torch.Tensor:
+                     flip: bool = False, perm: Optional[torch.Tensor] = None, math: str = "exact") -> torch.Tensor:
     """y[u] = sum_k W_k x[nbr[u, k]] for u < n_out (the gather-GEMM of Eq. 3).
     With `perm`, table row i holds the neighbours of output row perm[i]."""
     out_dtype = out_dtype or x.dtype
@@ -330,7 +340,7 @@ def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: 
     y = torch.empty((max(n_out, 1), w.n_out), dtype=out_dtype, device=x.device)
     wt = w.operand(x.dtype)
     ws = _lib.workspace(_lib.query("vp_conv_fwd_ws_bytes", w.n_in, w.n_out, K), x.device)
-    _lib.call("vp_conv_fwd", x.data_ptr(), _lib.dtype_code(x), max(x.shape[0], 1), w.n_in, wt.data_ptr(),
+    _lib.call("vp_conv_fwd", x.data_ptr(), _math_code(x, math), max(x.shape[0], 1), w.n_in, wt.data_ptr(),
               _lib.dtype_code(wt), w.n_out,
               K, nbr.data_ptr(), int(flip), _lib.ptr(perm), None, n_out, y.data_ptr(), _lib.dtype_code(y),
               ws.data_ptr(), ws.numel(), _lib.stream())
@@ -338,14 +348,14 @@ def conv_forward_raw(x: torch.Tensor, w: ConvWeights, nbr: torch.Tensor, n_out: 
 
 
 def conv_dgrad_raw(g: torch.Tensor, w: ConvWeights, table: torch.Tensor, n_in: int, flip: bool,
-                   out_dtype=None, perm: Optional[torch.Tensor] = None) -> torch.Tensor:
+                   out_dtype=None, perm: Optional[torch.Tensor] = None, math: str = "exact") -> torch.Tensor:
     """grad_in[v] = sum_k W_k^T g[table[v, k]] (conv.py:240)."""
     out_dtype = out_dtype or g.dtype
     K = w.num_offsets
     gi = torch.empty((max(n_in, 1), w.n_in), dtype=out_dtype, device=g.device)
     wt = w.operand(g.dtype)
     ws = _lib.workspace(_lib.query("vp_conv_dgrad_ws_bytes", w.n_in, w.n_out, K), g.device)
-    _lib.call("vp_conv_dgrad", g.data_ptr(), _lib.dtype_code(g), max(g.shape[0], 1), w.n_out, wt.data_ptr(),
+    _lib.call("vp_conv_dgrad", g.data_ptr(), _math_code(g, math), max(g.shape[0], 1), w.n_out, wt.data_ptr(),
               _lib.dtype_code(wt),
               w.n_in, K, table.data_ptr(), int(flip), _lib.ptr(perm), None, n_in, gi.data_ptr(), _lib.dtype_code(gi),
               ws.data_ptr(), ws.numel(), _lib.stream())
@@ -366,20 +376,23 @@ def conv_wgrad_raw(x: torch.Tensor, g: torch.Tensor, w_shape: tuple, kmap: Kerne
     return gw
 
 
-def sparse_conv_forward(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride=1) -> SparseTensor:
+def sparse_conv_forward(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride=1, *,
+                        math: str = "exact") -> SparseTensor:
     """conv.py:186-208 — x_out[u] = sum over offsets i with u+i occupied of
-    W_i x_in[u+i]; output rows at generate_output_coords(t, stride)."""
+    W_i x_in[u+i]; output rows at generate_output_coords(t, stride).
+    math="tf32": fp32 features on the tensor cores (tf32 multiplies)."""
     _check_weights(t, w, shape)
     st = _stride3(stride, t.dim)
     out4, ns = _output_coords4(t.coords4, t.tensor_stride, st, t.dim)
     km = _kernel_map4(t.coords4, out4, shape, t.tensor_stride, t.dim, with_pairs=False)
     n_out = out4.shape[0]
     perm, table = sort_table(km.nbr, n_out) if _sortable(km.nbr) else (None, km.nbr)
-    y = conv_forward_raw(t.features, w, table, n_out, perm=perm)
+    y = conv_forward_raw(t.features, w, table, n_out, perm=perm, math=math)
     return SparseTensor(out4, y, ns, _trusted=True, _dim=t.dim)
 
 
-def sparse_conv_backward(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride, grad_out):
+def sparse_conv_backward(t: SparseTensor, w: ConvWeights, shape: KernelShape, stride, grad_out, *,
+                         math: str = "exact"):
     """conv.py:211-242 — (grad_in (N_in, n_in) in the feature dtype,
     grad_w (K, n_out, n_in) fp32).  Recomputes coords and map as the
     reference does."""
@@ -400,7 +413,7 @@ def sparse_conv_backward(t: SparseTensor, w: ConvWeights, shape: KernelShape, st
     perm = None
     if _sortable(table):  # the flipped table's hit masks are bit-reversed: same grouping
         perm, table = sort_table(table, len(t))
-    gi = conv_dgrad_raw(g, w, table, len(t), flip, perm=perm)
+    gi = conv_dgrad_raw(g, w, table, len(t), flip, perm=perm, math=math)
     gw = conv_wgrad_raw(t.features, g, tuple(w.matrices.shape), km)
     return gi, gw
 

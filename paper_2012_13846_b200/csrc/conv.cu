@@ -657,6 +657,25 @@ static BnEpi make_epi(int32_t mode, void* bn_part, const void* add, const void* 
 
 // ------------------------------------------------------------------ dispatch
 static bool tc_width(int64_t c) { return c == 32 || c == 64 || c == 128 || c == 256; }
+// tile width of a tensor-core operand of c 2-byte units (c % 8 == 0: 16 B
+// rows), 0 when the tensor cores do not take it
+static int64_t tc_pad(int64_t c) {
+  if (c < 8 || c % 8 != 0 || c > 256) return 0;
+  return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : 256;
+}
+
+// wt[k, ci, co] = w[k, co, ci] in fp32 (the tf32 dgrad's K-major B operand)
+__global__ void transpose_w_f32_kernel(const void* __restrict__ w, int wd, float* __restrict__ wt, int K, int cout,
+                                   int cin) {
+  ::vp::pdl_begin();
+  const int64_t total = (int64_t)K * cin * cout;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / ((int64_t)cin * cout);
+    const int64_t r = e - k * cin * cout;
+    const int ci = (int)(r / cout), co = (int)(r - (int64_t)ci * cout);
+    wt[e] = ldf(w, wd, (k * cout + co) * cin + ci);
+  }
+}
 
 template <bool BMN>
 static int conv_tc(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
@@ -745,8 +764,10 @@ int vp_debug_conv_trace(long long* buf) {
   return VP_OK;
 }
 
+// weights cast / transposed (up to fp32) + the split-K partials of the padded tile width
+static int64_t split_width(int64_t c) { return std::max<int64_t>(tc_pad(c), std::min<int64_t>(c, 256)); }
 size_t vp_conv_fwd_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
-  return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cout);
+  return align_up((size_t)K * cin * cout * 4, 256) + split_ws_bytes(split_width(cout));
 }
 
 static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype,
@@ -789,10 +810,32 @@ static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t
              "output dtype must be f32, bf16 or f64");
   if (cap_out <= 0) return epi_after(VP_OK);
   const bool f64 = x_dtype == VP_F64 || w_dtype == VP_F64 || y_dtype == VP_F64;
-  if (!f64 && x_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
+  if (x_dtype == VP_TF32) {
+    // fp32 features, tf32 tensor-core math: the bf16 tile machinery over
+    // 2-byte units (an fp32 row of C is 2C units; K = 8 tf32 per MMA = 32 B)
+    if (!f64 && tc_pad(2 * cin) && tc_pad(cout) && y_dtype != VP_F64) {
+      VP_REQUIRE(ws && ws_bytes >= vp_conv_fwd_ws_bytes(cin, cout, K), VP_EVALIDATION, "conv_fwd: workspace too small");
+      const float* wf = (const float*)w;
+      if (w_dtype != VP_F32 && w_dtype != VP_TF32) {
+        const int64_t cnt = (int64_t)K * cin * cout;
+        ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st, w, w_dtype, ws, VP_F32, cnt);
+        VP_CHECK_LAUNCH("conv_fwd: cast w (tf32)");
+        wf = (const float*)ws;
+      }
+      char* part = (char*)ws + align_up((size_t)K * cin * cout * 4, 256);
+      FwdParams p{(const bf16*)x, (const bf16*)wf, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
+      p.kreal = (int)(2 * cin);
+      p.nreal = (int)cout;
+      return epi_after(conv_tc_tf32(tc_pad(2 * cin), tc_pad(cout), p, part, st));
+    }
+    x_dtype = VP_F32;  // exact fp32 SIMT path
+  }
+  if (w_dtype == VP_TF32) w_dtype = VP_F32;
+  if (!f64 && x_dtype == VP_BF16 && tc_pad(cin) && tc_pad(cout)) {
     VP_REQUIRE(ws && ws_bytes >= vp_conv_fwd_ws_bytes(cin, cout, K), VP_EVALIDATION, "conv_fwd: workspace too small");
+    const bool exact = tc_pad(cin) == cin && tc_pad(cout) == cout;
     const bf16* wb = (const bf16*)w;
-    char* part = (char*)ws + align_up((size_t)K * cin * cout * 2, 256);
+    char* part = (char*)ws + align_up((size_t)K * cin * cout * 4, 256);
     if (w_dtype != VP_BF16) {
       int64_t cnt = (int64_t)K * cin * cout;
       ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st, w, w_dtype, ws, VP_BF16, cnt);
@@ -800,15 +843,18 @@ static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t
       wb = (const bf16*)ws;
     }
     (void)x_rows;  // the cp.async gather zero-fills missing neighbours itself
-    if (rows32_ok(cin, cout, K))
+    if (exact && rows32_ok(cin, cout, K))
       return epi_after(
           launch_rows32<false>((const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, st));
     FwdParams p{(const bf16*)x, wb, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype, nullptr, 1, 0, 0};
-    if (y_dtype == VP_BF16) {
+    p.kreal = (int)cin;
+    p.nreal = (int)cout;
+    if (y_dtype == VP_BF16 && exact) {
       p.epi = epi;  // fused into the epilogue / split-K reduction
       return conv_tc<false>(cin, cout, p, part, st);
     }
-    return epi_after(conv_tc<false>(cin, cout, p, part, st));
+    if (exact) return epi_after(conv_tc<false>(cin, cout, p, part, st));
+    return epi_after(conv_tc_pad_fwd(tc_pad(cin), tc_pad(cout), p, part, st));
   }
   if (!f64 && small_fwd_ok(cin, cout, K)) {
     bool fused = false;
@@ -826,7 +872,7 @@ static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t
 }
 
 size_t vp_conv_dgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
-  return align_up((size_t)K * cin * cout * 2, 256) + split_ws_bytes(cin);
+  return align_up((size_t)K * cin * cout * 4, 256) + split_ws_bytes(split_width(cin));
 }
 
 static int conv_dgrad_impl(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cout, const void* w, int32_t w_dtype,
@@ -866,11 +912,30 @@ static int conv_dgrad_impl(const void* g, int32_t g_dtype, int64_t g_rows, int64
              "grad_in dtype must be f32, bf16 or f64");
   if (cap_in <= 0) return epi_after(VP_OK);
   const bool f64 = g_dtype == VP_F64 || w_dtype == VP_F64 || gi_dtype == VP_F64;
-  if (!f64 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
+  if (g_dtype == VP_TF32) {
+    // tf32: grad_in = sum_k W_k^T g[table] with W^T staged K-major in fp32
+    if (!f64 && tc_pad(2 * cout) && tc_pad(cin) && gi_dtype != VP_F64) {
+      VP_REQUIRE(ws && ws_bytes >= vp_conv_dgrad_ws_bytes(cin, cout, K), VP_EVALIDATION,
+                 "conv_dgrad: workspace too small");
+      const int64_t cnt = (int64_t)K * cin * cout;
+      ::vp::launch(transpose_w_f32_kernel, (int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st, w,
+                   w_dtype == VP_TF32 ? (int)VP_F32 : (int)w_dtype, (float*)ws, K, (int)cout, (int)cin);
+      VP_CHECK_LAUNCH("conv_dgrad: transpose w (tf32)");
+      char* part = (char*)ws + align_up((size_t)K * cin * cout * 4, 256);
+      FwdParams p{(const bf16*)g, (const bf16*)ws, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1, 0, 0};
+      p.kreal = (int)(2 * cout);
+      p.nreal = (int)cin;
+      return epi_after(conv_tc_tf32(tc_pad(2 * cout), tc_pad(cin), p, part, st));
+    }
+    g_dtype = VP_F32;
+  }
+  if (w_dtype == VP_TF32) w_dtype = VP_F32;
+  if (!f64 && g_dtype == VP_BF16 && tc_pad(cin) && tc_pad(cout)) {
     VP_REQUIRE(ws && ws_bytes >= vp_conv_dgrad_ws_bytes(cin, cout, K), VP_EVALIDATION,
                "conv_dgrad: workspace too small");
+    const bool exact = tc_pad(cin) == cin && tc_pad(cout) == cout;
     const bf16* wb = (const bf16*)w;
-    char* part = (char*)ws + align_up((size_t)K * cin * cout * 2, 256);
+    char* part = (char*)ws + align_up((size_t)K * cin * cout * 4, 256);
     if (w_dtype != VP_BF16) {
       int64_t cnt = (int64_t)K * cin * cout;
       ::vp::launch(cast_kernel, (int)std::min<int64_t>(ceil_div(cnt, 256), 1184), 256, 0, st, w, w_dtype, ws, VP_BF16, cnt);
@@ -879,15 +944,18 @@ static int conv_dgrad_impl(const void* g, int32_t g_dtype, int64_t g_rows, int64
     }
     // grad_in = sum_k W_k^T g[table]: GEMM K-dim = C_out, N = C_in, W read as MN-major B
     (void)g_rows;
-    if (rows32_ok(cout, cin, K))
+    if (exact && rows32_ok(cout, cin, K))
       return epi_after(
           launch_rows32<true>((const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, st));
     FwdParams p{(const bf16*)g, wb, K, table, flip, perm, n_in_dev, cap_in, gi, gi_dtype, nullptr, 1, 0, 0};
-    if (gi_dtype == VP_BF16) {
+    p.kreal = (int)cout;
+    p.nreal = (int)cin;
+    if (gi_dtype == VP_BF16 && exact) {
       p.epi = epi;
       return conv_tc<true>(cout, cin, p, part, st);
     }
-    return epi_after(conv_tc<true>(cout, cin, p, part, st));
+    if (exact) return epi_after(conv_tc<true>(cout, cin, p, part, st));
+    return epi_after(conv_tc_pad_dgrad(tc_pad(cout), tc_pad(cin), p, part, st));
   }
   const int64_t total = cap_in * cin;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
@@ -918,6 +986,8 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(ws && ws_bytes >= vp_conv_wgrad_ws_bytes(cin, cout, K, cap_pairs), VP_EVALIDATION,
              "conv_wgrad: workspace too small");
+  if (x_dtype == VP_TF32) x_dtype = VP_F32;  // fp32 storage; the weight gradient is exact fp32
+  if (g_dtype == VP_TF32) g_dtype = VP_F32;
   const int chunk = wgrad_chunk(cap_pairs);
   const int max_items = (int)(cap_pairs / chunk + K + 1);
   float* part = (float*)ws;

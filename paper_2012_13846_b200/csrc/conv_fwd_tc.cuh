@@ -47,6 +47,11 @@ struct FwdParams {
   int dbg;        // experiments only: bit0 no MMA, bit1 no B copies, bit2 no A copies, bit3 plain arrive for empty, bit4 every offset active (no mask scan)
   BnEpi epi;      // BN statistics of the output (bn_epi.cuh); mode 0 = off.  Needs a bf16 output.
   long long* trace;  // debug timeline of CTA 0 (null = off)
+  // real widths in 2-byte units (the kernel's KD / ND are the padded tile
+  // widths): gathered row length (C_in, or 2 C_in for tf32) and output
+  // columns.  Chunks past kreal load zeros, columns past nreal are not stored.
+  int kreal;
+  int nreal;
 };
 
 constexpr int kTcProd = 128, kTcEpi = 128, kTcThreads = kTcProd + kTcEpi + 32;
@@ -77,8 +82,12 @@ constexpr int tmem_cols_pow2(int c) {
 // slab is fetched once and feeds TT MMAs into TT TMEM accumulators, so at
 // large N (no split-K needed) the L2->SMEM traffic of the weights, 1/2 to
 // 2/3 of all staged bytes at C >= 128, is divided by TT.
-template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1>
+// MODE: 0 = bf16 at exact tile widths (compile-time strides, the hot path);
+// 1 = bf16 padded to the tile widths (runtime kreal / nreal); 2 = tf32
+// (fp32 storage, padded like 1)
+template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1, int MODE = 0>
 struct FwdTC {
+  static constexpr bool TF32 = MODE == 2;
   static constexpr bool PAIR = (KD == 32);
   static constexpr int NCH = PAIR ? 1 : KD / 64;
   static constexpr int A_BYTES = 128 * 128;
@@ -96,7 +105,7 @@ struct FwdTC {
   static constexpr int ACC = (tmem_cols_pow2(2 * TT * ND) * CPS <= 512) ? 2 : 1;
   static constexpr int COLS = ACC * TT * ND;
   static constexpr int TMEM_COLS = tmem_cols_pow2(COLS);
-  static constexpr uint32_t IDESC = tc::idesc_bf16(128, ND, 0, BMN ? 1 : 0);
+  static constexpr uint32_t IDESC = TF32 ? tc::idesc_tf32(128, ND, 0, BMN ? 1 : 0) : tc::idesc_bf16(128, ND, 0, BMN ? 1 : 0);
   static constexpr int SMEM_BASE = STAGES * STAGE + 1024 + BOOK;
   static constexpr int SMEM_MAX = SMEM_BASE + 2 * TT * 128 * kTblK * 4;
   static int smem_bytes(int K, bool tbl) { return SMEM_BASE + (tbl ? 2 * TT * 128 * K * 4 : 0); }
@@ -112,10 +121,13 @@ __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) 
   return s > max_split ? max_split : s;
 }
 
-template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL, int TT = 1>
+template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL, int TT = 1, int MODE = 0>
 __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_constant__ FwdParams p) {
   ::vp::pdl_begin();
-  using C = FwdTC<KD, ND, BMN, CPS, RB, TT>;
+  using C = FwdTC<KD, ND, BMN, CPS, RB, TT, MODE>;
+  constexpr bool TF32 = C::TF32;
+  static_assert(!(TF32 && BMN), "tf32: dgrad reads a K-major transposed weight copy");
+  const int kreal = MODE == 0 ? KD : p.kreal, nreal = MODE == 0 ? ND : p.nreal;
   constexpr int TR = 128 * TT;  // rows per work item
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -270,7 +282,9 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
             const uint32_t a_s = a_s0 + t * C::A_BYTES;
             const int kq = C::PAIR ? (q < 4 ? ka : kb) : ka;
             const int col = p.flip ? K - 1 - kq : kq;
-            const char* xq = xb + 2 * (C::PAIR ? (q & 3) * 8 : cs * 64 + q * 8);
+            const int ch = C::PAIR ? (q & 3) * 8 : cs * 64 + q * 8;  // first element of this lane's 16 B chunk
+            const bool chv = ch < kreal;                               // padded widths: zero chunk
+            const char* xq = xb + 2 * (chv ? ch : 0);
             int vr[8];
             const bool noa = p.dbg & 4;
 #pragma unroll
@@ -283,7 +297,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
             for (int i = 0; i < 8; ++i) {
               const int v = vr[i];
               tc::cp_async16(a_s + ((i & 1) ? a_off1 : a_off0) + i * 512,
-                             xq + (int64_t)(v > 0 ? v : 0) * (KD * 2), v >= 0 ? 16 : 0);
+                             xq + (int64_t)(v > 0 ? v : 0) * (kreal * 2), (v >= 0 && chv) ? 16 : 0);
             }
           }
           // ---- B
@@ -293,10 +307,15 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
           } else if (!BMN) {  // B[n][kk] = W[k][n][slice] (K-major rows of W); thread: chunk qq = tid & 7, rows n = tid/8 + 16j
             const int qq = tid & 7, n0 = tid >> 3;
             const int k = (C::PAIR && qq >= 4) ? kB : kA;
-            const bf16* src = p.w + ((int64_t)k * ND + n0) * KD + (C::PAIR ? (qq & 3) * 8 : cs * 64 + qq * 8);
+            const int bc = C::PAIR ? (qq & 3) * 8 : cs * 64 + qq * 8;
+            const bool bcv = bc < kreal;
+            const bf16* src = p.w + ((int64_t)k * nreal + n0) * kreal + (bcv ? bc : 0);
             const uint32_t dst = b_s + n0 * 128 + ((qq ^ (n0 & 7)) << 4);
 #pragma unroll
-            for (int j = 0; j < ND / 16; ++j) tc::cp_async16(dst + j * 2048, src + (int64_t)j * 16 * KD, 16);
+            for (int j = 0; j < ND / 16; ++j) {
+              const bool ok = bcv && n0 + j * 16 < nreal;
+              tc::cp_async16(dst + j * 2048, ok ? src + (int64_t)j * 16 * kreal : p.w, ok ? 16 : 0);
+            }
           } else {  // B(n, kk) = W[k][kk][n]: row kk of W_k is N-contiguous (MN-major)
             constexpr int NCHK = ND / 8;        // 16 B chunks per kk row
             constexpr int KKS = kTcProd / NCHK;  // kk rows per pass
@@ -305,15 +324,19 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
             for (int j = 0; j < 64 / KKS; ++j) {
               const int kk = kk0 + j * KKS;
               const bf16* src;
+              int kr;  // row of W_k (the gathered width)
               if (C::PAIR) {
                 const int k = kk < 32 ? kA : kB;
-                src = p.w + ((int64_t)k * KD + (kk & 31)) * ND + jn * 8;
+                kr = kk & 31;
+                src = p.w + ((int64_t)k * kreal + kr) * nreal + jn * 8;
               } else {
-                src = p.w + ((int64_t)kA * KD + cs * 64 + kk) * ND + jn * 8;
+                kr = cs * 64 + kk;
+                src = p.w + ((int64_t)kA * kreal + kr) * nreal + jn * 8;
               }
+              const bool ok = kr < kreal && jn * 8 < nreal;
               const uint32_t off =
                   (uint32_t)((jn >> 3) * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + (((jn & 7) ^ (kk & 7)) << 4));
-              tc::cp_async16(b_s + off, src, 16);
+              tc::cp_async16(b_s + off, ok ? src : p.w, ok ? 16 : 0);
             }
           }
         }
@@ -468,7 +491,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 #pragma unroll
             for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           } else if (p.y_dtype == VP_BF16) {
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p.y) + orow * ND + c0);
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p.y) + orow * nreal + c0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               uint4 pk;
@@ -480,12 +503,13 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
               pk.y = *reinterpret_cast<uint32_t*>(&h1);
               pk.z = *reinterpret_cast<uint32_t*>(&h2);
               pk.w = *reinterpret_cast<uint32_t*>(&h3);
-              dst[q] = pk;
+              if (c0 + 8 * q < nreal) dst[q] = pk;
             }
           } else {
-            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.y) + orow * ND + c0);
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.y) + orow * nreal + c0);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            for (int q = 0; q < 8; ++q)
+              if (c0 + 4 * q < nreal) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           }
         }
       }
@@ -526,7 +550,8 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 #pragma unroll
             for (int t = 0; t < TT; ++t) {
               const uint64_t ad = tc::smem_desc(a_s + t * C::A_BYTES + kk * 32, 16, 1024, tc::kSwizzle128);
-              tc::mma_bf16(d + t * ND, ad, bd, C::IDESC, (sj > 0 || at > 0 || kk > 0) ? 1u : 0u);
+              if constexpr (TF32) tc::mma_tf32(d + t * ND, ad, bd, C::IDESC, (sj > 0 || at > 0 || kk > 0) ? 1u : 0u);
+              else tc::mma_bf16(d + t * ND, ad, bd, C::IDESC, (sj > 0 || at > 0 || kk > 0) ? 1u : 0u);
             }
           }
         }
@@ -564,7 +589,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 // out[r, n] = sum over splits of the fp32 partials, in split order.
 static __global__ void split_reduce_kernel(const float* __restrict__ part, const int32_t* n_out_dev, int64_t cap_out, int ND,
                                     int grid, int max_split, const int32_t* __restrict__ perm, void* __restrict__ y,
-                                    int y_dtype) {
+                                    int y_dtype, int nreal) {
   ::vp::pdl_begin();
   const int n_out = load_count(n_out_dev, cap_out);
   const int ntiles = (n_out + 127) / 128;
@@ -585,7 +610,8 @@ static __global__ void split_reduce_kernel(const float* __restrict__ part, const
       acc.z += v.z;
       acc.w += v.w;
     }
-    const int64_t oidx = perm ? (int64_t)__ldg(perm + r) * ND + n : idx;
+    if (n >= nreal) continue;  // padded columns
+    const int64_t oidx = (perm ? (int64_t)__ldg(perm + r) : r) * nreal + n;
     if (y_dtype == VP_BF16) {
       __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<bf16*>(y) + oidx);
       d[0] = __floats2bfloat162_rn(acc.x, acc.y);

@@ -13,11 +13,12 @@ namespace vp {
 
 constexpr int kMaxSplit = 16;
 
-template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1>
+template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1, int MODE = 0>
 inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
-  using C = FwdTC<KD, ND, BMN, CPS, RB, TT>;
+  using C = FwdTC<KD, ND, BMN, CPS, RB, TT, MODE>;
   const bool tbl = p0.K <= kTblK && ((uintptr_t)p0.table & 15) == 0;
-  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true, TT> : conv_tc_kernel<KD, ND, BMN, CPS, RB, false, TT>;
+  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true, TT, MODE>
+                  : conv_tc_kernel<KD, ND, BMN, CPS, RB, false, TT, MODE>;
   static_assert(C::SMEM_MAX <= 227 * 1024, "conv_tc: shared memory over the per-CTA limit");
   static bool attr_t = false, attr_f = false;  // immutable per-instantiation attribute cache
   bool& attr = tbl ? attr_t : attr_f;
@@ -49,7 +50,7 @@ inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   } else if (part) {
     const int64_t work = p.cap_out * ND / 4;
     ::vp::launch(split_reduce_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), grid_cap(8))), 256, 0, st, 
-        (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.perm, p.y, p.y_dtype);
+        (const float*)part, p.n_out_dev, p.cap_out, ND, grid, p.max_split, p.perm, p.y, p.y_dtype, p.nreal);
     VP_CHECK_LAUNCH("split_reduce");
   }
   return VP_OK;
@@ -128,6 +129,44 @@ inline int conv_tc_nd(int64_t nd, const FwdParams& p, void* part, cudaStream_t s
   return VP_EINTERNAL;
 }
 
+
+// padded bf16 (MODE 1) and tf32 (MODE 2, K-major weights only): the default
+// config and its fallbacks
+template <int KD, int ND, bool BMN, int MODE>
+inline int launch_conv_mode(const FwdParams& p, void* part, cudaStream_t st) {
+  if constexpr (FwdTC<KD, ND, BMN, kCfgCps[3], kCfgRb[3], 1, MODE>::FITS)
+    return launch_conv_tc<KD, ND, BMN, kCfgCps[3], kCfgRb[3], 1, MODE>(p, part, st);
+  else if constexpr (FwdTC<KD, ND, BMN, kCfgCps[0], kCfgRb[0], 1, MODE>::FITS)
+    return launch_conv_tc<KD, ND, BMN, kCfgCps[0], kCfgRb[0], 1, MODE>(p, part, st);
+  else
+    return launch_conv_tc<KD, ND, BMN, 1, 1, 1, MODE>(p, part, st);
+}
+
+template <int KD, bool BMN, int MODE>
+inline int conv_mode_nd(int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
+  switch (nd) {
+    case 32: return launch_conv_mode<KD, 32, BMN, MODE>(p, part, st);
+    case 64: return launch_conv_mode<KD, 64, BMN, MODE>(p, part, st);
+    case 128: return launch_conv_mode<KD, 128, BMN, MODE>(p, part, st);
+    case 256: return launch_conv_mode<KD, 256, BMN, MODE>(p, part, st);
+  }
+  return VP_EINTERNAL;
+}
+
+template <bool BMN, int MODE>
+inline int conv_mode(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaStream_t st) {
+  switch (kd) {
+    case 32: return conv_mode_nd<32, BMN, MODE>(nd, p, part, st);
+    case 64: return conv_mode_nd<64, BMN, MODE>(nd, p, part, st);
+    case 128: return conv_mode_nd<128, BMN, MODE>(nd, p, part, st);
+    case 256: return conv_mode_nd<256, BMN, MODE>(nd, p, part, st);
+  }
+  return VP_EINTERNAL;
+}
+
+int conv_tc_tf32(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaStream_t st);      // conv_tc_tf32.cu
+int conv_tc_pad_fwd(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaStream_t st);   // conv_tc_pad.cu
+int conv_tc_pad_dgrad(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaStream_t st); // conv_tc_pad.cu
 
 // one translation unit each (conv_tc_k<KD>_<f|d>.cu)
 #define VP_CONV_TC_DECL(KD, T) int conv_tc_k##KD##_##T(int64_t nd, const FwdParams& p, void* part, cudaStream_t st);

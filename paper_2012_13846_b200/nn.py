@@ -132,12 +132,13 @@ class SparseConvFunction(torch.autograd.Function):
     """y = sparse_conv(x; W) on a fixed plan (conv.py:186-242)."""
 
     @staticmethod
-    def forward(ctx, x: torch.Tensor, w: torch.Tensor, plan: ConvPlan):
+    def forward(ctx, x: torch.Tensor, w: torch.Tensor, plan: ConvPlan, math: str = "exact"):
         x = x.contiguous()
         cw = _weights(w, x)
-        y = C.conv_forward_raw(x, cw, plan.fwd_table, plan.n_out, perm=plan.fwd_perm)
+        y = C.conv_forward_raw(x, cw, plan.fwd_table, plan.n_out, perm=plan.fwd_perm, math=math)
         ctx.save_for_backward(x, w)
         ctx.plan = plan
+        ctx.math = math
         return y
 
     @staticmethod
@@ -148,21 +149,23 @@ class SparseConvFunction(torch.autograd.Function):
         cw = _weights(w, x)
         gx = gw = None
         if ctx.needs_input_grad[0]:
-            gx = C.conv_dgrad_raw(g, cw, plan.dg_table, plan.n_in, plan.dg_flip, perm=plan.dg_perm)
+            gx = C.conv_dgrad_raw(g, cw, plan.dg_table, plan.n_in, plan.dg_flip, perm=plan.dg_perm, math=ctx.math)
         if ctx.needs_input_grad[1]:
             gw = C.conv_wgrad_raw(x, g, tuple(w.shape), plan.kmap).to(w.dtype)
-        return gx, gw, None
+        return gx, gw, None, None
 
 
-def sparse_conv(t: SparseTensor, weight: torch.Tensor, shape: C.KernelShape, stride=1) -> SparseTensor:
+def sparse_conv(t: SparseTensor, weight: torch.Tensor, shape: C.KernelShape, stride=1,
+                math: str = "exact") -> SparseTensor:
     """Differentiable sparse_conv_forward (conv.py:186-208): features and
-    weight (K, n_out, n_in) carry autograd."""
+    weight (K, n_out, n_in) carry autograd.  math="tf32": fp32 features on
+    the tensor cores (forward and dgrad; the weight gradient stays fp32)."""
     if weight.dim() != 3 or weight.shape[0] != shape.num_offsets:
         raise StructuralError("weights must supply one (n_out, n_in) matrix per offset")
     if weight.shape[2] != t.feature_width:
         raise StructuralError(f"weight n_in {weight.shape[2]} != input feature width {t.feature_width}")
     plan = conv_plan(t, shape, stride)
-    y = SparseConvFunction.apply(t.features, weight, plan)
+    y = SparseConvFunction.apply(t.features, weight, plan, math)
     plans = t.plans if plan.out4 is t.coords4 else None
     return SparseTensor(plan.out4, y, plan.out_stride, _trusted=True, _dim=t.dim, _plans=plans)
 
@@ -192,10 +195,12 @@ class SparseConv3d(torch.nn.Module):
     `generator` (or torch's default RNG)."""
 
     def __init__(self, in_channels: int, out_channels: int, kernel_size=3, stride=1, dim: int = 3,
-                 device=None, dtype=torch.float32, generator: Optional[torch.Generator] = None):
+                 device=None, dtype=torch.float32, generator: Optional[torch.Generator] = None,
+                 allow_tf32: bool = False):
         super().__init__()
         self.shape = _kernel_shape(dim, kernel_size)
         self.stride = stride
+        self.math = "tf32" if allow_tf32 else "exact"  # fp32 features: tf32 tensor cores or exact SIMT
         self.in_channels, self.out_channels = int(in_channels), int(out_channels)
         K = self.shape.num_offsets
         w = torch.randn((K, out_channels, in_channels), generator=generator, dtype=torch.float64)
@@ -203,7 +208,7 @@ class SparseConv3d(torch.nn.Module):
         self.weight = torch.nn.Parameter(w.to(device) if device is not None else w)
 
     def forward(self, t: SparseTensor) -> SparseTensor:
-        return sparse_conv(t, self.weight, self.shape, self.stride)
+        return sparse_conv(t, self.weight, self.shape, self.stride, self.math)
 
     def extra_repr(self):
         return (f"{self.in_channels}, {self.out_channels}, offsets={self.shape.num_offsets}, "

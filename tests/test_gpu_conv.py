@@ -341,3 +341,64 @@ def test_rows32_kernel_opt_in():
                        env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "2 passed" in r.stdout
+
+
+@pytest.mark.parametrize("cin,cout", [(16, 48), (40, 24), (8, 8), (96, 200), (256, 136), (24, 256)])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_tc_general_widths(cin, cout, stride):
+    """Widths that are multiples of 8 but not tile widths run on the tensor
+    cores padded to 32/64/128/256 (zero chunks, masked stores): bf16 bounds."""
+    from paper_2012_13846_b200 import conv
+    pts, offs = O.synthetic_batch(3, 600, 32, seed=cin * 3 + cout, dtype=np.float64)
+    coords, _ = O.voxelize_batch(pts, offs, 1.0, 32)
+    rng = np.random.default_rng(cin * 11 + cout)
+    x = rng.normal(size=(len(coords), cin)).astype(np.float32)
+    w = (rng.normal(size=(27, cout, cin)) / np.sqrt(27 * cin)).astype(np.float32)
+    xr, wr = bf16_round(x), bf16_round(w)
+    off = O.hypercubic_offsets(3, 3)
+    t, W, shape, y = run_layer(coords, x, w, stride, torch.bfloat16)
+    _, ry, _ = O.sparse_conv_forward(coords, xr, (1, 1, 1), wr, off, stride)
+    err = np.abs(y.features.float().cpu().numpy() - ry)
+    assert (err <= abs_bound(coords, xr, wr, off, stride, 1e-2)).all(), err.max()
+    gy = rng.normal(size=ry.shape).astype(np.float32)
+    gr = bf16_round(gy)
+    gi, gw = conv.sparse_conv_backward(t, W, shape, stride, torch.from_numpy(gy).cuda().to(torch.bfloat16))
+    rgi, _ = O.sparse_conv_backward(coords, xr, (1, 1, 1), wr, off, stride, gr)
+    bgi, _ = O.sparse_conv_backward(coords, np.abs(xr), (1, 1, 1), np.abs(wr), off, stride, np.abs(gr))
+    ei = np.abs(gi.float().cpu().numpy() - rgi)
+    assert (ei <= 1e-2 * bgi + 1e-6).all(), (ei / (bgi + 1e-9)).max()
+
+
+@pytest.mark.parametrize("cin,cout", [(16, 32), (32, 32), (64, 64), (128, 256), (24, 40), (128, 32)])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_tf32_mode(cin, cout, stride):
+    """fp32 features with math="tf32" (kind::tf32 tensor cores, fp32 storage
+    and accumulation): |d| <= 2e-3 * sum|W||x| per element
+    against the f64 oracle on the same fp32 inputs, forward and dgrad."""
+    from paper_2012_13846_b200 import conv
+    pts, offs = O.synthetic_batch(3, 600, 32, seed=cin + 5 * cout, dtype=np.float64)
+    coords, _ = O.voxelize_batch(pts, offs, 1.0, 32)
+    rng = np.random.default_rng(cin * 13 + cout)
+    x = rng.normal(size=(len(coords), cin)).astype(np.float32)
+    w = (rng.normal(size=(27, cout, cin)) / np.sqrt(27 * cin)).astype(np.float32)
+    xr, wr = x.astype(np.float64), w.astype(np.float64)
+    off = O.hypercubic_offsets(3, 3)
+    from paper_2012_13846_b200.tensor import SparseTensor
+    shape = conv.KernelShape.hypercubic(3, 3)
+    t = SparseTensor(coords, np.zeros((len(coords), 1)), (1, 1, 1)).with_features(torch.from_numpy(x).cuda())
+    W = conv.ConvWeights(torch.from_numpy(w).cuda())
+    y = conv.sparse_conv_forward(t, W, shape, stride, math="tf32")
+    assert y.features.dtype == torch.float32
+    _, ry, _ = O.sparse_conv_forward(coords, xr, (1, 1, 1), wr, off, stride)
+    err = np.abs(y.features.cpu().numpy() - ry)
+    bound = abs_bound(coords, xr, wr, off, stride, 2e-3)
+    assert (err <= bound).all(), (err / bound).max()
+    # tf32 is really in use: the exact fp32 path agrees with the oracle ~1000x tighter
+    ye = conv.sparse_conv_forward(t, W, shape, stride)
+    assert np.abs(ye.features.cpu().numpy() - ry).max() < err.max() or err.max() == 0
+    gy = rng.normal(size=ry.shape).astype(np.float32)
+    gi, gw = conv.sparse_conv_backward(t, W, shape, stride, torch.from_numpy(gy).cuda(), math="tf32")
+    rgi, rgw = O.sparse_conv_backward(coords, xr, (1, 1, 1), wr, off, stride, gy.astype(np.float64))
+    bgi, _ = O.sparse_conv_backward(coords, np.abs(xr), (1, 1, 1), np.abs(wr), off, stride, np.abs(gy.astype(np.float64)))
+    ei = np.abs(gi.cpu().numpy() - rgi)
+    assert (ei <= 2e-3 * bgi + 1e-6).all(), (ei / (bgi + 1e-9)).max()

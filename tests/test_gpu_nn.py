@@ -233,3 +233,26 @@ def test_plans_are_cached_per_coordinate_set():
     n = len(t.plans)
     b(h)
     assert len(t.plans) == n
+
+
+def test_tf32_module_equals_functional_api():
+    """SparseConv3d(allow_tf32=True) on fp32 features runs the kind::tf32
+    tensor-core kernels: bitwise equal to sparse_conv_forward/backward with
+    math="tf32", and within 2e-3 (relative to max) of the exact fp32 module."""
+    from paper_2012_13846_b200 import conv, nn
+    t, coords = _tensor(6, clouds=3, npts=1200, res=32, width=32, dtype=torch.float32)
+    layer = nn.SparseConv3d(32, 64, 3, stride=1, device="cuda", allow_tf32=True)
+    x = t.features.clone().requires_grad_(True)
+    y = layer(t.with_features(x))
+    g = torch.randn(y.features.shape, device="cuda")
+    y.features.backward(g)
+    W = conv.ConvWeights(layer.weight.detach())
+    shape = conv.KernelShape.hypercubic(3, 3)
+    ry = conv.sparse_conv_forward(t, W, shape, 1, math="tf32")
+    rgi, rgw = conv.sparse_conv_backward(t, W, shape, 1, g, math="tf32")
+    assert torch.equal(y.features.detach(), ry.features)
+    assert torch.equal(x.grad, rgi)
+    assert torch.equal(layer.weight.grad, rgw)
+    ye = conv.sparse_conv_forward(t, W, shape, 1)
+    d = (ye.features - ry.features).abs().max() / ye.features.abs().max()
+    assert 0 < float(d) < 2e-3
