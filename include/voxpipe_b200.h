@@ -219,6 +219,19 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t c_in, const void* g, i
                   const int32_t* pair_ptr, int64_t cap_pairs, void* grad_w,
                   void* ws, size_t ws_bytes, vp_stream_t stream);
 
+/* vp_conv_wgrad + momentum SGD of W in the reduction kernel (the training
+ * step's per-layer update without a separate pass): m = momentum*m + grad_w,
+ * p -= lr*m, p_bf16 (nullable) = bf16(p); grad_w is still written.
+ * phase 0: everything; 1: the chunk partials only (no parameter access);
+ * 2: the reduction + SGD over the partials phase 1 left in ws — so the
+ * caller can start the partials early and order phase 2 after every reader
+ * of p / p_bf16 (the layer's dgrad). */
+int vp_conv_wgrad_sgd(const void* x, int32_t x_dtype, int64_t c_in, const void* g, int32_t g_dtype,
+                      int64_t c_out, int32_t K, const int32_t* pair_in, const int32_t* pair_out,
+                      const int32_t* pair_ptr, int64_t cap_pairs, void* grad_w, void* ws, size_t ws_bytes,
+                      float* p, float* m, void* p_bf16, float lr, float momentum, int32_t phase,
+                      vp_stream_t stream);
+
 /* ---------------------------------------------------------------- glue
  * Model glue for the SparseResNet training step (no reference
  * implementation: SPEC.md:185 non-goal — parity self-defined). */

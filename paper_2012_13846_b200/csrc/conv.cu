@@ -66,9 +66,19 @@ __device__ __forceinline__ T tree_sum(const T* __restrict__ p, int64_t stride, i
 }
 
 // sum the chunk partials of each offset, pairwise in chunk order (deterministic)
+// optional momentum SGD fused into the reduction (sgd_kernel's arithmetic,
+// glue.cu): the finished gradient element updates its parameter at once
+struct SgdFuse {
+  float* p;
+  float* m;
+  __nv_bfloat16* pb;  // bf16 shadow of p (nullable)
+  float lr, mom;
+};
+
 template <typename T>
 __global__ void wgrad_reduce_kernel(const T* __restrict__ part, const int32_t* __restrict__ pptr,
-                                    int K, int chunk, int64_t per, T* __restrict__ gw, const int* chunk_dev) {
+                                    int K, int chunk, int64_t per, T* __restrict__ gw, const int* chunk_dev,
+                                    const SgdFuse sgd) {
   ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
   if (chunk_dev) chunk = *chunk_dev;  // chosen on the device by the partial kernel
@@ -86,7 +96,15 @@ __global__ void wgrad_reduce_kernel(const T* __restrict__ part, const int32_t* _
        e += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(e / per);
     const int64_t o = e - (int64_t)k * per;
-    gw[e] = tree_sum(part + (int64_t)s_pref[k] * per + o, per, s_pref[k + 1] - s_pref[k]);
+    const T g = tree_sum(part + (int64_t)s_pref[k] * per + o, per, s_pref[k + 1] - s_pref[k]);
+    gw[e] = g;
+    if (sgd.p) {  // m = mom * m + g ; p -= lr * m ; shadow
+      const float mi = sgd.mom * sgd.m[e] + (float)g;
+      const float pi = sgd.p[e] - sgd.lr * mi;
+      sgd.m[e] = mi;
+      sgd.p[e] = pi;
+      if (sgd.pb) sgd.pb[e] = __float2bfloat16_rn(pi);
+    }
   }
 }
 
@@ -979,10 +997,32 @@ size_t vp_conv_wgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K, int64_t cap_
   return align_up((size_t)items * cin * cout * 4, 256) + kWgHeader;  // + the device-chosen chunk word
 }
 
+// phase: 0 = partials + reduction, 1 = partials only, 2 = reduction only
+static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
+                           int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
+                           void* gw_out, void* ws, size_t ws_bytes, const SgdFuse& sgd, int phase, cudaStream_t st);
+
 int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
                   int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
                   void* gw_out, void* ws, size_t ws_bytes, vp_stream_t stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return conv_wgrad_impl(x, x_dtype, cin, g, g_dtype, cout, K, pin, pout, pptr, cap_pairs, gw_out, ws, ws_bytes,
+                         SgdFuse{}, 0, (cudaStream_t)stream);
+}
+
+int vp_conv_wgrad_sgd(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
+                      int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
+                      void* gw_out, void* ws, size_t ws_bytes, float* p, float* m, void* p_bf16, float lr,
+                      float momentum, int32_t phase, vp_stream_t stream) {
+  VP_REQUIRE(p && m, VP_EVALIDATION, "conv_wgrad_sgd: parameter and momentum buffers required");
+  VP_REQUIRE(phase >= 0 && phase <= 2, VP_EVALIDATION, "conv_wgrad_sgd: phase must be 0, 1 or 2");
+  VP_REQUIRE(x_dtype != VP_F64 && g_dtype != VP_F64, VP_EVALIDATION, "conv_wgrad_sgd: fp32 parameters only");
+  return conv_wgrad_impl(x, x_dtype, cin, g, g_dtype, cout, K, pin, pout, pptr, cap_pairs, gw_out, ws, ws_bytes,
+                         SgdFuse{p, m, (__nv_bfloat16*)p_bf16, lr, momentum}, phase, (cudaStream_t)stream);
+}
+
+static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
+                           int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
+                           void* gw_out, void* ws, size_t ws_bytes, const SgdFuse& sgd, int phase, cudaStream_t st) {
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(ws && ws_bytes >= vp_conv_wgrad_ws_bytes(cin, cout, K, cap_pairs), VP_EVALIDATION,
              "conv_wgrad: workspace too small");
@@ -998,12 +1038,12 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     const int dchunk = 2 * std::min(chunk, kWgSimtChunk);
     const int ditems = (int)(cap_pairs / dchunk + K + 1);
     double* dpart = (double*)ws;
-    ::vp::launch(wgrad_simt_kernel<double>, std::max(1, std::min(ditems, grid_cap(8))), kWgSimtThreads, 0, st, x,
+    if (phase != 2) ::vp::launch(wgrad_simt_kernel<double>, std::max(1, std::min(ditems, grid_cap(8))), kWgSimtThreads, 0, st, x,
                  x_dtype, (int)cin, g, g_dtype, (int)cout, K, pin, pout, pptr, dchunk, dpart);
-    VP_CHECK_LAUNCH("conv_wgrad_simt_f64");
-    ::vp::launch(wgrad_reduce_kernel<double>, rblocks, 256, 0, st, (const double*)dpart, pptr, K, dchunk,
-                 (int64_t)cin * cout, (double*)gw_out, (const int*)nullptr);
-    VP_CHECK_LAUNCH("wgrad_reduce_f64");
+    if (phase != 2) VP_CHECK_LAUNCH("conv_wgrad_simt_f64");
+    if (phase != 1) ::vp::launch(wgrad_reduce_kernel<double>, rblocks, 256, 0, st, (const double*)dpart, pptr, K, dchunk,
+                 (int64_t)cin * cout, (double*)gw_out, (const int*)nullptr, SgdFuse{});
+    if (phase != 1) VP_CHECK_LAUNCH("wgrad_reduce_f64");
     return VP_OK;
   }
   if (x_dtype == VP_BF16 && g_dtype == VP_BF16 && tc_width(cin) && tc_width(cout)) {
@@ -1022,11 +1062,13 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, static_chunk ? chunk : 0, part,
                (int)std::min<int64_t>(ws_items, 1 << 30), chunk_dev, chunk_min};
     const int grid_items = static_chunk ? max_items : (int)std::min<int64_t>(ws_items, 1 << 30);
-    int rc = wg_tc(cin, cout, p, grid_items, st);
-    if (rc != VP_OK) return rc;
-    ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, chunk,
-                 (int64_t)cin * cout, gw, static_chunk ? (const int*)nullptr : (const int*)chunk_dev);
-    VP_CHECK_LAUNCH("wgrad_reduce");
+    if (phase != 2) {
+      int rc = wg_tc(cin, cout, p, grid_items, st);
+      if (rc != VP_OK) return rc;
+    }
+    if (phase != 1) ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, chunk,
+                 (int64_t)cin * cout, gw, static_chunk ? (const int*)nullptr : (const int*)chunk_dev, sgd);
+    if (phase != 1) VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }
   if (cin == 1 && (cout == 16 || cout == 32 || cout == 64) && x_dtype == VP_BF16 && g_dtype == VP_BF16) {
@@ -1034,27 +1076,28 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, in
     const int items = (int)(cap_pairs / kWgStemChunk + K + 1);
     const int grid = std::max(1, std::min(items, grid_cap(8)));
     const bf16 *xb = (const bf16*)x, *gb = (const bf16*)g;
-    if (cout == 16)
+    if (phase == 2) {
+    } else if (cout == 16)
       ::vp::launch(wgrad_stem_kernel<16>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
     else if (cout == 32)
       ::vp::launch(wgrad_stem_kernel<32>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
     else
       ::vp::launch(wgrad_stem_kernel<64>, grid, kWgStemThreads, 0, st, xb, gb, K, pin, pout, pptr, part);
-    VP_CHECK_LAUNCH("conv_wgrad_stem");
-    ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, kWgStemChunk,
-                 (int64_t)cin * cout, gw, (const int*)nullptr);
-    VP_CHECK_LAUNCH("wgrad_reduce");
+    if (phase != 2) VP_CHECK_LAUNCH("conv_wgrad_stem");
+    if (phase != 1) ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, kWgStemChunk,
+                 (int64_t)cin * cout, gw, (const int*)nullptr, sgd);
+    if (phase != 1) VP_CHECK_LAUNCH("wgrad_reduce");
     return VP_OK;
   }
   const int schunk = std::min(chunk, kWgSimtChunk);
   const int sitems = (int)(cap_pairs / schunk + K + 1);
   const int grid = std::max(1, std::min(sitems, grid_cap(8)));
-  ::vp::launch(wgrad_simt_kernel<float>, grid, kWgSimtThreads, 0, st, x, x_dtype, (int)cin, g, g_dtype, (int)cout, K,
+  if (phase != 2) ::vp::launch(wgrad_simt_kernel<float>, grid, kWgSimtThreads, 0, st, x, x_dtype, (int)cin, g, g_dtype, (int)cout, K,
                pin, pout, pptr, schunk, part);
-  VP_CHECK_LAUNCH("conv_wgrad_simt");
-  ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, schunk,
-               (int64_t)cin * cout, gw, (const int*)nullptr);
-  VP_CHECK_LAUNCH("wgrad_reduce");
+  if (phase != 2) VP_CHECK_LAUNCH("conv_wgrad_simt");
+  if (phase != 1) ::vp::launch(wgrad_reduce_kernel<float>, rblocks, 256, 0, st, (const float*)part, pptr, K, schunk,
+               (int64_t)cin * cout, gw, (const int*)nullptr, sgd);
+  if (phase != 1) VP_CHECK_LAUNCH("wgrad_reduce");
   return VP_OK;
 }
 

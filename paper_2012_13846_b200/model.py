@@ -272,6 +272,8 @@ class SparseResNetTrainer:
         # BN statistics from the producing conv's epilogue (vp_conv_fwd_bn /
         # vp_conv_dgrad_bn) instead of a separate statistics pass
         self.bn_fuse = __import__("os").environ.get("VP_BN_EPI", "1") != "0"
+        # per-layer momentum SGD inside the weight-gradient reduction
+        self.fuse_sgd = __import__("os").environ.get("VP_FUSE_SGD", "1") != "0"
 
     # ------------------------------------------------------------------ setup
     def _width_at(self, level):
@@ -625,6 +627,8 @@ class SparseResNetTrainer:
         x = L["x"]
         if _DBG_SKIP_WGRAD:  # experiments only: the step without weight gradients (never for results)
             return self._dgrad_only(L, prev, prev_add, need_dgrad, st)
+        if self._fuse_sgd():
+            return self._wgrad_sgd_after_dgrad(L, prev, prev_add, need_dgrad, st)
         if self.concurrent:  # weight gradient off the critical path
             ws = self.side[3 - (L["index"] % 2)]
             self._forked.add(id(ws))
@@ -655,6 +659,35 @@ class SparseResNetTrainer:
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
             self._layer_sgd(L, ws if self.concurrent else None, ev, st)
+        return gin
+
+    def _fuse_sgd(self):
+        """Per-layer SGD inside the weight-gradient reduction: single-process
+        training with side streams (no gradient all-reduce between them)."""
+        return self.fuse_sgd and self._sgd_in_backward and self.grad_allreduce is None and self.concurrent
+
+    def _wgrad_sgd_after_dgrad(self, L, prev, prev_add, need_dgrad, st):
+        """The layer's weight-gradient partials on a side stream as soon as
+        its gradient exists, dgrad on the critical path, then the partial
+        reduction with the momentum SGD fused in (vp_conv_wgrad_sgd phases
+        1 / 2) once the dgrad — the step's last reader of W — is issued."""
+        main = torch.cuda.current_stream()
+        ws = self.side[3 - (L["index"] % 2)]
+        self._forked.add(id(ws))
+        ws.wait_stream(main)
+        m, fc, pb = L["map"], self.fcode, self.params
+        off, shape = pb.offsets[L["name"] + ".w"]
+        x = L["x"]
+        args = (x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"], self.K, m.pin.data_ptr(),
+                m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(), L["gw"].data_ptr(), L["wg_ws"].data_ptr(),
+                L["wg_ws"].numel(), pb.p.data_ptr() + 4 * off, pb.m.data_ptr() + 4 * off, pb.pb.data_ptr() + 2 * off,
+                float(self.lr), float(self.momentum))
+        with torch.cuda.stream(ws):
+            self._c("vp_conv_wgrad_sgd", *args, 1, ws.cuda_stream)
+        gin = self._dgrad_only(L, prev, prev_add, need_dgrad, st)
+        ws.wait_stream(main)
+        with torch.cuda.stream(ws):
+            self._c("vp_conv_wgrad_sgd", *args, 2, ws.cuda_stream)
         return gin
 
     def _dgrad_only(self, L, prev, prev_add, need_dgrad, st):
