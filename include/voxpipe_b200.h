@@ -280,19 +280,32 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gy_dtype, const void
  *               zeroed where bn_act <= 0 (ReLU mask; bn_act nullable),
  *               stored rounded; partials (sum g, sum g*(bn_pre - bn_mean)).
  *   bn_add/bn_act/bn_pre: same dtype and shape as the conv output.
- * A bf16 tensor-core conv fuses it into its epilogue (or its split-K
- * reduction); every other path runs one extra pass over the output. */
+ *   bn_out_a/bn_out_b (nullable together): also finalize the statistics in
+ *             the producer chain — mode 1: mean / rstd (biased variance,
+ *             bn_eps); mode 2: ggamma = bn_rstd * sum g*(pre-mean), gbeta =
+ *             sum g — so the BN apply follows the conv directly.
+ * bn_part must be ZERO-FILLED before its first use (a self-re-arming ticket
+ * lives in the header).  A bf16 tensor-core conv fuses the statistics into
+ * its epilogue and the finalize into its split-K reduction kernel; every
+ * other path runs one extra pass over the output. */
 size_t vp_bn_part_bytes(int64_t C);
 int vp_conv_fwd_bn(const void* x, int32_t x_dtype, int64_t x_rows, int64_t c_in, const void* w, int32_t w_dtype,
                    int64_t c_out, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
                    const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
                    int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act, const void* bn_pre,
-                   const float* bn_mean, vp_stream_t stream);
+                   const float* bn_mean, float bn_eps, float* bn_out_a, float* bn_out_b, const float* bn_rstd,
+                   vp_stream_t stream);
 int vp_conv_dgrad_bn(const void* g, int32_t g_dtype, int64_t g_rows, int64_t c_out, const void* w, int32_t w_dtype,
                      int64_t c_in, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
                      const int32_t* n_in_dev, int64_t cap_in, void* grad_in, int32_t gi_dtype, void* ws,
                      size_t ws_bytes, int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act,
-                     const void* bn_pre, const float* bn_mean, vp_stream_t stream);
+                     const void* bn_pre, const float* bn_mean, float bn_eps, float* bn_out_a, float* bn_out_b,
+                     const float* bn_rstd, vp_stream_t stream);
+/* BN backward apply from finished (ggamma, gbeta) and the stored masked
+ * gradient gm: grad_x = gamma*rstd*(gm - gbeta/n - xhat*ggamma/n). */
+int vp_bn_backward_apply(const void* gm, int32_t gm_dtype, const void* x, int32_t x_dtype, const int32_t* n_dev,
+                         int64_t cap_n, int64_t C, const float* mean, const float* rstd, const float* gamma,
+                         const float* ggamma, const float* gbeta, void* grad_x, int32_t gx_dtype, vp_stream_t stream);
 /* vp_bn_apply with the statistics reduced from a mode-1 bn_part (fixed
  * order); also stores mean/rstd for the backward. */
 int vp_bn_apply_part(const void* x, int32_t x_dtype, const int32_t* n_dev, int64_t cap_n, int64_t C, float eps,

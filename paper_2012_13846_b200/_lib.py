@@ -69,9 +69,10 @@ SIGNATURES = {
     "vp_conv_wgrad_sgd": (C.c_int, [P, I32, I64, P, I32, I64, I32, P, P, P, I64, P, P, SZ, P, P, P, F32, F32, I32, P]),
     "vp_bn_part_bytes": (SZ, [I64]),
     "vp_conv_fwd_bn": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, P, I64, P, I32, P, SZ,
-                                 I32, P, P, P, P, P, P]),
+                                 I32, P, P, P, P, P, F32, P, P, P, P]),
     "vp_conv_dgrad_bn": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, P, I64, P, I32, P, SZ,
-                                   I32, P, P, P, P, P, P]),
+                                   I32, P, P, P, P, P, F32, P, P, P, P]),
+    "vp_bn_backward_apply": (C.c_int, [P, I32, P, I32, P, I64, I64, P, P, P, P, P, P, I32, P]),
     "vp_bn_apply_part": (C.c_int, [P, I32, P, I64, I64, F32, P, P, P, P, P, P, I32, I32, P, I32, P]),
     "vp_bn_backward_part": (C.c_int, [P, I32, P, I32, P, I64, I64, P, P, P, P, P, I32, P, P, P]),
     "vp_bn_stats_ws_bytes": (SZ, [I64, I64]),

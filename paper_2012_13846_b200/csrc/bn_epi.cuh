@@ -33,7 +33,64 @@ struct BnEpi {
   const void* act;        // mode 2, nullable: ReLU output of the BN layer (mask act > 0)
   const void* pre;        // mode 2: BN input (the BN layer's conv output)
   const float* mean;      // mode 2: BN batch mean
+  // finalize in the producer chain (out_a != null): mode 1 -> out_a = mean,
+  // out_b = rstd (eps); mode 2 -> out_a = ggamma = rstd * sum g(x-mean),
+  // out_b = gbeta = sum g
+  float* out_a;
+  float* out_b;
+  const float* rstd;
+  float eps;
+  unsigned int* ticket;   // header word (zero before first use; re-arms itself)
+  int early;              // trigger the dependent (apply) launch at the start of the finalizing kernel
 };
+
+constexpr int kBnTicketOffset = 64;  // bytes into the header
+
+// The partial rows -> the BN statistics, channels [32 cb, 32 cb + 32): a
+// 1024-thread block, lane = channel, warps 0-15 sum column 0 (sum y | sum g)
+// and 16-31 column 1 over rows w, w + 16, ... (8 loads in flight), in double,
+// then the 16 warps in order.  Fixed order -> deterministic.
+__device__ __forceinline__ void bn_finalize_block(const float* __restrict__ part, int nb, int C, int n, int mode,
+                                                  float eps, const float* __restrict__ rstd_in, float* __restrict__ out_a,
+                                                  float* __restrict__ out_b, int cb, double (*s)[33]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = warp >> 4, wg = warp & 15;
+  const int c = cb * 32 + lane;
+  double acc = 0.0;
+  if (c < C) {
+    for (int b0 = wg; b0 < nb; b0 += 16 * 8) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int b = b0 + 16 * q;
+        v[q] = b < nb ? __ldcg(part + ((int64_t)b * 2 + h) * C + c) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v[q];
+    }
+  }
+  s[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && c < C) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) {
+      s0 += s[w][lane];
+      s1 += s[16 + w][lane];
+    }
+    if (mode == 1) {
+      const double mu = n > 0 ? s0 / n : 0.0;
+      double var = n > 0 ? s1 / n - mu * mu : 0.0;
+      if (var < 0) var = 0;
+      out_a[c] = (float)mu;
+      out_b[c] = (float)(1.0 / sqrt(var + (double)eps));
+    } else {
+      out_a[c] = (float)(s1 * (double)rstd_in[c]);
+      out_b[c] = (float)s0;
+    }
+  }
+  __syncthreads();
+}
 
 __device__ __forceinline__ float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
@@ -141,6 +198,16 @@ __device__ __forceinline__ void bn_epi_chunk32(const BnEpi& e, const float (&v)[
   }
   s1 = a[0];
   s2 = b[0];
+}
+
+// standalone finalize (producers without a fused split-K reduction): one
+// 1024-thread block per 32 channels
+static __global__ void __launch_bounds__(1024)
+bn_finalize_kernel(const BnEpi e, int C, const int32_t* n_dev, int64_t cap) {
+  ::vp::pdl_begin();
+  if (e.early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ double s[32][33];
+  bn_finalize_block(e.part, *e.nb, C, load_count(n_dev, cap), e.mode, e.eps, e.rstd, e.out_a, e.out_b, blockIdx.x, s);
 }
 
 }  // namespace vp

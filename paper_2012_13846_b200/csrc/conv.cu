@@ -650,18 +650,31 @@ bn_epi_rows_kernel(void* __restrict__ y, int yd, const int32_t* n_dev, int64_t c
   }
 }
 
+static int launch_bn_finalize(const BnEpi& e, int64_t C, const int32_t* n_dev, int64_t cap, cudaStream_t st) {
+  if (e.mode == 0 || e.out_a == nullptr) return VP_OK;
+  ::vp::launch(bn_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, e, (int)C, n_dev, cap);
+  VP_CHECK_LAUNCH("bn_finalize");
+  return VP_OK;
+}
+
 static int launch_bn_epi_rows(void* y, int yd, const int32_t* n_dev, int64_t cap, int64_t C, const BnEpi& e,
                               cudaStream_t st) {
   const int64_t lanes = std::max<int64_t>(1, 256 / std::min<int64_t>(C, 256));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(cap, 1), lanes * 8), kNumSMs));
   ::vp::launch(bn_epi_rows_kernel, grid, 256, 0, st, y, yd, n_dev, cap, (int)C, e);
   VP_CHECK_LAUNCH("bn_epi_rows");
-  return VP_OK;
+  return launch_bn_finalize(e, C, n_dev, cap, st);
 }
 
-// caller buffer -> BnEpi (header int nb, partial rows after kBnPartHeader bytes)
+static int bn_early_env() {  // early programmatic launch of the BN apply behind the finalize (VP_BN_EARLY)
+  static const int v = getenv("VP_BN_EARLY") ? atoi(getenv("VP_BN_EARLY")) : 1;
+  return v;
+}
+
+// caller buffer -> BnEpi (header: int nb at 0, the finalize ticket at
+// kBnTicketOffset; partial rows after kBnPartHeader bytes)
 static BnEpi make_epi(int32_t mode, void* bn_part, const void* add, const void* act, const void* pre,
-                      const float* mean) {
+                      const float* mean, float eps, float* out_a, float* out_b, const float* rstd) {
   BnEpi e{};
   e.mode = bn_part ? mode : 0;
   e.nb = (int*)bn_part;
@@ -670,6 +683,12 @@ static BnEpi make_epi(int32_t mode, void* bn_part, const void* add, const void* 
   e.act = act;
   e.pre = pre;
   e.mean = mean;
+  e.out_a = out_a;
+  e.out_b = out_b;
+  e.rstd = rstd;
+  e.eps = eps;
+  e.ticket = bn_part ? (unsigned int*)((char*)bn_part + kBnTicketOffset) : nullptr;
+  e.early = bn_early_env();
   return e;
 }
 
@@ -806,11 +825,16 @@ int vp_conv_fwd_bn(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, 
                    int64_t cout, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
                    const int32_t* n_out_dev, int64_t cap_out, void* y, int32_t y_dtype, void* ws, size_t ws_bytes,
                    int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act, const void* bn_pre,
-                   const float* bn_mean, vp_stream_t stream) {
+                   const float* bn_mean, float bn_eps, float* bn_out_a, float* bn_out_b, const float* bn_rstd,
+                   vp_stream_t stream) {
   VP_REQUIRE(bn_mode >= 0 && bn_mode <= 2 && (bn_mode == 0 || bn_part), VP_EVALIDATION, "conv_fwd_bn: bad bn mode");
   VP_REQUIRE(bn_mode != 2 || (bn_pre && bn_mean), VP_EVALIDATION, "conv_fwd_bn: mode 2 needs pre and mean");
+  VP_REQUIRE(!bn_out_a == !bn_out_b && (bn_mode != 2 || !bn_out_a || bn_rstd), VP_EVALIDATION,
+             "conv_fwd_bn: finalize outputs (and rstd for mode 2) go together");
   return conv_fwd_impl(x, x_dtype, x_rows, cin, w, w_dtype, cout, K, table, flip, perm, n_out_dev, cap_out, y, y_dtype,
-                       ws, ws_bytes, make_epi(bn_mode, bn_part, bn_add, bn_act, bn_pre, bn_mean), (cudaStream_t)stream);
+                       ws, ws_bytes,
+                       make_epi(bn_mode, bn_part, bn_add, bn_act, bn_pre, bn_mean, bn_eps, bn_out_a, bn_out_b, bn_rstd),
+                       (cudaStream_t)stream);
 }
 
 static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t cin, const void* w, int32_t w_dtype,
@@ -878,7 +902,8 @@ static int conv_fwd_impl(const void* x, int32_t x_dtype, int64_t x_rows, int64_t
     bool fused = false;
     const int rc = launch_small_fwd(x, x_dtype, (int)cin, w, w_dtype, (int)cout, K, table, flip, perm, n_out_dev,
                                     cap_out, y, y_dtype, st, epi, &fused);
-    return fused ? rc : epi_after(rc);
+    if (rc != VP_OK) return rc;
+    return fused ? launch_bn_finalize(epi, cout, n_out_dev, cap_out, st) : epi_after(rc);
   }
   const int64_t total = cap_out * cout;
   int blocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(16));
@@ -909,11 +934,15 @@ int vp_conv_dgrad_bn(const void* g, int32_t g_dtype, int64_t g_rows, int64_t cou
                      int64_t cin, int32_t K, const int32_t* table, int32_t flip, const int32_t* perm,
                      const int32_t* n_in_dev, int64_t cap_in, void* gi, int32_t gi_dtype, void* ws, size_t ws_bytes,
                      int32_t bn_mode, void* bn_part, const void* bn_add, const void* bn_act, const void* bn_pre,
-                     const float* bn_mean, vp_stream_t stream) {
+                     const float* bn_mean, float bn_eps, float* bn_out_a, float* bn_out_b, const float* bn_rstd,
+                     vp_stream_t stream) {
   VP_REQUIRE(bn_mode >= 0 && bn_mode <= 2 && (bn_mode == 0 || bn_part), VP_EVALIDATION, "conv_dgrad_bn: bad bn mode");
   VP_REQUIRE(bn_mode != 2 || (bn_pre && bn_mean), VP_EVALIDATION, "conv_dgrad_bn: mode 2 needs pre and mean");
+  VP_REQUIRE(!bn_out_a == !bn_out_b && (bn_mode != 2 || !bn_out_a || bn_rstd), VP_EVALIDATION,
+             "conv_dgrad_bn: finalize outputs (and rstd for mode 2) go together");
   return conv_dgrad_impl(g, g_dtype, g_rows, cout, w, w_dtype, cin, K, table, flip, perm, n_in_dev, cap_in, gi,
-                         gi_dtype, ws, ws_bytes, make_epi(bn_mode, bn_part, bn_add, bn_act, bn_pre, bn_mean),
+                         gi_dtype, ws, ws_bytes,
+                         make_epi(bn_mode, bn_part, bn_add, bn_act, bn_pre, bn_mean, bn_eps, bn_out_a, bn_out_b, bn_rstd),
                          (cudaStream_t)stream);
 }
 

@@ -633,10 +633,19 @@ split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev
                         int max_split, const int32_t* __restrict__ perm, bf16* __restrict__ y, const BnEpi e) {
   ::vp::pdl_begin();
   __shared__ float s_red[2][kSplitEpiThreads][4];
+  __shared__ double s_fin[32][33];
+  __shared__ unsigned int s_last;
   const int n_out = load_count(n_out_dev, cap_out);
   const int ntiles = (n_out + 127) / 128;
   const int S = split_count(ntiles, grid < kSplitItems ? grid : kSplitItems, max_split);
-  if (S <= 1) return;
+  if (e.out_a && e.early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (S <= 1) {
+    // the conv epilogue wrote the partial rows: finalize them here (one
+    // 32-channel block per CTA) instead of in a separate launch
+    if (e.out_a && (int)blockIdx.x * 32 < ND)
+      bn_finalize_block(e.part, *e.nb, ND, n_out, e.mode, e.eps, e.rstd, e.out_a, e.out_b, blockIdx.x, s_fin);
+    return;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) *e.nb = gridDim.x;
   const int n = (threadIdx.x * 4) % ND;
   float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
@@ -706,6 +715,16 @@ split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev
     for (int m = 0; m < M; ++m) acc += s_red[hh][c / 4 + m * G][c % 4];
     e.part[((int64_t)blockIdx.x * 2 + hh) * ND + c] = acc;
   }
+  if (e.out_a == nullptr) return;
+  // the last block to finish (self-re-arming ticket) finalizes every channel
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicInc(e.ticket, gridDim.x - 1) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int cb = 0; cb * 32 < ND; ++cb)
+    bn_finalize_block(e.part, (int)gridDim.x, ND, n_out, e.mode, e.eps, e.rstd, e.out_a, e.out_b, cb, s_fin);
 }
 
 }  // namespace vp

@@ -43,10 +43,25 @@ inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   VP_CHECK_LAUNCH("conv_tc");
   if (part && p.epi.mode != 0) {  // bf16 output + BN statistics: at most one partial row per SM
     const int64_t work = p.cap_out * ND / 4;
-    ::vp::launch(split_reduce_epi_kernel<ND>,
-                 (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, kSplitEpiThreads), kNumSMs)),
-                 kSplitEpiThreads, 0, st, (const float*)part, p.n_out_dev, p.cap_out, grid, p.max_split, p.perm, (bf16*)p.y, p.epi);
+    // >= one block per 32 channels: without a split they finalize the conv's partial rows.
+    // When even the capacity's tile count is split for sure (few rows), the
+    // ~148 reduction rows are finalized by a separate 32-channel-per-block
+    // kernel instead of the split kernel's last block (a serial tail).
+    const int64_t tiles_cap = ceil_div(p.cap_out, 128);
+    const bool split_sure = tiles_cap * 2 <= std::min<int64_t>(grid, kSplitItems) && p.max_split > 1;
+    BnEpi e = p.epi;
+    if (split_sure) e.out_a = e.out_b = nullptr;
+    const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(work, kSplitEpiThreads), kNumSMs), ND / 32);
+    ::vp::launch(split_reduce_epi_kernel<ND>, (int)blocks, kSplitEpiThreads, 0, st, (const float*)part, p.n_out_dev,
+                 p.cap_out, grid, p.max_split, p.perm, (bf16*)p.y, e);
     VP_CHECK_LAUNCH("split_reduce_epi");
+    if (split_sure && p.epi.out_a) {
+      ::vp::launch(bn_finalize_kernel, (int)ceil_div(ND, 32), 1024, 0, st, p.epi, ND, p.n_out_dev, p.cap_out);
+      VP_CHECK_LAUNCH("bn_finalize");
+    }
+  } else if (p.epi.mode != 0 && p.epi.out_a) {  // statistics rows from the epilogue only: finalize them
+    ::vp::launch(bn_finalize_kernel, (int)ceil_div(ND, 32), 1024, 0, st, p.epi, ND, p.n_out_dev, p.cap_out);
+    VP_CHECK_LAUNCH("bn_finalize");
   } else if (part) {
     const int64_t work = p.cap_out * ND / 4;
     ::vp::launch(split_reduce_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), grid_cap(8))), 256, 0, st, 

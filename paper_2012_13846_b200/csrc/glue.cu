@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <initializer_list>
 
+#include "bn_epi.cuh"
 #include "common.cuh"
 
 namespace vp {
@@ -910,57 +911,9 @@ int vp_bn_backward(const void* gy, const void* gy2, int32_t gyd, const void* y, 
   return VP_OK;
 }
 
-// Reduce a producer's partial rows (bn_epi.cuh layout) to the BN
-// statistics once: block = 32 channels x 32 warps; warps 0-15 sum column 0
-// (sum y | sum g), warps 16-31 column 1, each warp over rows w, w+16, ...
-// (8 loads in flight), in double; then the 16 warps in order.  mode 1:
-// mean / rstd (biased variance, training BN); mode 2: ggamma = rstd * sum
-// g*(x-mean), gbeta = sum g.  A few blocks of L2 reads instead of every
-// apply block re-reducing up to 444 rows.
-__global__ void __launch_bounds__(1024)
-bn_part_finalize_kernel(const void* __restrict__ bn_part, int C, const int32_t* n_dev, int64_t cap, float eps, int mode,
-                        const float* __restrict__ rstd_in, float* __restrict__ out_a, float* __restrict__ out_b) {
-  ::vp::pdl_begin();
-  __shared__ double s[32][33];
-  const int nb = *reinterpret_cast<const int*>(bn_part);
-  const float* part = reinterpret_cast<const float*>(reinterpret_cast<const char*>(bn_part) + 256);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = warp >> 4, wg = warp & 15;
-  const int c = blockIdx.x * 32 + lane;
-  double acc = 0.0;
-  if (c < C) {
-    for (int b0 = wg; b0 < nb; b0 += 16 * 8) {
-      float v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int b = b0 + 16 * q;
-        v[q] = b < nb ? __ldcg(part + ((int64_t)b * 2 + h) * C + c) : 0.f;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc += v[q];
-    }
-  }
-  s[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && c < C) {
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int w = 0; w < 16; ++w) {
-      s0 += s[w][lane];
-      s1 += s[16 + w][lane];
-    }
-    if (mode == 1) {
-      const int n = load_count(n_dev, cap);
-      const double mu = n > 0 ? s0 / n : 0.0;
-      double var = n > 0 ? s1 / n - mu * mu : 0.0;
-      if (var < 0) var = 0;
-      out_a[c] = (float)mu;
-      out_b[c] = (float)(1.0 / sqrt(var + (double)eps));
-    } else {
-      out_a[c] = (float)(s1 * (double)rstd_in[c]);
-      out_b[c] = (float)s0;
-    }
-  }
+static int bn_early() {  // early programmatic launch of the apply behind the finalize (VP_BN_EARLY)
+  static const int v = getenv("VP_BN_EARLY") ? atoi(getenv("VP_BN_EARLY")) : 1;
+  return v;
 }
 
 // The apply halves of the forward / backward BN whose statistics partials a
@@ -972,9 +925,16 @@ int vp_bn_apply_part(const void* x, int32_t xd, const int32_t* n_dev, int64_t ca
   VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   VP_REQUIRE(bn_part, VP_EVALIDATION, "bn_apply_part: partials required");
   cudaStream_t st = (cudaStream_t)stream;
-  ::vp::launch(bn_part_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, bn_part, (int)C, n_dev, cap, eps, 1,
-               (const float*)nullptr, mean, rstd);
-  VP_CHECK_LAUNCH("bn_part_finalize");
+  BnEpi e{};
+  e.mode = 1;
+  e.nb = (int*)bn_part;
+  e.part = (float*)((char*)bn_part + kBnPartHeader);
+  e.out_a = mean;
+  e.out_b = rstd;
+  e.eps = eps;
+  e.early = bn_early();
+  ::vp::launch(bn_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, e, (int)C, n_dev, cap);
+  VP_CHECK_LAUNCH("bn_finalize");
   if (cap <= 0) return VP_OK;
   VP_BN_LAUNCH(bn_apply_kernel, C, one_dtype({xd, yd, res ? rd : xd}), bn_grid_rows(cap, C), kGlueThreads, 0, st, x,
                xd, n_dev, cap, (int)C, (const float*)mean, (const float*)rstd, gamma, beta, res, rd, relu, y, yd,
@@ -989,9 +949,26 @@ int vp_bn_backward_part(const void* gm, int32_t gmd, const void* x, int32_t xd, 
   VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
   VP_REQUIRE(bn_part, VP_EVALIDATION, "bn_backward_part: partials required");
   cudaStream_t st = (cudaStream_t)stream;
-  ::vp::launch(bn_part_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, bn_part, (int)C, n_dev, cap, 0.f, 2, rstd,
-               ggamma, gbeta);
-  VP_CHECK_LAUNCH("bn_part_finalize");
+  BnEpi e{};
+  e.mode = 2;
+  e.nb = (int*)bn_part;
+  e.part = (float*)((char*)bn_part + kBnPartHeader);
+  e.out_a = ggamma;
+  e.out_b = gbeta;
+  e.rstd = rstd;
+  e.early = bn_early();
+  ::vp::launch(bn_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, e, (int)C, n_dev, cap);
+  VP_CHECK_LAUNCH("bn_finalize");
+  return vp_bn_backward_apply(gm, gmd, x, xd, n_dev, cap, C, mean, rstd, gamma, ggamma, gbeta, gx, gxd, stream);
+}
+
+// the apply half of the BN backward from finished (ggamma, gbeta): gm is the
+// masked gradient the producer stored (vp_conv_dgrad_bn with finalize)
+int vp_bn_backward_apply(const void* gm, int32_t gmd, const void* x, int32_t xd, const int32_t* n_dev, int64_t cap,
+                         int64_t C, const float* mean, const float* rstd, const float* gamma, const float* ggamma,
+                         const float* gbeta, void* gx, int32_t gxd, vp_stream_t stream) {
+  VP_REQUIRE(bn_shape_ok(C), VP_EVALIDATION, "bn: channels must be <= 256 or a multiple of 8 <= 2048");
+  cudaStream_t st = (cudaStream_t)stream;
   if (cap <= 0) return VP_OK;
   VP_BN_LAUNCH(bn_backward_apply_kernel, C, one_dtype({xd, gmd, gxd}), bn_grid_rows(cap, C), kGlueThreads, 0, st, gm,
                (const void*)nullptr, gmd, (const void*)nullptr, gmd, x, xd, n_dev, cap, (int)C, mean, rstd, gamma, 0,

@@ -224,8 +224,8 @@ class SparseResNetTrainer:
                                      device=dev)
             # BN statistics partials written by the producing conv's epilogue
             # (forward: this conv; backward: the dgrad of the next conv)
-            L["fpart"] = _lib.workspace(_lib.query("vp_bn_part_bytes", L["cout"]), dev)
-            L["bpart"] = _lib.workspace(_lib.query("vp_bn_part_bytes", L["cout"]), dev)
+            L["fpart"] = _lib.workspace(_lib.query("vp_bn_part_bytes", L["cout"]), dev, zero=True)
+            L["bpart"] = _lib.workspace(_lib.query("vp_bn_part_bytes", L["cout"]), dev, zero=True)
         # gradient buffers per level for the activation flowing back
         self.gact = [torch.zeros((lv.cap, self._width_at(i)), dtype=feature_dtype, device=dev)
                      for i, lv in enumerate(self.levels)]
@@ -551,10 +551,11 @@ class SparseResNetTrainer:
         if self.bn_fuse:
             # conv with the BN statistics from its epilogue, then normalise
             # (+ residual) (+ ReLU) from those partials: two launches
-            self._c("vp_conv_fwd_bn", *conv, 1, L["fpart"].data_ptr(), None, None, None, None, st)
-            self._c("vp_bn_apply_part", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], self.eps,
-                    L["fpart"].data_ptr(), L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(),
-                    L["beta"].data_ptr(), _lib.ptr(res), fc, int(relu), L["a"].data_ptr(), fc, st)
+            self._c("vp_conv_fwd_bn", *conv, 1, L["fpart"].data_ptr(), None, None, None, None, self.eps,
+                    L["mean"].data_ptr(), L["rstd"].data_ptr(), None, st)
+            self._c("vp_bn_apply", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], L["mean"].data_ptr(),
+                    L["rstd"].data_ptr(), L["gamma"].data_ptr(), L["beta"].data_ptr(), _lib.ptr(res), fc, int(relu),
+                    L["a"].data_ptr(), fc, st)
         else:
             self._c("vp_conv_fwd", *conv, st)
             # batch statistics + normalise (+ residual) (+ ReLU)
@@ -615,10 +616,10 @@ class SparseResNetTrainer:
         gradient."""
         dst, src, m = L["dst"], L["src"], L["map"]
         fc = self.fcode
-        if prepared:
-            self._c("vp_bn_backward_part", g_out.data_ptr(), fc, L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap,
+        if prepared:  # (ggamma, gbeta) were finalized by the producer chain
+            self._c("vp_bn_backward_apply", g_out.data_ptr(), fc, L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap,
                     L["cout"], L["mean"].data_ptr(), L["rstd"].data_ptr(), L["gamma"].data_ptr(),
-                    L["bpart"].data_ptr(), L["gy"].data_ptr(), fc, L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), st)
+                    L["ggamma"].data_ptr(), L["gbeta"].data_ptr(), L["gy"].data_ptr(), fc, st)
         else:
             self._c("vp_bn_backward", g_out.data_ptr(), _lib.ptr(g_out2), fc, L["a"].data_ptr(), fc,
                     L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], L["mean"].data_ptr(),
@@ -651,7 +652,8 @@ class SparseResNetTrainer:
             gin = self._gm_buf(prev)
             self._c("vp_conv_dgrad_bn", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), 2,
                     prev["bpart"].data_ptr(), _lib.ptr(prev_add), prev["a"].data_ptr(), prev["y"].data_ptr(),
-                    prev["mean"].data_ptr(), st)
+                    prev["mean"].data_ptr(), 0.0, prev["ggamma"].data_ptr(), prev["gbeta"].data_ptr(),
+                    prev["rstd"].data_ptr(), st)
         else:
             gin = self.gact[self.levels.index(src)]
             self._c("vp_conv_dgrad", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
@@ -701,7 +703,8 @@ class SparseResNetTrainer:
         if prev is not None and self.bn_fuse:
             self._c("vp_conv_dgrad_bn", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), 2,
                     prev["bpart"].data_ptr(), _lib.ptr(prev_add), prev["a"].data_ptr(), prev["y"].data_ptr(),
-                    prev["mean"].data_ptr(), st)
+                    prev["mean"].data_ptr(), 0.0, prev["ggamma"].data_ptr(), prev["gbeta"].data_ptr(),
+                    prev["rstd"].data_ptr(), st)
         else:
             self._c("vp_conv_dgrad", *dgrad, gin.data_ptr(), fc, L["dg_ws"].data_ptr(), L["dg_ws"].numel(), st)
         return gin

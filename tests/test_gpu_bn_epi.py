@@ -63,16 +63,22 @@ def _run(kind, mode, cin, cout, n, dt, seed=0):
     y0 = torch.zeros((n, kout), dtype=dt, device="cuda")
     conv("vp_conv_fwd" if kind == "fwd" else "vp_conv_dgrad", y0)
     y1 = torch.full((n, kout), 7.0, dtype=dt, device="cuda")
-    part = _lib.workspace(_lib.query("vp_bn_part_bytes", kout), x.device)
+    part = _lib.workspace(_lib.query("vp_bn_part_bytes", kout), x.device, zero=True)
     add = torch.randn((n, kout), generator=gen).cuda().to(dt)
     act = torch.relu(torch.randn((n, kout), generator=gen)).cuda().to(dt)
     pre = torch.randn((n, kout), generator=gen).cuda().to(dt)
     mean = torch.randn(kout, generator=gen).cuda()
     fn = "vp_conv_fwd_bn" if kind == "fwd" else "vp_conv_dgrad_bn"
+    # finalize in the producer chain too (mode 1: mean / rstd; mode 2: ggamma / gbeta)
+    oa = torch.full((kout,), 3.0, device="cuda")
+    ob = torch.full((kout,), 3.0, device="cuda")
+    rstd_in = torch.rand(kout, generator=gen).cuda() + 0.5
+    eps = 1e-5
     if mode == 1:
-        conv(fn, y1, 1, part.data_ptr(), None, None, None, None)
+        conv(fn, y1, 1, part.data_ptr(), None, None, None, None, eps, oa.data_ptr(), ob.data_ptr(), None)
     else:
-        conv(fn, y1, 2, part.data_ptr(), add.data_ptr(), act.data_ptr(), pre.data_ptr(), mean.data_ptr())
+        conv(fn, y1, 2, part.data_ptr(), add.data_ptr(), act.data_ptr(), pre.data_ptr(), mean.data_ptr(), 0.0,
+             oa.data_ptr(), ob.data_ptr(), rstd_in.data_ptr())
     torch.cuda.synchronize()
     if mode == 1:
         exp = y0
@@ -89,6 +95,17 @@ def _run(kind, mode, cin, cout, n, dt, seed=0):
     scale = torch.stack([t1.abs().sum(0), t2.abs().sum(0)]).cpu().numpy()
     err = np.abs(got - ref)
     assert (err <= 1e-5 * scale + 1e-6).all(), float((err / (scale + 1e-6)).max())
+    # the finalized statistics (fixed-order double sums of the partials)
+    if mode == 1:
+        mu = ref[0] / n
+        var = np.maximum(ref[1] / n - mu * mu, 0.0)
+        ea, eb = mu, 1.0 / np.sqrt(var + eps)
+        sa = scale[0] / n
+    else:
+        ea, eb = ref[1] * rstd_in.double().cpu().numpy(), ref[0]
+        sa = scale[1] * rstd_in.double().cpu().numpy()
+    np.testing.assert_allclose(oa.double().cpu().numpy(), ea, rtol=1e-4, atol=1e-5 * sa.max() + 1e-6)
+    np.testing.assert_allclose(ob.double().cpu().numpy(), eb, rtol=1e-4, atol=1e-5 * scale[0].max() / max(n, 1) + 1e-6)
 
 
 @pytest.mark.parametrize("kind", ["fwd", "dgrad"])

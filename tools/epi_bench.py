@@ -49,7 +49,7 @@ for i, L in enumerate(tr.layers):
             tr.fwd_table(L).data_ptr(), 0, _lib.ptr(tr.fwd_perm(L)), dst.n.data_ptr(), dst.cap,
             L["y"].data_ptr(), fc, L["fwd_ws"].data_ptr(), L["fwd_ws"].numel())
     f0 = timed(lambda: _lib.call("vp_conv_fwd", *conv, _lib.stream()))
-    f1 = timed(lambda: _lib.call("vp_conv_fwd_bn", *conv, 1, L["fpart"].data_ptr(), None, None, None, None, _lib.stream()))
+    f1 = timed(lambda: _lib.call("vp_conv_fwd_bn", *conv, 1, L["fpart"].data_ptr(), None, None, None, None, 1e-5, L["mean"].data_ptr(), L["rstd"].data_ptr(), None, _lib.stream()))
     ap = timed(lambda: _lib.call("vp_bn_apply_part", L["y"].data_ptr(), fc, dst.n.data_ptr(), dst.cap, L["cout"], 1e-5,
                                  L["fpart"].data_ptr(), L["mean"].data_ptr(), L["rstd"].data_ptr(),
                                  L["gamma"].data_ptr(), L["beta"].data_ptr(), None, fc, 1, L["a"].data_ptr(), fc, _lib.stream()))
@@ -72,7 +72,7 @@ for i, L in enumerate(tr.layers):
               L["dg_ws"].data_ptr(), L["dg_ws"].numel())
         d0 = timed(lambda: _lib.call("vp_conv_dgrad", *dg, _lib.stream()))
         d2 = timed(lambda: _lib.call("vp_conv_dgrad_bn", *dg, 2, P["bpart"].data_ptr(), None, P["a"].data_ptr(),
-                                     P["y"].data_ptr(), P["mean"].data_ptr(), _lib.stream()))
+                                     P["y"].data_ptr(), P["mean"].data_ptr(), 0.0, P["ggamma"].data_ptr(), P["gbeta"].data_ptr(), P["rstd"].data_ptr(), _lib.stream()))
         bp = timed(lambda: _lib.call("vp_bn_backward_part", gin.data_ptr(), fc, P["y"].data_ptr(), fc,
                                      P["dst"].n.data_ptr(), P["dst"].cap, P["cout"], P["mean"].data_ptr(),
                                      P["rstd"].data_ptr(), P["gamma"].data_ptr(), P["bpart"].data_ptr(),

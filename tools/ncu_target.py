@@ -57,10 +57,10 @@ def main():
         P = tr.layers[idx[a.layer] - 1] if idx[a.layer] > 0 else None
         launches = {
             "fwd": lambda: _lib.call("vp_conv_fwd", *conv, st),
-            "fwd_bn": lambda: _lib.call("vp_conv_fwd_bn", *conv, 1, L["fpart"].data_ptr(), None, None, None, None, st),
+            "fwd_bn": lambda: _lib.call("vp_conv_fwd_bn", *conv, 1, L["fpart"].data_ptr(), None, None, None, None, 1e-5, L["mean"].data_ptr(), L["rstd"].data_ptr(), None, st),
             "dgrad": lambda: _lib.call("vp_conv_dgrad", *dg, st),
             "dgrad_bn": lambda: _lib.call("vp_conv_dgrad_bn", *dg, 2, P["bpart"].data_ptr(), None, P["a"].data_ptr(),
-                                          P["y"].data_ptr(), P["mean"].data_ptr(), st),
+                                          P["y"].data_ptr(), P["mean"].data_ptr(), 0.0, P["ggamma"].data_ptr(), P["gbeta"].data_ptr(), P["rstd"].data_ptr(), st),
             "wgrad": lambda: _lib.call("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
                                        tr.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(),
                                        L["gw"].data_ptr(), L["wg_ws"].data_ptr(), L["wg_ws"].numel(), st),
