@@ -317,6 +317,25 @@ int vp_bn_backward_part(const void* gm, int32_t gm_dtype, const void* x, int32_t
                         int64_t cap_n, int64_t C, const float* mean, const float* rstd, const float* gamma,
                         const void* bn_part, void* grad_x, int32_t gx_dtype, float* ggamma, float* gbeta,
                         vp_stream_t stream);
+/* per-batch-index row segments of batch-contiguous rows: seg[0:B] =
+ * counts, seg[B:2B] = starts (int32, device) */
+int vp_batch_segments(const int32_t* coords, const int32_t* n_dev, int64_t cap_n, int32_t B, int32_t* seg,
+                      vp_stream_t stream);
+/* The classifier head of the training step, fused (two launches): per-cloud
+ * mean pool of a [n, C], logits = pooled W^T + bias, softmax cross entropy
+ * (mean over B) and its gradients (g_w, g_b fp32), and the gradient of every
+ * row of a (pool backward) — masked by bn_act > 0 and stored in gm (a's
+ * dtype); with bn_pre (the last BN's input) also that BN's backward
+ * statistics, finalized to ggamma / gbeta (bn_rstd) so its backward apply
+ * (vp_bn_backward_apply) follows directly.  bn_part: vp_bn_part_bytes(C),
+ * zero-filled before first use.  Same arithmetic and summation order as
+ * vp_global_pool + vp_linear_xent + vp_global_pool_backward. */
+size_t vp_sparse_head_ws_bytes(int32_t B, int64_t C, int32_t classes);
+int vp_sparse_head(const void* a, int32_t a_dtype, const int32_t* seg, int32_t B, int64_t C, const float* w,
+                   const float* bias, int32_t classes, const int32_t* labels, float* pooled, float* logits, float* loss,
+                   float* g_w, float* g_b, const void* bn_act, const void* bn_pre, const float* bn_mean,
+                   const float* bn_rstd, void* gm, void* bn_part, float* ggamma, float* gbeta, void* ws,
+                   size_t ws_bytes, vp_stream_t stream);
 /* global average pool per batch index (rows batch-contiguous):
  * out [B, C] fp32, counts [B] int32 */
 int vp_global_pool(const void* x, int32_t x_dtype, const int32_t* coords, const int32_t* n_dev,

@@ -759,6 +759,176 @@ __global__ void xent_reduce_kernel(const float* __restrict__ pooled, int B, int 
   }
 }
 
+// ------------------------------------------------------------------ fused head
+// The classifier head of the training step in two launches: head_kernel runs
+// one block per cloud (rows [starts[b], starts[b] + counts[b]), batch-
+// contiguous): mean pool -> logits (warp per class, fixed xor tree) ->
+// softmax / loss -> g_logits = (p - onehot) / B -> g_pooled = g_logits W ->
+// the gradient of every row of the cloud, g = g_pooled / count, masked by
+// the last BN's ReLU (act > 0) and stored rounded (gm) with that BN's
+// backward statistics per cloud (sum gm, sum gm (pre - mean): bn_epi.cuh
+// partial row b); head_reduce_kernel (one block) sums the fc gradients and
+// the loss over clouds in order and finalizes the BN statistics.  Same
+// arithmetic and order as pool + xent + pool_backward + the unfused BN
+// statistics pass.
+struct HeadBn {
+  const void* act;    // last BN output (ReLU mask source), nullable
+  const void* pre;    // last BN input (conv output), nullable = no statistics
+  const float* mean;
+  void* gm;           // [n, C] row gradients (masked)
+  float* part;        // bn_epi partial rows (B of them)
+  int* nb;
+};
+
+template <int DT>
+__global__ void __launch_bounds__(256)
+head_kernel(const void* __restrict__ a, int dtype, const int32_t* __restrict__ seg, int B, int C,
+            const float* __restrict__ w, const float* __restrict__ bias, int classes, const int32_t* __restrict__ labels,
+            float* __restrict__ pooled, float* __restrict__ logits, float* __restrict__ g_logits,
+            float* __restrict__ loss_b, float* __restrict__ g_pooled, const HeadBn hb) {
+  ::vp::pdl_begin();
+  extern __shared__ float sm[];
+  float* s_x = sm;                 // C: pooled row
+  float* s_gp = sm + C;            // C: g_pooled row
+  float* s_logit = sm + 2 * C;     // classes
+  float* s_g = s_logit + classes;  // classes
+  __shared__ float s_max, s_sum;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int cnt = seg[b], st = seg[B + b];
+  if (b == 0 && threadIdx.x == 0 && hb.nb) *hb.nb = B;
+  auto ld = [&](const void* p, int64_t i) -> float {
+    return DT == VP_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i])
+           : DT == VP_F32 ? reinterpret_cast<const float*>(p)[i] : ldf(p, dtype, i);
+  };
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < cnt; ++r) acc += ld(a, (int64_t)(st + r) * C + c);
+    const float v = cnt > 0 ? acc / (float)cnt : 0.f;
+    s_x[c] = v;
+    pooled[(int64_t)b * C + c] = v;
+  }
+  __syncthreads();
+  for (int j = warp; j < classes; j += nw) {
+    float acc = 0.f;
+#pragma unroll 4
+    for (int c = lane; c < C; c += 32) acc += w[(int64_t)j * C + c] * s_x[c];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (lane == 0) {
+      const float v = acc + bias[j];
+      s_logit[j] = v;
+      logits[(int64_t)b * classes + j] = v;
+    }
+  }
+  __syncthreads();
+  const int lab = labels[b];
+  if (threadIdx.x == 0) {
+    float m = -INFINITY;
+    for (int j = 0; j < classes; ++j) m = fmaxf(m, s_logit[j]);
+    float sum = 0.f;
+    for (int j = 0; j < classes; ++j) sum += expf(s_logit[j] - m);
+    s_max = m;
+    s_sum = sum;
+    loss_b[b] = -(s_logit[lab] - m - logf(sum));
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < classes; j += blockDim.x) {
+    const float pj = expf(s_logit[j] - s_max) / s_sum;
+    const float gj = (pj - (j == lab ? 1.f : 0.f)) / (float)B;
+    s_g[j] = gj;
+    g_logits[(int64_t)b * classes + j] = gj;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < classes; ++j) acc += s_g[j] * w[(int64_t)j * C + c];
+    s_gp[c] = acc;
+    g_pooled[(int64_t)b * C + c] = acc;
+  }
+  __syncthreads();
+  // the rows' gradient (pool backward) + the last BN's masked gradient and
+  // statistics for this cloud
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float g0 = cnt > 0 ? s_gp[c] / (float)cnt : 0.f;
+    const float gr = DT == VP_BF16 ? __bfloat162float(__float2bfloat16_rn(g0)) : g0;
+    const float mu = hb.pre ? hb.mean[c] : 0.f;
+    float s1 = 0.f, s2 = 0.f;
+    constexpr int U = 8;  // rows per batch: every load of a batch issued before any store
+    for (int r0 = 0; r0 < cnt; r0 += U) {
+      float av[U], pv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = (int64_t)(st + r0 + u) * C + c;
+        const bool in = r0 + u < cnt;
+        av[u] = (in && hb.act) ? ld(hb.act, i) : 1.f;
+        pv[u] = (in && hb.pre) ? ld(hb.pre, i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r0 + u >= cnt) break;
+        const int64_t i = (int64_t)(st + r0 + u) * C + c;
+        const float g = av[u] > 0.f ? gr : 0.f;
+        stf(hb.gm, DT >= 0 ? DT : dtype, i, g);
+        if (hb.pre) {
+          s1 += g;
+          s2 += g * (pv[u] - mu);
+        }
+      }
+    }
+    if (hb.pre) {
+      hb.part[((int64_t)b * 2) * C + c] = s1;
+      hb.part[((int64_t)b * 2 + 1) * C + c] = s2;
+    }
+  }
+}
+
+// one 1024-thread block: fc gradients and the mean loss summed over clouds in
+// order (as xent_reduce_kernel), then the last BN's finalize from the B
+// per-cloud rows
+// blocks [0, classes): row j of g_w (thread per channel, pooled rows read
+// coalesced, the class's g_logits column staged in shared memory) summed over
+// b in order; block `classes`: g_b and the mean loss; blocks after: the BN
+// finalize of 32 channels each
+__global__ void __launch_bounds__(256)
+head_reduce_kernel(const float* __restrict__ pooled, int B, int C, int classes, const float* __restrict__ g_logits,
+                   const float* __restrict__ loss_b, float* __restrict__ g_w, float* __restrict__ g_b,
+                   float* __restrict__ loss, const BnEpi e) {
+  ::vp::pdl_begin();
+  __shared__ float s_g[1024];
+  const int j = blockIdx.x;
+  if (j < classes) {
+    for (int b0 = 0; b0 < B; b0 += 1024) {
+      const int nb = min(1024, B - b0);
+      __syncthreads();
+      for (int bb = threadIdx.x; bb < nb; bb += blockDim.x) s_g[bb] = g_logits[(int64_t)(b0 + bb) * classes + j];
+      __syncthreads();
+      for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        float acc = b0 == 0 ? 0.f : g_w[(int64_t)j * C + c];
+#pragma unroll 16
+        for (int bb = 0; bb < nb; ++bb) acc += s_g[bb] * pooled[(int64_t)(b0 + bb) * C + c];
+        g_w[(int64_t)j * C + c] = acc;
+      }
+    }
+    return;
+  }
+  if (j == classes) {
+    for (int jj = threadIdx.x; jj < classes; jj += blockDim.x) {
+      float acc = 0.f;
+      for (int bb = 0; bb < B; ++bb) acc += g_logits[(int64_t)bb * classes + jj];
+      g_b[jj] = acc;
+    }
+    if (threadIdx.x == 0) {
+      float sum = 0.f;
+      for (int bb = 0; bb < B; ++bb) sum += loss_b[bb];
+      *loss = sum / (float)B;
+    }
+    return;
+  }
+}
+
 __global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ m, const float* __restrict__ g, int64_t n,
                            float lr, float mom, __nv_bfloat16* __restrict__ pb, int64_t nb) {
   ::vp::pdl_begin();
@@ -1022,6 +1192,66 @@ int vp_linear_xent(const float* pooled, int32_t B, int32_t C, const float* w, co
   ::vp::launch(xent_reduce_kernel, grid_for((int64_t)classes * (C + 1)), 256, 0, st, pooled, B, C, classes, g_logits, loss_b,
                                                                           g_w, g_b, loss);
   VP_CHECK_LAUNCH("xent_reduce");
+  return VP_OK;
+}
+
+int vp_batch_segments(const int32_t* coords, const int32_t* n_dev, int64_t cap, int32_t B, int32_t* seg,
+                      vp_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  VP_REQUIRE(B >= 1, VP_EVALIDATION, "batch_segments: B must be positive");
+  cudaMemsetAsync(seg, 0, sizeof(int32_t) * B, st);
+  VP_CHECK_ASYNC("batch_segments(memset)");
+  if (cap > 0) {
+    ::vp::launch(batch_count_kernel, grid_for(cap), 256, 0, st, (const int4*)coords, n_dev, cap, B, seg);
+    VP_CHECK_LAUNCH("batch_count");
+  }
+  ::vp::launch(batch_starts_kernel, 1, 1024, 0, st, (const int32_t*)seg, B, seg + B);
+  VP_CHECK_LAUNCH("batch_starts");
+  return VP_OK;
+}
+
+size_t vp_sparse_head_ws_bytes(int32_t B, int64_t C, int32_t classes) {
+  return align_up((size_t)B * classes * 4, 256) + align_up((size_t)B * 4, 256) + align_up((size_t)B * C * 4, 256);
+}
+
+int vp_sparse_head(const void* a, int32_t a_dtype, const int32_t* seg, int32_t B, int64_t C, const float* w,
+                   const float* bias, int32_t classes, const int32_t* labels, float* pooled, float* logits, float* loss,
+                   float* g_w, float* g_b, const void* bn_act, const void* bn_pre, const float* bn_mean,
+                   const float* bn_rstd, void* gm, void* bn_part, float* ggamma, float* gbeta, void* ws,
+                   size_t ws_bytes, vp_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  VP_REQUIRE(B >= 1 && C >= 1 && classes >= 1 && classes <= 4096, VP_EVALIDATION, "sparse_head: bad shape");
+  VP_REQUIRE(ws && ws_bytes >= vp_sparse_head_ws_bytes(B, C, classes), VP_EVALIDATION, "sparse_head: workspace too small");
+  VP_REQUIRE(!bn_pre || (bn_mean && bn_rstd && bn_part && ggamma && gbeta && B <= kBnPartRows), VP_EVALIDATION,
+             "sparse_head: the BN statistics need mean, rstd, partial rows and outputs");
+  VP_REQUIRE(gm, VP_EVALIDATION, "sparse_head: row gradient output required");
+  char* p = (char*)ws;
+  float* g_logits = (float*)p;
+  p += align_up((size_t)B * classes * 4, 256);
+  float* loss_b = (float*)p;
+  p += align_up((size_t)B * 4, 256);
+  float* g_pooled = (float*)p;
+  HeadBn hb{bn_act, bn_pre, bn_mean, gm, bn_part ? (float*)((char*)bn_part + kBnPartHeader) : nullptr, (int*)bn_part};
+  const size_t smem = (size_t)(2 * C + 2 * classes) * sizeof(float);
+  auto hk = a_dtype == VP_BF16 ? head_kernel<VP_BF16> : a_dtype == VP_F32 ? head_kernel<VP_F32> : head_kernel<-1>;
+  ::vp::launch(hk, B, 256, smem, st, a, a_dtype, seg, B, (int)C, w, bias, classes, labels, pooled, logits, g_logits,
+               loss_b, g_pooled, hb);
+  VP_CHECK_LAUNCH("sparse_head");
+  BnEpi e{};
+  e.mode = 2;
+  e.part = hb.part;
+  e.out_a = bn_pre ? ggamma : nullptr;
+  e.out_b = gbeta;
+  e.rstd = bn_rstd;
+  // the finalize blocks need 1024 threads: a separate tiny launch keeps the fc blocks at 256
+  ::vp::launch(head_reduce_kernel, classes + 1, 256, 0, st, (const float*)pooled, B, (int)C, classes,
+               (const float*)g_logits, (const float*)loss_b, g_w, g_b, loss, e);
+  VP_CHECK_LAUNCH("sparse_head_reduce");
+  if (bn_pre) {
+    e.nb = (int*)bn_part;
+    ::vp::launch(bn_finalize_kernel, (int)ceil_div(C, 32), 1024, 0, st, e, (int)C, (const int32_t*)nullptr, (int64_t)B);
+    VP_CHECK_LAUNCH("bn_finalize");
+  }
   return VP_OK;
 }
 

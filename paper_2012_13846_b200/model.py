@@ -37,6 +37,7 @@ class Level:
     n: torch.Tensor  # (1,) int32, live rows
     cap: int
     stride: int
+    seg: Optional[torch.Tensor] = None  # (2B,) int32 per-cloud row counts / starts (the head's level)
 
 
 @dataclass(eq=False)
@@ -147,6 +148,7 @@ class SparseResNetTrainer:
             caps.append(min(caps[-1], batch * cells ** 3))
         self.levels = [Level(torch.zeros((caps[i], 4), dtype=torch.int32, device=dev),
                              torch.zeros(1, dtype=torch.int32, device=dev), caps[i], 2 ** i) for i in range(nlev)]
+        self.levels[-1].seg = torch.zeros(2 * batch, dtype=torch.int32, device=dev)
         self.feat0 = torch.zeros((cap, in_channels), dtype=feature_dtype, device=dev)
         self.vox_ws = _lib.workspace(_lib.query("vp_voxelize_ws_bytes", cap), dev)
         self.oc_ws = _lib.workspace(_lib.query("vp_output_coords_ws_bytes", cap), dev)
@@ -251,6 +253,7 @@ class SparseResNetTrainer:
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
         self.g_pooled = torch.zeros((batch, C), dtype=torch.float32, device=dev)
         self.xent_ws = _lib.workspace(_lib.query("vp_linear_xent_ws_bytes", batch, classes), dev)
+        self.head_ws = _lib.workspace(_lib.query("vp_sparse_head_ws_bytes", batch, C, classes), dev)
         self.graph: Optional[torch.cuda.CUDAGraph] = None
         self.launch_count = 0
         # side streams: the coordinate chain, kernel maps and weight gradients
@@ -474,7 +477,14 @@ class SparseResNetTrainer:
                     lv[i].coords.data_ptr(), lv[i].n.data_ptr(), None, self.oc_ws.data_ptr(), self.oc_ws.numel(),
                     stream)
 
+        def segments(stream):  # per-cloud row segments of the head's level (vp_sparse_head)
+            if self.last:
+                lx = lv[ext]
+                self._c("vp_batch_segments", lx.coords.data_ptr(), lx.n.data_ptr(), lx.cap, self.B, lx.seg.data_ptr(),
+                        stream)
+
         lev_ev = {}
+        self.seg_event = None
         if conc:
             chain = self.int_side[0]
             self._forked.add(id(chain))
@@ -484,9 +494,13 @@ class SparseResNetTrainer:
                     out_coords(i, chain.cuda_stream)
                     lev_ev[i] = torch.cuda.Event()
                     lev_ev[i].record(chain)
+                segments(chain.cuda_stream)
+                self.seg_event = torch.cuda.Event()
+                self.seg_event.record(chain)
         else:
             for i in range(ent + 1, ext + 1):
                 out_coords(i, st)
+            segments(st)
 
         def needs(stream, i, maps):
             if not conc:
@@ -581,6 +595,21 @@ class SparseResNetTrainer:
             return x
         last = self.levels[-1]
         C = self.planes[-1]
+        if self.bn_fuse:
+            # pool + linear + cross entropy + the rows' gradient masked by the
+            # last BN's ReLU with that BN's backward statistics, fused
+            if getattr(self, "seg_event", None) is not None and not self.prefetch:
+                torch.cuda.current_stream().wait_event(self.seg_event)
+            pb = self.params
+            Ll = self.layers[-1]
+            self._c("vp_sparse_head", x.data_ptr(), self.fcode, last.seg.data_ptr(), self.B, C,
+                    pb.view(pb.p, "fc.w").data_ptr(), pb.view(pb.p, "fc.b").data_ptr(), self.classes,
+                    self.labels.data_ptr(), self.pooled.data_ptr(), self.logits.data_ptr(), self.loss.data_ptr(),
+                    pb.view(pb.g, "fc.w").data_ptr(), pb.view(pb.g, "fc.b").data_ptr(), Ll["a"].data_ptr(),
+                    Ll["y"].data_ptr(), Ll["mean"].data_ptr(), Ll["rstd"].data_ptr(), self._gm_buf(Ll).data_ptr(),
+                    Ll["bpart"].data_ptr(), Ll["ggamma"].data_ptr(), Ll["gbeta"].data_ptr(), self.head_ws.data_ptr(),
+                    self.head_ws.numel(), st)
+            return x
         self._c("vp_global_pool", x.data_ptr(), self.fcode, last.coords.data_ptr(), last.n.data_ptr(), last.cap, C,
                 self.B, self.pooled.data_ptr(), self.pool_counts.data_ptr(), self.pool_ws.data_ptr(),
                 self.pool_ws.numel(), st)
@@ -736,7 +765,11 @@ class SparseResNetTrainer:
             self._c("vp_sgd_momentum", *args, side.cuda_stream)
 
     def _backward(self, st):
-        if self.last:
+        prepared = False  # g already holds the masked gradient + BN statistics (fused producer)
+        if self.last and self.bn_fuse:
+            g = self._gm_buf(self.layers[-1])  # written by vp_sparse_head in the forward
+            prepared = True
+        elif self.last:
             last = self.levels[-1]
             C = self.planes[-1]
             g = self.gact[-1]
@@ -748,7 +781,6 @@ class SparseResNetTrainer:
         units = self.units[self.unit_range[0]:self.unit_range[1] + 1]
         # the layer whose activation feeds each layer (None: the engine's input)
         prev_of = {id(L): (self.layers[i - 1] if i > 0 else None) for i, L in enumerate(self.layers)}
-        prepared = False  # g already holds the masked gradient + BN partials (fused producer)
         for u in reversed(units):
             Ls = u["layers"]
             if u["kind"] == "block":
@@ -865,7 +897,8 @@ class SparseResNetTrainer:
             return
         a = self._state()
         dev = self.device
-        levels = [Level(torch.zeros_like(lv.coords), torch.zeros_like(lv.n), lv.cap, lv.stride) for lv in self.levels]
+        levels = [Level(torch.zeros_like(lv.coords), torch.zeros_like(lv.n), lv.cap, lv.stride,
+                        None if lv.seg is None else torch.zeros_like(lv.seg)) for lv in self.levels]
         lmap = dict(zip(map(id, self.levels), levels))
 
         def clone_map(m):
