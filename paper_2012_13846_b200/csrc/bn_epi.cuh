@@ -42,6 +42,7 @@ struct BnEpi {
   float eps;
   unsigned int* ticket;   // header word (zero before first use; re-arms itself)
   int early;              // trigger the dependent (apply) launch at the start of the finalizing kernel
+  int rows_pass;          // conv epilogue stores raw rows; the split-K reduction kernel transforms them
 };
 
 constexpr int kBnTicketOffset = 64;  // bytes into the header

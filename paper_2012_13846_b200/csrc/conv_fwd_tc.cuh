@@ -432,10 +432,11 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
         scan_item(w + gridDim.x, ii + 1);
       }
       const int a = ii % C::ACC;
-      if (epi && p.epi.mode == 2 && (p.dbg & 96)) {
-        // experiment (VP_CONV_DBG bit 5: bulk, bit 6: per-line): this item's
-        // rows of the BN operands (add / act / pre) head for L2 while the
-        // accumulator is still being produced
+      if (epi && p.epi.mode == 2 && !(p.dbg & 256)) {
+        // this item's rows of the BN operands (add / act / pre) head for L2
+        // while the accumulator is still being produced: per-line prefetch
+        // (C3 51.6k -> 51.9k clouds/s; VP_CONV_DBG bit 5: bulk prefetch
+        // instead, bit 8: off)
 #pragma unroll 1
         for (int t = 0; t < TT; ++t) {
           const int64_t row = (int64_t)tile * TR + t * 128 + ep * 32 + lane;
@@ -639,7 +640,8 @@ split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev
   const int ntiles = (n_out + 127) / 128;
   const int S = split_count(ntiles, grid < kSplitItems ? grid : kSplitItems, max_split);
   if (e.out_a && e.early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (S <= 1) {
+  const bool rows = S <= 1 && e.rows_pass;  // the conv stored raw rows: transform them here
+  if (S <= 1 && !rows) {
     // the conv epilogue wrote the partial rows: finalize them here (one
     // 32-channel block per CTA) instead of in a separate launch
     if (e.out_a && (int)blockIdx.x * 32 < ND)
@@ -654,15 +656,24 @@ split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev
     const int64_t r = el * 4 / ND;
     const int tile = (int)(r >> 7), lr = (int)(r & 127);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t oidx;
+    if (rows) {  // output rows are already in place (perm applied by the conv)
+      oidx = r * ND + n;
+      const uint2 raw = *reinterpret_cast<const uint2*>(y + oidx);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+      acc = make_float4(f0.x, f0.y, f1.x, f1.y);
+    } else {
 #pragma unroll 4
-    for (int s = 0; s < S; ++s) {  // loads batched, sums stay in split order
-      const float4 v = *reinterpret_cast<const float4*>(part + (((int64_t)s * ntiles + tile) * 128 + lr) * ND + n);
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
+      for (int s = 0; s < S; ++s) {  // loads batched, sums stay in split order
+        const float4 v = *reinterpret_cast<const float4*>(part + (((int64_t)s * ntiles + tile) * 128 + lr) * ND + n);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      oidx = (perm ? (int64_t)__ldg(perm + r) : r) * ND + n;
     }
-    const int64_t oidx = (perm ? (int64_t)__ldg(perm + r) : r) * ND + n;
     float v[4] = {acc.x, acc.y, acc.z, acc.w}, o[4], h[4];
     if (e.mode == 2) {
       uint2 ra = e.add ? __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(e.add) + oidx))

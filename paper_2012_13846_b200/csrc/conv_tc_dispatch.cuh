@@ -32,6 +32,17 @@ inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * kMaxSplit, (int64_t)kNumSMs * CPS));
   FwdParams p = p0;
   p.part = (float*)part;
+  // backward-BN transform of wide outputs as a row pass in the split-K
+  // reduction kernel instead of the epilogue (VP_EPI_ROWS_MIN_ND, default 64)
+  static const int rows_min_nd = getenv("VP_EPI_ROWS_MIN_ND") ? atoi(getenv("VP_EPI_ROWS_MIN_ND")) : 64;
+  BnEpi rows_epi{};
+  bool rows_pass = false;
+  if (p.epi.mode == 2 && ND >= rows_min_nd && rows_min_nd > 0 && part != nullptr) {
+    rows_pass = true;
+    rows_epi = p.epi;
+    rows_epi.rows_pass = 1;
+    p.epi = BnEpi{};  // plain epilogue
+  }
   static const int max_split = getenv("VP_CONV_MAX_SPLIT") ? std::max(1, std::min(kMaxSplit, atoi(getenv("VP_CONV_MAX_SPLIT"))))
                                                           : kMaxSplit;  // tuning
   p.max_split = part ? max_split : 1;
@@ -41,7 +52,19 @@ inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   p.trace = g_conv_trace_host;
   ::vp::launch(kern, grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st, p);
   VP_CHECK_LAUNCH("conv_tc");
-  if (part && p.epi.mode != 0) {  // bf16 output + BN statistics: at most one partial row per SM
+  if (rows_pass) {
+    const int64_t work = p.cap_out * ND / 4;
+    const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(work, kSplitEpiThreads), kNumSMs), 1);
+    BnEpi e = rows_epi;
+    e.out_a = e.out_b = nullptr;  // finalized by the 32-channel-per-block kernel below
+    ::vp::launch(split_reduce_epi_kernel<ND>, (int)blocks, kSplitEpiThreads, 0, st, (const float*)part, p.n_out_dev,
+                 p.cap_out, grid, p.max_split, p.perm, (bf16*)p.y, e);
+    VP_CHECK_LAUNCH("split_reduce_epi");
+    if (rows_epi.out_a) {
+      ::vp::launch(bn_finalize_kernel, (int)ceil_div(ND, 32), 1024, 0, st, rows_epi, ND, p.n_out_dev, p.cap_out);
+      VP_CHECK_LAUNCH("bn_finalize");
+    }
+  } else if (part && p.epi.mode != 0) {  // bf16 output + BN statistics: at most one partial row per SM
     const int64_t work = p.cap_out * ND / 4;
     // >= one block per 32 channels: without a split they finalize the conv's partial rows.
     // When even the capacity's tile count is split for sure (few rows), the
