@@ -150,14 +150,19 @@ int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, co
                        const int32_t* n_out_dev, int64_t cap_out, const int32_t* offsets_host, int32_t K,
                        const int32_t* in_stride_host3, int32_t* nbr, int32_t* pair_in, int32_t* pair_out,
                        int32_t* pair_ptr, void* ws, size_t ws_bytes, vp_stream_t stream);
-/* Neighbour-mask row ordering (kmap_sort.cu): stable radix sort of the
- * table's rows by their K-bit hit mask (K <= 30) -> perm [cap] (table row
- * order -> row id) and table_sorted [cap, K] = table[perm].  Passing
+/* Neighbour-pattern row grouping (kmap_sort.cu): stable counting sort of
+ * the live table rows by a 9-bit key of their 3^3 hit mask — key_mode 0:
+ * which (dx, dy) columns hold a hit (stride-1 tables), 1: which dx / dy /
+ * dz planes hold a hit (strided inverse tables) — into perm [n] (table row
+ * order -> row id) and table_sorted [n, K] = table[perm].  Passing
  * (table_sorted, perm) to vp_conv_fwd / vp_conv_dgrad gives results
- * identical to (table, NULL) with far fewer active offsets per 128-row tile. */
+ * identical to (table, NULL) with far fewer active offsets per 128-row tile.
+ * vp_kernel_map_sort = key mode 1.  No library sort; deterministic. */
 size_t vp_kernel_map_sort_ws_bytes(int64_t cap, int32_t K);
 int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, int32_t K, int32_t* perm,
                        int32_t* table_sorted, void* ws, size_t ws_bytes, vp_stream_t stream);
+int vp_kernel_map_group(const int32_t* table, const int32_t* n_dev, int64_t cap, int32_t K, int32_t key_mode,
+                        int32_t* perm, int32_t* table_sorted, void* ws, size_t ws_bytes, vp_stream_t stream);
 /* Two-level ("brick") index for bounded lattices, the same contract as the
  * dense grid with ~64x less memory: a coarse table over 4^3 bricks plus a
  * pool of 256 B bricks allocated only where rows exist (kmap_brick.cu).

@@ -50,6 +50,7 @@ SIGNATURES = {
     "vp_kernel_map": (C.c_int, [P, P, I64, P, P, I64, P, I32, P, P, P, P, P, P, SZ, P]),
     "vp_kernel_map_sort_ws_bytes": (SZ, [I64, I32]),
     "vp_kernel_map_sort": (C.c_int, [P, P, I64, I32, P, P, P, SZ, P]),
+    "vp_kernel_map_group": (C.c_int, [P, P, I64, I32, I32, P, P, P, SZ, P]),
     "vp_brick_pool": (I64, [I64, I32, I32]),
     "vp_brick_bytes": (SZ, [I64, I32, I32]),
     "vp_brick_init": (C.c_int, [P, I64, I32, I32, P]),

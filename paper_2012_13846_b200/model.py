@@ -289,7 +289,7 @@ class SparseResNetTrainer:
     SORT_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_MIN_ROWS", 1 << 18))
     SORT_INV_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_INV_MIN_ROWS", 0))
     # levels whose forward tables are sorted regardless of size
-    SORT_LEVELS = tuple(int(v) for v in __import__("os").environ.get("VP_SORT_LEVELS", "1").split(",") if v)
+    SORT_LEVELS = tuple(int(v) for v in __import__("os").environ.get("VP_SORT_LEVELS", "1,2,3").split(",") if v)
     # prefetch mode: fork the next batch's integer stage at the start of the
     # step, concurrent with the forward too (VP_PREFETCH_EARLY=0: after the
     # forward; measured 42.5k -> 43.8k clouds/s at C3 with the early fork)
@@ -423,10 +423,10 @@ class SparseResNetTrainer:
             self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
                     m.inv.data_ptr(), m.src.cap, st)
         if m.perm is not None:
-            self._c("vp_kernel_map_sort", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K, m.perm.data_ptr(),
+            self._c("vp_kernel_map_group", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K, 0, m.perm.data_ptr(),
                     m.nbr_s.data_ptr(), m.sort_ws.data_ptr(), m.sort_ws.numel(), st)
         if m.iperm is not None:
-            self._c("vp_kernel_map_sort", m.inv.data_ptr(), m.src.n.data_ptr(), m.src.cap, self.K,
+            self._c("vp_kernel_map_group", m.inv.data_ptr(), m.src.n.data_ptr(), m.src.cap, self.K, 1,
                     m.iperm.data_ptr(), m.inv_s.data_ptr(), m.sort_ws.data_ptr(), m.sort_ws.numel(), st)
 
     @staticmethod

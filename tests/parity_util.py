@@ -83,17 +83,36 @@ def ref_integer_stage(points, offsets, res, nlev=5):
     return "oracle", levels, s1, dn
 
 
-def _check_perm_table(perm, table_s, table, n, what):
-    """A neighbour-mask sorted table: perm is a permutation of 0..n-1 and
-    table_s[i] == table[perm[i]] row for row, rows grouped by ascending hit
-    mask (vp_kernel_map_sort)."""
+def group_key(table, mode):
+    """The 9-bit grouping key of csrc/kmap_sort.cu for 3^3 tables: mode 0 =
+    which (dx, dy) columns hold a hit, mode 1 = which dx / dy / dz planes."""
+    hit = np.asarray(table) >= 0
+    n = hit.shape[0]
+    if mode == 0:
+        bits = hit.reshape(n, 9, 3).any(2)
+    else:
+        h = hit.reshape(n, 3, 3, 3)
+        bits = np.concatenate([h.any((2, 3)), h.any((1, 3)), h.any((1, 2))], 1)
+    return (bits.astype(np.int64) << np.arange(9, dtype=np.int64)).sum(1)
+
+
+def check_grouping(p, ts, mode, what):
+    """Rows in ascending key order, stable (equal keys keep row order)."""
+    key = group_key(ts, mode)
+    d = np.diff(key)
+    assert (d >= 0).all(), f"{what}: rows not grouped by key"
+    assert (np.diff(p)[d == 0] > 0).all(), f"{what}: grouping not stable"
+
+
+def _check_perm_table(perm, table_s, table, n, what, mode=1):
+    """A grouped table (vp_kernel_map_group): perm is a permutation of
+    0..n-1, table_s[i] == table[perm[i]] row for row, rows in ascending
+    stable key order."""
     p = perm[:n].cpu().numpy().astype(np.int64)
     assert np.array_equal(np.sort(p), np.arange(n)), f"{what}: perm is not a permutation"
     ts = table_s[:n].cpu().numpy()
     np.testing.assert_array_equal(ts, table[p], err_msg=f"{what}: sorted table != table[perm]")
-    K = ts.shape[1]
-    mask = ((ts >= 0).astype(np.int64) << np.arange(K, dtype=np.int64)).sum(1)
-    assert (np.diff(mask) >= 0).all(), f"{what}: sorted table rows not grouped by hit mask"
+    check_grouping(p, ts, mode, what)
 
 
 def check_map(m, pairs, what):
@@ -119,9 +138,9 @@ def check_map(m, pairs, what):
     if exp_inv is not None:
         np.testing.assert_array_equal(m.inv[:ns].cpu().numpy(), exp_inv, err_msg=f"{what}: inverse table")
     if m.perm is not None:
-        _check_perm_table(m.perm, m.nbr_s, exp_nbr, nd, f"{what} forward")
+        _check_perm_table(m.perm, m.nbr_s, exp_nbr, nd, f"{what} forward", mode=0)
     if m.iperm is not None:
-        _check_perm_table(m.iperm, m.inv_s, exp_inv, ns, f"{what} inverse")
+        _check_perm_table(m.iperm, m.inv_s, exp_inv, ns, f"{what} inverse", mode=1)
     return int(exp_ptr[-1])
 
 

@@ -182,8 +182,9 @@ def test_transposed_conv_adjoint():
 @pytest.mark.parametrize("c", [32, 128, 256])
 @pytest.mark.parametrize("stride", [1, 2])
 def test_mask_sorted_rows_bitwise_equal(c, stride):
-    """vp_kernel_map_sort: perm is a permutation of the live rows, the sorted
-    table is table[perm], and forward / dgrad over (sorted table, perm) equal
+    """vp_kernel_map_sort (the 9-bit plane-key grouping, kmap_sort.cu): perm
+    is a permutation of the live rows in stable key order, the sorted table
+    is table[perm], and forward / dgrad over (sorted table, perm) equal
     the unsorted launch (bit for bit when no tile splits or offset pairing
     regroups the fp32 sums; within one bf16 rounding otherwise)."""
     from paper_2012_13846_b200 import conv
@@ -199,8 +200,8 @@ def test_mask_sorted_rows_bitwise_equal(c, stride):
     p = perm.cpu().numpy()
     assert np.array_equal(np.sort(p), np.arange(n_out))
     assert torch.equal(ts, km.nbr[perm.long()])
-    masks = ((ts >= 0).int() * (1 << torch.arange(27, device=ts.device))).sum(1).cpu().numpy()
-    assert np.all(np.diff(masks) >= 0)
+    from parity_util import check_grouping
+    check_grouping(p, ts.cpu().numpy(), 1, "forward table")
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(n, c, device="cuda", generator=g).to(torch.bfloat16)
     W = conv.ConvWeights(torch.randn(27, c, c, device="cuda", generator=g) / (27 * c) ** 0.5)
