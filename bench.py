@@ -85,6 +85,7 @@ def parse():
     ap.add_argument("--blocks", type=int, default=1)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true", help="skip the per-kernel roofline timing (quick A/B runs)")
     ap.add_argument("--cpu-sample", type=int, default=64,
                     help="clouds per CPU-baseline step (default: the full 64-cloud C3 batch)")
     ap.add_argument("--profile-only", action="store_true", help="warm-up + a few steps, no JSON (for ncu)")
@@ -366,7 +367,7 @@ def main():
     e2e_value = world * args.batch * args.steps / (e2e_ms / 1e3)
 
     # ---------------- roofline of the dominant kernel (standalone, same data)
-    roof = roofline(tr, dev, CONFIG_TAG)
+    roof = None if args.no_roofline else roofline(tr, dev, CONFIG_TAG)
 
     if world > 1:
         dist.barrier()

@@ -624,16 +624,16 @@ static __global__ void split_reduce_kernel(const float* __restrict__ part, const
 }
 
 // split_reduce_kernel + the BN epilogue (bn_epi.cuh) for a bf16 output:
-// thread t always owns channels [(4t) % ND, +4) (ND divides 4096), so its
+// thread t always owns channels [(4t) % ND, +4) (ND divides 4 NT), so its
 // statistics accumulate in registers; the block then sums its threads in a
 // fixed order into partial row blockIdx.x.
 constexpr int kSplitEpiThreads = 1024;  // wide blocks: <= 148 partial rows, as many threads as the plain reduction
-template <int ND>
-__global__ void __launch_bounds__(kSplitEpiThreads)
+template <int ND, int NT = kSplitEpiThreads>
+__global__ void __launch_bounds__(NT)
 split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev, int64_t cap_out, int grid,
                         int max_split, const int32_t* __restrict__ perm, bf16* __restrict__ y, const BnEpi e) {
   ::vp::pdl_begin();
-  __shared__ float s_red[2][kSplitEpiThreads][4];
+  __shared__ float s_red[2][NT][4];
   __shared__ double s_fin[32][33];
   __shared__ unsigned int s_last;
   const int n_out = load_count(n_out_dev, cap_out);
@@ -644,8 +644,10 @@ split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev
   if (S <= 1 && !rows) {
     // the conv epilogue wrote the partial rows: finalize them here (one
     // 32-channel block per CTA) instead of in a separate launch
-    if (e.out_a && (int)blockIdx.x * 32 < ND)
-      bn_finalize_block(e.part, *e.nb, ND, n_out, e.mode, e.eps, e.rstd, e.out_a, e.out_b, blockIdx.x, s_fin);
+    if constexpr (NT == 1024) {  // the finalize needs 1024-thread blocks
+      if (e.out_a && (int)blockIdx.x * 32 < ND)
+        bn_finalize_block(e.part, *e.nb, ND, n_out, e.mode, e.eps, e.rstd, e.out_a, e.out_b, blockIdx.x, s_fin);
+    }
     return;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *e.nb = gridDim.x;
@@ -718,7 +720,7 @@ split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev
     s_red[1][threadIdx.x][c] = b[c];
   }
   __syncthreads();
-  constexpr int G = ND / 4, M = kSplitEpiThreads * 4 / ND;  // channel quads, threads per quad
+  constexpr int G = ND / 4, M = NT * 4 / ND;  // channel quads, threads per quad
   for (int idx = threadIdx.x; idx < 2 * ND; idx += blockDim.x) {
     const int hh = idx / ND, c = idx - hh * ND;
     float acc = 0.f;
@@ -734,8 +736,9 @@ split_reduce_epi_kernel(const float* __restrict__ part, const int32_t* n_out_dev
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int cb = 0; cb * 32 < ND; ++cb)
-    bn_finalize_block(e.part, (int)gridDim.x, ND, n_out, e.mode, e.eps, e.rstd, e.out_a, e.out_b, cb, s_fin);
+  if constexpr (NT == 1024)
+    for (int cb = 0; cb * 32 < ND; ++cb)
+      bn_finalize_block(e.part, (int)gridDim.x, ND, n_out, e.mode, e.eps, e.rstd, e.out_a, e.out_b, cb, s_fin);
 }
 
 }  // namespace vp

@@ -53,11 +53,14 @@ inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   ::vp::launch(kern, grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st, p);
   VP_CHECK_LAUNCH("conv_tc");
   if (rows_pass) {
+    // 256-thread blocks: schedulable next to the side-stream kernels (1024-thread
+    // blocks waited for half an SM); up to kBnPartRows partial rows
+    constexpr int NT = 256;
     const int64_t work = p.cap_out * ND / 4;
-    const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(work, kSplitEpiThreads), kNumSMs), 1);
+    const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(work, NT * 4), kBnPartRows), 1);
     BnEpi e = rows_epi;
     e.out_a = e.out_b = nullptr;  // finalized by the 32-channel-per-block kernel below
-    ::vp::launch(split_reduce_epi_kernel<ND>, (int)blocks, kSplitEpiThreads, 0, st, (const float*)part, p.n_out_dev,
+    ::vp::launch(split_reduce_epi_kernel<ND, NT>, (int)blocks, NT, 0, st, (const float*)part, p.n_out_dev,
                  p.cap_out, grid, p.max_split, p.perm, (bf16*)p.y, e);
     VP_CHECK_LAUNCH("split_reduce_epi");
     if (rows_epi.out_a) {

@@ -51,13 +51,20 @@ __device__ __forceinline__ int group_key(const int32_t* __restrict__ t, int K, i
   return key;
 }
 
-// keys of the block's live rows + the block's bucket histogram (bucket-major)
+constexpr int kScanTile = 4096;  // hist entries per block of the look-back scan (4 per thread)
+
+// keys of the block's live rows + the block's bucket histogram (bucket-major);
+// block 0 also zeroes the scan's look-back state for the next kernel
 __global__ void __launch_bounds__(kGroupThreads)
 group_hist_kernel(const int32_t* __restrict__ table, const int32_t* n_dev, int64_t cap, int K, int mode,
-                  uint16_t* __restrict__ keys, int32_t* __restrict__ hist, int nblocks) {
+                  uint16_t* __restrict__ keys, int32_t* __restrict__ hist, int nblocks, ScanState ss, int scan_tiles) {
   ::vp::pdl_begin();
   __shared__ int s_h[kGroupBuckets];
   const int n = load_count(n_dev, cap);
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < scan_tiles; i += blockDim.x) ss.status[i] = 0ull;
+    if (threadIdx.x == 0) *ss.counter = 0u;
+  }
   for (int b = threadIdx.x; b < kGroupBuckets; b += blockDim.x) s_h[b] = 0;
   __syncthreads();
   const int64_t r0 = (int64_t)blockIdx.x * kGroupTile;
@@ -74,22 +81,35 @@ group_hist_kernel(const int32_t* __restrict__ table, const int32_t* n_dev, int64
 }
 
 // exclusive scan of hist in place (bucket-major: bucket b's rows of block j
-// start at the sum over all (bucket < b) plus (bucket b, block < j))
-__global__ void __launch_bounds__(1024) group_scan_kernel(int32_t* hist, int total) {
+// start at the sum over all (bucket < b) plus (bucket b, block < j)):
+// single pass, kScanTile entries per block, decoupled look-back across tiles
+__global__ void __launch_bounds__(1024) group_scan_kernel(int32_t* hist, int total, ScanState ss) {
   ::vp::pdl_begin();
   __shared__ int s_warp[1024 / 32 + 1];
-  __shared__ int s_carry;
-  if (threadIdx.x == 0) s_carry = 0;
+  __shared__ int s_tile;
+  __shared__ long long s_prefix;
+  if (threadIdx.x == 0) s_tile = scan_next_tile(ss);
   __syncthreads();
-  for (int base = 0; base < total; base += 1024) {
-    const int i = base + threadIdx.x;
-    int tot;
-    const int v = i < total ? hist[i] : 0;
-    const int e = block_exclusive_scan<1024>(v, s_warp, &tot);
-    if (i < total) hist[i] = s_carry + e;
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry += tot;
-    __syncthreads();
+  const int tile = s_tile;
+  const int i0 = tile * kScanTile + threadIdx.x * 4;
+  int v[4], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[j] = i0 + j < total ? hist[i0 + j] : 0;
+    sum += v[j];
+  }
+  int tot;
+  const int excl = block_exclusive_scan<1024>(sum, s_warp, &tot);
+  if (threadIdx.x < 32) {
+    const long long p = scan_lookback_warp(ss, tile, tot);
+    if (threadIdx.x == 0) s_prefix = p;
+  }
+  __syncthreads();
+  int run = (int)s_prefix + excl;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (i0 + j < total) hist[i0 + j] = run;
+    run += v[j];
   }
 }
 
@@ -164,6 +184,8 @@ size_t vp_kernel_map_sort_ws_bytes(int64_t cap, int32_t K) {
   Carver c(nullptr, 0);
   c.take<uint16_t>(std::max<int64_t>(cap, 1));
   c.take<int32_t>(nblocks * kGroupBuckets);
+  c.take<unsigned int>(4);
+  c.take<unsigned long long>(ceil_div(nblocks * kGroupBuckets, kScanTile));
   return c.off;
 }
 
@@ -178,10 +200,15 @@ int vp_kernel_map_group(const int32_t* table, const int32_t* n_dev, int64_t cap,
   Carver c(ws, ws_bytes);
   uint16_t* keys = c.take<uint16_t>(cap);
   int32_t* hist = c.take<int32_t>((int64_t)nblocks * kGroupBuckets);
+  const int total = nblocks * kGroupBuckets;
+  const int scan_tiles = (int)ceil_div(total, kScanTile);
+  ScanState ss{c.take<unsigned int>(4), nullptr};
+  ss.status = c.take<unsigned long long>(scan_tiles);
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "kernel_map_group: workspace too small");
-  ::vp::launch(group_hist_kernel, nblocks, kGroupThreads, 0, st, table, n_dev, cap, K, key_mode, keys, hist, nblocks);
+  ::vp::launch(group_hist_kernel, nblocks, kGroupThreads, 0, st, table, n_dev, cap, K, key_mode, keys, hist, nblocks,
+               ss, scan_tiles);
   VP_CHECK_LAUNCH("map_group: hist");
-  ::vp::launch(group_scan_kernel, 1, 1024, 0, st, hist, nblocks * kGroupBuckets);
+  ::vp::launch(group_scan_kernel, scan_tiles, 1024, 0, st, hist, total, ss);
   VP_CHECK_LAUNCH("map_group: scan");
   ::vp::launch(group_scatter_kernel, nblocks, kGroupThreads, 0, st, (const uint16_t*)keys, n_dev, cap,
                (const int32_t*)hist, nblocks, perm);
