@@ -153,7 +153,8 @@ int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, co
 /* Neighbour-pattern row grouping (kmap_sort.cu): stable counting sort of
  * the live table rows by a 9-bit key of their 3^3 hit mask — key_mode 0:
  * which (dx, dy) columns hold a hit (stride-1 tables), 1: which dx / dy /
- * dz planes hold a hit (strided inverse tables) — into perm [n] (table row
+ * dz planes hold a hit (strided inverse tables), 2: the whole 27-bit mask
+ * (three stable 9-bit passes; ~1M-row levels) — into perm [n] (table row
  * order -> row id) and table_sorted [n, K] = table[perm].  Passing
  * (table_sorted, perm) to vp_conv_fwd / vp_conv_dgrad gives results
  * identical to (table, NULL) with far fewer active offsets per 128-row tile.

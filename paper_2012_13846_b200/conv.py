@@ -298,10 +298,12 @@ def _check_weights(t: SparseTensor, w: ConvWeights, shape: KernelShape):
         raise StructuralError("kernel shape dimension != tensor dimension")
 
 
-def sort_table(table: torch.Tensor, n_rows: int):
-    """Neighbour-mask row ordering (vp_kernel_map_sort): -> (perm, table[perm])
-    with rows grouped by their hit mask, so each 128-row tile of the implicit
-    GEMM touches few kernel offsets.  Results of the conv are unchanged."""
+def sort_table(table: torch.Tensor, n_rows: int, key_mode: int = 0):
+    """Neighbour-pattern row grouping (vp_kernel_map_group): -> (perm,
+    table[perm]) with rows grouped by a 9-bit key of their hit mask, so each
+    128-row tile of the implicit GEMM touches few kernel offsets.  key_mode
+    0 (columns) for neighbour tables, 1 (planes) for strided inverse tables.
+    Results of the conv are unchanged."""
     K = table.shape[1]
     cap = max(n_rows, 1)
     perm = torch.empty(cap, dtype=torch.int32, device=table.device)
@@ -309,12 +311,15 @@ def sort_table(table: torch.Tensor, n_rows: int):
     if n_rows == 0:
         return perm[:0], ts[:0]
     ws = _lib.workspace(_lib.query("vp_kernel_map_sort_ws_bytes", n_rows, K), table.device)
-    _lib.call("vp_kernel_map_sort", table.data_ptr(), None, n_rows, K, perm.data_ptr(), ts.data_ptr(), ws.data_ptr(),
-              ws.numel(), _lib.stream())
+    if n_rows >= FULL_MASK_ROWS and K <= 27:
+        key_mode = 2  # large tables: the full 27-bit mask (three passes) groups best
+    _lib.call("vp_kernel_map_group", table.data_ptr(), None, n_rows, K, int(key_mode), perm.data_ptr(), ts.data_ptr(),
+              ws.data_ptr(), ws.numel(), _lib.stream())
     return perm, ts
 
 
 SORT_MIN_ROWS = 1 << 17  # below this the sort's launches cost more than it saves
+FULL_MASK_ROWS = 1 << 18  # from here on the grouping sorts by the whole hit mask (key mode 2)
 
 
 def _sortable(table: torch.Tensor) -> bool:
@@ -412,7 +417,7 @@ def sparse_conv_backward(t: SparseTensor, w: ConvWeights, shape: KernelShape, st
         table, flip = km.inverse(), False
     perm = None
     if _sortable(table):  # the flipped table's hit masks are bit-reversed: same grouping
-        perm, table = sort_table(table, len(t))
+        perm, table = sort_table(table, len(t), 0 if flip else 1)
     gi = conv_dgrad_raw(g, w, table, len(t), flip, perm=perm, math=math)
     gw = conv_wgrad_raw(t.features, g, tuple(w.matrices.shape), km)
     return gi, gw
@@ -434,7 +439,7 @@ def sparse_conv_transposed(t: SparseTensor, w: ConvWeights, shape: KernelShape, 
     km = _kernel_map4(fine4, t.coords4, shape, fine_stride, t.dim, with_pairs=False)
     inv = km.inverse()  # [N_fine, K] -> coarse row
     # y[v] = sum_k W_k x[inv[v,k]] : a forward conv over the inverse table
-    perm, tbl = sort_table(inv, fine4.shape[0]) if _sortable(inv) else (None, inv)
+    perm, tbl = sort_table(inv, fine4.shape[0], 1) if _sortable(inv) else (None, inv)
     y = conv_forward_raw(t.features, w, tbl, fine4.shape[0], perm=perm)
     return SparseTensor(fine4, y, fine_stride, _trusted=True, _dim=t.dim)
 

@@ -16,10 +16,13 @@
 // column key 13.7; level-0->1 inverse table: 25.9, 2.0, plane key 2.2):
 //   key 0 "columns": which of the 9 (dx, dy) columns hold a hit;
 //   key 1 "planes" : which dx / dy / dz planes hold a hit (3 + 3 + 3 bits).
-// Stable counting sort over the LIVE rows into 512 buckets, three passes
-// (block histograms; bucket-major exclusive scan; per-warp ordered scatter
-// with __match_any_sync ranks) plus a coalesced row permute.  No library
-// sort; the order depends only on the table -> deterministic.
+// Stable counting sort over the LIVE rows into 512 buckets, three kernels
+// (block histograms; bucket-major look-back scan; per-warp ordered scatter
+// with __match_any_sync ranks) plus a coalesced row permute.  key 2 "mask"
+// runs three such stable passes over 9-bit digits of the full 27-bit mask
+// (LSD) — the order of a stable sort by the whole mask, which groups best
+// when levels hold ~1M rows (C2 / C5).  No library sort; the order depends
+// only on the table -> deterministic.
 #include "common.cuh"
 
 namespace vp {
@@ -55,9 +58,20 @@ constexpr int kScanTile = 4096;  // hist entries per block of the look-back scan
 
 // keys of the block's live rows + the block's bucket histogram (bucket-major);
 // block 0 also zeroes the scan's look-back state for the next kernel
+// full-mask mode (key_mode 2): masks[r] = the row's 27-bit hit mask, and the
+// key of pass p is bits [9p, 9p + 9) of the mask of the row at position i of
+// the previous pass's order (LSD radix: three stable passes = the order of a
+// stable sort by the whole mask)
+__device__ __forceinline__ uint32_t full_mask(const int32_t* __restrict__ t, int K) {
+  uint32_t m = 0;
+  for (int k = 0; k < K && k < 27; ++k) m |= (uint32_t)(__ldg(t + k) >= 0) << k;
+  return m;
+}
+
 __global__ void __launch_bounds__(kGroupThreads)
 group_hist_kernel(const int32_t* __restrict__ table, const int32_t* n_dev, int64_t cap, int K, int mode,
-                  uint16_t* __restrict__ keys, int32_t* __restrict__ hist, int nblocks, ScanState ss, int scan_tiles) {
+                  uint16_t* __restrict__ keys, int32_t* __restrict__ hist, int nblocks, ScanState ss, int scan_tiles,
+                  uint32_t* __restrict__ masks, const int32_t* __restrict__ order_in, int shift) {
   ::vp::pdl_begin();
   __shared__ int s_h[kGroupBuckets];
   const int n = load_count(n_dev, cap);
@@ -71,7 +85,19 @@ group_hist_kernel(const int32_t* __restrict__ table, const int32_t* n_dev, int64
   for (int i = threadIdx.x; i < kGroupTile; i += blockDim.x) {
     const int64_t r = r0 + i;
     if (r < n) {
-      const int key = group_key(table + r * K, K, mode);
+      int key;
+      if (mode == 2) {  // position r of the previous pass's order
+        uint32_t m;
+        if (order_in == nullptr) {
+          m = full_mask(table + r * K, K);
+          masks[r] = m;
+        } else {
+          m = masks[order_in[r]];
+        }
+        key = (int)((m >> shift) & (kGroupBuckets - 1));
+      } else {
+        key = group_key(table + r * K, K, mode);
+      }
       keys[r] = (uint16_t)key;
       atomicAdd(&s_h[key], 1);  // a count: order-independent
     }
@@ -118,7 +144,8 @@ __global__ void __launch_bounds__(1024) group_scan_kernel(int32_t* hist, int tot
 // bucket) bases = the block's scanned base + the earlier warps' counts
 __global__ void __launch_bounds__(kGroupThreads)
 group_scatter_kernel(const uint16_t* __restrict__ keys, const int32_t* n_dev, int64_t cap,
-                     const int32_t* __restrict__ offs, int nblocks, int32_t* __restrict__ perm) {
+                     const int32_t* __restrict__ offs, int nblocks, int32_t* __restrict__ perm,
+                     const int32_t* __restrict__ order_in) {
   ::vp::pdl_begin();
   constexpr int W = kGroupThreads / 32, RW = kGroupTile / W;
   __shared__ int s_cnt[W][kGroupBuckets];
@@ -151,7 +178,7 @@ group_scatter_kernel(const uint16_t* __restrict__ keys, const int32_t* n_dev, in
     const unsigned m = __match_any_sync(0xffffffffu, key);
     if (live) {
       const int pos = s_cnt[warp][key] + __popc(m & lt);
-      perm[pos] = (int32_t)r;
+      perm[pos] = order_in ? order_in[r] : (int32_t)r;
     }
     __syncwarp();
     if (live && (m & lt) == 0) s_cnt[warp][key] += __popc(m);  // the group's leader advances the base
@@ -186,6 +213,8 @@ size_t vp_kernel_map_sort_ws_bytes(int64_t cap, int32_t K) {
   c.take<int32_t>(nblocks * kGroupBuckets);
   c.take<unsigned int>(4);
   c.take<unsigned long long>(ceil_div(nblocks * kGroupBuckets, kScanTile));
+  c.take<uint32_t>(std::max<int64_t>(cap, 1));  // full-mask mode: masks + an order buffer
+  c.take<int32_t>(std::max<int64_t>(cap, 1));
   return c.off;
 }
 
@@ -193,7 +222,7 @@ int vp_kernel_map_group(const int32_t* table, const int32_t* n_dev, int64_t cap,
                         int32_t* perm, int32_t* table_sorted, void* ws, size_t ws_bytes, vp_stream_t stream) {
   cudaStream_t st = (cudaStream_t)stream;
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
-  VP_REQUIRE(key_mode == 0 || key_mode == 1, VP_EVALIDATION, "kernel_map_group: key mode must be 0 or 1");
+  VP_REQUIRE(key_mode >= 0 && key_mode <= 2, VP_EVALIDATION, "kernel_map_group: key mode must be 0, 1 or 2");
   if (cap <= 0) return VP_OK;
   VP_REQUIRE(cap < (1ll << 31), VP_EVALIDATION, "kernel_map_group: too many rows");
   const int nblocks = (int)ceil_div(cap, kGroupTile);
@@ -204,15 +233,29 @@ int vp_kernel_map_group(const int32_t* table, const int32_t* n_dev, int64_t cap,
   const int scan_tiles = (int)ceil_div(total, kScanTile);
   ScanState ss{c.take<unsigned int>(4), nullptr};
   ss.status = c.take<unsigned long long>(scan_tiles);
+  uint32_t* masks = nullptr;
+  int32_t* order = nullptr;
+  if (key_mode == 2) {
+    masks = c.take<uint32_t>(cap);
+    order = c.take<int32_t>(cap);
+  }
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "kernel_map_group: workspace too small");
-  ::vp::launch(group_hist_kernel, nblocks, kGroupThreads, 0, st, table, n_dev, cap, K, key_mode, keys, hist, nblocks,
-               ss, scan_tiles);
-  VP_CHECK_LAUNCH("map_group: hist");
-  ::vp::launch(group_scan_kernel, scan_tiles, 1024, 0, st, hist, total, ss);
-  VP_CHECK_LAUNCH("map_group: scan");
-  ::vp::launch(group_scatter_kernel, nblocks, kGroupThreads, 0, st, (const uint16_t*)keys, n_dev, cap,
-               (const int32_t*)hist, nblocks, perm);
-  VP_CHECK_LAUNCH("map_group: scatter");
+  // one pass (9-bit key) or three stable LSD passes over the 27-bit mask,
+  // alternating between `order` and `perm` so the last pass lands in perm
+  const int passes = key_mode == 2 ? 3 : 1;
+  int32_t* bufs[2] = {perm, order};  // pass p writes bufs[p % 2]: the last (p = 0 or 2) lands in perm
+  for (int ps = 0; ps < passes; ++ps) {
+    const int32_t* in = ps == 0 ? nullptr : bufs[(ps - 1) % 2];
+    int32_t* out = bufs[ps % 2];
+    ::vp::launch(group_hist_kernel, nblocks, kGroupThreads, 0, st, table, n_dev, cap, K, key_mode, keys, hist, nblocks,
+                 ss, scan_tiles, masks, in, 9 * ps);
+    VP_CHECK_LAUNCH("map_group: hist");
+    ::vp::launch(group_scan_kernel, scan_tiles, 1024, 0, st, hist, total, ss);
+    VP_CHECK_LAUNCH("map_group: scan");
+    ::vp::launch(group_scatter_kernel, nblocks, kGroupThreads, 0, st, (const uint16_t*)keys, n_dev, cap,
+                 (const int32_t*)hist, nblocks, out, in);
+    VP_CHECK_LAUNCH("map_group: scatter");
+  }
   const int pblocks = (int)std::min<int64_t>(ceil_div(cap * K, 256), grid_cap(16));
   ::vp::launch(permute_rows_kernel, pblocks, 256, 0, st, table, (const int32_t*)perm, n_dev, cap, K, table_sorted);
   VP_CHECK_LAUNCH("map_group: permute");

@@ -288,6 +288,9 @@ class SparseResNetTrainer:
     # than the 1.3-1.7x fewer active offsets per tile save (tools/sweep_c2.py)
     SORT_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_MIN_ROWS", 1 << 18))
     SORT_INV_MIN_ROWS = int(__import__("os").environ.get("VP_SORT_INV_MIN_ROWS", 0))
+    # forward tables of levels with at least this many rows (capacity) group by
+    # the full 27-bit mask (three passes) instead of the 9-bit column key
+    FULL_MASK_ROWS = int(__import__("os").environ.get("VP_FULL_MASK_ROWS", 1 << 18))
     # levels whose forward tables are sorted regardless of size
     SORT_LEVELS = tuple(int(v) for v in __import__("os").environ.get("VP_SORT_LEVELS", "1,2,3").split(",") if v)
     # prefetch mode: fork the next batch's integer stage at the start of the
@@ -423,7 +426,8 @@ class SparseResNetTrainer:
             self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
                     m.inv.data_ptr(), m.src.cap, st)
         if m.perm is not None:
-            self._c("vp_kernel_map_group", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K, 0, m.perm.data_ptr(),
+            self._c("vp_kernel_map_group", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
+                    2 if m.dst.cap >= self.FULL_MASK_ROWS else 0, m.perm.data_ptr(),
                     m.nbr_s.data_ptr(), m.sort_ws.data_ptr(), m.sort_ws.numel(), st)
         if m.iperm is not None:
             self._c("vp_kernel_map_group", m.inv.data_ptr(), m.src.n.data_ptr(), m.src.cap, self.K, 1,

@@ -83,7 +83,7 @@ def conv_plan(t: SparseTensor, shape: C.KernelShape, stride) -> ConvPlan:
         dtab, flip = km.inverse(), False
     dperm = None
     if C._sortable(dtab):
-        dperm, dtab = C.sort_table(dtab, n_in)
+        dperm, dtab = C.sort_table(dtab, n_in, 0 if flip else 1)
     plan = ConvPlan(out4, ns, n_in, n_out, km, ftab, fperm, dtab, flip, dperm)
     t.plans[key] = plan
     return plan
@@ -109,7 +109,7 @@ def transposed_plan(t: SparseTensor, shape: C.KernelShape, stride, out: SparseTe
     else:
         km = C._kernel_map4(out.coords4, t.coords4, shape, fine_stride, t.dim)
     inv = km.inverse()  # [N_fine, K] -> coarse row
-    fperm, ftab = C.sort_table(inv, len(out)) if C._sortable(inv) else (None, inv)
+    fperm, ftab = C.sort_table(inv, len(out), 1) if C._sortable(inv) else (None, inv)
     # backward: grad_x[u] = sum_k Wt_k^T g[nbr[u, k]]  (nbr of the strided map, no flip)
     swapped = C.KernelMap(km.offsets, km.nbr, km.pair_out, km.pair_in, km.pair_ptr, n_in=len(t))
     plan = ConvPlan(out.coords4, fine_stride, len(t), len(out), swapped, ftab, fperm, km.nbr, False, None)

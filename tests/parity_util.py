@@ -84,10 +84,13 @@ def ref_integer_stage(points, offsets, res, nlev=5):
 
 
 def group_key(table, mode):
-    """The 9-bit grouping key of csrc/kmap_sort.cu for 3^3 tables: mode 0 =
-    which (dx, dy) columns hold a hit, mode 1 = which dx / dy / dz planes."""
+    """The grouping key of csrc/kmap_sort.cu for 3^3 tables: mode 0 = which
+    (dx, dy) columns hold a hit, 1 = which dx / dy / dz planes, 2 = the whole
+    27-bit mask."""
     hit = np.asarray(table) >= 0
     n = hit.shape[0]
+    if mode == 2:  # the whole hit mask
+        return (hit.astype(np.int64) << np.arange(hit.shape[1], dtype=np.int64)).sum(1)
     if mode == 0:
         bits = hit.reshape(n, 9, 3).any(2)
     else:
@@ -138,7 +141,9 @@ def check_map(m, pairs, what):
     if exp_inv is not None:
         np.testing.assert_array_equal(m.inv[:ns].cpu().numpy(), exp_inv, err_msg=f"{what}: inverse table")
     if m.perm is not None:
-        _check_perm_table(m.perm, m.nbr_s, exp_nbr, nd, f"{what} forward", mode=0)
+        from paper_2012_13846_b200 import model as _model
+        fmode = 2 if m.dst.cap >= _model.SparseResNetTrainer.FULL_MASK_ROWS else 0
+        _check_perm_table(m.perm, m.nbr_s, exp_nbr, nd, f"{what} forward", mode=fmode)
     if m.iperm is not None:
         _check_perm_table(m.iperm, m.inv_s, exp_inv, ns, f"{what} inverse", mode=1)
     return int(exp_ptr[-1])

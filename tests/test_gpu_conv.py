@@ -182,7 +182,8 @@ def test_transposed_conv_adjoint():
 @pytest.mark.parametrize("c", [32, 128, 256])
 @pytest.mark.parametrize("stride", [1, 2])
 def test_mask_sorted_rows_bitwise_equal(c, stride):
-    """vp_kernel_map_sort (the 9-bit plane-key grouping, kmap_sort.cu): perm
+    """vp_kernel_map_group (9-bit key grouping, kmap_sort.cu; column key for
+    neighbour tables, plane key for strided inverse tables): perm
     is a permutation of the live rows in stable key order, the sorted table
     is table[perm], and forward / dgrad over (sorted table, perm) equal
     the unsorted launch (bit for bit when no tile splits or offset pairing
@@ -201,7 +202,7 @@ def test_mask_sorted_rows_bitwise_equal(c, stride):
     assert np.array_equal(np.sort(p), np.arange(n_out))
     assert torch.equal(ts, km.nbr[perm.long()])
     from parity_util import check_grouping
-    check_grouping(p, ts.cpu().numpy(), 1, "forward table")
+    check_grouping(p, ts.cpu().numpy(), 0, "forward table")
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(n, c, device="cuda", generator=g).to(torch.bfloat16)
     W = conv.ConvWeights(torch.randn(27, c, c, device="cuda", generator=g) / (27 * c) ** 0.5)
@@ -213,7 +214,8 @@ def test_mask_sorted_rows_bitwise_equal(c, stride):
         tab, flip = km.nbr, True
     else:
         tab, flip = km.inverse(), False
-    ip, its = conv.sort_table(tab, n)
+    ip, its = conv.sort_table(tab, n, 0 if flip else 1)
+    check_grouping(ip.cpu().numpy().astype(np.int64), its.cpu().numpy(), 0 if flip else 1, "dgrad table")
     d0 = conv.conv_dgrad_raw(gy, W, tab, n, flip)
     d1 = conv.conv_dgrad_raw(gy, W, its, n, flip, perm=ip)
     torch.testing.assert_close(d1.float(), d0.float(), rtol=1e-2, atol=1e-2)
@@ -403,3 +405,21 @@ def test_tf32_mode(cin, cout, stride):
     bgi, _ = O.sparse_conv_backward(coords, np.abs(xr), (1, 1, 1), np.abs(wr), off, stride, np.abs(gy.astype(np.float64)))
     ei = np.abs(gi.cpu().numpy() - rgi)
     assert (ei <= 2e-3 * bgi + 1e-6).all(), (ei / (bgi + 1e-9)).max()
+
+
+def test_full_mask_grouping_is_the_stable_mask_sort():
+    """key mode 2 (three stable 9-bit LSD passes) orders the live rows
+    exactly like a stable argsort by the whole 27-bit hit mask."""
+    from paper_2012_13846_b200 import _lib, conv
+    from paper_2012_13846_b200.tensor import SparseTensor
+    pts, offs = O.synthetic_batch(150, 2048, 64, seed=5, dtype=np.float32)
+    c0, _ = O.voxelize_batch(pts.astype(np.float64), offs, 1.0, 64)
+    assert len(c0) >= conv.FULL_MASK_ROWS
+    t = SparseTensor(c0, np.zeros((len(c0), 1)), (1, 1, 1))
+    km = conv._kernel_map4(t.coords4, t.coords4, conv.KernelShape.hypercubic(3, 3), (1, 1, 1), 3, with_pairs=False)
+    n = len(c0)
+    perm, ts = conv.sort_table(km.nbr, n)  # >= FULL_MASK_ROWS: mode 2
+    nb = km.nbr[:n].cpu().numpy()
+    mask = ((nb >= 0).astype(np.int64) << np.arange(27, dtype=np.int64)).sum(1)
+    np.testing.assert_array_equal(perm.cpu().numpy(), np.argsort(mask, kind="stable"))
+    assert torch.equal(ts[:n], km.nbr[perm.long()][:n])

@@ -80,12 +80,12 @@ def main():
             print(json.dumps(rec), flush=True)
             out.write(json.dumps(rec) + "\n")
             inv = km.inverse() if stride > 1 else None
-            # neighbour-mask row ordering (vp_kernel_map_sort), as the training engine uses it
+            # neighbour-pattern row grouping (vp_kernel_map_group), as the training engine uses it
             fwd_perm, fwd_tbl = conv.sort_table(km.nbr, n_out) if a.sort else (None, km.nbr)
             if inv is None:
                 dg_perm, dg_tbl = fwd_perm, fwd_tbl
             else:
-                dg_perm, dg_tbl = conv.sort_table(inv, n) if a.sort else (None, inv)
+                dg_perm, dg_tbl = conv.sort_table(inv, n, 1) if a.sort else (None, inv)
             if a.sort:
                 ts = timeit(lambda: conv.sort_table(km.nbr, n_out), a.iters)
                 rec_sort = {"mode": f"map_sort_s{stride}", "N": n_out, "us": round(ts * 1e6, 2)}
