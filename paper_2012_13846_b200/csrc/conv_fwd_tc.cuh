@@ -121,8 +121,14 @@ __device__ __forceinline__ int split_count(int ntiles, int grid, int max_split) 
   return s > max_split ? max_split : s;
 }
 
-template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL, int TT = 1, int MODE = 0>
-__global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_constant__ FwdParams p) {
+// PW producer warps (4, or 8 for the small-row tiles: the gathers are bound
+// by cp.async issue per warp); then 4 epilogue warps and the MMA warp
+template <int PW>
+constexpr int tc_threads() { return 32 * PW + kTcEpi + 32; }
+
+template <int KD, int ND, bool BMN, int CPS, int RB, bool TBL, int TT = 1, int MODE = 0, int PW = 4>
+__global__ void __launch_bounds__(tc_threads<PW>(), CPS) conv_tc_kernel(const __grid_constant__ FwdParams p) {
+  constexpr int PROD = 32 * PW, RPT = 32 / PW;  // producer threads; rows per thread per 128-row tile
   ::vp::pdl_begin();
   using C = FwdTC<KD, ND, BMN, CPS, RB, TT, MODE>;
   constexpr bool TF32 = C::TF32;
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
 
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      tc::mbar_init(&full[s], kTcProd);
+      tc::mbar_init(&full[s], PROD);
       tc::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < C::ACC; ++a) {
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
     }
     tc::fence_mbar_init();
   }
-  if (warp == 8) tc::tmem_alloc(s_tmem, C::TMEM_COLS);
+  if (warp == PW + 4) tc::tmem_alloc(s_tmem, C::TMEM_COLS);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
   float bs1[ND / 32], bs2[ND / 32];
 #pragma unroll
   for (int j = 0; j < ND / 32; ++j) bs1[j] = bs2[j] = 0.f;
-  if (warp < 4) {
+  if (warp < PW) {
     // ============================ producers ============================
     constexpr bool tbl = TBL;
     // stage work item w's [rows, K] table block into buffer `buf` (thread 0):
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       const int rows = min(TR, n_out - tile * TR);
       const int32_t* tt = s_tbl + (ii & 1) * TR * K;  // this item's staged table
       if (tbl) tc::mbar_wait(&tbar[ii & 1], (ii >> 1) & 1);  // landed (the scan waited too): makes it visible here
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(PROD) : "memory");
       // the epilogue warps scanned this item's offset activity (scan_item)
       if (warp == 0 && lane == 0) {
         tc::mbar_wait(&sready[ii & 1], (ii >> 1) & 1);
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
         // every producer is past tile ii-1 (barrier below at ii-1's end): its buffer is free
         if (tbl && w + (int)gridDim.x < total) issue_tbl(w + gridDim.x, (ii + 1) & 1);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(PROD) : "memory");
       const int u0 = s_work[0], nun = s_work[1], na = s_work[2];
       const int neff = nun > 0 ? nun : 1;
       // unit -> (offset of A's first half / whole row, second half, 64-col slice)
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       // r_i = r0 + 4i, i < 8.  Row r_i's chunk lands at a_s + r_i*128 +
       // ((q ^ (r_i & 7)) << 4) and r_i & 7 = (lane/8) + 4*(i&1).
       const int q = lane & 7;
-      const int r0 = warp * 32 + (lane >> 3);
+      const int r0 = warp * (128 / PW) + (lane >> 3);
       const uint32_t a_off0 = r0 * 128 + ((q ^ (lane >> 3)) << 4);
       const uint32_t a_off1 = r0 * 128 + ((q ^ ((lane >> 3) + 4)) << 4);
       const uint32_t tt_s = tc::smem_u32(tt) + r0 * K * 4;  // row r0's staged table entries
@@ -285,16 +291,16 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
             const int ch = C::PAIR ? (q & 3) * 8 : cs * 64 + q * 8;  // first element of this lane's 16 B chunk
             const bool chv = ch < kreal;                               // padded widths: zero chunk
             const char* xq = xb + 2 * (chv ? ch : 0);
-            int vr[8];
+            int vr[RPT];
             const bool noa = p.dbg & 4;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < RPT; ++i) {
               if (kq < 0 || noa) vr[i] = -1;
               else if (TBL) vr[i] = tc::lds_s32(tt_s + (uint32_t)((t * 128 * K + i * 4 * K + col) * 4));
               else vr[i] = (t * 128 + r0 + 4 * i < rows) ? __ldg(trow0 + (t * 128 + i * 4) * K + col) : -1;
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < RPT; ++i) {
               const int v = vr[i];
               tc::cp_async16(a_s + ((i & 1) ? a_off1 : a_off0) + i * 512,
                              xq + (int64_t)(v > 0 ? v : 0) * (kreal * 2), (v >= 0 && chv) ? 16 : 0);
@@ -311,14 +317,15 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
             const bool bcv = bc < kreal;
             const bf16* src = p.w + ((int64_t)k * nreal + n0) * kreal + (bcv ? bc : 0);
             const uint32_t dst = b_s + n0 * 128 + ((qq ^ (n0 & 7)) << 4);
+            constexpr int NR = PROD / 8;  // B rows per pass
 #pragma unroll
-            for (int j = 0; j < ND / 16; ++j) {
-              const bool ok = bcv && n0 + j * 16 < nreal;
-              tc::cp_async16(dst + j * 2048, ok ? src + (int64_t)j * 16 * kreal : p.w, ok ? 16 : 0);
+            for (int j = 0; j < ND / NR; ++j) {
+              const bool ok = bcv && n0 + j * NR < nreal;
+              tc::cp_async16(dst + j * NR * 128, ok ? src + (int64_t)j * NR * kreal : p.w, ok ? 16 : 0);
             }
           } else {  // B(n, kk) = W[k][kk][n]: row kk of W_k is N-contiguous (MN-major)
             constexpr int NCHK = ND / 8;        // 16 B chunks per kk row
-            constexpr int KKS = kTcProd / NCHK;  // kk rows per pass
+            constexpr int KKS = PROD / NCHK;  // kk rows per pass
             const int jn = tid % NCHK, kk0 = tid / NCHK;
 #pragma unroll
             for (int j = 0; j < 64 / KKS; ++j) {
@@ -346,10 +353,10 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
       }
     }
     tc::cp_async_wait<0>();
-  } else if (warp < 8) {
+  } else if (warp < PW + 4) {
     // ============================ epilogue ============================
-    const int ep = warp - 4;
-    const int etid = tid - 128;
+    const int ep = warp - PW;
+    const int etid = tid - PROD;
     // Offset-activity scan of the CTA's iiw-th item (work item wi) into buffer
     // iiw & 1: OR of the rows' neighbour-hit masks -> ascending active-offset
     // list + count, then sready.  Run here, in the epilogue warps' slack, so
@@ -564,12 +571,12 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_tc_kernel(const __grid_c
     }
   }
   __syncthreads();
-  if (warp == 8) tc::tmem_dealloc(tmem, C::TMEM_COLS);
-  if (epi && warp >= 4 && warp < 8) {
+  if (warp == PW + 4) tc::tmem_dealloc(tmem, C::TMEM_COLS);
+  if (epi && warp >= PW && warp < PW + 4) {
     // the 4 warps' sums in warp order -> this CTA's partial row (the stage
     // ring is free: every copy and MMA has completed)
     float* red = reinterpret_cast<float*>(smem);  // [4][2][ND]
-    const int ep = warp - 4, etid = tid - 128;
+    const int ep = warp - PW, etid = tid - PROD;
 #pragma unroll
     for (int j = 0; j < ND / 32; ++j) {
       red[(ep * 2 + 0) * ND + 32 * j + lane] = bs1[j];

@@ -13,12 +13,12 @@ namespace vp {
 
 constexpr int kMaxSplit = 16;
 
-template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1, int MODE = 0>
+template <int KD, int ND, bool BMN, int CPS, int RB, int TT = 1, int MODE = 0, int PW = 4>
 inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   using C = FwdTC<KD, ND, BMN, CPS, RB, TT, MODE>;
   const bool tbl = p0.K <= kTblK && ((uintptr_t)p0.table & 15) == 0;
-  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true, TT, MODE>
-                  : conv_tc_kernel<KD, ND, BMN, CPS, RB, false, TT, MODE>;
+  auto kern = tbl ? conv_tc_kernel<KD, ND, BMN, CPS, RB, true, TT, MODE, PW>
+                  : conv_tc_kernel<KD, ND, BMN, CPS, RB, false, TT, MODE, PW>;
   static_assert(C::SMEM_MAX <= 227 * 1024, "conv_tc: shared memory over the per-CTA limit");
   static bool attr_t = false, attr_f = false;  // immutable per-instantiation attribute cache
   bool& attr = tbl ? attr_t : attr_f;
@@ -50,7 +50,7 @@ inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
   static const int dbg = getenv("VP_CONV_DBG") ? atoi(getenv("VP_CONV_DBG")) : 0;
   p.dbg = dbg;
   p.trace = g_conv_trace_host;
-  ::vp::launch(kern, grid, kTcThreads, C::smem_bytes(p0.K, p.stage_tbl), st, p);
+  ::vp::launch(kern, grid, tc_threads<PW>(), C::smem_bytes(p0.K, p.stage_tbl), st, p);
   VP_CHECK_LAUNCH("conv_tc");
   if (rows_pass) {
     // 256-thread blocks: schedulable next to the side-stream kernels (1024-thread
