@@ -138,14 +138,36 @@ int vp_kernel_map(const int32_t* in, const int32_t* n_in_dev, int64_t cap_in,
                   int32_t* nbr, int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr,
                   void* ws, size_t ws_bytes, vp_stream_t stream);
 /* Dense-grid index for bounded lattices (batch < B, every axis a multiple
- * of s in [0, R*s)): cells [B*R^3] int32, initialised to 0x7fffffff once by
- * the caller; vp_grid_set writes each row's index (clear=0) or restores the
- * empty value for exactly those cells (clear=1) so the grid is reusable.
+ * of s in [0, R*s)): `cells` is vp_grid_words(B, R) int32 words — the cell
+ * table [B*R^3] (cell -> row) followed by an occupancy bitmap
+ * [ceil(B*R^3/32)] — initialised once with vp_grid_init (zeroes the bitmap;
+ * cell values are meaningful only where their bit is set).  vp_grid_set
+ * writes each row's cell and bit (clear=0) or zeroes exactly the bitmap
+ * words of those rows (clear=1), so the grid is reusable.  The probe reads
+ * the bitmap for every neighbour and the cell only for hits.
  * vp_kernel_map_grid is build_kernel_map with the grid as the index: the
  * same nbr / pair outputs, bit-exact with the hash path on such lattices. */
+int64_t vp_grid_words(int32_t B, int32_t R);
+int vp_grid_init(int32_t* cells, int32_t B, int32_t R, vp_stream_t stream);
 int vp_grid_set(const int32_t* coords, const int32_t* n_dev, int64_t cap, int32_t* cells, int32_t B,
                 int32_t R, int32_t s, int32_t clear, vp_stream_t stream);
 size_t vp_kernel_map_grid_ws_bytes(int64_t cap_out, int32_t K);
+/* Lattice kernel map for the operator API (build_kernel_map on rows that
+ * sit on one bounded lattice of spacing s; conv.py:149-183):
+ * vp_coords_bbox writes bbox[9] (device int32) = the minimum over both row
+ * sets of (b, x, y, z, -b, -x, -y, -z) and 1 if every row is on the spacing
+ * lattice else 0; the caller reads it back, picks lattice_host =
+ * {B, R, ox, oy, oz} (origin a multiple of s, R^3 cells per batch) and calls
+ * vp_kernel_map_lattice: grid set + probe + scan + emit + clear on `grid`
+ * (vp_grid_words(B, R) int32 words, bitmap zero on entry and on return).
+ * Outputs and ws (vp_kernel_map_grid_ws_bytes) as vp_kernel_map_grid;
+ * results identical to vp_kernel_map. */
+int vp_coords_bbox(const int32_t* a, int64_t n_a, const int32_t* b, int64_t n_b, int32_t s, int32_t* bbox,
+                   vp_stream_t stream);
+int vp_kernel_map_lattice(const int32_t* in, int64_t n_in, const int32_t* out, int64_t n_out,
+                          const int32_t* offsets_host, int32_t K, int32_t s, const int32_t* lattice_host,
+                          int32_t* grid, int64_t grid_words, int32_t* nbr, int32_t* pair_in, int32_t* pair_out,
+                          int32_t* pair_ptr, void* ws, size_t ws_bytes, vp_stream_t stream);
 int vp_kernel_map_grid(const int32_t* cells, int32_t B, int32_t R, int32_t s, const int32_t* out,
                        const int32_t* n_out_dev, int64_t cap_out, const int32_t* offsets_host, int32_t K,
                        const int32_t* in_stride_host3, int32_t* nbr, int32_t* pair_in, int32_t* pair_out,

@@ -58,6 +58,10 @@ SIGNATURES = {
     "vp_kernel_map_brick_ws_bytes": (SZ, [I64, I32]),
     "vp_kernel_map_brick": (C.c_int, [P, I64, I32, I32, I32, P, P, I64, P, I32, P, P, P, P, P, P, SZ, P]),
     "vp_kernel_map_inverse": (C.c_int, [P, P, I64, I32, P, I64, P]),
+    "vp_grid_words": (I64, [I32, I32]),
+    "vp_coords_bbox": (C.c_int, [P, I64, P, I64, I32, P, P]),
+    "vp_kernel_map_lattice": (C.c_int, [P, I64, P, I64, P, I32, I32, P, P, I64, P, P, P, P, P, SZ, P]),
+    "vp_grid_init": (C.c_int, [P, I32, I32, P]),
     "vp_grid_set": (C.c_int, [P, P, I64, P, I32, I32, I32, I32, P]),
     "vp_kernel_map_grid_ws_bytes": (SZ, [I64, I32]),
     "vp_kernel_map_grid": (C.c_int, [P, I32, I32, I32, P, P, I64, P, I32, P, P, P, P, P, P, SZ, P]),

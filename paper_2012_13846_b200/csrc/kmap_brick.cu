@@ -114,7 +114,7 @@ constexpr int kBrickSmemK = 32;
 __global__ void __launch_bounds__(kBrickTile)
 map_probe_brick_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t cap_out, BrickSpec g,
                        const __grid_constant__ BrickOffsets offs, int K, int32_t* __restrict__ nbr, int32_t* counts,
-                       int ntiles) {
+                       int ntiles, uint32_t* __restrict__ masks) {
   ::vp::pdl_begin();
   __shared__ int s_nbr[kBrickTile * (kBrickSmemK + 1)];
   __shared__ int s_cnt[kBrickTile / 32][VP_MAX_OFFSETS];
@@ -135,6 +135,7 @@ map_probe_brick_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, i
   }
   const unsigned R = (unsigned)g.R;
   constexpr int KB = 27;
+  uint32_t hitm = 0;
   for (int kb = 0; kb < K; kb += KB) {
     int cid[KB], loc[KB];
 #pragma unroll
@@ -159,6 +160,7 @@ map_probe_brick_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, i
       const int k = kb + j;
       if (k >= K) break;
       const int x = v[j] == kBrickEmpty ? -1 : v[j];
+      if (k < 32 && x >= 0) hitm |= 1u << k;
       if (staged) s_nbr[tid * (kBrickSmemK + 1) + k] = x;
       else if (valid) nbr[(u0 + tid) * K + k] = x;
       const unsigned m = __ballot_sync(0xffffffffu, x >= 0);
@@ -171,6 +173,7 @@ map_probe_brick_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, i
     for (int rr = warp; rr < rows; rr += kBrickTile / 32)
       if (lane < K) dst[rr * K + lane] = s_nbr[rr * (kBrickSmemK + 1) + lane];
   }
+  if (masks && valid) masks[u0 + tid] = hitm;
   for (int k = tid; k < K; k += kBrickTile) {
     int c = 0;
 #pragma unroll
@@ -182,7 +185,7 @@ map_probe_brick_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, i
 // defined in kmap.cu (shared with the dense-grid and hash paths)
 int map_scan_emit(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out, int K, int32_t* counts,
                   int32_t* totals, int ntiles, int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr,
-                  cudaStream_t st);
+                  const uint32_t* masks, cudaStream_t st);
 
 }  // namespace vp
 
@@ -269,6 +272,7 @@ int vp_kernel_map_brick(const void* index, int64_t index_cap, int32_t B, int32_t
   const int ntiles = (int)ceil_div(std::max<int64_t>(cap_out, 1), kBrickTile);
   int32_t* counts = c.take<int32_t>((int64_t)ntiles * K);
   int32_t* totals = c.take<int32_t>(K + 1);
+  uint32_t* masks = c.take<uint32_t>(std::max<int64_t>(cap_out, 1));
   VP_REQUIRE(c.ok(), VP_EVALIDATION, "kernel_map_brick: workspace too small");
   for (int a = 0; a < 3; ++a)
     VP_REQUIRE(in_stride[a] >= 1 && in_stride[a] % s == 0, VP_EVALIDATION,
@@ -287,9 +291,9 @@ int vp_kernel_map_brick(const void* index, int64_t index_cap, int32_t B, int32_t
   }
   BrickSpec g = brick_spec(const_cast<void*>(index), index_cap, B, R, s);
   ::vp::launch(map_probe_brick_kernel, ntiles, kBrickTile, 0, st, (const int4*)out, n_out_dev, cap_out, g, offs, K, nbr,
-               counts, ntiles);
+               counts, ntiles, masks);
   VP_CHECK_LAUNCH("map_probe_brick");
-  return map_scan_emit(nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out, pair_ptr, st);
+  return map_scan_emit(nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out, pair_ptr, masks, st);
 }
 
 size_t vp_kernel_map_brick_ws_bytes(int64_t cap_out, int32_t K) { return vp_kernel_map_grid_ws_bytes(cap_out, K); }

@@ -23,7 +23,7 @@ namespace vp {
 
 int map_scan_emit(const int32_t* nbr, const int32_t* n_out_dev, int64_t cap_out, int K, int32_t* counts,
                   int32_t* totals, int ntiles, int32_t* pair_in, int32_t* pair_out, int32_t* pair_ptr,
-                  cudaStream_t st);
+                  const uint32_t* masks, cudaStream_t st);
 
 constexpr int kWideMaxD1 = 8;  // batch + up to 7 axes
 constexpr int kWideTile = 128;  // output rows per probe tile (== kmap.cu kMapTile)
@@ -321,7 +321,7 @@ int vp_wide_kernel_map(const int64_t* in, int64_t n_in, const int64_t* out, int6
   ::vp::launch(wide_probe_kernel, ntiles, kWideTile, 0, st, in, out, n_out, D1, (const uint32_t*)t, cap - 1, offs, K,
                nbr, counts, ntiles);
   VP_CHECK_LAUNCH("wide_probe");
-  return map_scan_emit(nbr, nullptr, n_out, K, counts, totals, ntiles, pair_in, pair_out, pair_ptr, st);
+  return map_scan_emit(nbr, nullptr, n_out, K, counts, totals, ntiles, pair_in, pair_out, pair_ptr, nullptr, st);
 }
 
 }  // extern "C"

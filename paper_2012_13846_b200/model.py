@@ -168,7 +168,9 @@ class SparseResNetTrainer:
         self.use_grid = index in ("grid", "brick")  # a lattice index (dense cells or 4^3 bricks)
         self.grids = None
         if index == "grid":
-            self.grids = [torch.full((batch * r ** 3,), 0x7FFFFFFF, dtype=torch.int32, device=dev) for r in self.grid_R]
+            # cells + occupancy bitmap (vp_grid_words); zeros = an empty bitmap
+            self.grids = [torch.zeros(int(_lib.query("vp_grid_words", batch, r)), dtype=torch.int32, device=dev)
+                          for r in self.grid_R]
         elif index == "brick":
             self.grids = []
             for i, r in enumerate(self.grid_R):

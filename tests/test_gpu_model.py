@@ -80,8 +80,8 @@ def test_trainer_kernel_maps_bit_exact(index):
             col[eo] = ei
             np.testing.assert_array_equal(nbr[:, k], col)
     if index == "grid":
-        for g in tr.grids:
-            assert bool((g == 0x7FFFFFFF).all())
+        for g, r in zip(tr.grids, tr.grid_R):  # occupancy bitmap (after the B*R^3 cells) all clear
+            assert bool((g[tr.B * r ** 3:] == 0).all())
     if index == "brick":  # coarse table, brick pool and owner list back to their initial state
         for i, g in enumerate(tr.grids):
             r = tr.grid_R[i]

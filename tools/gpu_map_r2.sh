@@ -1,0 +1,5 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest -x -q -m gpu tests/test_gpu_model.py tests/test_gpu_intstage.py tests/test_gpu_bench_parity.py tests/test_gpu_vs_reference.py tests/test_gpu_wide.py 2>&1 | tail -5
+timeout 300 python bench.py --steps 30 --warmup 5 2>&1 | tail -1 > gpurun_out/m_bench.json; cat gpurun_out/m_bench.json | python -c "import json,sys;d=json.loads(sys.stdin.read());print(d['value'],d['ms_per_step'],d['roofline']['map'])"
+timeout 300 python tools/sweep_c2.py --clouds 6,552 --channels 32 --iters 10 --out gpurun_out/m_sweep.jsonl 2>&1 | grep map
