@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kMapTile)
 map_probe_grid_cube_kernel(const int4* __restrict__ out, const int32_t* n_out_dev, int64_t cap_out, GridSpec g,
                            const __grid_constant__ GridOffsets offs, const __grid_constant__ GridCube cube,
                            int32_t* __restrict__ nbr, int32_t* counts, int ntiles, uint32_t* __restrict__ masks,
-                           int32_t* __restrict__ own, int32_t* __restrict__ scratch, int dbg) {
+                           int32_t* __restrict__ own, int32_t* __restrict__ scratch) {
   ::vp::pdl_begin();
   constexpr int K = 27;
   __shared__ int s_nbr[kMapTile * (kMapSmemK + 1)];
@@ -353,7 +353,7 @@ map_probe_grid_cube_kernel(const int4* __restrict__ out, const int32_t* n_out_de
   const int R = g.R;
   const unsigned long long* __restrict__ b64 = reinterpret_cast<const unsigned long long*>(g.bits);
   uint32_t hit = 0;
-  if (on && !(dbg & 2)) {
+  if (on) {
     const int zs = cz > 0 ? cz - 1 : 0;  // first bit of the run (dz = -1, or dz = 0 at the z = 0 face)
     unsigned long long lo[9];
     int q[9];
@@ -382,8 +382,7 @@ map_probe_grid_cube_kernel(const int4* __restrict__ out, const int32_t* n_out_de
   }
   int v[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k)
-    v[k] = ((hit >> k) & 1u) ? ((dbg & 1) ? base : __ldg(g.cells + base + offs.lin[k])) : -1;
+  for (int k = 0; k < K; ++k) v[k] = ((hit >> k) & 1u) ? __ldg(g.cells + base + offs.lin[k]) : -1;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     s_nbr[tid * (kMapSmemK + 1) + k] = v[k];
@@ -392,9 +391,8 @@ map_probe_grid_cube_kernel(const int4* __restrict__ out, const int32_t* n_out_de
   }
   __syncthreads();
   int32_t* dst = nbr + u0 * K;
-  if (!(dbg & 4))
-    for (int rr = warp; rr < rows; rr += kMapTile / 32)
-      if (lane < K) dst[rr * K + lane] = s_nbr[rr * (kMapSmemK + 1) + lane];
+  for (int rr = warp; rr < rows; rr += kMapTile / 32)
+    if (lane < K) dst[rr * K + lane] = s_nbr[rr * (kMapSmemK + 1) + lane];
   if (masks && valid) masks[u0 + tid] = hit;
   if (warp == 0) {  // the tile's per-offset counts: k-major for the scan, tile-major + offsets for the emit
     int c = 0;
@@ -906,8 +904,7 @@ static int map_grid_g(GridSpec g, const int32_t* out, const int32_t* n_out_dev, 
     static const bool slab_on = !getenv("VP_MAP_SLAB") || atoi(getenv("VP_MAP_SLAB")) != 0;
     ::vp::launch(map_probe_grid_cube_kernel, ntiles, kMapTile, 0, st, (const int4*)out, n_out_dev, cap_out,
                  g, offs, cube, nbr, counts, ntiles,
-                 slab_on ? nullptr : masks, slab_on ? own : nullptr, slab_on ? slab : nullptr,
-                 getenv("VP_MAP_DBG") ? atoi(getenv("VP_MAP_DBG")) : 0);
+                 slab_on ? nullptr : masks, slab_on ? own : nullptr, slab_on ? slab : nullptr);
     VP_CHECK_LAUNCH("map_probe_grid_cube");
     if (!slab_on)
       return map_scan_emit(nbr, n_out_dev, cap_out, K, counts, totals, ntiles, pair_in, pair_out, pair_ptr, masks,
