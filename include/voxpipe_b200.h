@@ -186,6 +186,21 @@ int vp_kernel_map_sort(const int32_t* table, const int32_t* n_dev, int64_t cap, 
                        int32_t* table_sorted, void* ws, size_t ws_bytes, vp_stream_t stream);
 int vp_kernel_map_group(const int32_t* table, const int32_t* n_dev, int64_t cap, int32_t K, int32_t key_mode,
                         int32_t* perm, int32_t* table_sorted, void* ws, size_t ws_bytes, vp_stream_t stream);
+/* vp_kernel_map_group with a tile schedule for a conv launched with
+ * sched_grid CTAs (vp_conv_tc_grid; 0 = plain vp_kernel_map_group): rows are
+ * grouped in DESCENDING key order (the partial last tile gets the sparsest
+ * rows), then whole 128-row tiles are placed so that the conv's round-robin
+ * tile -> CTA assignment approximates longest-processing-time-first (tile
+ * cost = its active offsets; the ragged last tile stays last).  The moves
+ * apply when sched_grid < tiles <= 4 sched_grid and K <= 32; every row keeps
+ * its tile mates, so per-row conv results are bitwise those of the
+ * descending grouping without moves (e.g. sched_grid = 1). */
+int vp_kernel_map_group_sched(const int32_t* table, const int32_t* n_dev, int64_t cap, int32_t K, int32_t key_mode,
+                              int32_t sched_grid, int32_t* perm, int32_t* table_sorted, void* ws, size_t ws_bytes,
+                              vp_stream_t stream);
+/* CTA count of the default tensor-core conv config writing nd-wide rows into
+ * cap_out rows (0 when nd takes no tensor-core path). */
+int32_t vp_conv_tc_grid(int64_t nd, int64_t cap_out);
 /* Two-level ("brick") index for bounded lattices, the same contract as the
  * dense grid with ~64x less memory: a coarse table over 4^3 bricks plus a
  * pool of 256 B bricks allocated only where rows exist (kmap_brick.cu).

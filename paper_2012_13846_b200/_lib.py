@@ -51,6 +51,8 @@ SIGNATURES = {
     "vp_kernel_map_sort_ws_bytes": (SZ, [I64, I32]),
     "vp_kernel_map_sort": (C.c_int, [P, P, I64, I32, P, P, P, SZ, P]),
     "vp_kernel_map_group": (C.c_int, [P, P, I64, I32, I32, P, P, P, SZ, P]),
+    "vp_kernel_map_group_sched": (C.c_int, [P, P, I64, I32, I32, I32, P, P, P, SZ, P]),
+    "vp_conv_tc_grid": (I32, [I64, I64]),
     "vp_brick_pool": (I64, [I64, I32, I32]),
     "vp_brick_bytes": (SZ, [I64, I32, I32]),
     "vp_brick_init": (C.c_int, [P, I64, I32, I32, P]),

@@ -357,12 +357,14 @@ def _check_weights(t: SparseTensor, w: ConvWeights, shape: KernelShape):
         raise StructuralError("kernel shape dimension != tensor dimension")
 
 
-def sort_table(table: torch.Tensor, n_rows: int, key_mode: int = 0):
+def sort_table(table: torch.Tensor, n_rows: int, key_mode: int = 0, sched_grid: int = 0):
     """Neighbour-pattern row grouping (vp_kernel_map_group): -> (perm,
     table[perm]) with rows grouped by a 9-bit key of their hit mask, so each
     128-row tile of the implicit GEMM touches few kernel offsets.  key_mode
     0 (columns) for neighbour tables, 1 (planes) for strided inverse tables.
-    Results of the conv are unchanged."""
+    sched_grid > 0: whole 128-row tiles are then placed for a conv launched
+    with that many CTAs (vp_kernel_map_group_sched; vp_conv_tc_grid gives the
+    default config's count).  Results of the conv are unchanged."""
     K = table.shape[1]
     cap = max(n_rows, 1)
     perm = torch.empty(cap, dtype=torch.int32, device=table.device)
@@ -372,8 +374,8 @@ def sort_table(table: torch.Tensor, n_rows: int, key_mode: int = 0):
     ws = _lib.workspace(_lib.query("vp_kernel_map_sort_ws_bytes", n_rows, K), table.device)
     if n_rows >= FULL_MASK_ROWS and K <= 27:
         key_mode = 2  # large tables: the full 27-bit mask (three passes) groups best
-    _lib.call("vp_kernel_map_group", table.data_ptr(), None, n_rows, K, int(key_mode), perm.data_ptr(), ts.data_ptr(),
-              ws.data_ptr(), ws.numel(), _lib.stream())
+    _lib.call("vp_kernel_map_group_sched", table.data_ptr(), None, n_rows, K, int(key_mode), int(sched_grid),
+              perm.data_ptr(), ts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
     return perm, ts
 
 

@@ -803,6 +803,15 @@ int vp_debug_conv_trace(long long* buf) {
 
 // weights cast / transposed (up to fp32) + the split-K partials of the padded tile width
 static int64_t split_width(int64_t c) { return std::max<int64_t>(tc_pad(c), std::min<int64_t>(c, 256)); }
+int32_t vp_conv_tc_grid(int64_t nd, int64_t cap_out) {
+  // the default config's CTA count of a tensor-core conv writing nd-wide rows
+  // (launch_conv_tc): the G of the grouping's tile schedule
+  const int64_t w = tc_pad(nd);
+  if (w == 0) return 0;
+  const int64_t tiles = ceil_div(std::max<int64_t>(cap_out, 1), 128);
+  return (int32_t)std::min<int64_t>(tiles * kMaxSplit, (int64_t)kNumSMs * kCfgCps[conv_cfg(w, cap_out)]);
+}
+
 size_t vp_conv_fwd_ws_bytes(int64_t cin, int64_t cout, int32_t K) {
   return align_up((size_t)K * cin * cout * 4, 256) + split_ws_bytes(split_width(cout));
 }

@@ -157,6 +157,9 @@ __global__ void __launch_bounds__(tc_threads<PW>(), CPS) conv_tc_kernel(const __
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
   long long* const trc = blockIdx.x == 0 ? p.trace : nullptr;
+  // per-CTA record (trace on): [2048 + 4 b] = start, end (globaltimer ns), items, stages
+  long long* const ctr = p.trace != nullptr ? p.trace + 2048 + 4 * blockIdx.x : nullptr;
+  if (ctr != nullptr && threadIdx.x == 0) ctr[0] = (long long)tc::globaltimer();
   const int n_out = load_count(p.n_out_dev, p.cap_out);
   const int ntiles = (n_out + TR - 1) / TR;
   // split partials are sized for kNumSMs work items
@@ -166,7 +169,10 @@ __global__ void __launch_bounds__(tc_threads<PW>(), CPS) conv_tc_kernel(const __
   // writes them instead when the tiles are split)
   const bool epi = p.epi.mode != 0 && S == 1;
   if (epi && blockIdx.x == 0 && tid == 0) *p.epi.nb = min((int)gridDim.x, total);
-  if ((int)blockIdx.x >= total) return;
+  if ((int)blockIdx.x >= total) {
+    if (ctr != nullptr && tid == 0) ctr[1] = (long long)tc::globaltimer();
+    return;
+  }
 
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -353,6 +359,10 @@ __global__ void __launch_bounds__(tc_threads<PW>(), CPS) conv_tc_kernel(const __
       }
     }
     tc::cp_async_wait<0>();
+    if (ctr != nullptr && tid == 0) {
+      ctr[2] = ii;
+      ctr[3] = g;
+    }
   } else if (warp < PW + 4) {
     // ============================ epilogue ============================
     const int ep = warp - PW;
@@ -571,6 +581,7 @@ __global__ void __launch_bounds__(tc_threads<PW>(), CPS) conv_tc_kernel(const __
     }
   }
   __syncthreads();
+  if (ctr != nullptr && tid == 0) ctr[1] = (long long)tc::globaltimer();
   if (warp == PW + 4) tc::tmem_dealloc(tmem, C::TMEM_COLS);
   if (epi && warp >= PW && warp < PW + 4) {
     // the 4 warps' sums in warp order -> this CTA's partial row (the stage

@@ -408,6 +408,18 @@ class SparseResNetTrainer:
         self._c("vp_grid_set", lv.coords.data_ptr(), lv.n.data_ptr(), lv.cap, self.grids[i].data_ptr(), self.B,
                 self.grid_R[i], lv.stride, int(clear), st)
 
+    # stride-1 forward tables of these levels are tile-scheduled for the conv
+    # grid that consumes them (vp_kernel_map_group_sched: their 4 convs per
+    # block; VP_TILE_SCHED=0: plain grouping everywhere)
+    TILE_SCHED = __import__("os").environ.get("VP_TILE_SCHED", "1") != "0"
+    TILE_SCHED_LEVELS = tuple(int(v) for v in __import__("os").environ.get("VP_TILE_SCHED_LEVELS", "1").split(",") if v)
+
+    def _sched_grid(self, m, level):
+        i = self.levels.index(level)
+        if not self.TILE_SCHED or m.dst is not m.src or i not in self.TILE_SCHED_LEVELS:
+            return 0
+        return int(_lib.query("vp_conv_tc_grid", self._width_at(i), level.cap))
+
     def _build_map(self, m, st):
         ist = _lib.i32_array((m.src.stride,) * 3)
         if self.index_kind == "brick":
@@ -427,13 +439,17 @@ class SparseResNetTrainer:
         if m.inv is not None:
             self._c("vp_kernel_map_inverse", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
                     m.inv.data_ptr(), m.src.cap, st)
+        # tile schedule for the consuming convs' grid (forward table: the
+        # convs writing the map's output level; inverse table: the strided
+        # dgrad writing its input level)
         if m.perm is not None:
-            self._c("vp_kernel_map_group", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
-                    2 if m.dst.cap >= self.FULL_MASK_ROWS else 0, m.perm.data_ptr(),
+            self._c("vp_kernel_map_group_sched", m.nbr.data_ptr(), m.dst.n.data_ptr(), m.dst.cap, self.K,
+                    2 if m.dst.cap >= self.FULL_MASK_ROWS else 0, self._sched_grid(m, m.dst), m.perm.data_ptr(),
                     m.nbr_s.data_ptr(), m.sort_ws.data_ptr(), m.sort_ws.numel(), st)
         if m.iperm is not None:
-            self._c("vp_kernel_map_group", m.inv.data_ptr(), m.src.n.data_ptr(), m.src.cap, self.K, 1,
-                    m.iperm.data_ptr(), m.inv_s.data_ptr(), m.sort_ws.data_ptr(), m.sort_ws.numel(), st)
+            self._c("vp_kernel_map_group_sched", m.inv.data_ptr(), m.src.n.data_ptr(), m.src.cap, self.K, 1,
+                    self._sched_grid(m, m.src), m.iperm.data_ptr(), m.inv_s.data_ptr(), m.sort_ws.data_ptr(),
+                    m.sort_ws.numel(), st)
 
     @staticmethod
     def fwd_table(L):

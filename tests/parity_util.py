@@ -107,15 +107,83 @@ def check_grouping(p, ts, mode, what):
     assert (np.diff(p)[d == 0] > 0).all(), f"{what}: grouping not stable"
 
 
+def stable_grouping(table, n, mode, desc=False):
+    """The row order of vp_kernel_map_group: stable sort of the live rows by
+    their grouping key (descending for vp_kernel_map_group_sched)."""
+    key = group_key(np.asarray(table)[:n], mode)
+    if desc:
+        key = ((1 << 27) - 1 if mode == 2 else 511) - key
+    return np.argsort(key, kind="stable").astype(np.int64)
+
+
+def tile_schedule(p0, table, n, G, ovh=3, rounds=4):
+    """numpy restatement of the grouping's tile schedule (kmap_sort.cu
+    tile_cost_kernel / tile_assign_kernel): whole 128-row tiles of the stable
+    grouping p0 placed by round-based LPT over the conv's round-robin slots.
+    Returns the composed row order."""
+    tab = np.asarray(table)
+    K = tab.shape[1]
+    ntiles = (n + 127) // 128
+    if not (0 < G <= 1024 and G < ntiles <= rounds * G and K <= 27):
+        return p0
+    hit = tab[p0] >= 0
+    cost = np.array([hit[t * 128:(t + 1) * 128].any(0).sum() for t in range(ntiles)], np.int64)
+    nfull = n // 128
+    R, rem = divmod(ntiles, G)
+    slots = np.array([R + (b < rem) for b in range(G)], np.int64)
+    used = np.zeros(G, np.int64)
+    load = np.zeros(G, np.int64)
+    tile_at = np.full(ntiles, -1, np.int64)
+    if nfull < ntiles:
+        br = (ntiles - 1) % G
+        load[br] = cost[-1] + ovh
+        slots[br] -= 1
+        tile_at[-1] = ntiles - 1
+    order = sorted(range(nfull), key=lambda t: (-cost[t], t))
+    nxt = 0
+    while nxt < nfull:  # LPT by rounds: one tile per CTA with a free slot
+        avail = sorted((b for b in range(G) if used[b] < slots[b]),
+                       key=lambda b: (load[b], slots[b] - used[b], b))
+        take = min(len(avail), nfull - nxt)
+        for i in range(take):
+            b, t = avail[i], order[nxt + i]
+            tile_at[b + used[b] * G] = t
+            used[b] += 1
+            load[b] += cost[t] + ovh
+        nxt += take
+    src = tile_at[np.arange(n) // 128] * 128 + np.arange(n) % 128
+    return p0[src]
+
+
+def check_tile_blocks(p, p0, n, what):
+    """p is p0 with whole 128-row tiles moved (the tile schedule), the ragged
+    last tile in place."""
+    ntiles = (n + 127) // 128
+    if np.array_equal(p, p0):
+        return
+    blocks0 = {tuple(p0[t * 128:(t + 1) * 128]): t for t in range(n // 128)}
+    seen = set()
+    for t in range(n // 128):
+        key = tuple(p[t * 128:(t + 1) * 128])
+        assert key in blocks0, f"{what}: position tile {t} is not a tile of the grouping"
+        seen.add(blocks0[key])
+    assert len(seen) == n // 128, f"{what}: tiles repeated"
+    if n % 128:
+        assert np.array_equal(p[(ntiles - 1) * 128:], p0[(ntiles - 1) * 128:n]), f"{what}: ragged tile moved"
+
+
 def _check_perm_table(perm, table_s, table, n, what, mode=1):
-    """A grouped table (vp_kernel_map_group): perm is a permutation of
-    0..n-1, table_s[i] == table[perm[i]] row for row, rows in ascending
-    stable key order."""
+    """A grouped table (vp_kernel_map_group[_sched]): perm is a permutation
+    of 0..n-1, table_s[i] == table[perm[i]] row for row, rows in ascending
+    stable key order up to whole-tile moves of the tile schedule."""
     p = perm[:n].cpu().numpy().astype(np.int64)
     assert np.array_equal(np.sort(p), np.arange(n)), f"{what}: perm is not a permutation"
     ts = table_s[:n].cpu().numpy()
     np.testing.assert_array_equal(ts, table[p], err_msg=f"{what}: sorted table != table[perm]")
-    check_grouping(p, ts, mode, what)
+    asc = stable_grouping(table, n, mode)
+    if np.array_equal(p, asc):
+        return
+    check_tile_blocks(p, stable_grouping(table, n, mode, desc=True), n, what)
 
 
 def check_map(m, pairs, what):
