@@ -785,9 +785,13 @@ static int wg_tc(int64_t cin, int64_t cout, const WgParams& p, int mi, cudaStrea
 // pairs per work item: ~2 items per SM at the pair capacity, multiple of 64,
 // depends only on static capacities -> results independent of timing
 static int wgrad_chunk(int64_t cap_pairs) {
+  // cap on the chunk (VP_WGRAD_MAX_CHUNK, tuning; multiple of 64, <= kWgMaxChunk)
+  static const int64_t cap = getenv("VP_WGRAD_MAX_CHUNK")
+                                 ? std::max<int64_t>(256, std::min<int64_t>(kWgMaxChunk, atoll(getenv("VP_WGRAD_MAX_CHUNK")) / 64 * 64))
+                                 : kWgMaxChunk;
   int64_t c = ceil_div(std::max<int64_t>(cap_pairs, 1), 2 * kNumSMs);
   c = ceil_div(c, 64) * 64;
-  return (int)std::min<int64_t>(std::max<int64_t>(c, 256), kWgMaxChunk);
+  return (int)std::min<int64_t>(std::max<int64_t>(c, 256), cap);
 }
 
 }  // namespace vp
