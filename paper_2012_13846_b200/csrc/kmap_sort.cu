@@ -68,7 +68,30 @@ __device__ __forceinline__ uint32_t full_mask(const int32_t* __restrict__ t, int
   return m;
 }
 
-__global__ void __launch_bounds__(kGroupThreads)
+// group_key of a 3^3 row from its 27-bit hit mask (bit k = offset k)
+__device__ __forceinline__ int key_of_mask27(uint32_t m, int mode) {
+  int key = 0;
+  if (mode == 0) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) key |= (((m >> (3 * c)) & 7u) != 0u) << c;
+  } else {
+    // planes: dx = k / 9, dy = (k / 3) % 3, dz = k % 3
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const uint32_t mx = 0x1FFu << (9 * d);
+      const uint32_t my = (0x7u << (3 * d)) | (0x7u << (9 + 3 * d)) | (0x7u << (18 + 3 * d));
+      const uint32_t mz = 0x1249249u << d;  // bits d, d + 3, ..., d + 24
+      key |= ((m & mx) != 0u) << d;
+      key |= ((m & my) != 0u) << (3 + d);
+      key |= ((m & mz) != 0u) << (6 + d);
+    }
+  }
+  return key;
+}
+
+constexpr int kHistThreads = 1024;  // 32 warps: two 32-row groups each, their loads in flight together
+
+__global__ void __launch_bounds__(kHistThreads)
 group_hist_kernel(const int32_t* __restrict__ table, const int32_t* n_dev, int64_t cap, int K, int mode,
                   uint16_t* __restrict__ keys, int32_t* __restrict__ hist, int nblocks, ScanState ss, int scan_tiles,
                   uint32_t* __restrict__ masks, const int32_t* __restrict__ order_in, int shift, int desc) {
@@ -82,6 +105,50 @@ group_hist_kernel(const int32_t* __restrict__ table, const int32_t* n_dev, int64
   for (int b = threadIdx.x; b < kGroupBuckets; b += blockDim.x) s_h[b] = 0;
   __syncthreads();
   const int64_t r0 = (int64_t)blockIdx.x * kGroupTile;
+  if (K == 27 && !(mode == 2 && order_in != nullptr)) {
+    // 3^3 tables: a warp reads 32 consecutive rows (864 contiguous words) with
+    // 27 coalesced loads; ballot j holds the hit bits of words 32 j .. 32 j + 31,
+    // so the 864-bit stream is the rows' 27-bit hit masks back to back
+    __shared__ uint32_t s_bal[kHistThreads / 32][27];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t words = cap * 27;
+    for (int g = warp * 32; g < kGroupTile; g += blockDim.x) {
+      const int64_t rb = r0 + g;
+      if (rb >= n) break;  // warp-uniform
+      // all 27 loads in flight before the first ballot (clamped, unconditional)
+      int32_t v[27];
+#pragma unroll
+      for (int j = 0; j < 27; ++j) v[j] = __ldg(table + min(rb * 27 + j * 32 + lane, words - 1));
+#pragma unroll
+      for (int j = 0; j < 27; ++j) {
+        const bool hit = rb * 27 + j * 32 + lane < words && v[j] >= 0;
+        const uint32_t b = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) s_bal[warp][j] = b;
+      }
+      __syncwarp();
+      const int64_t r = rb + lane;
+      int key = kGroupBuckets + lane;  // dead lanes: unique dummy keys
+      if (r < n) {
+        const int st = 27 * lane, wi = st >> 5, off = st & 31;
+        uint32_t m = s_bal[warp][wi] >> off;
+        if (off > 5) m |= s_bal[warp][wi + 1] << (32 - off);
+        m &= (1u << 27) - 1u;
+        if (mode == 2) {
+          masks[r] = m;
+          key = (int)((m >> shift) & (kGroupBuckets - 1));
+        } else {
+          key = key_of_mask27(m, mode);
+          if (masks != nullptr) masks[r] = m;  // the tile schedule's costs
+        }
+        if (desc) key = kGroupBuckets - 1 - key;
+        keys[r] = (uint16_t)key;
+      }
+      // neighbouring rows share keys: one shared atomic per distinct key in the warp (a count)
+      const unsigned same = __match_any_sync(0xffffffffu, key);
+      if (key < kGroupBuckets && (same & ((1u << lane) - 1u)) == 0) atomicAdd(&s_h[key], __popc(same));
+      __syncwarp();
+    }
+  } else
   for (int i = threadIdx.x; i < kGroupTile; i += blockDim.x) {
     const int64_t r = r0 + i;
     if (r < n) {
@@ -399,7 +466,7 @@ int vp_kernel_map_group_sched(const int32_t* table, const int32_t* n_dev, int64_
   for (int ps = 0; ps < passes; ++ps) {
     const int32_t* in = ps == 0 ? nullptr : bufs[(ps - 1) % 2];
     int32_t* out = bufs[ps % 2];
-    ::vp::launch(group_hist_kernel, nblocks, kGroupThreads, 0, st, table, n_dev, cap, K, key_mode, keys, hist, nblocks,
+    ::vp::launch(group_hist_kernel, nblocks, kHistThreads, 0, st, table, n_dev, cap, K, key_mode, keys, hist, nblocks,
                  ss, scan_tiles, (key_mode == 2 || (sched && ps == 0)) ? masks : nullptr, in, 9 * ps, (int)sched);
     VP_CHECK_LAUNCH("map_group: hist");
     ::vp::launch(group_scan_kernel, scan_tiles, 1024, 0, st, hist, total, ss);
