@@ -402,6 +402,36 @@ __global__ void permute_rows_kernel(const int32_t* __restrict__ table, const int
                                     const int32_t* __restrict__ tile_at, int32_t* __restrict__ perm_out) {
   ::vp::pdl_begin();
   const int n = load_count(n_dev, cap);
+  if (K == 27) {
+    // a warp writes 32 output rows (864 contiguous words): one perm load per
+    // lane, the source rows by shuffle, then 27 independent gathered loads in
+    // flight and 27 coalesced stores
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t rb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; rb < n; rb += nwarps * 32) {
+      const int64_t i = rb + lane;
+      int32_t row = 0;
+      if (i < n) {
+        const int64_t src = tile_at ? (int64_t)__ldg(tile_at + (i >> 7)) * 128 + (i & 127) : i;
+        row = __ldg(perm + src);
+        if (perm_out != nullptr) perm_out[i] = row;
+      }
+      const int live = (int)(n - rb < 32 ? n - rb : 32) * 27;
+      int32_t v[27];
+#pragma unroll
+      for (int j = 0; j < 27; ++j) {
+        const int w = j * 32 + lane;
+        const int r = __shfl_sync(0xffffffffu, row, w / 27);
+        v[j] = w < live ? __ldg(table + (int64_t)r * 27 + (w - (w / 27) * 27)) : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 27; ++j) {
+        const int w = j * 32 + lane;
+        if (w < live) out[rb * 27 + w] = v[j];
+      }
+    }
+    return;
+  }
   const int64_t total = (int64_t)n * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / K;
