@@ -81,12 +81,15 @@ __global__ void wgrad_reduce_kernel(const T* __restrict__ part, const int32_t* _
                                     const SgdFuse sgd) {
   ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
+  __shared__ int s_ptr[VP_MAX_OFFSETS + 1];
   if (chunk_dev) chunk = *chunk_dev;  // chosen on the device by the partial kernel
+  for (int k = threadIdx.x; k <= K; k += blockDim.x) s_ptr[k] = __ldg(pptr + k);  // all loads in flight
+  __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int k = 0; k < K; ++k) {
       s_pref[k] = acc;
-      acc += (pptr[k + 1] - pptr[k] + chunk - 1) / chunk;
+      acc += (s_ptr[k + 1] - s_ptr[k] + chunk - 1) / chunk;
     }
     s_pref[K] = acc;
   }
@@ -167,11 +170,14 @@ wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* 
   ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
   __shared__ T s_red[kWgSimtThreads / 32][32];
+  __shared__ int s_ptr[VP_MAX_OFFSETS + 1];
+  for (int k = threadIdx.x; k <= K; k += blockDim.x) s_ptr[k] = __ldg(pptr + k);  // all loads in flight
+  __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int k = 0; k < K; ++k) {
       s_pref[k] = acc;
-      acc += (pptr[k + 1] - pptr[k] + chunk - 1) / chunk;
+      acc += (s_ptr[k + 1] - s_ptr[k] + chunk - 1) / chunk;
     }
     s_pref[K] = acc;
   }
@@ -182,8 +188,8 @@ wgrad_simt_kernel(const void* __restrict__ x, int x_dtype, int cin, const void* 
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     int k = 0;
     while (s_pref[k + 1] <= item) ++k;
-    const int p0 = pptr[k] + (item - s_pref[k]) * chunk;
-    const int p1 = min(pptr[k + 1], p0 + chunk);
+    const int p0 = s_ptr[k] + (item - s_pref[k]) * chunk;
+    const int p1 = min(s_ptr[k + 1], p0 + chunk);
     for (int e0 = 0; e0 < per; e0 += 32) {
       const int e = e0 + lane;
       const int co = e / cin, ci = e - (e / cin) * cin;
@@ -217,11 +223,14 @@ wgrad_stem_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gy, int K
   ::vp::pdl_begin();
   __shared__ int s_pref[VP_MAX_OFFSETS + 1];
   __shared__ float s_red[kWgStemThreads / 32][COUT];
+  __shared__ int s_ptr[VP_MAX_OFFSETS + 1];
+  for (int k = threadIdx.x; k <= K; k += blockDim.x) s_ptr[k] = __ldg(pptr + k);  // all loads in flight
+  __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int k = 0; k < K; ++k) {
       s_pref[k] = acc;
-      acc += (pptr[k + 1] - pptr[k] + kWgStemChunk - 1) / kWgStemChunk;
+      acc += (s_ptr[k + 1] - s_ptr[k] + kWgStemChunk - 1) / kWgStemChunk;
     }
     s_pref[K] = acc;
   }
@@ -231,8 +240,8 @@ wgrad_stem_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gy, int K
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     int k = 0;
     while (s_pref[k + 1] <= item) ++k;
-    const int p0 = pptr[k] + (item - s_pref[k]) * kWgStemChunk;
-    const int p1 = min(pptr[k + 1], p0 + kWgStemChunk);
+    const int p0 = s_ptr[k] + (item - s_pref[k]) * kWgStemChunk;
+    const int p1 = min(s_ptr[k + 1], p0 + kWgStemChunk);
     float acc[COUT];
 #pragma unroll
     for (int c = 0; c < COUT; ++c) acc[c] = 0.f;

@@ -97,8 +97,13 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_wgrad_tc_kernel(const __
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
   __shared__ int s_chunk;
+  // the pair pointers, all K + 1 loads in flight (a serial loop over them
+  // costs K dependent L2 round trips before the first item)
+  __shared__ int s_ptr[VP_MAX_OFFSETS + 1];
+  for (int k = tid; k <= K; k += blockDim.x) s_ptr[k] = __ldg(p.pptr + k);
+  __syncthreads();
   if (tid == 0) {
-    s_chunk = p.chunk > 0 ? p.chunk : wg_device_chunk(p.pptr[K] - p.pptr[0], K, gridDim.x, p.max_items, p.chunk_min);
+    s_chunk = p.chunk > 0 ? p.chunk : wg_device_chunk(s_ptr[K] - s_ptr[0], K, gridDim.x, p.max_items, p.chunk_min);
     if (blockIdx.x == 0 && p.chunk_out) *p.chunk_out = s_chunk;
   }
   __syncthreads();
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_wgrad_tc_kernel(const __
     int acc = 0;
     for (int k = 0; k < K; ++k) {
       s_pref[k] = acc;
-      acc += (p.pptr[k + 1] - p.pptr[k] + chunk - 1) / chunk;
+      acc += (s_ptr[k + 1] - s_ptr[k] + chunk - 1) / chunk;
     }
     s_pref[K] = acc;
     for (int s = 0; s < C::STAGES; ++s) {
@@ -140,8 +145,8 @@ __global__ void __launch_bounds__(kTcThreads, CPS) conv_wgrad_tc_kernel(const __
   auto item_range = [&](int item, int& k, int& p0, int& p1) {
     k = 0;
     while (s_pref[k + 1] <= item) ++k;
-    p0 = p.pptr[k] + (item - s_pref[k]) * chunk;
-    p1 = min(p.pptr[k + 1], p0 + chunk);
+    p0 = s_ptr[k] + (item - s_pref[k]) * chunk;
+    p1 = min(s_ptr[k + 1], p0 + chunk);
   };
 
   if (warp < 4) {
