@@ -1,0 +1,10 @@
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_bn_epi.py tests/test_gpu_model.py -x -q > gpurun_out/pytest10.log 2>&1; echo "pytest rc=$?"; tail -n 3 gpurun_out/pytest10.log
+rm -f gpurun_out/exp10.txt
+for i in 1 2 3; do
+  timeout 600 python bench.py --steps 200 --no-cpu-baseline --no-roofline > gpurun_out/b.json 2>gpurun_out/b.err
+  python -c "import json;d=json.load(open('gpurun_out/b.json'));print('exp',d['value'],d['ms_per_step'])" >> gpurun_out/exp10.txt
+done
+VP_DBG_SKIP_WGRAD=1 VP_DBG_SKIP_PREFETCH=1 timeout 600 python tools/critical_path.py 2>/dev/null | tail -12 >> gpurun_out/exp10.txt
+cat gpurun_out/exp10.txt
