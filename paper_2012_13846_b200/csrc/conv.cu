@@ -736,7 +736,13 @@ static int conv_tc(int64_t kd, int64_t nd, const FwdParams& p, void* part, cudaS
 
 static size_t split_ws_bytes(int64_t nd) { return align_up((size_t)kSplitItems * 128 * nd * 4, 256); }
 
-constexpr int kWgSms = kNumSMs;
+// the split-phase weight gradient of the training step (vp_conv_wgrad_sgd,
+// phases 1 / 2) runs on the side streams beside the critical path: its
+// persistent grid is capped at 96 of the 148 SMs (VP_WGRAD_SMS; C3 A/B on
+// one box: 148 -> 54.65k, 130 -> 54.87k, 110 -> 55.1k, 96 -> 55.2k, 84-90
+// -> 55.2k, 74 -> 54.7k clouds/s).  A single-call weight gradient (the
+// operator API, phase 0) takes the whole GPU.
+constexpr int kWgSms = 96;
 
 static int wgrad_cps() {  // CTAs per SM of the weight-gradient kernel where two fit (VP_WGRAD_CPS overrides)
   static const int v = getenv("VP_WGRAD_CPS") ? atoi(getenv("VP_WGRAD_CPS")) : 2;
@@ -755,8 +761,7 @@ static int launch_wg_tc_cps(const WgParams& p, int max_items, cudaStream_t st) {
   // persistent, on at most kWgSms SMs: the weight gradient runs on a side
   // stream next to the critical path (BN / dgrad); leaving SMs free for the
   // high-priority kernels shortens the step (VP_WGRAD_SMS overrides)
-  static const int wg_sms = getenv("VP_WGRAD_SMS") ? atoi(getenv("VP_WGRAD_SMS")) : kWgSms;
-  const int grid = std::max(1, std::min(max_items, wg_sms * CPS));
+  const int grid = std::max(1, std::min(max_items, p.sms * CPS));
   ::vp::launch(kern, grid, kTcThreads, C::SMEM, st, p);
   VP_CHECK_LAUNCH("conv_wgrad_tc");
   return VP_OK;
@@ -1110,8 +1115,9 @@ static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const vo
     // floor: gathered bytes per item >= f/2 x its C_out x C_in fp32 partial (VP_WGRAD_MIN_F, default 1)
     static const int min_f = getenv("VP_WGRAD_MIN_F") ? std::max(0, atoi(getenv("VP_WGRAD_MIN_F"))) : 1;
     const int chunk_min = (int)std::min<int64_t>(2 * cin * cout / (cin + cout) * min_f, kWgMaxChunk);
+    static const int side_sms = getenv("VP_WGRAD_SMS") ? std::max(1, atoi(getenv("VP_WGRAD_SMS"))) : kWgSms;
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, static_chunk ? chunk : 0, part,
-               (int)std::min<int64_t>(ws_items, 1 << 30), chunk_dev, chunk_min};
+               (int)std::min<int64_t>(ws_items, 1 << 30), chunk_dev, chunk_min, phase != 0 ? side_sms : kNumSMs};
     const int grid_items = static_chunk ? max_items : (int)std::min<int64_t>(ws_items, 1 << 30);
     if (phase != 2) {
       int rc = wg_tc(cin, cout, p, grid_items, st);

@@ -28,6 +28,7 @@ struct WgParams {
   int max_items;    // partials the workspace holds (device-chosen chunk)
   int* chunk_out;   // device-chosen chunk, for wgrad_reduce_kernel
   int chunk_min;    // device-chosen chunk floor (keeps C_out x C_in partials small next to the gathers)
+  int sms;          // (host) SMs the persistent grid may occupy
 };
 
 // Pairs per work item from the LIVE pair count (pptr[K], on the device):
