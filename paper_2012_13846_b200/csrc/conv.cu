@@ -1089,7 +1089,11 @@ static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const vo
   float* part = (float*)ws;
   float* gw = (float*)gw_out;
   const int64_t total = (int64_t)K * cin * cout;
-  const int rblocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8));
+  int rblocks = (int)std::min<int64_t>(ceil_div(total, 256), grid_cap(8));
+  // the training step's reduction + SGD (phase 2) runs beside the critical
+  // path: blocks capped (VP_WGRAD_RED_BLOCKS, tuning)
+  static const int red_cap = getenv("VP_WGRAD_RED_BLOCKS") ? std::max(1, atoi(getenv("VP_WGRAD_RED_BLOCKS"))) : 0;
+  if (phase == 2 && red_cap > 0) rblocks = std::min(rblocks, red_cap);
   if (x_dtype == VP_F64 || g_dtype == VP_F64) {  // the reference's precision: f64 partials, f64 grad_w
     const int dchunk = 2 * std::min(chunk, kWgSimtChunk);
     const int ditems = (int)(cap_pairs / dchunk + K + 1);
