@@ -14,6 +14,6 @@ for v in "X=1" "VP_DBG_SKIP_WGRAD=1" "VP_DBG_SKIP_PREFETCH=1" "VP_DBG_SKIP_PREFE
   python -c "import json;d=json.load(open('gpurun_out/b.json'));print('$v',d['value'],d['ms_per_step'],d['gpu_launches_per_step'])" >> gpurun_out/decomposition.txt
 done
 VP_DBG_SKIP_WGRAD=1 VP_DBG_SKIP_PREFETCH=1 timeout 600 python tools/critical_path.py > gpurun_out/critical_path.txt 2>&1; echo "critical rc=$?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2c_launches.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG:-r2c}_launches.csv \
   python bench.py --profile-only --no-graph > gpurun_out/ncu_launch.log 2>&1; echo "ncu list rc=$?"
 cat gpurun_out/decomposition.txt
