@@ -743,6 +743,10 @@ static size_t split_ws_bytes(int64_t nd) { return align_up((size_t)kSplitItems *
 // -> 55.2k, 74 -> 54.7k clouds/s).  A single-call weight gradient (the
 // operator API, phase 0) takes the whole GPU.
 constexpr int kWgSms = 96;
+// ... for layers up to this pair capacity (C3's largest: 131,072 rows x 27);
+// the C5-scale layers' weight gradients (tens of millions of pairs) keep all
+// SMs (capped, C5 11.76k -> 11.53k clouds/s)
+constexpr int64_t kWgSideCapPairs = 4 << 20;
 
 static int wgrad_cps() {  // CTAs per SM of the weight-gradient kernel where two fit (VP_WGRAD_CPS overrides)
   static const int v = getenv("VP_WGRAD_CPS") ? atoi(getenv("VP_WGRAD_CPS")) : 2;
@@ -1121,7 +1125,8 @@ static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const vo
     const int chunk_min = (int)std::min<int64_t>(2 * cin * cout / (cin + cout) * min_f, kWgMaxChunk);
     static const int side_sms = getenv("VP_WGRAD_SMS") ? std::max(1, atoi(getenv("VP_WGRAD_SMS"))) : kWgSms;
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, static_chunk ? chunk : 0, part,
-               (int)std::min<int64_t>(ws_items, 1 << 30), chunk_dev, chunk_min, phase != 0 ? side_sms : kNumSMs};
+               (int)std::min<int64_t>(ws_items, 1 << 30), chunk_dev, chunk_min,
+               (phase != 0 && cap_pairs <= kWgSideCapPairs) ? side_sms : kNumSMs};
     const int grid_items = static_chunk ? max_items : (int)std::min<int64_t>(ws_items, 1 << 30);
     if (phase != 2) {
       int rc = wg_tc(cin, cout, p, grid_items, st);
