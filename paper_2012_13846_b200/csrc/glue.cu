@@ -768,9 +768,12 @@ __global__ void xent_reduce_kernel(const float* __restrict__ pooled, int B, int 
 // the last BN's ReLU (act > 0) and stored rounded (gm) with that BN's
 // backward statistics per cloud (sum gm, sum gm (pre - mean): bn_epi.cuh
 // partial row b); head_reduce_kernel (one block) sums the fc gradients and
-// the loss over clouds in order and finalizes the BN statistics.  Same
-// arithmetic and order as pool + xent + pool_backward + the unfused BN
-// statistics pass.
+// the loss over clouds in order and finalizes the BN statistics.  The
+// arithmetic of pool + xent + pool_backward + the unfused BN statistics
+// pass; the pool, pooled-gradient and statistics sums run in G thread
+// groups whose partials are added in group order (deterministic).
+constexpr int kHeadThreads = 1024;
+
 struct HeadBn {
   const void* act;    // last BN output (ReLU mask source), nullable
   const void* pre;    // last BN input (conv output), nullable = no statistics
@@ -780,31 +783,58 @@ struct HeadBn {
   int* nb;
 };
 
+// G = blockDim / C thread groups per channel (4 at C = 256 with 1024
+// threads) split the rows of the pool, the classes of the pooled gradient and
+// the rows of the backward pass; the groups' partials are summed in group
+// order (deterministic)
 template <int DT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kHeadThreads)
 head_kernel(const void* __restrict__ a, int dtype, const int32_t* __restrict__ seg, int B, int C,
             const float* __restrict__ w, const float* __restrict__ bias, int classes, const int32_t* __restrict__ labels,
             float* __restrict__ pooled, float* __restrict__ logits, float* __restrict__ g_logits,
             float* __restrict__ loss_b, float* __restrict__ g_pooled, const HeadBn hb) {
   ::vp::pdl_begin();
   extern __shared__ float sm[];
+  const bool grouped = C <= (int)blockDim.x;
+  const int G = grouped ? (int)blockDim.x / C : 1;
   float* s_x = sm;                 // C: pooled row
   float* s_gp = sm + C;            // C: g_pooled row
   float* s_logit = sm + 2 * C;     // classes
   float* s_g = s_logit + classes;  // classes
+  float* s_r1 = s_g + classes;     // [G][C] group partials
+  float* s_r2 = s_r1 + G * C;      // [G][C]
   __shared__ float s_max, s_sum;
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int grp = grouped ? (int)threadIdx.x / C : 0;
+  const int cstart = grouped ? (int)threadIdx.x % C : (int)threadIdx.x, cstride = grouped ? C : (int)blockDim.x;
+  const bool in_grp = grp < G;
   const int cnt = seg[b], st = seg[B + b];
   if (b == 0 && threadIdx.x == 0 && hb.nb) *hb.nb = B;
   auto ld = [&](const void* p, int64_t i) -> float {
     return DT == VP_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i])
            : DT == VP_F32 ? reinterpret_cast<const float*>(p)[i] : ldf(p, dtype, i);
   };
+  constexpr int U = 8;  // rows per batch: every load of a batch issued before any use
+  if (in_grp)
+    for (int c = cstart; c < C; c += cstride) {
+      float acc = 0.f;
+      for (int r0 = grp; r0 < cnt; r0 += U * G) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = r0 + u * G;
+          v[u] = r < cnt ? ld(a, (int64_t)(st + r) * C + c) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += v[u];
+      }
+      s_r1[grp * C + c] = acc;
+    }
+  __syncthreads();
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float acc = 0.f;
-#pragma unroll 8
-    for (int r = 0; r < cnt; ++r) acc += ld(a, (int64_t)(st + r) * C + c);
+    for (int q = 0; q < G; ++q) acc += s_r1[q * C + c];
     const float v = cnt > 0 ? acc / (float)cnt : 0.f;
     s_x[c] = v;
     pooled[(int64_t)b * C + c] = v;
@@ -841,47 +871,65 @@ head_kernel(const void* __restrict__ a, int dtype, const int32_t* __restrict__ s
     g_logits[(int64_t)b * classes + j] = gj;
   }
   __syncthreads();
+  if (in_grp)
+    for (int c = cstart; c < C; c += cstride) {
+      float acc = 0.f;
+#pragma unroll 8
+      for (int j = grp; j < classes; j += G) acc += s_g[j] * w[(int64_t)j * C + c];
+      s_r1[grp * C + c] = acc;
+    }
+  __syncthreads();
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float acc = 0.f;
-#pragma unroll 8
-    for (int j = 0; j < classes; ++j) acc += s_g[j] * w[(int64_t)j * C + c];
+    for (int q = 0; q < G; ++q) acc += s_r1[q * C + c];
     s_gp[c] = acc;
     g_pooled[(int64_t)b * C + c] = acc;
   }
   __syncthreads();
   // the rows' gradient (pool backward) + the last BN's masked gradient and
   // statistics for this cloud
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    const float g0 = cnt > 0 ? s_gp[c] / (float)cnt : 0.f;
-    const float gr = DT == VP_BF16 ? __bfloat162float(__float2bfloat16_rn(g0)) : g0;
-    const float mu = hb.pre ? hb.mean[c] : 0.f;
-    float s1 = 0.f, s2 = 0.f;
-    constexpr int U = 8;  // rows per batch: every load of a batch issued before any store
-    for (int r0 = 0; r0 < cnt; r0 += U) {
-      float av[U], pv[U];
+  if (in_grp)
+    for (int c = cstart; c < C; c += cstride) {
+      const float g0 = cnt > 0 ? s_gp[c] / (float)cnt : 0.f;
+      const float gr = DT == VP_BF16 ? __bfloat162float(__float2bfloat16_rn(g0)) : g0;
+      const float mu = hb.pre ? hb.mean[c] : 0.f;
+      float s1 = 0.f, s2 = 0.f;
+      for (int r0 = grp; r0 < cnt; r0 += U * G) {
+        float av[U], pv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i = (int64_t)(st + r0 + u) * C + c;
-        const bool in = r0 + u < cnt;
-        av[u] = (in && hb.act) ? ld(hb.act, i) : 1.f;
-        pv[u] = (in && hb.pre) ? ld(hb.pre, i) : 0.f;
-      }
+        for (int u = 0; u < U; ++u) {
+          const int r = r0 + u * G;
+          const int64_t i = (int64_t)(st + r) * C + c;
+          const bool in = r < cnt;
+          av[u] = (in && hb.act) ? ld(hb.act, i) : 1.f;
+          pv[u] = (in && hb.pre) ? ld(hb.pre, i) : 0.f;
+        }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (r0 + u >= cnt) break;
-        const int64_t i = (int64_t)(st + r0 + u) * C + c;
-        const float g = av[u] > 0.f ? gr : 0.f;
-        stf(hb.gm, DT >= 0 ? DT : dtype, i, g);
-        if (hb.pre) {
-          s1 += g;
-          s2 += g * (pv[u] - mu);
+        for (int u = 0; u < U; ++u) {
+          const int r = r0 + u * G;
+          if (r >= cnt) break;
+          const int64_t i = (int64_t)(st + r) * C + c;
+          const float g = av[u] > 0.f ? gr : 0.f;
+          stf(hb.gm, DT >= 0 ? DT : dtype, i, g);
+          if (hb.pre) {
+            s1 += g;
+            s2 += g * (pv[u] - mu);
+          }
         }
       }
+      s_r1[grp * C + c] = s1;
+      s_r2[grp * C + c] = s2;
     }
-    if (hb.pre) {
-      hb.part[((int64_t)b * 2) * C + c] = s1;
-      hb.part[((int64_t)b * 2 + 1) * C + c] = s2;
+  if (!hb.pre) return;
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s1 = 0.f, s2 = 0.f;
+    for (int q = 0; q < G; ++q) {
+      s1 += s_r1[q * C + c];
+      s2 += s_r2[q * C + c];
     }
+    hb.part[((int64_t)b * 2) * C + c] = s1;
+    hb.part[((int64_t)b * 2 + 1) * C + c] = s2;
   }
 }
 
@@ -1232,10 +1280,12 @@ int vp_sparse_head(const void* a, int32_t a_dtype, const int32_t* seg, int32_t B
   p += align_up((size_t)B * 4, 256);
   float* g_pooled = (float*)p;
   HeadBn hb{bn_act, bn_pre, bn_mean, gm, bn_part ? (float*)((char*)bn_part + kBnPartHeader) : nullptr, (int*)bn_part};
-  const size_t smem = (size_t)(2 * C + 2 * classes) * sizeof(float);
+  const int64_t groups = C <= kHeadThreads ? kHeadThreads / C : 1;
+  const size_t smem = (size_t)(2 * C + 2 * classes + 2 * groups * C) * sizeof(float);
   auto hk = a_dtype == VP_BF16 ? head_kernel<VP_BF16> : a_dtype == VP_F32 ? head_kernel<VP_F32> : head_kernel<-1>;
-  ::vp::launch(hk, B, 256, smem, st, a, a_dtype, seg, B, (int)C, w, bias, classes, labels, pooled, logits, g_logits,
-               loss_b, g_pooled, hb);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ::vp::launch(hk, B, kHeadThreads, smem, st, a, a_dtype, seg, B, (int)C, w, bias, classes, labels, pooled, logits,
+               g_logits, loss_b, g_pooled, hb);
   VP_CHECK_LAUNCH("sparse_head");
   BnEpi e{};
   e.mode = 2;
