@@ -4,7 +4,7 @@ timeout 900 python -m pytest tests/test_gpu_bn_epi.py tests/test_gpu_model.py te
 rm -f gpurun_out/exp16.txt
 for i in 1 2; do
   timeout 600 python bench.py --steps 300 --no-cpu-baseline --no-roofline > gpurun_out/b.json 2>gpurun_out/b.err
-  python -c "import json;d=json.load(open('gpurun_out/b.json'));print('head1024',d['value'],d['ms_per_step'])" >> gpurun_out/exp16.txt
+  python -c "import json;d=json.load(open('gpurun_out/b.json'));print('headred',d['value'],d['ms_per_step'])" >> gpurun_out/exp16.txt
 done
 VP_DBG_SKIP_WGRAD=1 VP_DBG_SKIP_PREFETCH=1 timeout 600 python tools/critical_path.py 2>/dev/null | grep -E "head|step span" >> gpurun_out/exp16.txt
 cat gpurun_out/exp16.txt
