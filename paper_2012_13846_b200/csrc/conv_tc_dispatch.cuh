@@ -57,7 +57,9 @@ inline int launch_conv_tc(const FwdParams& p0, void* part, cudaStream_t st) {
     // blocks waited for half an SM); up to kBnPartRows partial rows
     constexpr int NT = 256;
     const int64_t work = p.cap_out * ND / 4;
-    const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(work, NT * 4), kBnPartRows), 1);
+    // partial rows = blocks: the finalize below reads them all (VP_ROWS_PASS_BLOCKS caps them, tuning)
+    static const int64_t rp_cap = getenv("VP_ROWS_PASS_BLOCKS") ? std::max(1, atoi(getenv("VP_ROWS_PASS_BLOCKS"))) : kBnPartRows;
+    const int64_t blocks = std::max<int64_t>(std::min<int64_t>(ceil_div(work, NT * 4), std::min<int64_t>(rp_cap, kBnPartRows)), 1);
     BnEpi e = rows_epi;
     e.out_a = e.out_b = nullptr;  // finalized by the 32-channel-per-block kernel below
     ::vp::launch(split_reduce_epi_kernel<ND, NT>, (int)blocks, NT, 0, st, (const float*)part, p.n_out_dev,
