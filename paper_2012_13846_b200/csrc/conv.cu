@@ -394,7 +394,7 @@ constexpr int kStemRows = 128;
 // SM, so C3's ~900 tiles run as one wave (at 128 registers they took two).
 constexpr int kStemPass = 16;
 constexpr int kStemCluster = 4;  // CTAs per cluster when the stem also writes BN statistics
-template <int XT>
+template <int XT, bool MMA = false>
 __global__ void __launch_bounds__(kStemRows, 8)
 conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict__ w, int w_dtype, int cout,
                  const int32_t* __restrict__ table, int flip, const int32_t* __restrict__ perm,
@@ -443,10 +443,36 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
       for (int e = threadIdx.x; e < rows * 27; e += kStemRows) s_t[e] = __ldg(tb + e);
     }
     __syncthreads();
+    // bf16, C_out = 32: the tile is one 128 x 32 x 32 (K = 27 zero-padded)
+    // product on the tensor cores (mma.sync m16n8k16, fp32 accumulate): warp
+    // w owns rows 32 w .. 32 w + 31 (two m16 tiles), all four n8 tiles
+    static_assert(!MMA || XT == VP_BF16, "the tensor-core stem takes bf16 inputs and weights");
+    constexpr bool use_mma = MMA;  // launched only for C_out = 32
+    uint32_t af[2][2][4];  // A fragments [m16 tile][k16 step][reg], gathered once per tile
+    if (use_mma) {
+      const int t = threadIdx.x & 31, wq = threadIdx.x >> 5;
+      const unsigned short* xs = reinterpret_cast<const unsigned short*>(x);
+      auto xat = [&](int row, int k) -> uint32_t {  // raw bf16 bits of A[row][k]
+        if (row >= rows || k >= 27) return 0u;
+        const int e = s_t[row * 27 + (flip ? 26 - k : k)];
+        return e >= 0 ? (uint32_t)__ldg(xs + e) : 0u;
+      };
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int row = wq * 32 + mi * 16 + (t >> 2) + ((q & 1) ? 8 : 0);
+            const int k = ks * 16 + (t & 3) * 2 + ((q & 2) ? 8 : 0);
+            af[mi][ks][q] = xat(row, k) | (xat(row, k + 1) << 16);
+          }
+    }
     float xk[27];
     const bool valid = threadIdx.x < rows;
 #pragma unroll
     for (int k = 0; k < 27; ++k) {
+      if (use_mma) break;
       const int v = valid ? s_t[threadIdx.x * 27 + (flip ? 26 - k : k)] : -1;
       if (XT == VP_BF16)
         xk[k] = v >= 0 ? __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(x) + v)) : 0.f;
@@ -456,6 +482,41 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
         xk[k] = v >= 0 ? ldf(x, x_dtype, v) : 0.f;
     }
     for (int c0 = 0; c0 < cout; c0 += kStemPass) {
+      if (use_mma) {
+        // this pass's 16 channels = n8 tiles c0/8, c0/8 + 1: B fragments from
+        // the staged weights (exact bf16), 8 MMAs, packed pairs of rows r0, r0 + 8
+        const int t = threadIdx.x & 31, wq = threadIdx.x >> 5;
+        uint32_t bf[2][2][2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int k = ks * 16 + (t & 3) * 2 + h * 8, n = c0 + 8 * jj + (t >> 2);
+              const float w0 = k < 27 ? s_w[k * 32 + n] : 0.f, w1 = k + 1 < 27 ? s_w[(k + 1) * 32 + n] : 0.f;
+              __nv_bfloat162 hw = __floats2bfloat162_rn(w0, w1);
+              bf[jj][ks][h] = *reinterpret_cast<uint32_t*>(&hw);
+            }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+              asm volatile(
+                  "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                  "{%0,%1,%2,%3};"
+                  : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                  : "r"(af[mi][ks][0]), "r"(af[mi][ks][1]), "r"(af[mi][ks][2]), "r"(af[mi][ks][3]),
+                    "r"(bf[jj][ks][0]), "r"(bf[jj][ks][1]));
+            const int r0 = wq * 32 + mi * 16 + (t >> 2), pair = 4 * jj + (t & 3);
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(d[0], d[1]), h1 = __floats2bfloat162_rn(d[2], d[3]);
+            s_o[r0 * 9 + pair] = *reinterpret_cast<uint32_t*>(&h0);
+            s_o[(r0 + 8) * 9 + pair] = *reinterpret_cast<uint32_t*>(&h1);
+          }
+      } else {
       float acc[kStemPass];
 #pragma unroll
       for (int c = 0; c < kStemPass; ++c) acc[c] = 0.f;
@@ -476,6 +537,7 @@ conv_stem_kernel(const void* __restrict__ x, int x_dtype, const void* __restrict
         __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * c], acc[2 * c + 1]);
         s_o[threadIdx.x * 9 + c] = *reinterpret_cast<uint32_t*>(&h);
       }
+      }  // FMA path
       __syncthreads();
       // coalesced: word e of the tile -> row e / 8, pair e % 8
       for (int el = threadIdx.x; el < rows * 8; el += kStemRows) {
@@ -588,7 +650,10 @@ static int launch_small_fwd(const void* x, int xd, int cin, const void* w, int w
   if (cin == 1 && K == 27 && cout % 32 == 0 && cout <= 256 && yd == VP_BF16) {
     const size_t smem = (size_t)27 * cout * 4 + kStemRows * 27 * 4 + kStemRows * 9 * 4 + 2 * cout * 4 + 4 * 8 * 4 * 4;
     const int dt = xd == wd ? xd : -1;
-    auto kern = dt == VP_BF16 ? conv_stem_kernel<VP_BF16> : dt == VP_F32 ? conv_stem_kernel<VP_F32> : conv_stem_kernel<-1>;
+    // bf16 with C_out = 32: the mma.sync instance (VP_STEM_MMA=0: the FMA one)
+    static const bool stem_mma = !(getenv("VP_STEM_MMA") && atoi(getenv("VP_STEM_MMA")) == 0);
+    auto kern = dt == VP_BF16 ? ((stem_mma && cout == 32) ? conv_stem_kernel<VP_BF16, true> : conv_stem_kernel<VP_BF16>)
+                : dt == VP_F32 ? conv_stem_kernel<VP_F32> : conv_stem_kernel<-1>;
     BnEpi e = epi.mode == 1 ? epi : BnEpi{};
     if (e.mode == 1) {  // clusters of kStemCluster CTAs, one partial row each
       blocks = (int)std::min<int64_t>(ceil_div(blocks, kStemCluster) * kStemCluster, (int64_t)kBnPartRows * kStemCluster);
