@@ -261,6 +261,14 @@ int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t c_in, const void* g, i
                   int64_t c_out, int32_t K, const int32_t* pair_in, const int32_t* pair_out,
                   const int32_t* pair_ptr, int64_t cap_pairs, void* grad_w,
                   void* ws, size_t ws_bytes, vp_stream_t stream);
+/* vp_conv_wgrad for a weight gradient that runs on a side stream beside a
+ * critical path (the data-parallel training step): the persistent grid is
+ * capped like vp_conv_wgrad_sgd's (VP_WGRAD_SMS, 96 of 148 SMs, for pair
+ * capacities <= 4M); results identical to vp_conv_wgrad. */
+int vp_conv_wgrad_side(const void* x, int32_t x_dtype, int64_t c_in, const void* g, int32_t g_dtype,
+                       int64_t c_out, int32_t K, const int32_t* pair_in, const int32_t* pair_out,
+                       const int32_t* pair_ptr, int64_t cap_pairs, void* grad_w, void* ws, size_t ws_bytes,
+                       vp_stream_t stream);
 
 /* vp_conv_wgrad + momentum SGD of W in the reduction kernel (the training
  * step's per-layer update without a separate pass): m = momentum*m + grad_w,

@@ -73,6 +73,7 @@ SIGNATURES = {
     "vp_conv_dgrad": (C.c_int, [P, I32, I64, I64, P, I32, I64, I32, P, I32, P, P, I64, P, I32, P, SZ, P]),
     "vp_conv_wgrad_ws_bytes": (SZ, [I64, I64, I32, I64]),
     "vp_conv_wgrad": (C.c_int, [P, I32, I64, P, I32, I64, I32, P, P, P, I64, P, P, SZ, P]),  # grad_w: fp32 (f64 for f64 operands)
+    "vp_conv_wgrad_side": (C.c_int, [P, I32, I64, P, I32, I64, I32, P, P, P, I64, P, P, SZ, P]),
     "vp_conv_wgrad_sgd": (C.c_int, [P, I32, I64, P, I32, I64, I32, P, P, P, I64, P, P, SZ, P, P, P, F32, F32, I32, P]),
     "vp_batch_segments": (C.c_int, [P, P, I64, I32, P, P]),
     "vp_sparse_head_ws_bytes": (SZ, [I32, I64, I32]),

@@ -1125,13 +1125,21 @@ size_t vp_conv_wgrad_ws_bytes(int64_t cin, int64_t cout, int32_t K, int64_t cap_
 // phase: 0 = partials + reduction, 1 = partials only, 2 = reduction only
 static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
                            int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
-                           void* gw_out, void* ws, size_t ws_bytes, const SgdFuse& sgd, int phase, cudaStream_t st);
+                           void* gw_out, void* ws, size_t ws_bytes, const SgdFuse& sgd, int phase, cudaStream_t st,
+                           bool side = false);
 
 int vp_conv_wgrad(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
                   int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
                   void* gw_out, void* ws, size_t ws_bytes, vp_stream_t stream) {
   return conv_wgrad_impl(x, x_dtype, cin, g, g_dtype, cout, K, pin, pout, pptr, cap_pairs, gw_out, ws, ws_bytes,
                          SgdFuse{}, 0, (cudaStream_t)stream);
+}
+
+int vp_conv_wgrad_side(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
+                       int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
+                       void* gw_out, void* ws, size_t ws_bytes, vp_stream_t stream) {
+  return conv_wgrad_impl(x, x_dtype, cin, g, g_dtype, cout, K, pin, pout, pptr, cap_pairs, gw_out, ws, ws_bytes,
+                         SgdFuse{}, 0, (cudaStream_t)stream, true);
 }
 
 int vp_conv_wgrad_sgd(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
@@ -1147,7 +1155,8 @@ int vp_conv_wgrad_sgd(const void* x, int32_t x_dtype, int64_t cin, const void* g
 
 static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const void* g, int32_t g_dtype, int64_t cout,
                            int32_t K, const int32_t* pin, const int32_t* pout, const int32_t* pptr, int64_t cap_pairs,
-                           void* gw_out, void* ws, size_t ws_bytes, const SgdFuse& sgd, int phase, cudaStream_t st) {
+                           void* gw_out, void* ws, size_t ws_bytes, const SgdFuse& sgd, int phase, cudaStream_t st,
+                           bool side) {
   VP_REQUIRE(K >= 1 && K <= VP_MAX_OFFSETS, VP_EVALIDATION, "kernel offset count out of range");
   VP_REQUIRE(ws && ws_bytes >= vp_conv_wgrad_ws_bytes(cin, cout, K, cap_pairs), VP_EVALIDATION,
              "conv_wgrad: workspace too small");
@@ -1191,7 +1200,7 @@ static int conv_wgrad_impl(const void* x, int32_t x_dtype, int64_t cin, const vo
     static const int side_sms = getenv("VP_WGRAD_SMS") ? std::max(1, atoi(getenv("VP_WGRAD_SMS"))) : kWgSms;
     WgParams p{(const bf16*)x, (const bf16*)g, K, pin, pout, pptr, static_chunk ? chunk : 0, part,
                (int)std::min<int64_t>(ws_items, 1 << 30), chunk_dev, chunk_min,
-               (phase != 0 && cap_pairs <= kWgSideCapPairs) ? side_sms : kNumSMs};
+               ((phase != 0 || side) && cap_pairs <= kWgSideCapPairs) ? side_sms : kNumSMs};
     const int grid_items = static_chunk ? max_items : (int)std::min<int64_t>(ws_items, 1 << 30);
     if (phase != 2) {
       int rc = wg_tc(cin, cout, p, grid_items, st);

@@ -685,8 +685,8 @@ class SparseResNetTrainer:
             ws = self.side[3 - (L["index"] % 2)]
             self._forked.add(id(ws))
             ws.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(ws):
-                self._c("vp_conv_wgrad", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
+            with torch.cuda.stream(ws):  # the side-stream variant (SM-capped persistent grid)
+                self._c("vp_conv_wgrad_side", x.data_ptr(), fc, L["cin"], L["gy"].data_ptr(), fc, L["cout"],
                         self.K, m.pin.data_ptr(), m.pout.data_ptr(), m.ptr.data_ptr(), m.pin.numel(),
                         L["gw"].data_ptr(), L["wg_ws"].data_ptr(), L["wg_ws"].numel(), ws.cuda_stream)
         else:
